@@ -1,0 +1,184 @@
+"""oracle -- TEST INFRASTRUCTURE ONLY.
+
+ctypes wrapper around ``libgpa_oracle.so`` (plain single-threaded C of GPA's definitions,
+see gpa_oracle.h).  Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+``--impl reference`` leg may import this package; the product path never does.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgpa_oracle.so")
+
+P_U8 = ctypes.POINTER(ctypes.c_uint8)
+
+
+def build(force: bool = False) -> str:
+    src = os.path.join(_HERE, "gpa_oracle.c")
+    hdr = os.path.join(_HERE, "gpa_oracle.h")
+    if force or not os.path.exists(LIB_PATH) or os.path.getmtime(LIB_PATH) < max(
+            os.path.getmtime(src), os.path.getmtime(hdr)):
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-Wall", "-shared", "-fPIC", "-o",
+                               LIB_PATH, src, "-lm"])
+    return LIB_PATH
+
+
+class _Prog(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_uint32) for k in
+                ("n_instr", "n_reasons", "n_lines", "n_loops", "n_funcs", "n_kernels")] + [
+        (k, ctypes.c_void_p) for k in (
+            "opclass", "iflags", "latency", "line_id", "loop_id", "loop_parent", "func_begin",
+            "kernel_func_begin", "kernel_grid_blocks", "row_ptr", "edge_def", "edge_kind",
+            "edge_min_len", "edge_max_len", "edge_dom_k")]
+
+
+class Pattern(ctypes.Structure):
+    _fields_ = [("column_mask", ctypes.c_uint32), ("class_mask", ctypes.c_uint16),
+                ("sample_class", ctypes.c_uint8), ("model", ctypes.c_uint8),
+                ("flag_filter", ctypes.c_uint8), ("same_loop", ctypes.c_uint8),
+                ("parallel_rule", ctypes.c_uint8), ("pad", ctypes.c_uint8),
+                ("sm_count", ctypes.c_uint32),
+                ("ratio", ctypes.c_double), ("W", ctypes.c_double), ("W_new", ctypes.c_double),
+                ("f", ctypes.c_double)]
+
+
+class Estimate(ctypes.Structure):
+    _fields_ = [("speedup", ctypes.c_double), ("M", ctypes.c_double), ("eq3", ctypes.c_double),
+                ("eq4", ctypes.c_double), ("T", ctypes.c_uint64), ("A", ctypes.c_uint64),
+                ("best_scope", ctypes.c_int32), ("unbounded", ctypes.c_uint8),
+                ("matched", ctypes.c_uint8), ("model", ctypes.c_uint8), ("pad", ctypes.c_uint8)]
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        L = ctypes.CDLL(build())
+        vp = ctypes.c_void_p
+        L.or_histogram.argtypes = [vp, vp, ctypes.c_uint64, vp, vp]
+        L.or_blame.argtypes = [vp, vp, vp, vp, vp, vp]
+        L.or_rollup.argtypes = [vp] * 13
+        L.or_estimate_all.argtypes = [vp, vp, vp, vp, vp, vp, ctypes.c_uint32, vp]
+        for f in ("or_eq2", "or_eq4", "or_eq5", "or_eq10"):
+            getattr(L, f).restype = ctypes.c_double
+        L.or_eq2.argtypes = [ctypes.c_double] * 2
+        L.or_eq4.argtypes = [ctypes.c_double] * 3
+        L.or_eq5.argtypes = [ctypes.c_double] * 3
+        L.or_eq10.argtypes = [ctypes.c_double] * 4
+        L.or_ncol.argtypes = [ctypes.c_uint32]
+        L.or_ncol.restype = ctypes.c_uint32
+        _lib = L
+    return _lib
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data
+
+
+class OracleProgram:
+    """Keeps the numpy arrays alive and exposes the or_program struct."""
+
+    _DT = {"opclass": np.uint8, "iflags": np.uint8, "latency": np.uint32, "line_id": np.uint32,
+           "loop_id": np.int32, "loop_parent": np.int32, "func_begin": np.uint32,
+           "kernel_func_begin": np.uint32, "kernel_grid_blocks": np.uint32, "row_ptr": np.uint32,
+           "edge_def": np.uint32, "edge_kind": np.uint8, "edge_min_len": np.uint32,
+           "edge_max_len": np.uint32, "edge_dom_k": np.int32}
+
+    def __init__(self, prog):
+        self.arr = {k: np.ascontiguousarray(getattr(prog, k), dtype=dt) for k, dt in self._DT.items()}
+        self.n_instr = int(self.arr["opclass"].shape[0])
+        self.R = int(prog.n_reasons)
+        self.n_lines = int(prog.n_lines)
+        self.n_loops = int(self.arr["loop_parent"].shape[0])
+        self.n_funcs = int(self.arr["func_begin"].shape[0] - 1)
+        self.n_kernels = int(self.arr["kernel_func_begin"].shape[0] - 1)
+        self.E = int(self.arr["row_ptr"][-1])
+        self.ncol = int(lib().or_ncol(self.R))
+        self.s = _Prog(self.n_instr, self.R, self.n_lines, self.n_loops, self.n_funcs,
+                       self.n_kernels, *[_ptr(self.arr[k]) for k in (
+                           "opclass", "iflags", "latency", "line_id", "loop_id", "loop_parent",
+                           "func_begin", "kernel_func_begin", "kernel_grid_blocks", "row_ptr",
+                           "edge_def", "edge_kind", "edge_min_len", "edge_max_len", "edge_dom_k")])
+
+    @property
+    def ref(self):
+        return ctypes.byref(self.s)
+
+    # --- step 1
+    def new_counts(self) -> np.ndarray:
+        return np.zeros((self.n_instr, 2, self.R), np.uint64)
+
+    def histogram(self, records: np.ndarray, C: np.ndarray | None = None, stats=None):
+        """records: uint64 array (one 8-byte record each). Accumulates into C / stats."""
+        rec = np.ascontiguousarray(records).view(np.uint8)
+        if C is None:
+            C = self.new_counts()
+        if stats is None:
+            stats = np.zeros(3, np.uint64)
+        lib().or_histogram(self.ref, rec.ctypes.data, rec.size // 8, C.ctypes.data, stats.ctypes.data)
+        return C, stats
+
+    # --- steps 2-6
+    def blame(self, C: np.ndarray):
+        cand = np.zeros(self.E, np.uint8)
+        selff = np.zeros(self.n_instr, np.uint8)
+        share = np.zeros((self.E, 3), np.float64)
+        V = np.zeros((self.n_instr, self.ncol, 2), np.float64)
+        lib().or_blame(self.ref, C.ctypes.data, cand.ctypes.data, selff.ctypes.data,
+                       share.ctypes.data, V.ctypes.data)
+        return {"cand": cand, "self": selff, "share": share, "V": V}
+
+    # --- step 7
+    def rollup(self, C: np.ndarray, V: np.ndarray):
+        nc = self.ncol
+        out = {
+            "line_v": np.zeros((self.n_lines, nc, 2)), "line_al": np.zeros((self.n_lines, 2), np.uint64),
+            "loop_excl_v": np.zeros((self.n_loops, nc, 2)), "loop_excl_al": np.zeros((self.n_loops, 2), np.uint64),
+            "loop_incl_v": np.zeros((self.n_loops, nc, 2)), "loop_incl_al": np.zeros((self.n_loops, 2), np.uint64),
+            "func_v": np.zeros((self.n_funcs, nc, 2)), "func_al": np.zeros((self.n_funcs, 2), np.uint64),
+            "kern_v": np.zeros((self.n_kernels, nc, 2)), "kern_al": np.zeros((self.n_kernels, 2), np.uint64),
+        }
+        keys = ["line_v", "line_al", "loop_excl_v", "loop_excl_al", "loop_incl_v", "loop_incl_al",
+                "func_v", "func_al", "kern_v", "kern_al"]
+        lib().or_rollup(self.ref, C.ctypes.data, V.ctypes.data, *[_ptr(out[k]) for k in keys])
+        return out
+
+    # --- step 8
+    def estimate(self, C, blame, patterns):
+        pats = (Pattern * len(patterns))(*patterns)
+        out = (Estimate * (self.n_kernels * len(patterns)))()
+        lib().or_estimate_all(self.ref, C.ctypes.data, blame["cand"].ctypes.data,
+                              blame["self"].ctypes.data, blame["share"].ctypes.data,
+                              ctypes.addressof(pats), len(patterns), ctypes.addressof(out))
+        return [[out[k * len(patterns) + q] for q in range(len(patterns))]
+                for k in range(self.n_kernels)]
+
+    def run_all(self, records, patterns=None):
+        C, stats = self.histogram(records)
+        b = self.blame(C)
+        r = self.rollup(C, b["V"])
+        est = self.estimate(C, b, patterns) if patterns else None
+        return {"C": C, "stats": stats, **b, **r, "est": est}
+
+
+def eq2(T, M):
+    return lib().or_eq2(T, M)
+
+
+def eq4(T, A, ML):
+    return lib().or_eq4(T, A, ML)
+
+
+def eq5(T, A_nested, ML):
+    return lib().or_eq5(T, A_nested, ML)
+
+
+def eq10(W, W_new, R_I, f):
+    return lib().or_eq10(W, W_new, R_I, f)

@@ -1,0 +1,468 @@
+/*
+ * gpa_oracle.c -- TEST INFRASTRUCTURE ONLY (see gpa_oracle.h).
+ *
+ * Plain single-threaded C99, fp64, u64 counts, sums in the order the definitions are
+ * written (CSR order, instruction order).  No blocking, no fusion, no reordering.
+ * Each function cites the PAPER.md passage it follows ("P:n") and the DESIGN.md
+ * reading ("Q#") where the paper is silent.  Build: gcc -O2 -shared -fPIC.
+ */
+#include "gpa_oracle.h"
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+enum { R_NONE = 0, R_MEM = 1, R_EXEC = 2, R_SYNC = 3 };
+enum { C_GLOBAL = 0, C_LOCAL = 1, C_SHARED = 2, C_CONSTANT = 3, C_TEXTURE = 4,
+       C_ARITH_FIXED = 5, C_ARITH_LONG = 6, C_CONVERT = 7, C_CONTROL = 8, C_SYNC = 9, C_MISC = 10 };
+enum { K_REG = 1, K_PRED = 2, K_BAR = 4, K_WAR = 8 };
+enum { COL_MEM_GLOBAL = 0, COL_MEM_LOCAL = 1, COL_MEM_CONSTANT = 2, COL_EXEC_SHARED = 3,
+       COL_EXEC_ARITH = 4, COL_EXEC_WAR = 5, COL_SYNC = 6, COL_MEM_SELF = 7, COL_EXEC_SELF = 8,
+       COL_SYNC_SELF = 9, COL_PASS0 = 10 };
+
+uint32_t or_ncol(uint32_t R) { return 10u + (R - 4u); }
+
+static uint64_t cnt(const or_program *p, const uint64_t *C, uint32_t i, int c, uint32_t r) {
+  return C[((uint64_t)i * 2u + (uint64_t)c) * p->n_reasons + r];
+}
+
+/* ---------------------------------------------------------------- step 1: histogram
+ * every sample is an active sample (scheduler issuing) or a latency sample,
+ * with a stall reason "if any".  A record is a pre-aggregated run of `count` identical
+ * samples.  Q12: a latency sample without a stall reason is malformed and excluded;
+ * records with pc >= n_instr, reason >= R or unknown flag bits are excluded too and
+ * counted in the stats. */
+int or_histogram(const or_program *p, const uint8_t *rec, uint64_t n, uint64_t *C,
+                 uint64_t stats[3]) {
+  uint64_t k;
+  for (k = 0; k < n; ++k) {
+    const uint8_t *b = rec + 8u * k;
+    uint32_t pc = (uint32_t)b[0] | ((uint32_t)b[1] << 8) | ((uint32_t)b[2] << 16) |
+                  ((uint32_t)b[3] << 24);
+    uint32_t count = (uint32_t)b[4] | ((uint32_t)b[5] << 8);
+    uint32_t reason = b[6];
+    uint32_t flags = b[7];
+    int lat = (int)(flags & 1u);
+    int valid = pc < p->n_instr && reason < p->n_reasons && (flags & ~1u) == 0u &&
+                !(lat && reason == R_NONE);
+    if (!valid) {
+      stats[1] += 1u;
+      stats[2] += count;
+      continue;
+    }
+    C[((uint64_t)pc * 2u + (uint64_t)lat) * p->n_reasons + reason] += count;
+    stats[0] += count;
+  }
+  return 0;
+}
+
+/* ---------------------------------------------------------------- step 2-6: blame */
+
+/* Rule 1, opcode based pruning: memory dependency stalls only to memory
+ * instructions, synchronization stalls only to synchronization instructions.
+ * Q6: memory = {GLOBAL, LOCAL, CONSTANT, TEXTURE}; shared memory is an execution
+ * dependency source (Fig. 6); execution dependency has no opcode rule. */
+static int rule1_keeps(uint32_t r, uint32_t def_class) {
+  if (r == R_MEM)
+    return def_class == C_GLOBAL || def_class == C_LOCAL || def_class == C_CONSTANT ||
+           def_class == C_TEXTURE;
+  if (r == R_SYNC) return def_class == C_SYNC;
+  return 1;
+}
+
+/* Fig. 6: detailed category of an attributed dependency stall, chosen by
+ * the opcode of the source (def) instruction; WAR is the execution sub-category of
+ * P:412 (Q13); texture counts as global memory (Q14). */
+static uint32_t classify(uint32_t r, uint32_t def_class, uint32_t kind) {
+  if (r == R_MEM) {
+    if (def_class == C_LOCAL) return COL_MEM_LOCAL;
+    if (def_class == C_CONSTANT) return COL_MEM_CONSTANT;
+    return COL_MEM_GLOBAL;
+  }
+  if (r == R_EXEC) {
+    if (kind & K_WAR) return COL_EXEC_WAR;
+    if (def_class == C_SHARED) return COL_EXEC_SHARED;
+    return COL_EXEC_ARITH;
+  }
+  return COL_SYNC;
+}
+
+int or_blame(const or_program *p, const uint64_t *C, uint8_t *cand, uint8_t *self_flags,
+             double *share, double *V) {
+  const uint32_t n = p->n_instr, R = p->n_reasons, NC = or_ncol(R);
+  const uint32_t E = p->row_ptr[n];
+  uint32_t j, r, e;
+  memset(cand, 0, E);
+  memset(self_flags, 0, n);
+  memset(share, 0, sizeof(double) * 3u * E);
+  memset(V, 0, sizeof(double) * 2u * NC * n);
+
+  for (j = 0; j < n; ++j) {
+    /* S_j[r] (all samples of reason r at j) and SL_j[r] (latency samples) */
+    uint64_t S[16], SL[16];
+    uint64_t dep_total = 0;
+    for (r = 0; r < R; ++r) {
+      S[r] = cnt(p, C, j, 0, r) + cnt(p, C, j, 1, r);
+      SL[r] = cnt(p, C, j, 1, r);
+    }
+    for (r = R_MEM; r <= R_SYNC; ++r) dep_total += S[r];
+
+    /* the dependency graph is built from the def-use chains of instructions that
+     * carry samples; only rows with dependency stalls get in-edges. */
+    if (dep_total > 0) {
+      for (r = R_MEM; r <= R_SYNC; ++r) {
+        double W = 0.0;
+        int any = 0;
+        /* an edge i->j survives for reason r unless pruned by rule 1 (opcode),
+         * rule 2 (a non-predicated k reading the operand lies on every i->j path: the
+         * static field dom_k >= 0, Q7) or rule 3 (every i->j path is longer than
+         * latency(i): min_len > latency, Q8). */
+        for (e = p->row_ptr[j]; e < p->row_ptr[j + 1]; ++e) {
+          uint32_t d = p->edge_def[e];
+          int keep = rule1_keeps(r, p->opclass[d]) && p->edge_dom_k[e] < 0 &&
+                     p->edge_min_len[e] <= p->latency[d];
+          if (keep) {
+            cand[e] |= (uint8_t)(1u << (r - 1u));
+            any = 1;
+          }
+        }
+        if (!any) {
+          /* Q5: no surviving source -> the stall stays at j (self), never dropped. */
+          self_flags[j] |= (uint8_t)(1u << (r - 1u));
+          continue;
+        }
+        /* Eq. 1: weight R_path * R_issue with R_issue = issued (active)
+         * samples of the def (Q3; at least 1, Q4) and R_path = 1 / longest path
+         * length in instructions (Q1/Q2). */
+        for (e = p->row_ptr[j]; e < p->row_ptr[j + 1]; ++e) {
+          if (cand[e] & (1u << (r - 1u))) {
+            uint32_t d = p->edge_def[e];
+            uint64_t A_d = 0;
+            uint32_t rr;
+            for (rr = 0; rr < R; ++rr) A_d += cnt(p, C, d, 0, rr);
+            W += (double)(A_d > 0 ? A_d : 1u) / (double)p->edge_max_len[e];
+          }
+        }
+        for (e = p->row_ptr[j]; e < p->row_ptr[j + 1]; ++e) {
+          if (cand[e] & (1u << (r - 1u))) {
+            uint32_t d = p->edge_def[e];
+            uint64_t A_d = 0;
+            uint32_t rr, col;
+            double w, sh;
+            for (rr = 0; rr < R; ++rr) A_d += cnt(p, C, d, 0, rr);
+            w = (double)(A_d > 0 ? A_d : 1u) / (double)p->edge_max_len[e];
+            sh = w / W;
+            share[3u * e + (r - 1u)] = sh;
+            /* S_i = share * S_j, and the same share for latency samples. */
+            col = classify(r, p->opclass[d], p->edge_kind[e]);
+            V[((uint64_t)d * NC + col) * 2u + 0u] += (double)S[r] * sh;
+            V[((uint64_t)d * NC + col) * 2u + 1u] += (double)SL[r] * sh;
+          }
+        }
+      }
+    }
+    /* self-attributed dependency stalls stay at j */
+    for (r = R_MEM; r <= R_SYNC; ++r) {
+      if (self_flags[j] & (1u << (r - 1u))) {
+        uint32_t col = COL_MEM_SELF + (r - 1u);
+        V[((uint64_t)j * NC + col) * 2u + 0u] += (double)S[r];
+        V[((uint64_t)j * NC + col) * 2u + 1u] += (double)SL[r];
+      }
+    }
+    /* other stall reasons are caused by the instruction that suffers them. */
+    for (r = 4; r < R; ++r) {
+      uint32_t col = COL_PASS0 + (r - 4u);
+      V[((uint64_t)j * NC + col) * 2u + 0u] += (double)S[r];
+      V[((uint64_t)j * NC + col) * 2u + 1u] += (double)SL[r];
+    }
+  }
+  return 0;
+}
+
+/* ---------------------------------------------------------------- step 7: rollup */
+
+static int is_ancestor_or_self(const or_program *p, int32_t anc, int32_t l) {
+  while (l >= 0) {
+    if (l == anc) return 1;
+    l = p->loop_parent[l];
+  }
+  return 0;
+}
+
+/* function f with func_begin[f] <= i < func_begin[f+1] (binary search over the ranges) */
+static uint32_t func_of(const or_program *p, uint32_t i) {
+  uint32_t lo = 0, hi = p->n_funcs;
+  while (hi - lo > 1u) {
+    uint32_t mid = (lo + hi) / 2u;
+    if (p->func_begin[mid] <= i) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+static uint32_t kernel_of_func(const or_program *p, uint32_t f) {
+  uint32_t lo = 0, hi = p->n_kernels;
+  while (hi - lo > 1u) {
+    uint32_t mid = (lo + hi) / 2u;
+    if (p->kernel_func_begin[mid] <= f) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+static void add_row(double *dst, const double *src, uint32_t NC) {
+  uint32_t q;
+  for (q = 0; q < 2u * NC; ++q) dst[q] += src[q];
+}
+
+/* Program structure levels ("line, loop, function"), with loops both
+ * exclusive and inclusive of nested loops (Eq. 5's nested(l) contains l, Q16).
+ * Every instruction contributes its own V row (edge blame at the def, self and
+ * pass-through at the use) and its (A_i, L_i) counts. */
+int or_rollup(const or_program *p, const uint64_t *C, const double *V, double *line_v,
+              uint64_t *line_al, double *loop_excl_v, uint64_t *loop_excl_al,
+              double *loop_incl_v, uint64_t *loop_incl_al, double *func_v, uint64_t *func_al,
+              double *kern_v, uint64_t *kern_al) {
+  const uint32_t n = p->n_instr, R = p->n_reasons, NC = or_ncol(R);
+  uint32_t i, r, l;
+  if (line_v) memset(line_v, 0, sizeof(double) * 2u * NC * p->n_lines);
+  if (line_al) memset(line_al, 0, sizeof(uint64_t) * 2u * p->n_lines);
+  if (loop_excl_v) memset(loop_excl_v, 0, sizeof(double) * 2u * NC * p->n_loops);
+  if (loop_excl_al) memset(loop_excl_al, 0, sizeof(uint64_t) * 2u * p->n_loops);
+  if (loop_incl_v) memset(loop_incl_v, 0, sizeof(double) * 2u * NC * p->n_loops);
+  if (loop_incl_al) memset(loop_incl_al, 0, sizeof(uint64_t) * 2u * p->n_loops);
+  if (func_v) memset(func_v, 0, sizeof(double) * 2u * NC * p->n_funcs);
+  if (func_al) memset(func_al, 0, sizeof(uint64_t) * 2u * p->n_funcs);
+  if (kern_v) memset(kern_v, 0, sizeof(double) * 2u * NC * p->n_kernels);
+  if (kern_al) memset(kern_al, 0, sizeof(uint64_t) * 2u * p->n_kernels);
+
+  for (i = 0; i < n; ++i) {
+    const double *row = V + (uint64_t)i * NC * 2u;
+    uint64_t A = 0, L = 0;
+    uint32_t f, k, ln = p->line_id[i];
+    int32_t lp = p->loop_id[i];
+    for (r = 0; r < R; ++r) {
+      A += cnt(p, C, i, 0, r);
+      L += cnt(p, C, i, 1, r);
+    }
+    if (line_v) add_row(line_v + (uint64_t)ln * NC * 2u, row, NC);
+    if (line_al) { line_al[2u * ln] += A; line_al[2u * ln + 1u] += L; }
+    if (lp >= 0) {
+      if (loop_excl_v) add_row(loop_excl_v + (uint64_t)lp * NC * 2u, row, NC);
+      if (loop_excl_al) { loop_excl_al[2u * lp] += A; loop_excl_al[2u * lp + 1u] += L; }
+      /* nested(l) contains l: the instruction counts for its loop and every ancestor */
+      for (l = (uint32_t)lp; ; l = (uint32_t)p->loop_parent[l]) {
+        if (loop_incl_v) add_row(loop_incl_v + (uint64_t)l * NC * 2u, row, NC);
+        if (loop_incl_al) { loop_incl_al[2u * l] += A; loop_incl_al[2u * l + 1u] += L; }
+        if (p->loop_parent[l] < 0) break;
+      }
+    }
+    f = func_of(p, i);
+    k = kernel_of_func(p, f);
+    if (func_v) add_row(func_v + (uint64_t)f * NC * 2u, row, NC);
+    if (func_al) { func_al[2u * f] += A; func_al[2u * f + 1u] += L; }
+    if (kern_v) add_row(kern_v + (uint64_t)k * NC * 2u, row, NC);
+    if (kern_al) { kern_al[2u * k] += A; kern_al[2u * k + 1u] += L; }
+  }
+  return 0;
+}
+
+/* ---------------------------------------------------------------- step 8: estimators */
+
+/* Eq. 2: S^e = T / (T - M).  T = 0 -> 1 (no samples, nothing to gain);
+ * M >= T -> +inf (Q19). */
+double or_eq2(double T, double M) {
+  if (T <= 0.0) return 1.0;
+  if (M >= T) return INFINITY;
+  return T / (T - M);
+}
+
+/* Eq. 4: S^h = T / (T - min(A, M^L)). */
+double or_eq4(double T, double A, double ML) {
+  double m = A < ML ? A : ML;
+  return or_eq2(T, m);
+}
+
+/* Eq. 5: S^h_l = T / (T - min(sum_{l' in nested(l)} A_l', M^L_l)). */
+double or_eq5(double T, double A_nested, double ML_scope) {
+  double m = A_nested < ML_scope ? A_nested : ML_scope;
+  return or_eq2(T, m);
+}
+
+/* Eqs. 6-10: C_W = W_new / W; I = 1 - (1 - R_I)^W; I_new likewise;
+ * C_I = I_new / I (:= 1 when I = 0, Q18); S^p = (1 / C_W) * C_I * f. */
+double or_eq10(double W, double W_new, double R_I, double f) {
+  double C_W = W_new / W;
+  double I = 1.0 - pow(1.0 - R_I, W);
+  double I_new = 1.0 - pow(1.0 - R_I, W_new);
+  double C_I = (I == 0.0) ? 1.0 : I_new / I;
+  return (1.0 / C_W) * C_I * f;
+}
+
+static int32_t lca_loop(const or_program *p, int32_t a, int32_t b) {
+  int32_t x;
+  for (x = a; x >= 0; x = p->loop_parent[x])
+    if (is_ancestor_or_self(p, x, b)) return x;
+  return -1;
+}
+
+static int instr_passes(const or_program *p, const or_pattern *q, uint32_t i) {
+  if (!((q->class_mask >> p->opclass[i]) & 1u)) return 0;
+  if (q->flag_filter && !(p->iflags[i] & q->flag_filter)) return 0;
+  return 1;
+}
+
+/* Matched samples of pattern q contributed by one blamed item, and the loop it lives in
+ * (-2 = not matched).  Edge contributions live at lca(def loop, use loop); self and
+ * pass-through contributions at the use's loop (Q16). */
+static double match_edge(const or_program *p, const uint64_t *C, const uint8_t *cand,
+                         const double *share, const or_pattern *q, uint32_t e, uint32_t j) {
+  uint32_t d = p->edge_def[e], r;
+  double m = 0.0;
+  if (!instr_passes(p, q, d)) return 0.0;
+  if (q->same_loop && !(p->loop_id[d] >= 0 && p->loop_id[d] == p->loop_id[j])) return 0.0;
+  for (r = R_MEM; r <= R_SYNC; ++r) {
+    if (cand[e] & (1u << (r - 1u))) {
+      uint32_t col = classify(r, p->opclass[d], p->edge_kind[e]);
+      if ((q->column_mask >> col) & 1u) {
+        uint64_t X = cnt(p, C, j, 1, r) + (q->sample_class ? 0u : cnt(p, C, j, 0, r));
+        m += (double)X * share[3u * e + (r - 1u)];
+      }
+    }
+  }
+  return m;
+}
+
+static double match_instr(const or_program *p, const uint64_t *C, const uint8_t *self_flags,
+                          const or_pattern *q, uint32_t j) {
+  uint32_t r;
+  double m = 0.0;
+  if (!instr_passes(p, q, j)) return 0.0;
+  if (q->same_loop && p->loop_id[j] < 0) return 0.0;
+  for (r = R_MEM; r <= R_SYNC; ++r) {
+    if ((self_flags[j] & (1u << (r - 1u))) && ((q->column_mask >> (COL_MEM_SELF + r - 1u)) & 1u))
+      m += (double)(cnt(p, C, j, 1, r) + (q->sample_class ? 0u : cnt(p, C, j, 0, r)));
+  }
+  for (r = 4; r < p->n_reasons; ++r) {
+    if ((q->column_mask >> (COL_PASS0 + r - 4u)) & 1u)
+      m += (double)(cnt(p, C, j, 1, r) + (q->sample_class ? 0u : cnt(p, C, j, 0, r)));
+  }
+  return m;
+}
+
+/* Table 2 optimizers as patterns, the Loop Unrolling workflow,
+ * and the estimators of §5.2 per kernel launch context. */
+int or_estimate_all(const or_program *p, const uint64_t *C, const uint8_t *cand,
+                    const uint8_t *self_flags, const double *share, const or_pattern *pats,
+                    uint32_t n_pat, or_estimate *out) {
+  const uint32_t n = p->n_instr, R = p->n_reasons;
+  uint32_t k, qi, i, r, e, l, f;
+  double *loopM = (double *)calloc(p->n_loops ? p->n_loops : 1u, sizeof(double));
+  double *loopA = (double *)calloc(p->n_loops ? p->n_loops : 1u, sizeof(double));
+  double *funcM = (double *)calloc(p->n_funcs ? p->n_funcs : 1u, sizeof(double));
+  double *funcA = (double *)calloc(p->n_funcs ? p->n_funcs : 1u, sizeof(double));
+  int32_t *loop_func = (int32_t *)malloc(sizeof(int32_t) * (p->n_loops ? p->n_loops : 1u));
+  if (!loopM || !loopA || !funcM || !funcA || !loop_func) return -1;
+
+  /* function owning each loop: that of any instruction in the loop's subtree */
+  for (l = 0; l < p->n_loops; ++l) loop_func[l] = -1;
+  for (i = 0; i < n; ++i) {
+    int32_t x;
+    for (x = p->loop_id[i]; x >= 0; x = p->loop_parent[x])
+      if (loop_func[x] < 0) loop_func[x] = (int32_t)func_of(p, i);
+  }
+
+  for (k = 0; k < p->n_kernels; ++k) {
+    uint32_t f0 = p->kernel_func_begin[k], f1 = p->kernel_func_begin[k + 1];
+    uint32_t i0 = p->func_begin[f0], i1 = p->func_begin[f1];
+    uint64_t T = 0, A = 0;
+    double R_I;
+    /* T, A, L of the kernel; R_I = issued / all samples */
+    for (i = i0; i < i1; ++i)
+      for (r = 0; r < R; ++r) {
+        A += cnt(p, C, i, 0, r);
+        T += cnt(p, C, i, 0, r) + cnt(p, C, i, 1, r);
+      }
+    R_I = T ? (double)A / (double)T : 0.0;
+
+    for (qi = 0; qi < n_pat; ++qi) {
+      const or_pattern *q = &pats[qi];
+      or_estimate *o = &out[(uint64_t)k * n_pat + qi];
+      double M = 0.0, best = 1.0;
+      int32_t best_scope = -1;
+      memset(o, 0, sizeof(*o));
+      o->T = T;
+      o->A = A;
+      o->model = q->model;
+      o->best_scope = -1;
+
+      if (q->model == 5) {
+        /* Parallel optimizers (Table 2): Block Increase matches when the
+         * kernel has fewer blocks than SMs; Eq. 10 otherwise from caller W, W_new, f. */
+        int matched = q->parallel_rule == 1 ||
+                      (q->parallel_rule == 2 && p->kernel_grid_blocks &&
+                       p->kernel_grid_blocks[k] < q->sm_count);
+        o->matched = (uint8_t)matched;
+        o->speedup = matched ? or_eq10(q->W, q->W_new, R_I, q->f) : 1.0;
+        o->eq3 = o->eq4 = 1.0;
+        continue;
+      }
+
+      for (l = 0; l < p->n_loops; ++l) { loopM[l] = 0.0; loopA[l] = 0.0; }
+      for (f = 0; f < p->n_funcs; ++f) { funcM[f] = 0.0; funcA[f] = 0.0; }
+
+      for (i = i0; i < i1; ++i) {
+        uint32_t fi = func_of(p, i);
+        uint64_t Ai = 0;
+        double mi;
+        for (r = 0; r < R; ++r) Ai += cnt(p, C, i, 0, r);
+        int32_t x;
+        funcA[fi] += (double)Ai;
+        for (x = p->loop_id[i]; x >= 0; x = p->loop_parent[x]) loopA[x] += (double)Ai;
+        /* contributions of in-edges of use i */
+        for (e = p->row_ptr[i]; e < p->row_ptr[i + 1]; ++e) {
+          double me = match_edge(p, C, cand, share, q, e, i);
+          int32_t sc;
+          if (me == 0.0) continue;
+          M += me;
+          funcM[fi] += me;
+          sc = lca_loop(p, p->loop_id[p->edge_def[e]], p->loop_id[i]);
+          for (x = sc; x >= 0; x = p->loop_parent[x]) loopM[x] += me;
+        }
+        mi = match_instr(p, C, self_flags, q, i);
+        if (mi != 0.0) {
+          M += mi;
+          funcM[fi] += mi;
+          for (x = p->loop_id[i]; x >= 0; x = p->loop_parent[x]) loopM[x] += mi;
+        }
+      }
+      o->M = M;
+      o->matched = M > 0.0;
+      o->eq3 = or_eq2((double)T, M);                 /* Eq. 3 */
+      o->eq4 = or_eq4((double)T, (double)A, M);      /* Eq. 4 */
+      if (q->model == 0) {
+        o->speedup = or_eq2((double)T, q->ratio * M); /* Eq. 2 (x ratio, Q17) */
+      } else if (q->model == 1) {
+        o->speedup = o->eq4;
+      } else {
+        /* Eq. 5 per scope; the optimizer's estimate is its best scope (Q16). */
+        if (q->model == 2 || q->model == 4) {
+          for (l = 0; l < p->n_loops; ++l) {
+            double s;
+            if (loop_func[l] < (int32_t)f0 || loop_func[l] >= (int32_t)f1) continue;
+            s = or_eq5((double)T, loopA[l], loopM[l]);
+            if (best_scope < 0 || s > best) { best = s; best_scope = (int32_t)l; }
+          }
+        }
+        if (q->model == 3 || q->model == 4) {
+          for (f = f0; f < f1; ++f) {
+            double s = or_eq5((double)T, funcA[f], funcM[f]);
+            if (best_scope < 0 || s > best) { best = s; best_scope = (int32_t)(p->n_loops + f); }
+          }
+        }
+        o->speedup = best_scope < 0 ? 1.0 : best;
+        o->best_scope = best_scope;
+      }
+      o->unbounded = isinf(o->speedup) ? 1u : 0u;
+    }
+  }
+  free(loopM); free(loopA); free(funcM); free(funcA); free(loop_func);
+  return 0;
+}
