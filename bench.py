@@ -1,0 +1,321 @@
+#!/usr/bin/env python
+"""Benchmark of GPA's hot path on B200: PC samples/s attributed (ingest + blame + rollup +
+estimate), and the ingest kernel's achieved fraction of the measured HBM roofline.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload large|rodinia] [--impl reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...     (one rank per GPU, NCCL all-reduce)
+
+Workload: BASELINE.json config 3 -- the 50k-instruction PeleC/ExaTENSOR-shaped
+program with 10^9 synthetic PC-sample records per GPU (8 GB, device-resident, far larger than
+L2, so no flush is needed between steps).  At N > 1 rank r ingests records [r*1e9, (r+1)*1e9) of
+the same counter-based stream (config 5's sharding), the count table is all-reduced over NCCL,
+and blame / rollup / estimate run replicated: weak scaling.
+
+One step = reset -> ingest -> [all_reduce] -> blame -> aggregate -> estimate, all enqueued on one
+stream; timed with CUDA events, W warm-up steps, K timed steps, barrier + synchronize on both
+sides, max over ranks.  Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PC samples/sec attributed (ingest+blame+rollup) at 1/2/4/8 B200; % HBM peak"
+WORKLOADS = {
+    # name: (config id, records per GPU)
+    "large": (3, 1_000_000_000),
+    "rodinia": (2, 10_000_000),
+}
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _traffic_from_profile(workload):
+    """dram bytes per ingest launch from the committed ncu --set full summary, if present."""
+    path = os.path.join(ROOT, "profiles", "ncu_ingest_summary.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        e = d.get(workload, {})
+        return e.get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+def _cpu_count():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def oracle_throughput(prog, records: np.ndarray, patterns):
+    """Time the oracle (tests' CPU implementation, as it stands) on `records`: whole path."""
+    import oracle
+    from tests._common import oracle_pattern
+    op = oracle.OracleProgram(prog)
+    t0 = time.perf_counter()
+    C, _ = op.histogram(records)
+    b = op.blame(C)
+    op.rollup(C, b["V"])
+    op.estimate(C, b, [oracle_pattern(p) for p in patterns])
+    return time.perf_counter() - t0
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle on the host cores (rank 0 only), bounded samples."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import gpagen
+    from gpagen.patterns import table2
+    cfg, _ = WORKLOADS[args.workload]
+    prog = gpagen.config_program(cfg)
+    sample = args.ref_sample
+    recs = gpagen.config_stream(prog, cfg).host(0, sample)
+    pats = table2(prog.n_reasons)
+    for _ in range(args.warmup):
+        oracle_throughput(prog, recs, pats)
+    times = [oracle_throughput(prog, recs, pats) for _ in range(args.steps)]
+    t = sum(times) / len(times)
+    v = sample / t
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64+f64", "data": "synthetic",
+            "config": {"workload": f"{args.workload} (BASELINE config {cfg})", "records_per_step": sample},
+            "cpu_baseline": {"value": v, "unit": "samples/s", "cores": 1, "kind": "oracle",
+                             "sample": f"first {sample} records of the config-{cfg} stream per step"},
+            "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="large", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--records", type=int, default=0, help="override records per GPU")
+    ap.add_argument("--variant", default=None, help="force ingest variant (smem|part|l2)")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-sample", type=int, default=50_000_000)
+    ap.add_argument("--profile", action="store_true", help="one short step for ncu (no JSON rules)")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    import gpagen
+    from gpagen.patterns import table2
+    from paper_2009_04061_b200 import Program
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg, n_per = WORKLOADS[args.workload]
+    if args.records:
+        n_per = args.records
+    prog = gpagen.config_program(cfg)
+    pats = table2(prog.n_reasons)
+    P = Program(prog, device=dev)
+    if args.variant:
+        P.variant = args.variant
+    P.set_patterns(pats)
+    spec = gpagen.config_stream(prog, cfg)
+    recs = spec.device(rank * n_per, n_per)          # this rank's shard, device-resident
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    counts = P.view("counts")
+    stats = P.view("stats")
+
+    def step(ev_a=None, ev_b=None):
+        P.reset()
+        if ev_a is not None:
+            ev_a.record(stream)
+        P.ingest(recs)
+        if ev_b is not None:
+            ev_b.record(stream)
+        if world > 1:
+            dist.all_reduce(counts, op=dist.ReduceOp.SUM)
+            dist.all_reduce(stats, op=dist.ReduceOp.SUM)
+        P.blame()
+        P.aggregate()
+        P.estimate()
+
+    if args.profile:
+        step()
+        torch.cuda.synchronize()
+        return
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    ing = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = P.launches
+    torch.cuda.synchronize()
+    t0.record(stream)
+    for k in range(args.steps):
+        step(*ing[k])
+    t1.record(stream)
+    torch.cuda.synchronize()
+    launches = P.launches - l0
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    ms = t0.elapsed_time(t1)
+    ingest_ms = sum(a.elapsed_time(b) for a, b in ing) / args.steps
+    if world > 1:
+        t = torch.tensor([ms, ingest_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, ingest_ms = float(t[0]), float(t[1])
+    ms_per_step = ms / args.steps
+
+    # correctness guard on the timed output: every record of every rank was counted
+    st = P.stats()
+    total = n_per * world
+    assert st[0] + st[1] == total, (st, total)
+
+    # end to end through the C ABI from pinned host memory (H2D inside the timed region)
+    e2e = None
+    if args.e2e_steps > 0:
+        host = torch.empty(n_per * 8, dtype=torch.uint8, pin_memory=True)
+        host.copy_(recs)
+        est_bytes = P.n_kernels * P.n_patterns * 56
+        for _ in range(1):
+            P.reset(); P.ingest_host(host); P.blame(); P.aggregate(); P.estimate(); P.read_estimates()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = time.perf_counter()
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ea.record(stream)
+        for _ in range(args.e2e_steps):
+            P.reset()
+            P.ingest_host(host)
+            if world > 1:
+                dist.all_reduce(counts, op=dist.ReduceOp.SUM)
+                dist.all_reduce(stats, op=dist.ReduceOp.SUM)
+            P.blame()
+            P.aggregate()
+            P.estimate()
+            P.read_estimates()
+        eb.record(stream)
+        torch.cuda.synchronize()
+        e_ms = ea.elapsed_time(eb)
+        if world > 1:
+            t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t[0])
+        e2e = {"value": total * args.e2e_steps / (e_ms / 1e3), "unit": "samples/s",
+               "h2d_bytes_per_step": n_per * 8 * world, "d2h_bytes_per_step": est_bytes * world,
+               "ms_per_step": e_ms / args.e2e_steps, "path": "gpa_ingest_samples_host (pinned, 2x32 MB staging ring)"}
+        del host
+
+    peak, peak_kind = _peaks()
+    table_bytes = prog.n_instr * 2 * prog.n_reasons * 8
+    alg_bytes = n_per * 8 + 2 * table_bytes
+    achieved = alg_bytes / (ingest_ms / 1e3) / 1e9
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        sample = min(n_per, 1_000_000_000)
+        h = recs[: sample * 8].cpu().numpy().view(np.uint64)
+        t_or = oracle_throughput(prog, h, pats)
+        cpu = {"value": sample / t_or, "unit": "samples/s", "cores": 1, "kind": "oracle",
+               "sample": f"{sample} records (the same device stream, copied to host); histogram+blame+rollup+estimate",
+               "seconds": t_or}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": total / (ms_per_step / 1e3), "unit": "samples/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u64+f64", "data": "synthetic",
+            "config": {"workload": f"{args.workload}: BASELINE config {cfg}, {prog.n_instr} instrs, "
+                                   f"{prog.n_edges} edges, {prog.n_loops} loops, {n_per} records/GPU",
+                       "records_per_gpu": n_per, "records_total": total, "l2": "inputs larger than L2 (8 B/record)",
+                       "parallelism": f"dp{world} (sample-stream shards + NCCL all-reduce of counts)",
+                       "ingest_variant": P.variant},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": _traffic_from_profile(args.workload),
+                         "kernel": "ingest", "peak_kind": peak_kind, "alg_bytes_per_launch": alg_bytes,
+                         "ingest_ms": ingest_ms, "ingest_share_of_step": ingest_ms / ms_per_step},
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

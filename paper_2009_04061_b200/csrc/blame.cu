@@ -1,0 +1,146 @@
+// blame.cu -- rows a2-a6: summaries, candidate pruning (rules 1-3), Eq. 1 shares for all and
+// latency samples, self-attribution, Fig. 6 classification and the def-side reduction.
+//
+//   k_summaries   A_i, L_i from the count table (a2)
+//   k_blame_rows  one thread per use row j (a3, a4): rules 1-3 per in-edge, weights
+//                 max(A_i,1)/max_len (Q1-Q4), W summed in CSR order, shares w/W
+//                 (Eq. 1), self flags when no candidate survives (Q5)
+//   k_def_reduce  one thread per def i over the create-time def-major transpose (a5, a6):
+//                 S_j[r]*share and SL_j[r]*share summed into i's category
+// fp64 adds/multiplies use __dadd_rn/__dmul_rn (no FMA contraction), and every sum runs in
+// CSR/edge order, so results match a sequential evaluation of the definitions exactly.
+#include <algorithm>
+
+#include "gpa_internal.cuh"
+
+namespace gpa {
+namespace {
+
+__global__ void k_summaries(const uint64_t *__restrict__ C, uint32_t n, uint32_t R,
+                            uint64_t *__restrict__ AL) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const uint64_t *row = C + (uint64_t)i * 2 * R;
+    uint64_t a = 0, l = 0;
+    for (uint32_t r = 0; r < R; ++r) {
+      a += row[r];
+      l += row[R + r];
+    }
+    AL[2 * (uint64_t)i] = a;
+    AL[2 * (uint64_t)i + 1] = l;
+  }
+}
+
+// rule 1 (Q6): bit r-1 set when def class c may cause a stall of reason r
+__device__ __forceinline__ uint32_t rule1_mask(uint32_t c) {
+  const bool mem = c == OC_GLOBAL || c == OC_LOCAL || c == OC_CONSTANT || c == OC_TEXTURE;
+  return (mem ? 1u : 0u) | 2u | (c == OC_SYNC ? 4u : 0u);
+}
+
+__global__ void k_blame_rows(DevProgram p) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < p.n; j += gridDim.x * blockDim.x) {
+    const uint64_t *row = p.C + (uint64_t)j * 2 * p.R;
+    const uint64_t dep = row[R_MEM] + row[p.R + R_MEM] + row[R_EXEC] + row[p.R + R_EXEC] +
+                         row[R_SYNC] + row[p.R + R_SYNC];
+    const uint32_t e0 = p.row_ptr[j], e1 = p.row_ptr[j + 1];
+    if (dep == 0) {  // not a node of the dependency graph
+      for (uint32_t e = e0; e < e1; ++e) {
+        p.cand[e] = 0;
+        p.share[3 * (uint64_t)e] = 0.0;
+        p.share[3 * (uint64_t)e + 1] = 0.0;
+        p.share[3 * (uint64_t)e + 2] = 0.0;
+      }
+      p.selfm[j] = 0;
+      continue;
+    }
+    double W0 = 0.0, W1 = 0.0, W2 = 0.0;
+    for (uint32_t e = e0; e < e1; ++e) {
+      const uint32_t d = p.edge_def[e];
+      const bool keep = p.edge_dom[e] < 0 && p.edge_min[e] <= p.latency[d];   // rules 2, 3
+      if (!keep) continue;
+      const uint32_t m = rule1_mask(p.opclass[d]);
+      const uint64_t a = p.AL[2 * (uint64_t)d];
+      const double w = __ddiv_rn((double)(a ? a : 1ull), (double)p.edge_max[e]);
+      if (m & 1u) W0 = __dadd_rn(W0, w);
+      W1 = __dadd_rn(W1, w);
+      if (m & 4u) W2 = __dadd_rn(W2, w);
+    }
+    for (uint32_t e = e0; e < e1; ++e) {
+      const uint32_t d = p.edge_def[e];
+      const bool keep = p.edge_dom[e] < 0 && p.edge_min[e] <= p.latency[d];
+      const uint32_t m = keep ? rule1_mask(p.opclass[d]) : 0u;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+      if (m) {
+        const uint64_t a = p.AL[2 * (uint64_t)d];
+        const double w = __ddiv_rn((double)(a ? a : 1ull), (double)p.edge_max[e]);
+        if (m & 1u) s0 = __ddiv_rn(w, W0);
+        s1 = __ddiv_rn(w, W1);
+        if (m & 4u) s2 = __ddiv_rn(w, W2);
+      }
+      p.cand[e] = (uint8_t)m;
+      p.share[3 * (uint64_t)e] = s0;
+      p.share[3 * (uint64_t)e + 1] = s1;
+      p.share[3 * (uint64_t)e + 2] = s2;
+    }
+    p.selfm[j] = (uint8_t)((W0 > 0.0 ? 0u : 1u) | (W1 > 0.0 ? 0u : 2u) | (W2 > 0.0 ? 0u : 4u));
+  }
+}
+
+__global__ void k_def_reduce(DevProgram p) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += gridDim.x * blockDim.x) {
+    double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+    for (uint32_t k = p.def_ptr[i]; k < p.def_ptr[i + 1]; ++k) {
+      const uint32_t e = p.def_perm[k];
+      const uint32_t m = p.cand[e];
+      if (!m) continue;
+      const uint64_t *row = p.C + (uint64_t)p.edge_use[e] * 2 * p.R;
+#pragma unroll
+      for (uint32_t r = R_MEM; r <= R_SYNC; ++r) {
+        if (!(m & (1u << (r - 1)))) continue;
+        const double sh = p.share[3 * (uint64_t)e + (r - 1)];
+        const uint64_t lat = row[p.R + r], all = row[r] + lat;
+        const uint32_t g = r == R_MEM ? BG_MEM : r == R_SYNC ? BG_SYNC : ((p.edge_kind[e] & K_WAR) ? BG_WAR : BG_EXEC);
+        acc[g][0] = __dadd_rn(acc[g][0], __dmul_rn((double)all, sh));
+        acc[g][1] = __dadd_rn(acc[g][1], __dmul_rn((double)lat, sh));
+      }
+    }
+    double *out = p.B + 8 * (uint64_t)i;
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+      out[2 * g] = acc[g][0];
+      out[2 * g + 1] = acc[g][1];
+    }
+  }
+}
+
+__global__ void k_instr_vector(DevProgram p, double *__restrict__ out) {
+  const uint64_t total = (uint64_t)p.n * p.ncol * 2;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total; t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t i = (uint32_t)(t / (2 * p.ncol));
+    const uint32_t s = (uint32_t)(t % (2 * p.ncol));
+    out[t] = vvalue(p, i, s >> 1, s & 1);
+  }
+}
+
+inline uint32_t grid_for(uint64_t items, uint32_t threads, int n_sms) {
+  return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((items + threads - 1) / threads, (uint64_t)n_sms * 16));
+}
+
+}  // namespace
+
+cudaError_t launch_blame(const DevProgram &p, int n_sms, cudaStream_t s, uint64_t *launches) {
+  k_summaries<<<grid_for(p.n, 256, n_sms), 256, 0, s>>>(p.C, p.n, p.R, p.AL);
+  k_blame_rows<<<grid_for(p.n, 128, n_sms), 128, 0, s>>>(p);
+  k_def_reduce<<<grid_for(p.n, 128, n_sms), 128, 0, s>>>(p);
+  *launches += 3;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_instr_vector(const DevProgram &p, double *out, cudaStream_t s) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  k_instr_vector<<<grid_for((uint64_t)p.n * p.ncol * 2, 256, sms), 256, 0, s>>>(p, out);
+  return cudaGetLastError();
+}
+
+}  // namespace gpa

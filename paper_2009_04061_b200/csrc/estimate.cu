@@ -1,0 +1,227 @@
+// estimate.cu -- row a8: optimizer matching (Table 2; Loop Unrolling workflow
+// P:457-460) and the estimators of §5.2: Eq. 2, Eq. 3, Eq. 4
+// (P:496-503), Eq. 5 (Q16), Eqs. 6-10 (Q18), per kernel.
+//
+//   k_est_rows    one thread per use row j: for every pattern, the matched samples of each
+//                 in-edge (blamed at the def, scope loop = lca(def, use)) and of j itself
+//                 (self / pass-through columns, scope loop = loop of j); row totals mrow[q][j]
+//                 and, for loop-scoped patterns, per-item values for the loop reduction.
+//   k_segsum      one warp per (segment, pattern): fixed-order strided sums + xor-shuffle tree
+//                 (deterministic).  Stage 1: loop-exclusive (by scope-loop item lists) and
+//                 function sums; stage 2: loop-inclusive (preorder subtree ranges) and kernel sums.
+//   k_est_final   one thread per (kernel, pattern): T, A, R_I, M, Eqs. 2-5 / 10, best scope.
+#include <algorithm>
+#include <math.h>
+
+#include "gpa_internal.cuh"
+
+namespace gpa {
+namespace {
+
+__device__ __forceinline__ uint32_t classify(uint32_t r, uint32_t cls, uint32_t kind) {
+  if (r == R_MEM) return cls == OC_LOCAL ? COL_MEM_LOCAL : cls == OC_CONSTANT ? COL_MEM_CONSTANT : COL_MEM_GLOBAL;
+  if (r == R_EXEC) return (kind & K_WAR) ? COL_EXEC_WAR : cls == OC_SHARED ? COL_EXEC_SHARED : COL_EXEC_ARITH;
+  return COL_SYNC;
+}
+
+__device__ __forceinline__ bool passes(const gpa_pattern &q, uint32_t cls, uint32_t flags) {
+  return ((q.class_mask >> cls) & 1u) && (!q.flag_filter || (flags & q.flag_filter));
+}
+
+__global__ void k_est_rows(DevProgram p, EstimatePlan ep) {
+  __shared__ gpa_pattern sp[kPatternsMax];
+  for (uint32_t q = threadIdx.x; q < ep.n_pat; q += blockDim.x) sp[q] = ep.pats[q];
+  __syncthreads();
+  const uint64_t stride_items = (uint64_t)p.E + p.n;
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < p.n; j += gridDim.x * blockDim.x) {
+    const uint64_t *row = p.C + (uint64_t)j * 2 * p.R;
+    const uint32_t e0 = p.row_ptr[j], e1 = p.row_ptr[j + 1];
+    const int32_t loop_j = p.loop_id[j];
+    const uint32_t cls_j = p.opclass[j], fl_j = p.iflags[j], self_j = p.selfm[j];
+    for (uint32_t qi = 0; qi < ep.n_pat; ++qi) {
+      const gpa_pattern &q = sp[qi];
+      const int slot = ep.loop_slot[qi];
+      double sum = 0.0;
+      if (q.model == 5) {
+        ep.mrow[(uint64_t)qi * p.n + j] = 0.0;
+        continue;
+      }
+      for (uint32_t e = e0; e < e1; ++e) {
+        double me = 0.0;
+        const uint32_t m = p.cand[e];
+        const uint32_t d = p.edge_def[e];
+        if (m && passes(q, p.opclass[d], p.iflags[d]) &&
+            (!q.same_loop || (p.loop_id[d] >= 0 && p.loop_id[d] == loop_j))) {
+          for (uint32_t r = R_MEM; r <= R_SYNC; ++r) {
+            if (!((m >> (r - 1)) & 1u)) continue;
+            if (!((q.column_mask >> classify(r, p.opclass[d], p.edge_kind[e])) & 1u)) continue;
+            const uint64_t X = row[p.R + r] + (q.sample_class ? 0ull : row[r]);
+            me = __dadd_rn(me, __dmul_rn((double)X, p.share[3 * (uint64_t)e + (r - 1)]));
+          }
+        }
+        if (slot >= 0) ep.mval[(uint64_t)slot * stride_items + e] = me;
+        sum = __dadd_rn(sum, me);
+      }
+      double mi = 0.0;
+      if (passes(q, cls_j, fl_j) && (!q.same_loop || loop_j >= 0)) {
+        for (uint32_t r = R_MEM; r <= R_SYNC; ++r)
+          if (((self_j >> (r - 1)) & 1u) && ((q.column_mask >> (COL_MEM_SELF + r - 1)) & 1u))
+            mi = __dadd_rn(mi, (double)(row[p.R + r] + (q.sample_class ? 0ull : row[r])));
+        for (uint32_t r = 4; r < p.R; ++r)
+          if ((q.column_mask >> (COL_PASS0 + r - 4)) & 1u)
+            mi = __dadd_rn(mi, (double)(row[p.R + r] + (q.sample_class ? 0ull : row[r])));
+      }
+      if (slot >= 0) ep.mval[(uint64_t)slot * stride_items + p.E + j] = mi;
+      ep.mrow[(uint64_t)qi * p.n + j] = __dadd_rn(sum, mi);
+    }
+  }
+}
+
+struct SegFamily {
+  const double *values;     // value row v starts at values + v * row_stride
+  uint64_t row_stride;
+  const uint32_t *perm;     // position -> item (nullable)
+  const uint32_t *begin;    // [n_seg] (or ptr array of n_seg+1 when end == nullptr)
+  const uint32_t *end;
+  uint32_t n_seg;
+  double *out;              // out[q * n_seg + s]
+  int32_t vrow[kPatternsMax]; // pattern -> value row, -1 = not applicable (output 0)
+};
+
+struct SegLaunch {
+  SegFamily fam[2];
+  uint32_t n_fam, n_pat;
+};
+
+__global__ void k_segsum(SegLaunch L) {
+  const uint32_t lane = threadIdx.x & 31;
+  const SegFamily &F = L.fam[blockIdx.y];
+  const uint64_t items = (uint64_t)F.n_seg * L.n_pat;
+  const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+  for (uint64_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < items; w += warps) {
+    const uint32_t q = (uint32_t)(w / F.n_seg), s = (uint32_t)(w % F.n_seg);
+    const int32_t vr = F.vrow[q];
+    double acc = 0.0;
+    if (vr >= 0) {
+      const double *vals = F.values + (uint64_t)vr * F.row_stride;
+      const uint32_t b = F.begin[s], e = F.end ? F.end[s] : F.begin[s + 1];
+      for (uint32_t pos = b + lane; pos < e; pos += 32) acc = __dadd_rn(acc, vals[F.perm ? F.perm[pos] : pos]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+    }
+    if (lane == 0) F.out[(uint64_t)q * F.n_seg + s] = acc;
+  }
+}
+
+__device__ __forceinline__ double eq2(double T, double M) {
+  if (T <= 0.0) return 1.0;
+  if (M >= T) return INFINITY;
+  return T / (T - M);
+}
+
+__global__ void k_est_final(DevProgram p, EstimatePlan ep) {
+  const uint32_t total = p.n_kernels * ep.n_pat;
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    const uint32_t k = t / ep.n_pat, qi = t % ep.n_pat;
+    const gpa_pattern q = ep.pats[qi];
+    gpa_estimate_out o;
+    const uint64_t A = ep.kern_al[2 * (uint64_t)k], T = A + ep.kern_al[2 * (uint64_t)k + 1];
+    const double Td = (double)T, Ad = (double)A;
+    o.T = T;
+    o.A = A;
+    o.model = q.model;
+    o.pad = 0;
+    o.best_scope = -1;
+    if (q.model == 5) {
+      const double R_I = T ? Ad / Td : 0.0;
+      const uint32_t gb = p.kernel_grid_blocks[k];
+      const bool matched = q.parallel_rule == 1 || (q.parallel_rule == 2 && gb != 0xffffffffu && gb < q.sm_count);
+      double s = 1.0;
+      if (matched) {
+        const double C_W = q.W_new / q.W;
+        const double I = 1.0 - pow(1.0 - R_I, q.W);
+        const double In = 1.0 - pow(1.0 - R_I, q.W_new);
+        const double C_I = (I == 0.0) ? 1.0 : In / I;
+        s = (1.0 / C_W) * C_I * q.f;
+      }
+      o.speedup = s;
+      o.M = 0.0;
+      o.eq3 = o.eq4 = 1.0;
+      o.matched = matched;
+    } else {
+      const double M = ep.kM[(uint64_t)qi * p.n_kernels + k];
+      o.M = M;
+      o.matched = M > 0.0;
+      o.eq3 = eq2(Td, M);
+      o.eq4 = eq2(Td, fmin(Ad, M));
+      if (q.model == 0) {
+        o.speedup = eq2(Td, q.ratio * M);
+      } else if (q.model == 1) {
+        o.speedup = o.eq4;
+      } else {
+        double best = 1.0;
+        int32_t bs = -1;
+        if (q.model == 2 || q.model == 4) {
+          for (uint32_t x = ep.kloop_ptr[k]; x < ep.kloop_ptr[k + 1]; ++x) {
+            const uint32_t l = ep.kloops[x];
+            const double Al = (double)ep.loop_incl_al[2 * (uint64_t)l];
+            const double s = eq2(Td, fmin(Al, ep.lM_incl[(uint64_t)qi * p.n_loops + l]));
+            if (bs < 0 || s > best) { best = s; bs = (int32_t)l; }
+          }
+        }
+        if (q.model == 3 || q.model == 4) {
+          for (uint32_t f = p.kernel_func_begin[k]; f < p.kernel_func_begin[k + 1]; ++f) {
+            const double Af = (double)ep.func_al[2 * (uint64_t)f];
+            const double s = eq2(Td, fmin(Af, ep.fM[(uint64_t)qi * p.n_funcs + f]));
+            if (bs < 0 || s > best) { best = s; bs = (int32_t)(p.n_loops + f); }
+          }
+        }
+        o.speedup = bs < 0 ? 1.0 : best;
+        o.best_scope = bs;
+      }
+    }
+    o.unbounded = isinf(o.speedup) ? 1 : 0;
+    ep.out[t] = o;
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_estimate(const DevProgram &p, const EstimatePlan &ep, int n_sms, cudaStream_t s,
+                            uint64_t *launches) {
+  const uint32_t threads = 128;
+  const uint32_t g = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((p.n + threads - 1) / threads, (uint64_t)n_sms * 16));
+  k_est_rows<<<g, threads, 0, s>>>(p, ep);
+  SegLaunch a{};
+  a.n_pat = ep.n_pat;
+  a.n_fam = 2;
+  // stage 1: loops (exclusive, by scope-loop items) and functions
+  a.fam[0] = SegFamily{ep.mval, (uint64_t)p.E + p.n, ep.loop_items, ep.loop_item_ptr, nullptr, p.n_loops, ep.lM_excl, {}};
+  a.fam[1] = SegFamily{ep.mrow, p.n, nullptr, p.func_begin, nullptr, p.n_funcs, ep.fM, {}};
+  for (int q = 0; q < kPatternsMax; ++q) {
+    a.fam[0].vrow[q] = ep.loop_slot[q];
+    a.fam[1].vrow[q] = q < (int)ep.n_pat ? q : -1;
+  }
+  const uint64_t w1 = std::max<uint64_t>((uint64_t)p.n_loops, p.n_funcs) * ep.n_pat;
+  dim3 g1((uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((w1 + 3) / 4, (uint64_t)n_sms * 32)), 2);
+  k_segsum<<<g1, 128, 0, s>>>(a);
+  // stage 2: loops inclusive (preorder subtree ranges over exclusive sums) and kernels
+  SegLaunch b{};
+  b.n_pat = ep.n_pat;
+  b.n_fam = 2;
+  b.fam[0] = SegFamily{ep.lM_excl, p.n_loops, ep.pre_perm, ep.pre_begin, ep.pre_end, p.n_loops, ep.lM_incl, {}};
+  b.fam[1] = SegFamily{ep.fM, p.n_funcs, nullptr, p.kernel_func_begin, nullptr, p.n_kernels, ep.kM, {}};
+  for (int q = 0; q < kPatternsMax; ++q) {
+    b.fam[0].vrow[q] = ep.loop_slot[q] >= 0 ? q : -1;
+    b.fam[1].vrow[q] = q < (int)ep.n_pat ? q : -1;
+  }
+  const uint64_t w2 = std::max<uint64_t>((uint64_t)p.n_loops, p.n_kernels) * ep.n_pat;
+  dim3 g2((uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((w2 + 3) / 4, (uint64_t)n_sms * 32)), 2);
+  k_segsum<<<g2, 128, 0, s>>>(b);
+  const uint32_t total = p.n_kernels * ep.n_pat;
+  k_est_final<<<std::max<uint32_t>(1, std::min<uint32_t>((total + 127) / 128, n_sms * 8)), 128, 0, s>>>(p, ep);
+  *launches += 4;
+  return cudaGetLastError();
+}
+
+}  // namespace gpa

@@ -1,0 +1,147 @@
+// gpa_internal.cuh -- private declarations shared by the runtime and the sm_100a kernels.
+// Product code (the CUDA path).  Independent of oracle/ (no shared code or tables).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/gpa.h"
+
+namespace gpa {
+
+constexpr int kReasonsMax = 16;
+constexpr int kColsMax = kReasonsMax + 6;   // NCOL = R + 6
+constexpr int kSlotsMax = 2 * kColsMax + 2; // V values + (A, L)
+constexpr int kPatternsMax = 32;
+constexpr int kChunk = 128;                 // rollup chunk length (instructions)
+constexpr int kMaxIngestCtas = 256;         // per-CTA partial tables reserved (smem variant)
+constexpr size_t kSmemTableMax = 224 * 1024;// largest CTA-private table (bytes; sm_100a opt-in is 227 KB)
+
+// stall reasons
+constexpr uint32_t R_NONE = 0, R_MEM = 1, R_EXEC = 2, R_SYNC = 3;
+// opcode classes
+constexpr uint32_t OC_GLOBAL = 0, OC_LOCAL = 1, OC_SHARED = 2, OC_CONSTANT = 3, OC_TEXTURE = 4,
+                   OC_SYNC = 9, OC_COUNT = 11;
+constexpr uint8_t K_WAR = 8;
+// blame column indices
+constexpr uint32_t COL_MEM_GLOBAL = 0, COL_MEM_LOCAL = 1, COL_MEM_CONSTANT = 2,
+                   COL_EXEC_SHARED = 3, COL_EXEC_ARITH = 4, COL_EXEC_WAR = 5, COL_SYNC = 6,
+                   COL_MEM_SELF = 7, COL_PASS0 = 10;
+// per-instruction edge-blame groups (GPA_VIEW_INSTR_BLAME)
+constexpr uint32_t BG_MEM = 0, BG_EXEC = 1, BG_WAR = 2, BG_SYNC = 3;
+
+enum : int { ST_COUNTS = 1, ST_BLAMED = 2, ST_AGGREGATED = 4, ST_PATTERNS = 8 };
+enum : int { VAR_SMEM = 0, VAR_PART = 1, VAR_L2 = 2 };
+
+// Device-side view of a program: plain pointers into the workspace.
+struct DevProgram {
+  uint32_t n, E, R, ncol, n_lines, n_loops, n_funcs, n_kernels;
+  const uint8_t *opclass, *iflags;
+  const uint32_t *latency, *line_id;
+  const int32_t *loop_id;
+  const uint32_t *func_begin, *kernel_func_begin, *kernel_grid_blocks;
+  const uint32_t *row_ptr, *edge_def, *edge_min, *edge_max, *edge_use;
+  const int32_t *edge_dom, *edge_lca;
+  const uint8_t *edge_kind;
+  const uint32_t *def_ptr, *def_perm;
+  uint64_t *C, *stats, *AL;
+  uint32_t *partials;               // [kMaxIngestCtas][n*2R] per-CTA tables (smem variant)
+  uint8_t *cand, *selfm;
+  double *share, *B;
+};
+
+// Rollup plan (create-time): chunks over an instruction order, then segments.
+struct RollupPlan {
+  const uint32_t *order;        // [n_order] instruction ids: line-major | loop-major | identity
+  const uint32_t *chunk_begin;  // [n_chunks] positions in order
+  const uint32_t *chunk_end;
+  uint32_t n_chunks;
+  double *part_v;               // [n_chunks][2*ncol]
+  uint64_t *part_al;            // [n_chunks][2]
+  // stage 1: segments (lines, loops excl, funcs) over chunk ranges -> rows [0, n_seg1)
+  const uint32_t *seg1_begin, *seg1_end;
+  uint32_t n_seg1;
+  // stage 2: segments (loops incl, kernels) over rows via perm -> rows [n_seg1, n_seg1 + n_seg2)
+  const uint32_t *seg2_perm, *seg2_begin, *seg2_end;
+  uint32_t n_seg2;
+  double *rows_v;               // [n_rows][2*ncol]
+  uint64_t *rows_al;            // [n_rows][2]
+};
+
+struct EstimatePlan {
+  const gpa_pattern *pats;
+  uint32_t n_pat;
+  int8_t loop_slot[kPatternsMax];   // pattern -> slot in mval (models 2, 4) or -1
+  double *mval;                 // [n_pat][E + n]: edge part then instruction part
+  double *mrow;                 // [n_pat][n]: per use row (edges of the row + instruction part)
+  const uint32_t *loop_items;   // [n_items] item ids (edge e, or E + instruction) by scope loop
+  const uint32_t *loop_item_ptr;// [n_loops+1]
+  const uint32_t *pre_perm;     // [n_loops] loops in preorder
+  const uint32_t *pre_begin, *pre_end; // [n_loops] subtree range in preorder positions
+  const uint32_t *kloop_ptr, *kloops;  // kernel -> its loops
+  const int32_t *loop_func;     // [n_loops]
+  double *lM_excl, *lM_incl;    // [n_pat][n_loops]
+  double *fM, *kM;              // [n_pat][n_funcs], [n_pat][n_kernels]
+  const double *loop_incl_v;    // unused (kept for layout symmetry)
+  const uint64_t *loop_incl_al, *func_al, *kern_al;
+  gpa_estimate_out *out;        // [n_kernels][n_pat]
+};
+
+// kernel launchers (return cudaError_t of the launch)
+cudaError_t launch_ingest(const DevProgram &p, int variant, const void *records, uint64_t n,
+                          int n_sms, size_t smem_optin, cudaStream_t s);
+cudaError_t launch_blame(const DevProgram &p, int n_sms, cudaStream_t s, uint64_t *launches);
+cudaError_t launch_rollup(const DevProgram &p, const RollupPlan &rp, int n_sms, cudaStream_t s,
+                          uint64_t *launches);
+cudaError_t launch_estimate(const DevProgram &p, const EstimatePlan &ep, int n_sms,
+                            cudaStream_t s, uint64_t *launches);
+cudaError_t launch_instr_vector(const DevProgram &p, double *out, cudaStream_t s);
+size_t ingest_smem_bytes(const DevProgram &p);
+
+#ifdef __CUDACC__
+// Full per-instruction vector V[i][NCOL][2] from B, self flags and C.
+__device__ __forceinline__ double vvalue(const DevProgram &p, uint32_t i, uint32_t col, uint32_t c) {
+  const uint32_t cls = p.opclass[i];
+  if (col < 7) {
+    const double *b = p.B + 8 * (uint64_t)i;
+    switch (col) {
+      case COL_MEM_GLOBAL: return (cls != OC_LOCAL && cls != OC_CONSTANT) ? b[2 * BG_MEM + c] : 0.0;
+      case COL_MEM_LOCAL: return cls == OC_LOCAL ? b[2 * BG_MEM + c] : 0.0;
+      case COL_MEM_CONSTANT: return cls == OC_CONSTANT ? b[2 * BG_MEM + c] : 0.0;
+      case COL_EXEC_SHARED: return cls == OC_SHARED ? b[2 * BG_EXEC + c] : 0.0;
+      case COL_EXEC_ARITH: return cls != OC_SHARED ? b[2 * BG_EXEC + c] : 0.0;
+      case COL_EXEC_WAR: return b[2 * BG_WAR + c];
+      default: return b[2 * BG_SYNC + c];
+    }
+  }
+  const uint32_t r = col - 6;   // 7..9 -> MEM..SYNC (self); >= 10 -> pass-through reason
+  if (col < COL_PASS0 && !((p.selfm[i] >> (r - 1)) & 1u)) return 0.0;
+  const uint64_t *row = p.C + (uint64_t)i * 2 * p.R;
+  const uint64_t lat = row[p.R + r];
+  return (double)(c ? lat : row[r] + lat);
+}
+
+#endif
+
+}  // namespace gpa
+
+struct gpa_program {
+  int device = 0;
+  int n_sms = 148;
+  size_t smem_optin = 0;
+  uint8_t *ws = nullptr;
+  size_t ws_bytes = 0;
+  gpa::DevProgram d{};
+  gpa::RollupPlan rp{};
+  gpa::EstimatePlan ep{};
+  int state = 0;
+  int variant = gpa::VAR_SMEM;
+  uint64_t launches = 0;
+  uint64_t view_off[GPA_VIEW_COUNT_] = {};
+  uint64_t view_bytes[GPA_VIEW_COUNT_] = {};
+  gpa_pattern *pats_dev = nullptr;
+  // host ingest staging ring
+  void *staging = nullptr;
+  size_t staging_bytes = 0;
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
+};

@@ -1,0 +1,282 @@
+"""Thin Python binding of the C ABI in include/gpa.h (argument marshalling only).
+
+Every step of GPA's hot path runs in the sm_100a kernels of libgpa_b200.so; torch is used for
+device memory (the workspace is a torch uint8 tensor), streams and process groups.  There is
+no CPU fallback: importing without the built library, or creating a program without a CUDA
+device, raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgpa_b200.so")
+
+VIEW = {
+    "counts": 0, "stats": 1, "instr_al": 2, "cand": 3, "self": 4, "share": 5, "instr_blame": 6,
+    "line": 7, "line_al": 8, "loop_excl": 9, "loop_excl_al": 10, "loop_incl": 11,
+    "loop_incl_al": 12, "func": 13, "func_al": 14, "kernel": 15, "kernel_al": 16, "estimates": 17,
+}
+VARIANT = {"smem": 0, "part": 1, "l2": 2}
+
+
+class GpaError(RuntimeError):
+    pass
+
+
+class ProgramDesc(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_uint32) for k in
+                ("n_instr", "n_reasons", "n_lines", "n_loops", "n_funcs", "n_kernels")] + [
+        (k, ctypes.c_void_p) for k in (
+            "opclass", "iflags", "latency", "line_id", "loop_id", "loop_parent", "func_begin",
+            "kernel_func_begin", "kernel_grid_blocks", "row_ptr", "edge_def", "edge_kind",
+            "edge_min_len", "edge_max_len", "edge_dom_k")]
+
+
+class Pattern(ctypes.Structure):
+    _fields_ = [("column_mask", ctypes.c_uint32), ("class_mask", ctypes.c_uint16),
+                ("sample_class", ctypes.c_uint8), ("model", ctypes.c_uint8),
+                ("flag_filter", ctypes.c_uint8), ("same_loop", ctypes.c_uint8),
+                ("parallel_rule", ctypes.c_uint8), ("pad", ctypes.c_uint8),
+                ("sm_count", ctypes.c_uint32), ("ratio", ctypes.c_double), ("W", ctypes.c_double),
+                ("W_new", ctypes.c_double), ("f", ctypes.c_double)]
+
+
+class EstimateOut(ctypes.Structure):
+    _fields_ = [("speedup", ctypes.c_double), ("M", ctypes.c_double), ("eq3", ctypes.c_double),
+                ("eq4", ctypes.c_double), ("T", ctypes.c_uint64), ("A", ctypes.c_uint64),
+                ("best_scope", ctypes.c_int32), ("unbounded", ctypes.c_uint8),
+                ("matched", ctypes.c_uint8), ("model", ctypes.c_uint8), ("pad", ctypes.c_uint8)]
+
+
+EXPORTS = ["gpa_validate_program", "gpa_workspace_size", "gpa_program_create", "gpa_program_destroy",
+           "gpa_reset_counts", "gpa_ingest_samples", "gpa_ingest_samples_host", "gpa_blame",
+           "gpa_aggregate", "gpa_set_patterns", "gpa_estimate", "gpa_read_estimates", "gpa_get_stats",
+           "gpa_view", "gpa_instr_vector", "gpa_program_info", "gpa_ingest_variant",
+           "gpa_set_ingest_variant", "gpa_launch_count", "gpa_last_error", "gpa_version"]
+
+_lib = None
+
+
+def lib():
+    """Load libgpa_b200.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2009_04061_b200.build` "
+                              "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, u32, u64 = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64
+        sig = {
+            "gpa_validate_program": [vp], "gpa_workspace_size": [vp, vp],
+            "gpa_program_create": [vp, vp, ctypes.c_size_t, vp, vp], "gpa_program_destroy": [vp],
+            "gpa_reset_counts": [vp, vp], "gpa_ingest_samples": [vp, vp, u64, vp],
+            "gpa_ingest_samples_host": [vp, vp, u64, vp], "gpa_blame": [vp, vp],
+            "gpa_aggregate": [vp, vp], "gpa_set_patterns": [vp, vp, u32, vp],
+            "gpa_estimate": [vp, vp], "gpa_read_estimates": [vp, vp, vp], "gpa_get_stats": [vp, vp, vp],
+            "gpa_view": [vp, ctypes.c_int, vp, vp], "gpa_instr_vector": [vp, vp, vp],
+            "gpa_program_info": [vp, vp], "gpa_ingest_variant": [vp, vp],
+            "gpa_set_ingest_variant": [vp, ctypes.c_int], "gpa_launch_count": [vp, vp],
+        }
+        for name, args in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = ctypes.c_int
+        L.gpa_last_error.restype = ctypes.c_char_p
+        L.gpa_version.restype = ctypes.c_char_p
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        raise GpaError(f"{what} failed ({rc}): {lib().gpa_last_error().decode()}")
+
+
+_DT = {"opclass": np.uint8, "iflags": np.uint8, "latency": np.uint32, "line_id": np.uint32,
+       "loop_id": np.int32, "loop_parent": np.int32, "func_begin": np.uint32,
+       "kernel_func_begin": np.uint32, "kernel_grid_blocks": np.uint32, "row_ptr": np.uint32,
+       "edge_def": np.uint32, "edge_kind": np.uint8, "edge_min_len": np.uint32,
+       "edge_max_len": np.uint32, "edge_dom_k": np.int32}
+
+
+class _Desc:
+    """Host arrays of a program (kept alive) and the gpa_program_desc pointing at them."""
+
+    def __init__(self, prog):
+        self.arr = {}
+        for k, dt in _DT.items():
+            v = getattr(prog, k, None)
+            self.arr[k] = None if v is None else np.ascontiguousarray(v, dtype=dt)
+        n = int(self.arr["opclass"].shape[0])
+        self.d = ProgramDesc(
+            n, int(prog.n_reasons), int(prog.n_lines), int(self.arr["loop_parent"].shape[0]),
+            int(self.arr["func_begin"].shape[0] - 1), int(self.arr["kernel_func_begin"].shape[0] - 1),
+            *[None if self.arr[k] is None or self.arr[k].size == 0 else self.arr[k].ctypes.data for k in (
+                  "opclass", "iflags", "latency", "line_id", "loop_id", "loop_parent", "func_begin",
+                  "kernel_func_begin", "kernel_grid_blocks", "row_ptr", "edge_def", "edge_kind",
+                  "edge_min_len", "edge_max_len", "edge_dom_k")])
+
+
+def validate(prog) -> None:
+    """Host-only structural validation (gpa_validate_program); raises GpaError."""
+    d = _Desc(prog)
+    _check(lib().gpa_validate_program(ctypes.byref(d.d)), "gpa_validate_program")
+
+
+def workspace_size(prog) -> int:
+    d = _Desc(prog)
+    out = ctypes.c_size_t(0)
+    _check(lib().gpa_workspace_size(ctypes.byref(d.d), ctypes.byref(out)), "gpa_workspace_size")
+    return int(out.value)
+
+
+def _pattern_struct(p) -> Pattern:
+    if isinstance(p, Pattern):
+        return p
+    return Pattern(int(p["column_mask"]), int(p["class_mask"]), int(p["sample_class"]), int(p["model"]),
+                   int(p["flag_filter"]), int(p["same_loop"]), int(p["parallel_rule"]), 0,
+                   int(p["sm_count"]), float(p["ratio"]), float(p["W"]), float(p["W_new"]), float(p["f"]))
+
+
+class Program:
+    """One program's device workspace and handle (gpa_program_create)."""
+
+    def __init__(self, prog, device=None, stream=None):
+        import torch
+        if not torch.cuda.is_available():
+            raise GpaError("a CUDA device is required (there is no CPU fallback)")
+        self.torch = torch
+        self.device = torch.device(device if device is not None else "cuda")
+        self._desc = _Desc(prog)
+        size = ctypes.c_size_t(0)
+        _check(lib().gpa_workspace_size(ctypes.byref(self._desc.d), ctypes.byref(size)), "gpa_workspace_size")
+        self.ws = torch.empty(max(int(size.value), 256), dtype=torch.uint8, device=self.device)
+        self.handle = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            _check(lib().gpa_program_create(ctypes.byref(self._desc.d), self.ws.data_ptr(), self.ws.numel(),
+                                            self._s(stream), ctypes.byref(self.handle)), "gpa_program_create")
+        info = (ctypes.c_uint64 * 8)()
+        _check(lib().gpa_program_info(self.handle, info), "gpa_program_info")
+        (self.n_instr, self.n_edges, self.R, self.ncol, self.n_lines, self.n_loops, self.n_funcs,
+         self.n_kernels) = (int(x) for x in info)
+        self.n_patterns = 0
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            lib().gpa_program_destroy(h)
+            self.handle = None
+
+    def _s(self, stream):
+        s = stream if stream is not None else self.torch.cuda.current_stream(self.device)
+        return ctypes.c_void_p(s.cuda_stream)
+
+    # -------------------------------------------------------------- hot path (enqueue only)
+    def reset(self, stream=None):
+        _check(lib().gpa_reset_counts(self.handle, self._s(stream)), "gpa_reset_counts")
+
+    def ingest(self, samples, n=None, stream=None):
+        """samples: CUDA tensor holding 8-byte records (any dtype; uint8 of 8n bytes, or int64 of n)."""
+        t = samples
+        if not t.is_cuda:
+            raise GpaError("ingest() takes a device tensor; use ingest_host() for host memory")
+        nrec = int(t.numel() * t.element_size() // 8) if n is None else int(n)
+        _check(lib().gpa_ingest_samples(self.handle, t.data_ptr(), nrec, self._s(stream)), "gpa_ingest_samples")
+
+    def ingest_host(self, samples, n=None, stream=None):
+        """samples: host numpy array / CPU tensor of 8-byte records (pinned memory overlaps)."""
+        if hasattr(samples, "data_ptr"):
+            ptr, nbytes = samples.data_ptr(), samples.numel() * samples.element_size()
+        else:
+            a = np.ascontiguousarray(samples)
+            ptr, nbytes = a.ctypes.data, a.nbytes
+        nrec = nbytes // 8 if n is None else int(n)
+        _check(lib().gpa_ingest_samples_host(self.handle, ptr, nrec, self._s(stream)), "gpa_ingest_samples_host")
+
+    def blame(self, stream=None):
+        _check(lib().gpa_blame(self.handle, self._s(stream)), "gpa_blame")
+
+    def aggregate(self, stream=None):
+        _check(lib().gpa_aggregate(self.handle, self._s(stream)), "gpa_aggregate")
+
+    def set_patterns(self, patterns, stream=None):
+        arr = (Pattern * len(patterns))(*[_pattern_struct(p) for p in patterns])
+        _check(lib().gpa_set_patterns(self.handle, ctypes.addressof(arr), len(patterns), self._s(stream)),
+               "gpa_set_patterns")
+        self.n_patterns = len(patterns)
+
+    def estimate(self, stream=None):
+        _check(lib().gpa_estimate(self.handle, self._s(stream)), "gpa_estimate")
+
+    def step(self, samples, stream=None, estimate=True):
+        """One pass of the whole hot path over one batch of device-resident records."""
+        self.reset(stream)
+        self.ingest(samples, stream=stream)
+        self.blame(stream)
+        self.aggregate(stream)
+        if estimate and self.n_patterns:
+            self.estimate(stream)
+
+    # -------------------------------------------------------------- results
+    def read_estimates(self, stream=None):
+        out = (EstimateOut * (self.n_kernels * self.n_patterns))()
+        _check(lib().gpa_read_estimates(self.handle, ctypes.addressof(out), self._s(stream)), "gpa_read_estimates")
+        return [[out[k * self.n_patterns + q] for q in range(self.n_patterns)] for k in range(self.n_kernels)]
+
+    def stats(self, stream=None):
+        out = (ctypes.c_uint64 * 4)()
+        _check(lib().gpa_get_stats(self.handle, out, self._s(stream)), "gpa_get_stats")
+        return [int(x) for x in out]
+
+    def view(self, name):
+        """torch view (no copy) of a device result inside the workspace."""
+        torch = self.torch
+        off, nb = ctypes.c_uint64(0), ctypes.c_uint64(0)
+        _check(lib().gpa_view(self.handle, VIEW[name], ctypes.byref(off), ctypes.byref(nb)), "gpa_view")
+        raw = self.ws[off.value: off.value + nb.value]
+        nv = 2 * self.ncol
+        shapes = {
+            "counts": (torch.int64, (self.n_instr, 2, self.R)), "stats": (torch.int64, (4,)),
+            "instr_al": (torch.int64, (self.n_instr, 2)), "cand": (torch.uint8, (self.n_edges,)),
+            "self": (torch.uint8, (self.n_instr,)), "share": (torch.float64, (self.n_edges, 3)),
+            "instr_blame": (torch.float64, (self.n_instr, 4, 2)),
+            "line": (torch.float64, (self.n_lines, self.ncol, 2)), "line_al": (torch.int64, (self.n_lines, 2)),
+            "loop_excl": (torch.float64, (self.n_loops, self.ncol, 2)),
+            "loop_excl_al": (torch.int64, (self.n_loops, 2)),
+            "loop_incl": (torch.float64, (self.n_loops, self.ncol, 2)),
+            "loop_incl_al": (torch.int64, (self.n_loops, 2)),
+            "func": (torch.float64, (self.n_funcs, self.ncol, 2)), "func_al": (torch.int64, (self.n_funcs, 2)),
+            "kernel": (torch.float64, (self.n_kernels, self.ncol, 2)),
+            "kernel_al": (torch.int64, (self.n_kernels, 2)),
+        }
+        if name == "estimates":
+            return raw
+        dt, shape = shapes[name]
+        del nv
+        return raw.view(dt).view(shape)
+
+    def instr_vector(self, stream=None):
+        torch = self.torch
+        out = torch.empty((self.n_instr, self.ncol, 2), dtype=torch.float64, device=self.device)
+        _check(lib().gpa_instr_vector(self.handle, out.data_ptr(), self._s(stream)), "gpa_instr_vector")
+        return out
+
+    @property
+    def variant(self) -> str:
+        v = ctypes.c_int(0)
+        _check(lib().gpa_ingest_variant(self.handle, ctypes.byref(v)), "gpa_ingest_variant")
+        return {b: a for a, b in VARIANT.items()}[v.value]
+
+    @variant.setter
+    def variant(self, name: str):
+        _check(lib().gpa_set_ingest_variant(self.handle, VARIANT[name]), "gpa_set_ingest_variant")
+
+    @property
+    def launches(self) -> int:
+        v = ctypes.c_uint64(0)
+        _check(lib().gpa_launch_count(self.handle, ctypes.byref(v)), "gpa_launch_count")
+        return int(v.value)

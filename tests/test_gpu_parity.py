@@ -1,0 +1,144 @@
+"""Parity of the CUDA path (through the C ABI) with the CPU oracle on the same seeded inputs.
+
+Bar (BASELINE.json north_star): counts, stats, candidate masks and self flags bit-exact; blame,
+rollups and estimates in fp64 within 1e-9 relative, integer-valued columns exact.
+"""
+import numpy as np
+import pytest
+
+from gpagen import programs as gp
+from gpagen.patterns import table2
+from gpagen.streams import StreamSpec, config_stream
+from tests._common import compare, run_gpu, run_oracle
+
+pytestmark = pytest.mark.gpu
+
+REL = 1e-9
+
+
+@pytest.fixture(autouse=True)
+def _need_cuda(cuda_available):
+    if not cuda_available:
+        pytest.skip("no CUDA device")
+
+
+def test_tiny_fixture_bit_exact():
+    prog = gp.tiny_fixture()
+    recs = gp.tiny_records()
+    g = run_gpu(prog, recs)
+    o = run_oracle(prog, recs)
+    compare(g, o, rel=1e-15, exact_blame=True)
+    assert g["program"].variant == "smem"
+
+
+@pytest.mark.parametrize("seed,n_instr,R,count_max,invalid_ppm,n_rec", [
+    (21, 300, 9, 1, 0, 100_003),          # odd record count (ragged tail)
+    (22, 700, 9, 7, 30_000, 250_001),     # pre-aggregated counts + malformed records
+    (23, 1500, 16, 3, 5_000, 400_000),    # R = 16 (max), 32 pass-through columns
+    (24, 200, 4, 1, 0, 50_000),           # R = 4 (no pass-through reasons)
+])
+def test_random_programs(seed, n_instr, R, count_max, invalid_ppm, n_rec):
+    prog = gp.random_program(n_instr, 3, 10, 4, seed=seed, n_reasons=R)
+    spec = StreamSpec(prog, seed=seed * 101, count_max=count_max, invalid_ppm=invalid_ppm)
+    recs = spec.host(0, n_rec)
+    o = run_oracle(prog, recs)
+    compare(run_gpu(prog, recs), o, rel=REL)
+    # unaligned (8- but not 16-byte aligned) record pointer
+    compare(run_gpu(prog, recs, offset_records=1), o, rel=REL)
+
+
+@pytest.mark.parametrize("variant", ["smem", "l2"])
+def test_config2_rodinia(variant):
+    prog = gp.config_program(2)
+    recs = config_stream(prog, 2).host(0, 10_000_000)
+    o = run_oracle(prog, recs)
+    compare(run_gpu(prog, recs, variant=variant), o, rel=REL)
+
+
+def test_config3_large_program_reduced_stream():
+    """Config-3 program (50k instructions, 200 loops) on a 2*10^7-record prefix of its stream."""
+    prog = gp.config_program(3)
+    recs = config_stream(prog, 3).host(0, 20_000_000)
+    o = run_oracle(prog, recs)
+    g = run_gpu(prog, recs)
+    assert g["program"].variant == "l2"
+    compare(g, o, rel=REL)
+
+
+def test_host_ingest_equals_device_ingest():
+    prog = gp.config_program(2)
+    recs = config_stream(prog, 2, count_max=3).host(0, 9_000_001)
+    g1 = run_gpu(prog, recs)
+    g2 = run_gpu(prog, recs, host=True)
+    assert np.array_equal(g1["C"], g2["C"]) and np.array_equal(g1["V"], g2["V"])
+
+
+def test_deterministic_and_accumulating():
+    import torch
+    from paper_2009_04061_b200 import Program
+    prog = gp.config_program(2)
+    recs = config_stream(prog, 2).host(0, 3_000_000)
+    d = torch.from_numpy(recs.view(np.int64)).cuda()
+    P = Program(prog)
+    P.set_patterns(table2())
+    outs = []
+    for split in (None, 1_234_567):
+        P.reset()
+        if split is None:
+            P.ingest(d)
+        else:
+            P.ingest(d[:split])
+            P.ingest(d[split:])
+        P.blame()
+        P.aggregate()
+        P.estimate()
+        torch.cuda.synchronize()
+        outs.append((P.view("counts").clone(), P.instr_vector(), P.view("kernel").clone(),
+                     P.view("loop_incl").clone()))
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+
+
+def test_edge_cases_empty_and_invalid_streams():
+    prog = gp.random_program(100, 2, 3, 2, seed=5)
+    for recs in (np.zeros(0, np.uint64),
+                 StreamSpec(prog, seed=9, invalid_ppm=1_000_000).host(0, 10_001)):
+        o = run_oracle(prog, recs)
+        g = run_gpu(prog, recs)
+        compare(g, o, rel=REL)
+        assert g["C"].sum() == 0
+        for row in g["est"][0]:
+            assert row.T == 0
+            if row.model != 5:          # Eq. 10 with R_I = 0 is f / C_W by the C_I := 1 convention (Q18)
+                assert row.speedup == 1.0
+
+
+def test_program_without_edges_or_loops():
+    n = 64
+    prog = gp._finalize(9, [gp.GLOBAL] * n, [0] * n, [1024] * n, list(range(n)), [-1] * n, [],
+                        [0, 32, n], [0, 2], [4], [[] for _ in range(n)], n_lines=n)
+    recs = StreamSpec(gp.random_program(n, 2, 2, 2, seed=3), seed=4).host(0, 20_000)
+    compare(run_gpu(prog, recs), run_oracle(prog, recs), rel=REL)
+
+
+def test_multi_kernel_program():
+    prog = gp.random_program(3000, 12, 20, 3, seed=77, n_kernels=5)
+    recs = StreamSpec(prog, seed=78, count_max=2).host(0, 500_000)
+    compare(run_gpu(prog, recs), run_oracle(prog, recs), rel=REL)
+
+
+def test_call_order_errors():
+    import torch
+    from paper_2009_04061_b200 import GpaError, Program
+    P = Program(gp.tiny_fixture())
+    with pytest.raises(GpaError, match="before"):
+        P.blame()
+    P.reset()
+    with pytest.raises(GpaError, match="before"):
+        P.aggregate()
+    P.blame()
+    P.aggregate()
+    with pytest.raises(GpaError, match="patterns"):
+        P.estimate()
+    with pytest.raises(GpaError):
+        P.ingest(torch.zeros(3, dtype=torch.uint8, device="cuda")[1:])   # misaligned pointer
