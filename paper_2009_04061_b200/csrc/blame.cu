@@ -112,15 +112,6 @@ __global__ void k_def_reduce(DevProgram p) {
   }
 }
 
-__global__ void k_instr_vector(DevProgram p, double *__restrict__ out) {
-  const uint64_t total = (uint64_t)p.n * p.ncol * 2;
-  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total; t += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t i = (uint32_t)(t / (2 * p.ncol));
-    const uint32_t s = (uint32_t)(t % (2 * p.ncol));
-    out[t] = vvalue(p, i, s >> 1, s & 1);
-  }
-}
-
 inline uint32_t grid_for(uint64_t items, uint32_t threads, int n_sms) {
   return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((items + threads - 1) / threads, (uint64_t)n_sms * 16));
 }
@@ -132,14 +123,6 @@ cudaError_t launch_blame(const DevProgram &p, int n_sms, cudaStream_t s, uint64_
   k_blame_rows<<<grid_for(p.n, 128, n_sms), 128, 0, s>>>(p);
   k_def_reduce<<<grid_for(p.n, 128, n_sms), 128, 0, s>>>(p);
   *launches += 3;
-  return cudaGetLastError();
-}
-
-cudaError_t launch_instr_vector(const DevProgram &p, double *out, cudaStream_t s) {
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  k_instr_vector<<<grid_for((uint64_t)p.n * p.ncol * 2, 256, sms), 256, 0, s>>>(p, out);
   return cudaGetLastError();
 }
 

@@ -9,7 +9,7 @@
 //   k_segsum      one warp per (segment, pattern): fixed-order strided sums + xor-shuffle tree
 //                 (deterministic).  Stage 1: loop-exclusive (by scope-loop item lists) and
 //                 function sums; stage 2: loop-inclusive (preorder subtree ranges) and kernel sums.
-//   k_est_final   one thread per (kernel, pattern): T, A, R_I, M, Eqs. 2-5 / 10, best scope.
+//   k_est_final   one warp per (kernel, pattern): T, A, R_I, M, Eqs. 2-5 / 10, best scope.
 #include <algorithm>
 #include <math.h>
 
@@ -28,51 +28,68 @@ __device__ __forceinline__ bool passes(const gpa_pattern &q, uint32_t cls, uint3
   return ((q.class_mask >> cls) & 1u) && (!q.flag_filter || (flags & q.flag_filter));
 }
 
+constexpr int kPatRows = 16;   // patterns evaluated per row pass (gpa_set_patterns allows 16)
+
 __global__ void k_est_rows(DevProgram p, EstimatePlan ep) {
   __shared__ gpa_pattern sp[kPatternsMax];
   for (uint32_t q = threadIdx.x; q < ep.n_pat; q += blockDim.x) sp[q] = ep.pats[q];
   __syncthreads();
+  const uint32_t np = ep.n_pat;
   const uint64_t stride_items = (uint64_t)p.E + p.n;
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < p.n; j += gridDim.x * blockDim.x) {
     const uint64_t *row = p.C + (uint64_t)j * 2 * p.R;
+    uint64_t lat[4], all[4];
+#pragma unroll
+    for (int r = 1; r <= 3; ++r) {
+      lat[r] = row[p.R + r];
+      all[r] = row[r] + lat[r];
+    }
     const uint32_t e0 = p.row_ptr[j], e1 = p.row_ptr[j + 1];
     const int32_t loop_j = p.loop_id[j];
-    const uint32_t cls_j = p.opclass[j], fl_j = p.iflags[j], self_j = p.selfm[j];
-    for (uint32_t qi = 0; qi < ep.n_pat; ++qi) {
-      const gpa_pattern &q = sp[qi];
-      const int slot = ep.loop_slot[qi];
-      double sum = 0.0;
-      if (q.model == 5) {
-        ep.mrow[(uint64_t)qi * p.n + j] = 0.0;
-        continue;
-      }
-      for (uint32_t e = e0; e < e1; ++e) {
+    double sum[kPatRows];
+#pragma unroll
+    for (int q = 0; q < kPatRows; ++q) sum[q] = 0.0;
+    for (uint32_t e = e0; e < e1; ++e) {
+      const uint32_t m = p.cand[e];
+      const uint32_t d = p.edge_def[e];
+      const uint32_t cls = p.opclass[d], fl = p.iflags[d], kind = p.edge_kind[e];
+      const bool same = p.loop_id[d] >= 0 && p.loop_id[d] == loop_j;
+      const double sh1 = p.share[3 * (uint64_t)e], sh2 = p.share[3 * (uint64_t)e + 1], sh3 = p.share[3 * (uint64_t)e + 2];
+      const uint32_t c1 = classify(R_MEM, cls, kind), c2 = classify(R_EXEC, cls, kind), c3 = COL_SYNC;
+#pragma unroll
+      for (int qi = 0; qi < kPatRows; ++qi) {
+        if (qi >= (int)np) break;
+        const gpa_pattern &q = sp[qi];
         double me = 0.0;
-        const uint32_t m = p.cand[e];
-        const uint32_t d = p.edge_def[e];
-        if (m && passes(q, p.opclass[d], p.iflags[d]) &&
-            (!q.same_loop || (p.loop_id[d] >= 0 && p.loop_id[d] == loop_j))) {
-          for (uint32_t r = R_MEM; r <= R_SYNC; ++r) {
-            if (!((m >> (r - 1)) & 1u)) continue;
-            if (!((q.column_mask >> classify(r, p.opclass[d], p.edge_kind[e])) & 1u)) continue;
-            const uint64_t X = row[p.R + r] + (q.sample_class ? 0ull : row[r]);
-            me = __dadd_rn(me, __dmul_rn((double)X, p.share[3 * (uint64_t)e + (r - 1)]));
-          }
+        if (m && q.model != 5 && passes(q, cls, fl) && (!q.same_loop || same)) {
+          const bool L = q.sample_class != 0;
+          if ((m & 1u) && ((q.column_mask >> c1) & 1u)) me = __dadd_rn(me, __dmul_rn((double)(L ? lat[1] : all[1]), sh1));
+          if ((m & 2u) && ((q.column_mask >> c2) & 1u)) me = __dadd_rn(me, __dmul_rn((double)(L ? lat[2] : all[2]), sh2));
+          if ((m & 4u) && ((q.column_mask >> c3) & 1u)) me = __dadd_rn(me, __dmul_rn((double)(L ? lat[3] : all[3]), sh3));
         }
+        sum[qi] = __dadd_rn(sum[qi], me);
+        const int slot = ep.loop_slot[qi];
         if (slot >= 0) ep.mval[(uint64_t)slot * stride_items + e] = me;
-        sum = __dadd_rn(sum, me);
       }
+    }
+    const uint32_t cls_j = p.opclass[j], fl_j = p.iflags[j], self_j = p.selfm[j];
+#pragma unroll
+    for (int qi = 0; qi < kPatRows; ++qi) {
+      if (qi >= (int)np) break;
+      const gpa_pattern &q = sp[qi];
       double mi = 0.0;
-      if (passes(q, cls_j, fl_j) && (!q.same_loop || loop_j >= 0)) {
+      if (q.model != 5 && passes(q, cls_j, fl_j) && (!q.same_loop || loop_j >= 0)) {
+        const bool L = q.sample_class != 0;
         for (uint32_t r = R_MEM; r <= R_SYNC; ++r)
           if (((self_j >> (r - 1)) & 1u) && ((q.column_mask >> (COL_MEM_SELF + r - 1)) & 1u))
-            mi = __dadd_rn(mi, (double)(row[p.R + r] + (q.sample_class ? 0ull : row[r])));
+            mi = __dadd_rn(mi, (double)(L ? lat[r] : all[r]));
         for (uint32_t r = 4; r < p.R; ++r)
           if ((q.column_mask >> (COL_PASS0 + r - 4)) & 1u)
-            mi = __dadd_rn(mi, (double)(row[p.R + r] + (q.sample_class ? 0ull : row[r])));
+            mi = __dadd_rn(mi, (double)(row[p.R + r] + (L ? 0ull : row[r])));
       }
+      const int slot = ep.loop_slot[qi];
       if (slot >= 0) ep.mval[(uint64_t)slot * stride_items + p.E + j] = mi;
-      ep.mrow[(uint64_t)qi * p.n + j] = __dadd_rn(sum, mi);
+      ep.mrow[(uint64_t)qi * p.n + j] = q.model == 5 ? 0.0 : __dadd_rn(sum[qi], mi);
     }
   }
 }
@@ -105,7 +122,18 @@ __global__ void k_segsum(SegLaunch L) {
     if (vr >= 0) {
       const double *vals = F.values + (uint64_t)vr * F.row_stride;
       const uint32_t b = F.begin[s], e = F.end ? F.end[s] : F.begin[s + 1];
-      for (uint32_t pos = b + lane; pos < e; pos += 32) acc = __dadd_rn(acc, vals[F.perm ? F.perm[pos] : pos]);
+      double a1 = 0.0, a2 = 0.0, a3 = 0.0;   // four interleaved accumulators: loads in flight
+      uint32_t pos = b + lane;
+      for (; pos + 96 < e; pos += 128) {
+        const double x0 = vals[F.perm ? F.perm[pos] : pos], x1 = vals[F.perm ? F.perm[pos + 32] : pos + 32];
+        const double x2 = vals[F.perm ? F.perm[pos + 64] : pos + 64], x3 = vals[F.perm ? F.perm[pos + 96] : pos + 96];
+        acc = __dadd_rn(acc, x0);
+        a1 = __dadd_rn(a1, x1);
+        a2 = __dadd_rn(a2, x2);
+        a3 = __dadd_rn(a3, x3);
+      }
+      for (; pos < e; pos += 32) acc = __dadd_rn(acc, vals[F.perm ? F.perm[pos] : pos]);
+      acc = __dadd_rn(__dadd_rn(acc, a1), __dadd_rn(a2, a3));
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
     }
@@ -119,14 +147,19 @@ __device__ __forceinline__ double eq2(double T, double M) {
   return T / (T - M);
 }
 
+// one warp per (kernel, pattern); lanes stride over the kernel's scopes for Eq. 5 and the warp
+// takes the max with ties to the lowest scope id (loops before functions), as a sequential scan
+// in scope order would.
 __global__ void k_est_final(DevProgram p, EstimatePlan ep) {
+  const uint32_t lane = threadIdx.x & 31;
   const uint32_t total = p.n_kernels * ep.n_pat;
-  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+  const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < total; t += warps) {
     const uint32_t k = t / ep.n_pat, qi = t % ep.n_pat;
     const gpa_pattern q = ep.pats[qi];
-    gpa_estimate_out o;
     const uint64_t A = ep.kern_al[2 * (uint64_t)k], T = A + ep.kern_al[2 * (uint64_t)k + 1];
     const double Td = (double)T, Ad = (double)A;
+    gpa_estimate_out o;
     o.T = T;
     o.A = A;
     o.model = q.model;
@@ -159,29 +192,36 @@ __global__ void k_est_final(DevProgram p, EstimatePlan ep) {
       } else if (q.model == 1) {
         o.speedup = o.eq4;
       } else {
-        double best = 1.0;
+        double best = -1.0;
         int32_t bs = -1;
         if (q.model == 2 || q.model == 4) {
-          for (uint32_t x = ep.kloop_ptr[k]; x < ep.kloop_ptr[k + 1]; ++x) {
+          for (uint32_t x = ep.kloop_ptr[k] + lane; x < ep.kloop_ptr[k + 1]; x += 32) {
             const uint32_t l = ep.kloops[x];
             const double Al = (double)ep.loop_incl_al[2 * (uint64_t)l];
-            const double s = eq2(Td, fmin(Al, ep.lM_incl[(uint64_t)qi * p.n_loops + l]));
-            if (bs < 0 || s > best) { best = s; bs = (int32_t)l; }
+            const double sv = eq2(Td, fmin(Al, ep.lM_incl[(uint64_t)qi * p.n_loops + l]));
+            if (bs < 0 || sv > best) { best = sv; bs = (int32_t)l; }
           }
         }
         if (q.model == 3 || q.model == 4) {
-          for (uint32_t f = p.kernel_func_begin[k]; f < p.kernel_func_begin[k + 1]; ++f) {
+          for (uint32_t f = p.kernel_func_begin[k] + lane; f < p.kernel_func_begin[k + 1]; f += 32) {
             const double Af = (double)ep.func_al[2 * (uint64_t)f];
-            const double s = eq2(Td, fmin(Af, ep.fM[(uint64_t)qi * p.n_funcs + f]));
-            if (bs < 0 || s > best) { best = s; bs = (int32_t)(p.n_loops + f); }
+            const double sv = eq2(Td, fmin(Af, ep.fM[(uint64_t)qi * p.n_funcs + f]));
+            if (bs < 0 || sv > best) { best = sv; bs = (int32_t)(p.n_loops + f); }
           }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+          const int32_t os = __shfl_xor_sync(0xffffffffu, bs, off);
+          const bool take = os >= 0 && (bs < 0 || ob > best || (ob == best && os < bs));
+          if (take) { best = ob; bs = os; }
         }
         o.speedup = bs < 0 ? 1.0 : best;
         o.best_scope = bs;
       }
     }
     o.unbounded = isinf(o.speedup) ? 1 : 0;
-    ep.out[t] = o;
+    if (lane == 0) ep.out[t] = o;
   }
 }
 
@@ -219,7 +259,7 @@ cudaError_t launch_estimate(const DevProgram &p, const EstimatePlan &ep, int n_s
   dim3 g2((uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((w2 + 3) / 4, (uint64_t)n_sms * 32)), 2);
   k_segsum<<<g2, 128, 0, s>>>(b);
   const uint32_t total = p.n_kernels * ep.n_pat;
-  k_est_final<<<std::max<uint32_t>(1, std::min<uint32_t>((total + 127) / 128, n_sms * 8)), 128, 0, s>>>(p, ep);
+  k_est_final<<<std::max<uint32_t>(1, std::min<uint32_t>((total + 3) / 4, n_sms * 32)), 128, 0, s>>>(p, ep);
   *launches += 4;
   return cudaGetLastError();
 }

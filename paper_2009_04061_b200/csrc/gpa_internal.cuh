@@ -15,6 +15,14 @@ constexpr int kPatternsMax = 32;
 constexpr int kChunk = 128;                 // rollup chunk length (instructions)
 constexpr int kMaxIngestCtas = 256;         // per-CTA partial tables reserved (smem variant)
 constexpr size_t kSmemTableMax = 224 * 1024;// largest CTA-private table (bytes; sm_100a opt-in is 227 KB)
+// partitioned ingest (variant P): bucket exchange through L2
+constexpr int kPartThreads = 1024;
+constexpr int kPartChunk = 4096;            // records per CTA per chunk (32 KB, one TMA bulk copy)
+constexpr int kPartBufs = 4;                // exchange buffers in flight
+constexpr int kPartCap = 48;                // keys per (dst, src) slot per chunk (mean 27.7 at G=148);
+                                            // excess -> L2 atomics
+constexpr int kPartMaxCtas = 160;           // < 255: bucket ids fit a byte
+size_t part_smem_bytes(uint32_t bpb, uint32_t G);
 
 // stall reasons
 constexpr uint32_t R_NONE = 0, R_MEM = 1, R_EXEC = 2, R_SYNC = 3;
@@ -45,6 +53,9 @@ struct DevProgram {
   const uint32_t *def_ptr, *def_perm;
   uint64_t *C, *stats, *AL;
   uint32_t *partials;               // [kMaxIngestCtas][n*2R] per-CTA tables (smem variant)
+  uint32_t *part_x;                 // [kPartBufs][kPartMaxCtas][kPartMaxCtas][kPartCap] exchange keys
+  uint32_t *part_n;                 // [kPartBufs][kPartMaxCtas][kPartMaxCtas] keys per (dst, src)
+  unsigned int *part_sync;          // [2*kPartBufs]: per exchange buffer, CTAs that produced / consumed it
   uint8_t *cand, *selfm;
   double *share, *B;
 };
@@ -65,6 +76,7 @@ struct RollupPlan {
   uint32_t n_seg2;
   double *rows_v;               // [n_rows][2*ncol]
   uint64_t *rows_al;            // [n_rows][2]
+  double *vbuf;                 // [n][2*ncol] per-instruction vectors V
 };
 
 struct EstimatePlan {
@@ -94,8 +106,9 @@ cudaError_t launch_rollup(const DevProgram &p, const RollupPlan &rp, int n_sms, 
                           uint64_t *launches);
 cudaError_t launch_estimate(const DevProgram &p, const EstimatePlan &ep, int n_sms,
                             cudaStream_t s, uint64_t *launches);
-cudaError_t launch_instr_vector(const DevProgram &p, double *out, cudaStream_t s);
+cudaError_t launch_vrows(const DevProgram &p, double *vbuf, int n_sms, cudaStream_t s);
 size_t ingest_smem_bytes(const DevProgram &p);
+bool part_feasible(const DevProgram &p, int n_sms, size_t smem_optin);
 
 #ifdef __CUDACC__
 // Full per-instruction vector V[i][NCOL][2] from B, self flags and C.
@@ -135,6 +148,7 @@ struct gpa_program {
   gpa::EstimatePlan ep{};
   int state = 0;
   int variant = gpa::VAR_SMEM;
+  bool part_ok = false;
   uint64_t launches = 0;
   uint64_t view_off[GPA_VIEW_COUNT_] = {};
   uint64_t view_bytes[GPA_VIEW_COUNT_] = {};

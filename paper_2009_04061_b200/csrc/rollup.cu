@@ -1,14 +1,18 @@
 // rollup.cu -- row a7: per-instruction blame vectors summed over program structure
 // (line, loop exclusive/inclusive, function, kernel, Q16).
 //
-// Hand-written segmented reductions (no CUB), deterministic: every sum runs in a fixed order.
-//   k_rollup_chunks    one warp per <=128-instruction chunk of a create-time order (line-major
-//                      | loop-major | function ranges); lane s owns value slot s and s+32 of
-//                      V[i] = {NCOL x (all, lat)} + (A_i, L_i) and sums it over the chunk.
-//   k_rollup_segments  one warp per segment, summing rows (chunk partials, or earlier rows via
-//                      a permutation) over [begin, end).  Stage 1: lines, loops-exclusive,
-//                      functions from chunk partials.  Stage 2: loops-inclusive (subtree ranges
-//                      of the preorder) from loop-exclusive rows, kernels from function rows.
+// Hand-written segmented reductions (no CUB), deterministic: every sum has a fixed order.
+//   k_vrows            V[i] = {NCOL x (all, lat)} for every instruction, one
+//                      thread per value, written coalesced to a row-major buffer; this is also
+//                      the instruction level of the rollup (gpa_instr_vector).
+//   k_rollup_chunks    one warp per <=128-instruction chunk of a create-time order (line-major |
+//                      loop-major | function ranges); lane s owns value slot s (and s+32) of the
+//                      row, so each member row is one coalesced load; four interleaved
+//                      accumulators keep loads in flight.  Slots NV, NV+1 carry (A_i, L_i).
+//   k_rollup_segments  one warp per segment, same scheme over rows: chunk partials (stage 1:
+//                      lines, loops-exclusive, functions) or earlier rows through a permutation
+//                      (stage 2: loops-inclusive = preorder subtree ranges of the loop-exclusive
+//                      rows; kernels = their function rows).
 #include <algorithm>
 
 #include "gpa_internal.cuh"
@@ -16,51 +20,68 @@
 namespace gpa {
 namespace {
 
-__global__ void k_rollup_chunks(DevProgram p, RollupPlan rp) {
-  const uint32_t lane = threadIdx.x & 31;
+__global__ void k_vrows(DevProgram p, double *__restrict__ vbuf) {
   const uint32_t nv = 2 * p.ncol;
-  const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t ch = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; ch < rp.n_chunks; ch += warps) {
-    const uint32_t b = rp.chunk_begin[ch], e = rp.chunk_end[ch];
-    for (uint32_t s = lane; s < nv + 2; s += 32) {
-      if (s < nv) {
-        double acc = 0.0;
-        for (uint32_t pos = b; pos < e; ++pos) acc = __dadd_rn(acc, vvalue(p, rp.order[pos], s >> 1, s & 1));
-        rp.part_v[(uint64_t)ch * nv + s] = acc;
-      } else {
-        uint64_t acc = 0;
-        for (uint32_t pos = b; pos < e; ++pos) acc += p.AL[2 * (uint64_t)rp.order[pos] + (s - nv)];
-        rp.part_al[2 * (uint64_t)ch + (s - nv)] = acc;
+  const uint64_t total = (uint64_t)p.n * nv;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total; t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t i = (uint32_t)(t / nv), s = (uint32_t)(t % nv);
+    vbuf[t] = vvalue(p, i, s >> 1, s & 1);
+  }
+}
+
+// sum over positions [b, e) of rows it(pos): slot s < nv from vals, slots nv, nv+1 from al
+template <typename ItemFn>
+__device__ __forceinline__ void warp_sum_rows(uint32_t lane, uint32_t nv, uint32_t b, uint32_t e, ItemFn item,
+                                              const double *__restrict__ vals, const uint64_t *__restrict__ al,
+                                              double *__restrict__ out_v, uint64_t *__restrict__ out_al) {
+  for (uint32_t s = lane; s < nv + 2; s += 32) {
+    if (s < nv) {
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      uint32_t pos = b;
+      for (; pos + 4 <= e; pos += 4) {
+        const double x0 = vals[(uint64_t)item(pos) * nv + s], x1 = vals[(uint64_t)item(pos + 1) * nv + s];
+        const double x2 = vals[(uint64_t)item(pos + 2) * nv + s], x3 = vals[(uint64_t)item(pos + 3) * nv + s];
+        a0 = __dadd_rn(a0, x0);
+        a1 = __dadd_rn(a1, x1);
+        a2 = __dadd_rn(a2, x2);
+        a3 = __dadd_rn(a3, x3);
       }
+      for (; pos < e; ++pos) a0 = __dadd_rn(a0, vals[(uint64_t)item(pos) * nv + s]);
+      out_v[s] = __dadd_rn(__dadd_rn(a0, a1), __dadd_rn(a2, a3));
+    } else {
+      uint64_t acc = 0;
+      for (uint32_t pos = b; pos < e; ++pos) acc += al[2 * (uint64_t)item(pos) + (s - nv)];
+      out_al[s - nv] = acc;
     }
   }
 }
 
-__global__ void k_rollup_segments(uint32_t nv, const double *__restrict__ in_v,
-                                  const uint64_t *__restrict__ in_al, const uint32_t *__restrict__ perm,
-                                  const uint32_t *__restrict__ seg_begin, const uint32_t *__restrict__ seg_end,
-                                  uint32_t n_seg, double *__restrict__ out_v, uint64_t *__restrict__ out_al) {
+__global__ void __launch_bounds__(128) k_rollup_chunks(RollupPlan rp, uint32_t nv, const double *__restrict__ vbuf,
+                                                       const uint64_t *__restrict__ AL) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t ch = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; ch < rp.n_chunks; ch += warps) {
+    const uint32_t *order = rp.order;
+    warp_sum_rows(lane, nv, rp.chunk_begin[ch], rp.chunk_end[ch], [order](uint32_t pos) { return order[pos]; },
+                  vbuf, AL, rp.part_v + (uint64_t)ch * nv, rp.part_al + 2 * (uint64_t)ch);
+  }
+}
+
+__global__ void __launch_bounds__(128) k_rollup_segments(uint32_t nv, const double *__restrict__ in_v,
+                                                         const uint64_t *__restrict__ in_al,
+                                                         const uint32_t *__restrict__ perm,
+                                                         const uint32_t *__restrict__ seg_begin,
+                                                         const uint32_t *__restrict__ seg_end, uint32_t n_seg,
+                                                         double *__restrict__ out_v, uint64_t *__restrict__ out_al) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t sg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; sg < n_seg; sg += warps) {
-    const uint32_t b = seg_begin[sg], e = seg_end[sg];
-    for (uint32_t s = lane; s < nv + 2; s += 32) {
-      if (s < nv) {
-        double acc = 0.0;
-        for (uint32_t pos = b; pos < e; ++pos) {
-          const uint32_t it = perm ? perm[pos] : pos;
-          acc = __dadd_rn(acc, in_v[(uint64_t)it * nv + s]);
-        }
-        out_v[(uint64_t)sg * nv + s] = acc;
-      } else {
-        uint64_t acc = 0;
-        for (uint32_t pos = b; pos < e; ++pos) {
-          const uint32_t it = perm ? perm[pos] : pos;
-          acc += in_al[2 * (uint64_t)it + (s - nv)];
-        }
-        out_al[2 * (uint64_t)sg + (s - nv)] = acc;
-      }
-    }
+    if (perm)
+      warp_sum_rows(lane, nv, seg_begin[sg], seg_end[sg], [perm](uint32_t pos) { return perm[pos]; }, in_v, in_al,
+                    out_v + (uint64_t)sg * nv, out_al + 2 * (uint64_t)sg);
+    else
+      warp_sum_rows(lane, nv, seg_begin[sg], seg_end[sg], [](uint32_t pos) { return pos; }, in_v, in_al,
+                    out_v + (uint64_t)sg * nv, out_al + 2 * (uint64_t)sg);
   }
 }
 
@@ -71,16 +92,25 @@ inline uint32_t warp_grid(uint64_t warps, int n_sms) {
 
 }  // namespace
 
+cudaError_t launch_vrows(const DevProgram &p, double *vbuf, int n_sms, cudaStream_t s) {
+  const uint64_t total = (uint64_t)p.n * 2 * p.ncol;
+  const uint32_t g = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, (uint64_t)n_sms * 32));
+  k_vrows<<<g, 256, 0, s>>>(p, vbuf);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_rollup(const DevProgram &p, const RollupPlan &rp, int n_sms, cudaStream_t s,
                           uint64_t *launches) {
   const uint32_t nv = 2 * p.ncol;
-  if (rp.n_chunks) k_rollup_chunks<<<warp_grid(rp.n_chunks, n_sms), 128, 0, s>>>(p, rp);
+  cudaError_t e = launch_vrows(p, rp.vbuf, n_sms, s);
+  if (e != cudaSuccess) return e;
+  if (rp.n_chunks) k_rollup_chunks<<<warp_grid(rp.n_chunks, n_sms), 128, 0, s>>>(rp, nv, rp.vbuf, p.AL);
   k_rollup_segments<<<warp_grid(rp.n_seg1, n_sms), 128, 0, s>>>(
       nv, rp.part_v, rp.part_al, nullptr, rp.seg1_begin, rp.seg1_end, rp.n_seg1, rp.rows_v, rp.rows_al);
   k_rollup_segments<<<warp_grid(rp.n_seg2, n_sms), 128, 0, s>>>(
       nv, rp.rows_v, rp.rows_al, rp.seg2_perm, rp.seg2_begin, rp.seg2_end, rp.n_seg2,
       rp.rows_v + (uint64_t)rp.n_seg1 * nv, rp.rows_al + 2 * (uint64_t)rp.n_seg1);
-  *launches += rp.n_chunks ? 3 : 2;
+  *launches += rp.n_chunks ? 4 : 3;
   return cudaGetLastError();
 }
 

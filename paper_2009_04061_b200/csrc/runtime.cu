@@ -277,10 +277,11 @@ struct Offsets {
   size_t opclass, iflags, latency, line_id, loop_id, func_begin, kfb, kgb, row_ptr, edge_def, edge_min,
       edge_max, edge_use, edge_dom, edge_lca, edge_kind, def_ptr, def_perm;
   size_t order, chunk_begin, chunk_end, seg1_begin, seg1_end, seg2_perm, seg2_begin, seg2_end, part_v,
-      part_al, rows_v, rows_al;
+      part_al, rows_v, rows_al, vbuf;
   size_t pats, mval, mrow, loop_items, loop_item_ptr, pre_perm, pre_begin, pre_end, kloop_ptr, kloops,
       loop_func, lM_excl, lM_incl, fM, kM, est;
-  size_t C, stats, AL, cand, selfm, share, B, partials;
+  size_t C, stats, AL, cand, selfm, share, B, partials, part_x, part_n, part_sync;
+  bool part_reserved = false;
   size_t total;
 };
 
@@ -298,6 +299,14 @@ Offsets layout(const gpa_program_desc *d, const HostPlan &h) {
   o.share = a.take(E * 3 * 8);
   o.B = a.take(n * 8 * 8);
   o.partials = (n * 2 * R * 4 <= kSmemTableMax) ? a.take((size_t)kMaxIngestCtas * n * 2 * R * 4) : a.take(0);
+  {
+    const bool part = n * 2 * R * 4 > kSmemTableMax && n <= (size_t)kPartMaxCtas * 4095;
+    const size_t pairs = (size_t)kPartBufs * kPartMaxCtas * kPartMaxCtas;
+    o.part_x = a.take(part ? pairs * kPartCap * 4 : 0);
+    o.part_n = a.take(part ? pairs * 4 : 0);
+    o.part_sync = a.take(part ? 64 : 0);
+    o.part_reserved = part;
+  }
   o.opclass = a.take(n);
   o.iflags = a.take(n);
   o.latency = a.take(n * 4);
@@ -328,6 +337,7 @@ Offsets layout(const gpa_program_desc *d, const HostPlan &h) {
   o.part_al = a.take(h.chunk_begin.size() * 2 * 8);
   o.rows_v = a.take((size_t)h.n_rows * 2 * ncol * 8);
   o.rows_al = a.take((size_t)h.n_rows * 2 * 8);
+  o.vbuf = a.take(n * 2 * ncol * 8);
   o.pats = a.take(kPatWs * sizeof(gpa_pattern));
   o.mval = a.take((size_t)kLoopPatWs * (E + n) * 8);
   o.mrow = a.take((size_t)kPatWs * n * 8);
@@ -460,6 +470,7 @@ gpa_status gpa_program_create(const gpa_program_desc *d, void *d_workspace, size
   DP(C, uint64_t *, C); DP(stats, uint64_t *, stats); DP(AL, uint64_t *, AL);
   DP(cand, uint8_t *, cand); DP(selfm, uint8_t *, selfm); DP(share, double *, share);
   DP(B, double *, B); DP(partials, uint32_t *, partials);
+  DP(part_x, uint32_t *, part_x); DP(part_n, uint32_t *, part_n); DP(part_sync, unsigned int *, part_sync);
 #undef DP
   RollupPlan &rp = p->rp;
   rp.order = (const uint32_t *)(ws + o.order);
@@ -477,6 +488,7 @@ gpa_status gpa_program_create(const gpa_program_desc *d, void *d_workspace, size
   rp.n_seg2 = (uint32_t)h.seg2_begin.size();
   rp.rows_v = (double *)(ws + o.rows_v);
   rp.rows_al = (uint64_t *)(ws + o.rows_al);
+  rp.vbuf = (double *)(ws + o.vbuf);
   EstimatePlan &ep = p->ep;
   ep.pats = (const gpa_pattern *)(ws + o.pats);
   p->pats_dev = (gpa_pattern *)(ws + o.pats);
@@ -522,8 +534,11 @@ gpa_status gpa_program_create(const gpa_program_desc *d, void *d_workspace, size
   setv(GPA_VIEW_KERNEL_AL, o.rows_al + r_kern * rowal, d->n_kernels * rowal);
   setv(GPA_VIEW_ESTIMATES, o.est, 0);
 
-  // ingest variant: CTA-private shared-memory table when it fits, else L2 atomics
-  p->variant = ingest_smem_bytes(dp) <= p->smem_optin ? VAR_SMEM : VAR_L2;
+  // ingest variant: CTA-private shared-memory table when it fits, else the partitioned
+  // (bucket-exchange) kernel when its constraints hold, else L2 atomics
+  p->variant = VAR_SMEM;
+  p->part_ok = o.part_reserved && part_feasible(dp, p->n_sms, p->smem_optin);
+  if (ingest_smem_bytes(dp) > std::min(p->smem_optin, kSmemTableMax)) p->variant = p->part_ok ? VAR_PART : VAR_L2;
   *out = p;
   return GPA_OK;
 }
@@ -561,7 +576,7 @@ gpa_status gpa_ingest_samples(gpa_program *p, const gpa_sample *d_samples, uint6
   if (((uintptr_t)d_samples & 7u) != 0) return fail(GPA_ERR_INVALID_ARGUMENT, "d_samples not 8-byte aligned");
   cudaError_t e = launch_ingest(p->d, p->variant, d_samples, n, p->n_sms, p->smem_optin, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "ingest launch");
-  p->launches += (p->variant == VAR_SMEM) ? 2 : 1;
+  p->launches += (p->variant == VAR_L2) ? 1 : 2;
   p->state = (p->state | ST_COUNTS) & ~(ST_BLAMED | ST_AGGREGATED);
   return GPA_OK;
 }
@@ -693,7 +708,7 @@ gpa_status gpa_instr_vector(gpa_program *p, double *d_out, void *stream) {
   if (st) return st;
   if (!d_out) return fail(GPA_ERR_INVALID_ARGUMENT, "d_out is NULL");
   if (!(p->state & ST_BLAMED)) return fail(GPA_ERR_BAD_STATE, "gpa_instr_vector before gpa_blame");
-  cudaError_t e = launch_instr_vector(p->d, d_out, (cudaStream_t)stream);
+  cudaError_t e = launch_vrows(p->d, d_out, p->n_sms, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "instr vector launch");
   return GPA_OK;
 }
@@ -720,8 +735,10 @@ gpa_status gpa_set_ingest_variant(gpa_program *p, int variant) {
   gpa_status st = check_prog(p);
   if (st) return st;
   if (variant < 0 || variant > VAR_L2) return fail(GPA_ERR_INVALID_ARGUMENT, "variant %d unknown", variant);
-  if (variant == VAR_SMEM && ingest_smem_bytes(p->d) > p->smem_optin)
+  if (variant == VAR_SMEM && ingest_smem_bytes(p->d) > std::min(p->smem_optin, kSmemTableMax))
     return fail(GPA_ERR_INVALID_ARGUMENT, "count table does not fit shared memory");
+  if (variant == VAR_PART && !p->part_ok)
+    return fail(GPA_ERR_INVALID_ARGUMENT, "partitioned ingest not applicable to this program");
   p->variant = variant;
   return GPA_OK;
 }

@@ -55,14 +55,45 @@ def test_config2_rodinia(variant):
     compare(run_gpu(prog, recs, variant=variant), o, rel=REL)
 
 
-def test_config3_large_program_reduced_stream():
-    """Config-3 program (50k instructions, 200 loops) on a 2*10^7-record prefix of its stream."""
+@pytest.fixture(scope="module")
+def config3_case():
     prog = gp.config_program(3)
     recs = config_stream(prog, 3).host(0, 20_000_000)
-    o = run_oracle(prog, recs)
-    g = run_gpu(prog, recs)
-    assert g["program"].variant == "l2"
+    return prog, recs, run_oracle(prog, recs)
+
+
+@pytest.mark.parametrize("variant", [None, "l2"])
+def test_config3_large_program_reduced_stream(config3_case, variant):
+    """Config-3 program (50k instructions, 200 loops) on a 2*10^7-record prefix of its stream;
+    the default ingest for its 3.6 MB table is the partitioned (bucket-exchange) kernel."""
+    prog, recs, o = config3_case
+    g = run_gpu(prog, recs, variant=variant)
+    assert g["program"].variant == (variant or "part")
     compare(g, o, rel=REL)
+
+
+@pytest.mark.parametrize("n_rec,offset", [(1, 0), (2, 1), (4097, 1), (1_212_417, 0), (3_000_001, 1)])
+def test_part_ragged_and_small_streams(n_rec, offset):
+    """Streams shorter than one chunk per CTA, odd lengths and an 8-byte-aligned start."""
+    prog = gp.random_program(5000, 6, 20, 4, seed=31)
+    recs = StreamSpec(prog, seed=32, count_max=9, invalid_ppm=20_000).host(0, n_rec)
+    g = run_gpu(prog, recs, offset_records=offset)
+    assert g["program"].variant == "part"
+    compare(g, run_oracle(prog, recs), rel=REL)
+
+
+def test_part_skewed_stream_overflow():
+    """A hot PC takes half the samples: its bucket overflows the exchange slots and the excess
+    goes through L2 atomics; counts stay exact."""
+    prog = gp.random_program(6000, 6, 20, 4, seed=41)
+    w = prog.pc_weight.copy()
+    w[17] = w.sum()
+    w[4000] = w.sum() / 3
+    prog.pc_weight = w
+    recs = StreamSpec(prog, seed=42, count_max=65535).host(0, 4_000_000)
+    g = run_gpu(prog, recs)
+    assert g["program"].variant == "part"
+    compare(g, run_oracle(prog, recs), rel=REL)
 
 
 def test_host_ingest_equals_device_ingest():
@@ -141,4 +172,4 @@ def test_call_order_errors():
     with pytest.raises(GpaError, match="patterns"):
         P.estimate()
     with pytest.raises(GpaError):
-        P.ingest(torch.zeros(3, dtype=torch.uint8, device="cuda")[1:])   # misaligned pointer
+        P.ingest(torch.zeros(65, dtype=torch.uint8, device="cuda")[1:])  # 8 records, misaligned pointer
