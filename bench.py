@@ -195,7 +195,7 @@ def main():
     counts = P.view("counts")
     stats = P.view("stats")
 
-    def step(ev_a=None, ev_b=None):
+    def step(ev_a=None, ev_b=None, ev_c=None):
         P.reset()
         if ev_a is not None:
             ev_a.record(stream)
@@ -208,6 +208,8 @@ def main():
         P.blame()
         P.aggregate()
         P.estimate()
+        if ev_c is not None:
+            ev_c.record(stream)
 
     if args.profile:
         step()
@@ -222,7 +224,7 @@ def main():
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.3)
-    ing = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    ing = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(args.steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = P.launches
     torch.cuda.synchronize()
@@ -236,7 +238,8 @@ def main():
         dist.barrier()
     clocks = sampler.stop()
     ms = t0.elapsed_time(t1)
-    ingest_ms = sum(a.elapsed_time(b) for a, b in ing) / args.steps
+    ingest_ms = sum(a.elapsed_time(b) for a, b, _ in ing) / args.steps
+    analyze_ms = sum(b.elapsed_time(c) for _, b, c in ing) / args.steps
     if world > 1:
         t = torch.tensor([ms, ingest_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -309,7 +312,8 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": _traffic_from_profile(args.workload),
                          "kernel": "ingest", "peak_kind": peak_kind, "alg_bytes_per_launch": alg_bytes,
-                         "ingest_ms": ingest_ms, "ingest_share_of_step": ingest_ms / ms_per_step},
+                         "ingest_ms": ingest_ms, "ingest_share_of_step": ingest_ms / ms_per_step,
+                         "blame_rollup_estimate_ms": analyze_ms},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)

@@ -2,7 +2,7 @@
 // P:457-460) and the estimators of §5.2: Eq. 2, Eq. 3, Eq. 4
 // (P:496-503), Eq. 5 (Q16), Eqs. 6-10 (Q18), per kernel.
 //
-//   k_est_rows    one thread per use row j: for every pattern, the matched samples of each
+//   k_est_rows    one thread per (use row j, pattern): the matched samples of each
 //                 in-edge (blamed at the def, scope loop = lca(def, use)) and of j itself
 //                 (self / pass-through columns, scope loop = loop of j); row totals mrow[q][j]
 //                 and, for loop-scoped patterns, per-item values for the loop reduction.
@@ -28,69 +28,59 @@ __device__ __forceinline__ bool passes(const gpa_pattern &q, uint32_t cls, uint3
   return ((q.class_mask >> cls) & 1u) && (!q.flag_filter || (flags & q.flag_filter));
 }
 
-constexpr int kPatRows = 16;   // patterns evaluated per row pass (gpa_set_patterns allows 16)
-
+// one thread per (use row j, pattern q), pattern-major so a warp shares q (uniform control flow)
 __global__ void k_est_rows(DevProgram p, EstimatePlan ep) {
   __shared__ gpa_pattern sp[kPatternsMax];
   for (uint32_t q = threadIdx.x; q < ep.n_pat; q += blockDim.x) sp[q] = ep.pats[q];
   __syncthreads();
-  const uint32_t np = ep.n_pat;
   const uint64_t stride_items = (uint64_t)p.E + p.n;
-  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < p.n; j += gridDim.x * blockDim.x) {
-    const uint64_t *row = p.C + (uint64_t)j * 2 * p.R;
-    uint64_t lat[4], all[4];
-#pragma unroll
-    for (int r = 1; r <= 3; ++r) {
-      lat[r] = row[p.R + r];
-      all[r] = row[r] + lat[r];
+  const uint32_t rows_pad = (p.n + 31) & ~31u;
+  const uint64_t total = (uint64_t)rows_pad * ep.n_pat;
+  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total; t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t qi = (uint32_t)(t / rows_pad), j = (uint32_t)(t % rows_pad);
+    if (j >= p.n) continue;
+    const gpa_pattern &q = sp[qi];
+    const int slot = ep.loop_slot[qi];
+    if (q.model == 5) {
+      ep.mrow[(uint64_t)qi * p.n + j] = 0.0;
+      continue;
     }
+    const uint64_t *row = p.C + (uint64_t)j * 2 * p.R;
+    const bool L = q.sample_class != 0;
+    double X[4];
+#pragma unroll
+    for (int r = 1; r <= 3; ++r) X[r] = (double)(row[p.R + r] + (L ? 0ull : row[r]));
     const uint32_t e0 = p.row_ptr[j], e1 = p.row_ptr[j + 1];
     const int32_t loop_j = p.loop_id[j];
-    double sum[kPatRows];
-#pragma unroll
-    for (int q = 0; q < kPatRows; ++q) sum[q] = 0.0;
+    double sum = 0.0;
     for (uint32_t e = e0; e < e1; ++e) {
       const uint32_t m = p.cand[e];
       const uint32_t d = p.edge_def[e];
-      const uint32_t cls = p.opclass[d], fl = p.iflags[d], kind = p.edge_kind[e];
-      const bool same = p.loop_id[d] >= 0 && p.loop_id[d] == loop_j;
-      const double sh1 = p.share[3 * (uint64_t)e], sh2 = p.share[3 * (uint64_t)e + 1], sh3 = p.share[3 * (uint64_t)e + 2];
-      const uint32_t c1 = classify(R_MEM, cls, kind), c2 = classify(R_EXEC, cls, kind), c3 = COL_SYNC;
-#pragma unroll
-      for (int qi = 0; qi < kPatRows; ++qi) {
-        if (qi >= (int)np) break;
-        const gpa_pattern &q = sp[qi];
-        double me = 0.0;
-        if (m && q.model != 5 && passes(q, cls, fl) && (!q.same_loop || same)) {
-          const bool L = q.sample_class != 0;
-          if ((m & 1u) && ((q.column_mask >> c1) & 1u)) me = __dadd_rn(me, __dmul_rn((double)(L ? lat[1] : all[1]), sh1));
-          if ((m & 2u) && ((q.column_mask >> c2) & 1u)) me = __dadd_rn(me, __dmul_rn((double)(L ? lat[2] : all[2]), sh2));
-          if ((m & 4u) && ((q.column_mask >> c3) & 1u)) me = __dadd_rn(me, __dmul_rn((double)(L ? lat[3] : all[3]), sh3));
+      double me = 0.0;
+      if (m) {
+        const uint32_t cls = p.opclass[d];
+        if (passes(q, cls, p.iflags[d]) && (!q.same_loop || (p.loop_id[d] >= 0 && p.loop_id[d] == loop_j))) {
+          const uint32_t kind = p.edge_kind[e];
+          const double *sh = p.share + 3 * (uint64_t)e;
+          if ((m & 1u) && ((q.column_mask >> classify(R_MEM, cls, kind)) & 1u)) me = __dadd_rn(me, __dmul_rn(X[1], sh[0]));
+          if ((m & 2u) && ((q.column_mask >> classify(R_EXEC, cls, kind)) & 1u)) me = __dadd_rn(me, __dmul_rn(X[2], sh[1]));
+          if ((m & 4u) && ((q.column_mask >> COL_SYNC) & 1u)) me = __dadd_rn(me, __dmul_rn(X[3], sh[2]));
         }
-        sum[qi] = __dadd_rn(sum[qi], me);
-        const int slot = ep.loop_slot[qi];
-        if (slot >= 0) ep.mval[(uint64_t)slot * stride_items + e] = me;
       }
+      if (slot >= 0) ep.mval[(uint64_t)slot * stride_items + e] = me;
+      sum = __dadd_rn(sum, me);
     }
-    const uint32_t cls_j = p.opclass[j], fl_j = p.iflags[j], self_j = p.selfm[j];
-#pragma unroll
-    for (int qi = 0; qi < kPatRows; ++qi) {
-      if (qi >= (int)np) break;
-      const gpa_pattern &q = sp[qi];
-      double mi = 0.0;
-      if (q.model != 5 && passes(q, cls_j, fl_j) && (!q.same_loop || loop_j >= 0)) {
-        const bool L = q.sample_class != 0;
-        for (uint32_t r = R_MEM; r <= R_SYNC; ++r)
-          if (((self_j >> (r - 1)) & 1u) && ((q.column_mask >> (COL_MEM_SELF + r - 1)) & 1u))
-            mi = __dadd_rn(mi, (double)(L ? lat[r] : all[r]));
-        for (uint32_t r = 4; r < p.R; ++r)
-          if ((q.column_mask >> (COL_PASS0 + r - 4)) & 1u)
-            mi = __dadd_rn(mi, (double)(row[p.R + r] + (L ? 0ull : row[r])));
-      }
-      const int slot = ep.loop_slot[qi];
-      if (slot >= 0) ep.mval[(uint64_t)slot * stride_items + p.E + j] = mi;
-      ep.mrow[(uint64_t)qi * p.n + j] = q.model == 5 ? 0.0 : __dadd_rn(sum[qi], mi);
+    double mi = 0.0;
+    if (passes(q, p.opclass[j], p.iflags[j]) && (!q.same_loop || loop_j >= 0)) {
+      const uint32_t self_j = p.selfm[j];
+      for (uint32_t r = R_MEM; r <= R_SYNC; ++r)
+        if (((self_j >> (r - 1)) & 1u) && ((q.column_mask >> (COL_MEM_SELF + r - 1)) & 1u)) mi = __dadd_rn(mi, X[r]);
+      for (uint32_t r = 4; r < p.R; ++r)
+        if ((q.column_mask >> (COL_PASS0 + r - 4)) & 1u)
+          mi = __dadd_rn(mi, (double)(row[p.R + r] + (L ? 0ull : row[r])));
     }
+    if (slot >= 0) ep.mval[(uint64_t)slot * stride_items + p.E + j] = mi;
+    ep.mrow[(uint64_t)qi * p.n + j] = __dadd_rn(sum, mi);
   }
 }
 
@@ -230,7 +220,8 @@ __global__ void k_est_final(DevProgram p, EstimatePlan ep) {
 cudaError_t launch_estimate(const DevProgram &p, const EstimatePlan &ep, int n_sms, cudaStream_t s,
                             uint64_t *launches) {
   const uint32_t threads = 128;
-  const uint32_t g = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((p.n + threads - 1) / threads, (uint64_t)n_sms * 16));
+  const uint64_t work = (uint64_t)((p.n + 31) & ~31u) * ep.n_pat;
+  const uint32_t g = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((work + threads - 1) / threads, (uint64_t)n_sms * 32));
   k_est_rows<<<g, threads, 0, s>>>(p, ep);
   SegLaunch a{};
   a.n_pat = ep.n_pat;

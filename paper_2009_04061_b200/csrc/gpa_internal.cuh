@@ -17,9 +17,9 @@ constexpr int kMaxIngestCtas = 256;         // per-CTA partial tables reserved (
 constexpr size_t kSmemTableMax = 224 * 1024;// largest CTA-private table (bytes; sm_100a opt-in is 227 KB)
 // partitioned ingest (variant P): bucket exchange through L2
 constexpr int kPartThreads = 1024;
-constexpr int kPartChunk = 4096;            // records per CTA per chunk (32 KB, one TMA bulk copy)
-constexpr int kPartBufs = 4;                // exchange buffers in flight
-constexpr int kPartCap = 48;                // keys per (dst, src) slot per chunk (mean 27.7 at G=148);
+constexpr int kPartChunk = 6144;            // records per CTA per chunk (48 KB, one TMA bulk copy)
+constexpr int kPartBufs = 8;                // exchange buffers in flight
+constexpr int kPartCap = 56;                // keys per (dst, src) slot per chunk (mean 41.5 at G=148);
                                             // excess -> L2 atomics
 constexpr int kPartMaxCtas = 160;           // < 255: bucket ids fit a byte
 size_t part_smem_bytes(uint32_t bpb, uint32_t G);
@@ -53,7 +53,7 @@ struct DevProgram {
   const uint32_t *def_ptr, *def_perm;
   uint64_t *C, *stats, *AL;
   uint32_t *partials;               // [kMaxIngestCtas][n*2R] per-CTA tables (smem variant)
-  uint32_t *part_x;                 // [kPartBufs][kPartMaxCtas][kPartMaxCtas][kPartCap] exchange keys
+  uint32_t *part_x;                 // [kPartBufs][kPartMaxCtas dst][G src][kPartCap] 2-byte exchange keys
   uint32_t *part_n;                 // [kPartBufs][kPartMaxCtas][kPartMaxCtas] keys per (dst, src)
   unsigned int *part_sync;          // [2*kPartBufs]: per exchange buffer, CTAs that produced / consumed it
   uint8_t *cand, *selfm;

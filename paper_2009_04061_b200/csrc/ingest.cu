@@ -23,6 +23,9 @@
 //   the L2-resident u64 table.
 #include <algorithm>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "gpa_internal.cuh"
 
 namespace gpa {
@@ -189,15 +192,21 @@ struct PartArgs {
   uint32_t n_instr, R, bins, ppb, bpb;
   uint32_t mg;            // ceil(2^32 / G): pc / G = umulhi(pc, mg), exact for pc < 2^32 / G
   uint64_t *C, *stats;
-  uint32_t *X;            // [kPartBufs][kPartMaxCtas dst][kPartMaxCtas src][kPartCap] keys, 0-padded
+  uint16_t *X;            // [kPartBufs][src < kPartMaxCtas][dst < G][kPartCap] 2-byte keys, zero-padded
   unsigned int *sync;     // [kPartBufs] produced, [kPartBufs] consumed
 };
 
-constexpr int kProdThreads = kPartThreads / 2;    // warps 0-15: partition the record stream
-constexpr int kConsThreads = kPartThreads / 2;    // warps 16-31: drain this CTA's bucket
+constexpr int kProdThreads = 3 * kPartThreads / 4;  // warps 0-23: partition the record stream
+constexpr int kConsThreads = kPartThreads / 4;      // warps 24-31: drain this CTA's bucket
 constexpr int kProdRecs = kPartChunk / kProdThreads;   // records per producer thread per chunk
-constexpr int kRing = 4;                           // TMA ring depth (chunks in flight per CTA)
-constexpr int kConsVec = (kPartMaxCtas * kPartCap / 4 + kConsThreads - 1) / kConsThreads;  // uint4 per thread
+constexpr int kRing = 2;                           // TMA ring depth (input chunks)
+constexpr int kInbox = 3;                          // consumer inbox depth (exchange chunks)
+constexpr int kTrash = 32;                         // lane-distinct sink for dropped keys / padding
+constexpr uint32_t kLocalBits = 13;                // key = local bin (13 bits) | count (3 bits)
+constexpr uint32_t kMaxKeyCount = 7;
+constexpr uint64_t kWrapGuard = (uint64_t)kPartMaxCtas * kPartCap * kMaxKeyCount;   // max samples per chunk
+static_assert(kPartChunk % (2 * kProdThreads) == 0, "whole record pairs per producer thread");
+static_assert((kPartCap * 2) % 16 == 0, "slots must be whole 16-byte units for bulk copies");
 
 __device__ __forceinline__ void named_bar(uint32_t id, uint32_t threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
@@ -217,7 +226,6 @@ __device__ __forceinline__ void tma_bulk_load_ef(void *dst, const void *src, uin
       "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
       : "memory");
 }
-
 // shared -> global bulk copy (async proxy), tracked by this thread's bulk async-groups
 __device__ __forceinline__ void tma_bulk_store(void *gdst, const void *ssrc, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_addr(ssrc)),
@@ -225,28 +233,41 @@ __device__ __forceinline__ void tma_bulk_store(void *gdst, const void *ssrc, uin
                : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_le1() { asm volatile("cp.async.bulk.wait_group 1;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
-__global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a) {
+// 2-D TMA tile load: box {cap keys, G rows} at (x, y) of tensor map *tm -> smem, mbarrier tx
+__device__ __forceinline__ void tma_tile_load_2d(void *dst, const CUtensorMap *tm, uint32_t x, uint32_t y,
+                                                 uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_addr(dst)),
+      "l"(tm), "r"(x), "r"(y), "r"(smem_addr(bar))
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, const __grid_constant__ CUtensorMap xmap) {
   extern __shared__ __align__(128) uint8_t sm[];
-  const uint32_t tid = threadIdx.x, lane = tid & 31;
+  const uint32_t tid = threadIdx.x;
   const uint32_t G = gridDim.x, me = blockIdx.x;
-  const uint32_t slot_keys = G * kPartCap;                                       // one staging buffer
+  const uint32_t slot_keys = G * kPartCap;                                       // keys per staging / inbox buffer
   uint2 *ring = reinterpret_cast<uint2 *>(sm);                                   // [kRing][chunk] records
-  uint32_t *stag = reinterpret_cast<uint32_t *>(sm + kRing * kPartChunk * 8);  // [2][G][cap] keys
-  uint32_t *cnt = stag + 2 * slot_keys;                                         // [kPartMaxCtas]
-  uint64_t *bars = reinterpret_cast<uint64_t *>(cnt + kPartMaxCtas);            // [kRing]
-  uint32_t *tab = reinterpret_cast<uint32_t *>(bars + kRing);                   // [bpb]
-  (void)lane;
-  for (uint32_t i = tid; i < a.bpb; i += kPartThreads) tab[i] = 0;
-  for (uint32_t i = tid; i < 2 * slot_keys; i += kPartThreads) stag[i] = 0;
-  for (uint32_t i = tid; i < kPartMaxCtas; i += kPartThreads) cnt[i] = 0;
+  const uint32_t ibuf_keys = ((slot_keys * 2 + 127) & ~127u) / 2;             // inbox buffers 128-B aligned (TMA tile)
+  uint16_t *inbox = reinterpret_cast<uint16_t *>(sm + kRing * kPartChunk * 8); // [kInbox][G src][cap]
+  uint16_t *stag = inbox + kInbox * ibuf_keys;                                  // [2][G dst][cap]
+  uint32_t *trash = reinterpret_cast<uint32_t *>(stag + 2 * slot_keys);         // [kTrash]
+  uint32_t *cnt = trash + kTrash;                                                // [kPartMaxCtas + 8]
+  unsigned long long *ctotal = reinterpret_cast<unsigned long long *>(cnt + kPartMaxCtas + 8);   // [2]
+  uint64_t *bars = reinterpret_cast<uint64_t *>(ctotal + 2);                    // [kRing + kInbox]
+  uint32_t *tab = reinterpret_cast<uint32_t *>(bars + kRing + kInbox);          // [bpb + kTrash]
+  for (uint32_t i = tid; i < a.bpb + kTrash; i += kPartThreads) tab[i] = 0;
+  for (uint32_t i = tid; i < slot_keys; i += kPartThreads) reinterpret_cast<uint32_t *>(stag)[i] = 0;   // both buffers
+  for (uint32_t i = tid; i < kPartMaxCtas + 8; i += kPartThreads) cnt[i] = 0;
   if (tid == 0) {
-    for (int r = 0; r < kRing; ++r) mbar_init(&bars[r], 1);
+    for (int r = 0; r < kRing + kInbox; ++r) mbar_init(&bars[r], 1);
+    ctotal[0] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -257,12 +278,22 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a) {
     return start >= a.n_even ? 0u
                              : (uint32_t)(a.n_even - start < (uint64_t)kPartChunk ? a.n_even - start : (uint64_t)kPartChunk);
   };
+  // row (buf, src) of the exchange: G slots of kPartCap keys, one per destination; a producer
+  // writes its row with one bulk store, a consumer reads its column (x = dst * cap) with one
+  // 2-D TMA tile load (tensor map xmap: rows = kPartBufs * kPartMaxCtas, cols = G * cap)
+  auto xrow = [&](uint32_t buf, uint32_t src) -> uint16_t * {
+    return a.X + ((uint64_t)buf * kPartMaxCtas + src) * G * kPartCap;
+  };
+  const uint32_t twoR = 2 * a.R;
   IngestStats st{0, 0, 0};
   if (tid < kProdThreads) {
-    // ======================= producers: TMA ring -> decode + slot-shaped scatter -> bulk stores
-    const uint32_t ptid = tid;
+    // ======================= producers: TMA ring -> decode + slot-shaped scatter (2-byte keys)
+    //                         -> one bulk store of my exchange row; chunk k published during k+1
+    const uint32_t ptid = tid, lane = tid & 31;
     const uint64_t pol = evict_first_policy();
-    const uint32_t n_instr = a.n_instr, R = a.R, twoR = 2 * a.R, mg = a.mg;
+    const uint32_t n_instr = a.n_instr, R = a.R, mg = a.mg;
+    const uint32_t trash_addr = smem_addr(trash + lane);
+    const uint32_t cnt_addr = smem_addr(cnt), stag_addr = smem_addr(stag);
     auto issue = [&](uint32_t k) {
       uint64_t s0;
       const uint32_t len = slice_len(k, s0);
@@ -273,142 +304,132 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a) {
       }
     };
     if (ptid == 0)
-      for (uint32_t k = 0; k < kRing - 1 && k < n_chunks; ++k) issue(k);
+      for (uint32_t k = 0; k + 1 < (uint32_t)kRing && k < n_chunks; ++k) issue(k);
     for (uint32_t k = 0; k < n_chunks; ++k) {
       uint64_t s0;
       const uint32_t len = slice_len(k, s0);
       const uint32_t buf = k % kPartBufs;
-      uint32_t *sg = stag + (k & 1) * slot_keys;
-      if (ptid == 0) {
-        // ring slot (k+3)%4 held chunk k-1, decoded (and released by the barriers) last iteration
-        if (k + kRing - 1 < n_chunks) issue(k + kRing - 1);
-        // exchange buffer k%NBUF is free once every CTA drained chunk k-NBUF
-        if (k >= (uint32_t)kPartBufs) spin_until(&a.sync[kPartBufs + buf], G * (k / kPartBufs));
-      }
+      const uint32_t sg_addr = stag_addr + (k & 1) * slot_keys * 2;
+      if (ptid == 0 && k + kRing - 1 < n_chunks) issue(k + kRing - 1);   // slot held chunk k-1
       if (len) mbar_wait(&bars[k % kRing], (k / kRing) & 1);
-      named_bar(1, kProdThreads);
-      // ---- decode: branchless validity, bucket = pc mod G (interleaved PCs balance the load),
-      //      key = {local bin:16 | count:16}, local bin = (pc / G) * 2R + class * R + reason;
-      //      the key goes straight to position cnt[b]++ of bucket b's zero-padded slot
+      named_bar(1, kProdThreads);   // cnt zeroed and staging buffer k&1 cleared (iteration k-1)
+      // ---- decode + scatter, branch-free: bucket = pc mod G (interleaved PCs balance the load),
+      //      key = local bin (pc / G) * 2R + class * R + reason | count << 13, stored at position
+      //      cnt[b]++ of bucket b's zero-padded slot (invalid records count in the dummy bucket G,
+      //      dropped keys go to a trash word; counts > 7 and slot overflow go through L2 atomics)
       const uint4 *rs = reinterpret_cast<const uint4 *>(ring + (k % kRing) * kPartChunk);
-      uint32_t valid = 0, badr = 0, bads = 0;
+      uint32_t csum = 0, bads = 0, badr = 0;
+      const bool full = len == (uint32_t)kPartChunk;
 #pragma unroll
       for (int u = 0; u < kProdRecs / 2; ++u) {
         const uint32_t pair = u * kProdThreads + ptid;
-        const bool in = 2 * pair < len;   // len is even: both records of the pair or neither
+        const bool in = full || 2 * pair < len;   // len is even: both records of the pair or neither
         const uint4 v = in ? rs[pair] : make_uint4(0xffffffffu, 0, 0xffffffffu, 0);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const uint32_t pc = h ? v.z : v.x, w = h ? v.w : v.y;
-          const uint32_t reason = (w >> 16) & 0xffu, flags = w >> 24, c = w & 0xffffu;
-          const bool ok = pc < n_instr && reason < R && w < 0x2000000u && (w >> 16) != 0x100u;
+          const uint32_t t = w >> 16, reason = t & 0xffu, c = w & 0xffffu;
+          const bool ok = pc < n_instr && reason < R && t < 0x200u && t != 0x100u;
           const uint32_t q = __umulhi(pc, mg), b = pc - q * G;
-          const uint32_t local = q * twoR + flags * R + reason;
-          if (ok) {
-            const uint32_t pos = atomicAdd(&cnt[b], 1u);
-            if (pos < (uint32_t)kPartCap) {
-              sg[b * kPartCap + pos] = __byte_perm(local, w, 0x5410);
-            } else {   // slot overflow (extreme skew): exact via L2 atomics
-              atomicAdd((unsigned long long *)&a.C[((uint64_t)q * G + b) * twoR + flags * R + reason],
-                        (unsigned long long)c);
-            }
-          }
-          valid += ok ? c : 0u;
+          const uint32_t local = q * twoR + (t >> 8) * R + reason;
+          const bool small = c <= kMaxKeyCount;
+          const uint32_t be = ok && small ? b : G;   // invalid, padding, big-count records -> bucket G
+          uint32_t pos;
+          asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(pos) : "r"(cnt_addr + be * 4) : "memory");
+          const bool keep = ok && small && pos < (uint32_t)kPartCap;
+          const uint32_t dst = keep ? sg_addr + (be * kPartCap + pos) * 2 : trash_addr;
+          asm volatile("st.shared.u16 [%0], %1;" ::"r"(dst), "h"((unsigned short)(local | (c << kLocalBits)))
+                       : "memory");
+          if (ok && !keep)   // count > 7 or slot overflow (skew): exact via L2 atomics
+            atomicAdd((unsigned long long *)&a.C[(uint64_t)pc * twoR + (t >> 8) * R + reason], (unsigned long long)c);
+          csum += c;        // padding records have count 0
+          bads += ok ? 0u : c;
           badr += (in && !ok) ? 1u : 0u;
-          bads += (in && !ok) ? c : 0u;
         }
       }
-      st.valid += valid;
-      st.bad_records += badr;
+      st.valid += csum - bads;
       st.bad_samples += bads;
+      st.bad_records += badr;
       // every thread that wrote the staging buffer orders its generic-proxy writes before the
       // async-proxy bulk stores issued after the barrier
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       named_bar(1, kProdThreads);
-      if (ptid < G) {   // one bulk store per destination: slot (dst = ptid, src = me) of buffer k%NBUF
-        const uint64_t slot = ((uint64_t)buf * kPartMaxCtas + ptid) * kPartMaxCtas + me;
-        tma_bulk_store(a.X + slot * kPartCap, sg + ptid * kPartCap, kPartCap * 4);
+      if (ptid == 0) {
+        // exchange buffer k%NBUF is free once every CTA drained chunk k-NBUF
+        if (k >= (uint32_t)kPartBufs) spin_until(&a.sync[kPartBufs + buf], G * (k / kPartBufs));
+        tma_bulk_store(xrow(buf, me), stag + (k & 1) * slot_keys, slot_keys * 2);   // my row, all G slots
         bulk_commit();
-        cnt[ptid] = 0;
-        if (k > 0) {      // chunk k-1's stores are now complete (global writes and smem reads)
-          bulk_wait_le1();
+        if (k > 0) {   // chunk k-1's store (one iteration ago) is complete: publish it
+          asm volatile("cp.async.bulk.wait_group 1;" ::: "memory");
           fence_proxy_async_global();
-        }
-      }
-      named_bar(1, kProdThreads);
-      if (k > 0) {
-        if (ptid == 0) {
           __threadfence();
           atomicAdd(&a.sync[(k - 1) % kPartBufs], 1u);   // this CTA produced chunk k-1
         }
-        uint4 *old = reinterpret_cast<uint4 *>(stag + ((k - 1) & 1) * slot_keys);   // re-zero for chunk k+1
-        for (uint32_t i = ptid; i < slot_keys / 4; i += kProdThreads) old[i] = make_uint4(0, 0, 0, 0);
+      }
+      named_bar(1, kProdThreads);   // chunk k-1's staging buffer is free again
+      for (uint32_t i = ptid; i <= G; i += kProdThreads) cnt[i] = 0;
+      if (k + 1 < n_chunks) {   // clear the buffer chunk k+1 will use (it held chunk k-1)
+        uint4 *z = reinterpret_cast<uint4 *>(stag + ((k + 1) & 1) * slot_keys);
+        for (uint32_t i = ptid; i < slot_keys / 8; i += kProdThreads) z[i] = make_uint4(0, 0, 0, 0);
       }
     }
-    if (n_chunks) {
-      if (ptid < G) {
-        bulk_wait_all();
-        fence_proxy_async_global();
-      }
-      named_bar(1, kProdThreads);
-      if (ptid == 0) {
-        __threadfence();
-        atomicAdd(&a.sync[(n_chunks - 1) % kPartBufs], 1u);
-      }
+    if (n_chunks && ptid == 0) {
+      bulk_wait_all();
+      fence_proxy_async_global();
+      __threadfence();
+      atomicAdd(&a.sync[(n_chunks - 1) % kPartBufs], 1u);
     }
   } else {
-    // ======================= consumers: my bucket's slot row (contiguous, L2) -> table
+    // ======================= consumers: my column of the exchange buffer -> smem inbox (one 2-D
+    //                         TMA tile load per chunk, kInbox deep) -> table
     const uint32_t ctid = tid - kProdThreads;
-    const uint32_t nvec = slot_keys / 4;
-    auto wait_chunk = [&](uint32_t j) {
-      if (ctid == 0) spin_until(&a.sync[j % kPartBufs], G * (j / kPartBufs + 1));
-      named_bar(2, kConsThreads);
+    const uint32_t tab_addr = smem_addr(tab), dummy_addr = smem_addr(tab + a.bpb + (ctid & 31));
+    uint64_t *ibars = bars + kRing;
+    auto fetch = [&](uint32_t j) {   // ctid 0: wait for chunk j everywhere, then load my column
+      spin_until(&a.sync[j % kPartBufs], G * (j / kPartBufs + 1));
+      fence_proxy_async_global();
+      mbar_expect_tx(&ibars[j % kInbox], slot_keys * 2);
+      tma_tile_load_2d(inbox + (j % kInbox) * ibuf_keys, &xmap, me * kPartCap, (j % kPartBufs) * kPartMaxCtas,
+                       &ibars[j % kInbox]);
     };
-    auto load_chunk = [&](uint32_t j, uint4 (&r)[kConsVec]) {
-      const uint4 *row = reinterpret_cast<const uint4 *>(
-          a.X + ((uint64_t)(j % kPartBufs) * kPartMaxCtas + me) * kPartMaxCtas * kPartCap);
-#pragma unroll
-      for (int u = 0; u < kConsVec; ++u) {
-        const uint32_t idx = ctid + u * kConsThreads;
-        r[u] = idx < nvec ? __ldcg(row + idx) : make_uint4(0, 0, 0, 0);
-      }
-    };
-    auto add_key = [&](uint32_t kk) {
-      const uint32_t c = kk >> 16;
-      if (c) {
-        const uint32_t lb = kk & 0xffffu;
-        const uint32_t old = atomicAdd(&tab[lb], c);
-        if (old > 0xffffffffu - c)
-          atomicAdd((unsigned long long *)&a.C[((uint64_t)(lb / (2 * a.R)) * G + me) * (2 * a.R) + lb % (2 * a.R)],
-                    1ull << 32);   // u32 wrap
-      }
-    };
-    uint4 cur[kConsVec], nxt[kConsVec];
-    if (n_chunks) {
-      wait_chunk(0);
-      load_chunk(0, cur);
-    }
+    if (ctid == 0)
+      for (uint32_t j = 0; j + 1 < (uint32_t)kInbox && j < n_chunks; ++j) fetch(j);
     for (uint32_t j = 0; j < n_chunks; ++j) {
-      if (j + 1 < n_chunks) {
-        wait_chunk(j + 1);
-        load_chunk(j + 1, nxt);
+      if (ctid == 0 && j + kInbox - 1 < n_chunks) fetch(j + kInbox - 1);   // inbox slot freed at end of j-1
+      mbar_wait(&ibars[j % kInbox], (j / kInbox) & 1);
+      const uint4 *in4 = reinterpret_cast<const uint4 *>(inbox + (j % kInbox) * ibuf_keys);
+      uint32_t tot = 0;
+      for (uint32_t v = ctid; v < slot_keys / 8; v += kConsThreads) {
+        const uint4 kv = in4[v];
+        const uint32_t w4[4] = {kv.x, kv.y, kv.z, kv.w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const uint32_t key = (w4[e >> 1] >> ((e & 1) * 16)) & 0xffffu;
+          const uint32_t c = key >> kLocalBits;
+          const uint32_t addr = c ? tab_addr + (key & ((1u << kLocalBits) - 1)) * 4 : dummy_addr;   // padding -> dummy
+          asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(c) : "memory");
+          tot += c;
+        }
       }
 #pragma unroll
-      for (int u = 0; u < kConsVec; ++u) {
-        add_key(cur[u].x);
-        add_key(cur[u].y);
-        add_key(cur[u].z);
-        add_key(cur[u].w);
-      }
-      named_bar(2, kConsThreads);
+      for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+      if ((ctid & 31) == 0) atomicAdd(&ctotal[0], (unsigned long long)tot);
+      named_bar(2, kConsThreads);   // inbox slot j%kInbox fully read
       if (ctid == 0) atomicAdd(&a.sync[kPartBufs + j % kPartBufs], 1u);   // this CTA drained chunk j
-#pragma unroll
-      for (int u = 0; u < kConsVec; ++u) cur[u] = nxt[u];
+      if (ctotal[0] + kWrapGuard >= 0xffffffffull) {   // rare: flush the table to global and restart
+        for (uint32_t i = ctid; i < a.bpb; i += kConsThreads) {
+          const uint32_t bin = ((i / twoR) * G + me) * twoR + i % twoR;
+          if (tab[i]) atomicAdd((unsigned long long *)&a.C[bin], (unsigned long long)tab[i]);
+          tab[i] = 0;
+        }
+        named_bar(2, kConsThreads);
+        if (ctid == 0) ctotal[0] = 0;
+        named_bar(2, kConsThreads);
+      }
     }
   }
   __syncthreads();
   flush_stats(st, a.stats);
-  const uint32_t twoR = 2 * a.R;
   for (uint32_t i = tid; i < a.bpb; i += kPartThreads) {
     const uint32_t bin = ((i / twoR) * G + me) * twoR + i % twoR;   // local (pc/G, class, reason) -> bin
     if (bin < a.bins && tab[i]) atomicAdd((unsigned long long *)&a.C[bin], (unsigned long long)tab[i]);
@@ -438,9 +459,30 @@ __global__ void k_ingest_edges(const uint2 *rec, uint64_t n_rec, uint32_t head, 
 
 }  // namespace
 
+// 2-D view of the exchange buffers for the consumers' column loads: element = 2-byte key,
+// cols = G * cap (one row = a producer's G slots), rows = kPartBufs * kPartMaxCtas, box = {cap, G}
+static cudaError_t make_exchange_map(CUtensorMap *tm, void *X, uint32_t G) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn) return cudaErrorNotSupported;
+    encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }
+  const cuuint64_t dims[2] = {(cuuint64_t)G * kPartCap, (cuuint64_t)kPartBufs * kPartMaxCtas};
+  const cuuint64_t strides[1] = {(cuuint64_t)G * kPartCap * 2};
+  const cuuint32_t box[2] = {(cuuint32_t)kPartCap, G};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, X, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
 size_t part_smem_bytes(uint32_t bpb, uint32_t G) {
-  return (size_t)kRing * kPartChunk * 8 + (size_t)2 * G * kPartCap * 4 + kPartMaxCtas * 4 + kRing * 8 +
-         (size_t)bpb * 4;
+  return (size_t)kRing * kPartChunk * 8 + (size_t)kInbox * ((G * kPartCap * 2 + 127) & ~127u) +
+         (size_t)2 * G * kPartCap * 2 + kTrash * 4 + (kPartMaxCtas + 8) * 4 + 16 + (kRing + kInbox) * 8 +
+         (size_t)(bpb + kTrash) * 4;
 }
 
 static uint32_t part_grid(int n_sms) { return (uint32_t)std::min(n_sms, kPartMaxCtas); }
@@ -451,7 +493,7 @@ static bool part_shape(const DevProgram &p, int n_sms, uint32_t &G, uint32_t &pp
   G = part_grid(n_sms);
   ppb = (p.n + G - 1) / G;
   bpb = ppb * 2 * p.R;
-  return ppb < 4096 && bpb < 65536;
+  return ppb < 4096 && bpb < (1u << kLocalBits) && G <= 256;   // 2-byte keys: 13-bit local bins; TMA box <= 256
 }
 
 bool part_feasible(const DevProgram &p, int n_sms, size_t smem_optin) {
@@ -502,7 +544,7 @@ cudaError_t launch_ingest(const DevProgram &p, int variant, const void *records,
     a.mg = (uint32_t)(((1ull << 32) + G - 1) / G);
     a.C = p.C;
     a.stats = p.stats;
-    a.X = p.part_x;
+    a.X = reinterpret_cast<uint16_t *>(p.part_x);
     a.sync = p.part_sync;
     const size_t smem = part_smem_bytes(a.bpb, G);
     cudaError_t e = cudaFuncSetAttribute(k_ingest_part, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -515,7 +557,10 @@ cudaError_t launch_ingest(const DevProgram &p, int variant, const void *records,
       if (e != cudaSuccess) return e;
     }
     if (a.n_even == 0) return cudaSuccess;
-    void *args[] = {&a};
+    CUtensorMap xmap;
+    e = make_exchange_map(&xmap, p.part_x, G);
+    if (e != cudaSuccess) return e;
+    void *args[] = {&a, &xmap};
     return cudaLaunchCooperativeKernel((const void *)k_ingest_part, dim3(G), dim3(kPartThreads), args, smem, s);
   }
   return cudaErrorNotSupported;

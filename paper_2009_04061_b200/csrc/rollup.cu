@@ -3,12 +3,13 @@
 //
 // Hand-written segmented reductions (no CUB), deterministic: every sum has a fixed order.
 //   k_vrows            V[i] = {NCOL x (all, lat)} for every instruction, one
-//                      thread per value, written coalesced to a row-major buffer; this is also
-//                      the instruction level of the rollup (gpa_instr_vector).
+//                      warp per (32 instructions, value slot) so control flow is warp-uniform;
+//                      this is also the instruction level of the rollup (gpa_instr_vector).
 //   k_rollup_chunks    one warp per <=128-instruction chunk of a create-time order (line-major |
-//                      loop-major | function ranges); lane s owns value slot s (and s+32) of the
-//                      row, so each member row is one coalesced load; four interleaved
-//                      accumulators keep loads in flight.  Slots NV, NV+1 carry (A_i, L_i).
+//                      loop-major | function ranges); member ids are loaded once and broadcast by
+//                      shuffles, lane s owns value slot s (and s+32) of the row, so each member
+//                      row is one coalesced load and four interleaved accumulators keep loads in
+//                      flight.  Slots NV, NV+1 carry (A_i, L_i).
 //   k_rollup_segments  one warp per segment, same scheme over rows: chunk partials (stage 1:
 //                      lines, loops-exclusive, functions) or earlier rows through a permutation
 //                      (stage 2: loops-inclusive = preorder subtree ranges of the loop-exclusive
@@ -20,12 +21,14 @@
 namespace gpa {
 namespace {
 
+// one warp per (32 instructions, slot): uniform control flow across the warp
 __global__ void k_vrows(DevProgram p, double *__restrict__ vbuf) {
-  const uint32_t nv = 2 * p.ncol;
-  const uint64_t total = (uint64_t)p.n * nv;
-  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total; t += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t i = (uint32_t)(t / nv), s = (uint32_t)(t % nv);
-    vbuf[t] = vvalue(p, i, s >> 1, s & 1);
+  const uint32_t nv = 2 * p.ncol, lane = threadIdx.x & 31;
+  const uint64_t groups = (uint64_t)((p.n + 31) / 32) * nv;
+  const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < groups; w += warps) {
+    const uint32_t s = (uint32_t)(w % nv), i = (uint32_t)(w / nv) * 32 + lane;
+    if (i < p.n) vbuf[(uint64_t)i * nv + s] = vvalue(p, i, s >> 1, s & 1);
   }
 }
 
@@ -56,14 +59,51 @@ __device__ __forceinline__ void warp_sum_rows(uint32_t lane, uint32_t nv, uint32
   }
 }
 
+// chunk of <= 128 members: member ids are loaded once (4 per lane) and broadcast by shuffles, so
+// the row loads of consecutive members are independent and stay in flight together
 __global__ void __launch_bounds__(128) k_rollup_chunks(RollupPlan rp, uint32_t nv, const double *__restrict__ vbuf,
                                                        const uint64_t *__restrict__ AL) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t ch = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; ch < rp.n_chunks; ch += warps) {
-    const uint32_t *order = rp.order;
-    warp_sum_rows(lane, nv, rp.chunk_begin[ch], rp.chunk_end[ch], [order](uint32_t pos) { return order[pos]; },
-                  vbuf, AL, rp.part_v + (uint64_t)ch * nv, rp.part_al + 2 * (uint64_t)ch);
+    const uint32_t b = rp.chunk_begin[ch], len = rp.chunk_end[ch] - b;
+    uint32_t ids[kChunk / 32];
+#pragma unroll
+    for (int t = 0; t < kChunk / 32; ++t) ids[t] = (lane + 32 * t < len) ? rp.order[b + lane + 32 * t] : 0u;
+    for (uint32_t s0 = 0; s0 < nv + 2; s0 += 32) {   // uniform trip count: shuffles need all lanes
+      const uint32_t s = s0 + lane;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      uint64_t al = 0;
+      const bool is_v = s < nv, is_al = s >= nv && s < nv + 2;
+#pragma unroll
+      for (int t = 0; t < kChunk / 32; ++t) {
+        const uint32_t m_end = len > 32u * t ? min(32u, len - 32u * t) : 0u;
+        for (uint32_t m = 0; m < m_end; m += 4) {
+          const uint32_t i0 = __shfl_sync(0xffffffffu, ids[t], m);
+          const uint32_t i1 = __shfl_sync(0xffffffffu, ids[t], m + 1 < 32 ? m + 1 : 31);
+          const uint32_t i2 = __shfl_sync(0xffffffffu, ids[t], m + 2 < 32 ? m + 2 : 31);
+          const uint32_t i3 = __shfl_sync(0xffffffffu, ids[t], m + 3 < 32 ? m + 3 : 31);
+          if (is_v) {
+            const double x0 = vbuf[(uint64_t)i0 * nv + s];
+            const double x1 = m + 1 < m_end ? vbuf[(uint64_t)i1 * nv + s] : 0.0;
+            const double x2 = m + 2 < m_end ? vbuf[(uint64_t)i2 * nv + s] : 0.0;
+            const double x3 = m + 3 < m_end ? vbuf[(uint64_t)i3 * nv + s] : 0.0;
+            a0 = __dadd_rn(a0, x0);
+            a1 = __dadd_rn(a1, x1);
+            a2 = __dadd_rn(a2, x2);
+            a3 = __dadd_rn(a3, x3);
+          } else if (is_al) {
+            const uint32_t c = s - nv;
+            al += AL[2 * (uint64_t)i0 + c];
+            if (m + 1 < m_end) al += AL[2 * (uint64_t)i1 + c];
+            if (m + 2 < m_end) al += AL[2 * (uint64_t)i2 + c];
+            if (m + 3 < m_end) al += AL[2 * (uint64_t)i3 + c];
+          }
+        }
+      }
+      if (is_v) rp.part_v[(uint64_t)ch * nv + s] = __dadd_rn(__dadd_rn(a0, a1), __dadd_rn(a2, a3));
+      else if (is_al) rp.part_al[2 * (uint64_t)ch + (s - nv)] = al;
+    }
   }
 }
 
@@ -93,7 +133,7 @@ inline uint32_t warp_grid(uint64_t warps, int n_sms) {
 }  // namespace
 
 cudaError_t launch_vrows(const DevProgram &p, double *vbuf, int n_sms, cudaStream_t s) {
-  const uint64_t total = (uint64_t)p.n * 2 * p.ncol;
+  const uint64_t total = (uint64_t)((p.n + 31) / 32) * 32 * 2 * p.ncol;
   const uint32_t g = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, (uint64_t)n_sms * 32));
   k_vrows<<<g, 256, 0, s>>>(p, vbuf);
   return cudaGetLastError();

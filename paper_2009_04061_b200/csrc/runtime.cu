@@ -300,7 +300,7 @@ Offsets layout(const gpa_program_desc *d, const HostPlan &h) {
   o.B = a.take(n * 8 * 8);
   o.partials = (n * 2 * R * 4 <= kSmemTableMax) ? a.take((size_t)kMaxIngestCtas * n * 2 * R * 4) : a.take(0);
   {
-    const bool part = n * 2 * R * 4 > kSmemTableMax && n <= (size_t)kPartMaxCtas * 4095;
+    const bool part = n * 2 * R * 4 > kSmemTableMax && n <= (size_t)kPartMaxCtas * 4095;  // see part_feasible
     const size_t pairs = (size_t)kPartBufs * kPartMaxCtas * kPartMaxCtas;
     o.part_x = a.take(part ? pairs * kPartCap * 4 : 0);
     o.part_n = a.take(part ? pairs * 4 : 0);
