@@ -205,9 +205,7 @@ def main():
         if world > 1:
             dist.all_reduce(counts, op=dist.ReduceOp.SUM)
             dist.all_reduce(stats, op=dist.ReduceOp.SUM)
-        P.blame()
-        P.aggregate()
-        P.estimate()
+        P.analyze()          # blame + aggregate + estimate (one CUDA graph of the library's kernels)
         if ev_c is not None:
             ev_c.record(stream)
 
@@ -258,7 +256,7 @@ def main():
         host.copy_(recs)
         est_bytes = P.n_kernels * P.n_patterns * 56
         for _ in range(1):
-            P.reset(); P.ingest_host(host); P.blame(); P.aggregate(); P.estimate(); P.read_estimates()
+            P.reset(); P.ingest_host(host); P.analyze(); P.read_estimates()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -271,9 +269,7 @@ def main():
             if world > 1:
                 dist.all_reduce(counts, op=dist.ReduceOp.SUM)
                 dist.all_reduce(stats, op=dist.ReduceOp.SUM)
-            P.blame()
-            P.aggregate()
-            P.estimate()
+            P.analyze()
             P.read_estimates()
         eb.record(stream)
         torch.cuda.synchronize()

@@ -189,6 +189,11 @@ gpa_status gpa_set_patterns(gpa_program *prog, const gpa_pattern *patterns, uint
  * gpa_aggregate and gpa_set_patterns. */
 gpa_status gpa_estimate(gpa_program *prog, void *stream);
 
+/* gpa_blame + gpa_aggregate + (gpa_estimate when patterns are set) as one CUDA graph, captured
+ * on first use (and again after gpa_set_patterns changes the pattern count), replayed on `stream`
+ * (enqueue).  Same results as the three calls; fewer launch gaps. */
+gpa_status gpa_analyze(gpa_program *prog, void *stream);
+
 /* Copy the estimates to host memory h_out[n_kernels * n_patterns] (synchronizes). */
 gpa_status gpa_read_estimates(gpa_program *prog, gpa_estimate_out *h_out, void *stream);
 

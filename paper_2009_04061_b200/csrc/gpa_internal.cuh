@@ -17,9 +17,9 @@ constexpr int kMaxIngestCtas = 256;         // per-CTA partial tables reserved (
 constexpr size_t kSmemTableMax = 224 * 1024;// largest CTA-private table (bytes; sm_100a opt-in is 227 KB)
 // partitioned ingest (variant P): bucket exchange through L2
 constexpr int kPartThreads = 1024;
-constexpr int kPartChunk = 6144;            // records per CTA per chunk (48 KB, one TMA bulk copy)
+constexpr int kPartChunk = 5888;            // records per CTA per chunk (46 KB, one TMA bulk copy)
 constexpr int kPartBufs = 8;                // exchange buffers in flight
-constexpr int kPartCap = 56;                // keys per (dst, src) slot per chunk (mean 41.5 at G=148);
+constexpr int kPartCap = 56;                // keys per (src, dst) slot per chunk (mean 39.8 at G=148);
                                             // excess -> L2 atomics
 constexpr int kPartMaxCtas = 160;           // < 255: bucket ids fit a byte
 size_t part_smem_bytes(uint32_t bpb, uint32_t G);
@@ -158,4 +158,9 @@ struct gpa_program {
   size_t staging_bytes = 0;
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
+  // blame + aggregate + estimate captured once as a CUDA graph (gpa_analyze)
+  cudaStream_t capture_stream = nullptr;
+  cudaGraphExec_t analyze_exec = nullptr;
+  uint32_t analyze_npat = 0xffffffffu;
+  uint64_t analyze_launches = 0;
 };

@@ -172,9 +172,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_addr(bar)),
-      "r"(parity)
+      "r"(parity), "r"(1000000u)   // suspend-time hint (ns): park the warp instead of spinning
       : "memory");
 }
 __device__ __forceinline__ void spin_until(const unsigned int *ctr, unsigned int target) {
@@ -196,20 +196,30 @@ struct PartArgs {
   unsigned int *sync;     // [kPartBufs] produced, [kPartBufs] consumed
 };
 
-constexpr int kProdThreads = 3 * kPartThreads / 4;  // warps 0-23: partition the record stream
-constexpr int kConsThreads = kPartThreads / 4;      // warps 24-31: drain this CTA's bucket
-constexpr int kProdRecs = kPartChunk / kProdThreads;   // records per producer thread per chunk
+// warp roles of the 1024-thread CTA
+constexpr int kDecodeWarps = 23;                    // warps 0-22: decode + scatter records
+constexpr int kCtrlWarp = 23;                       // warp 23: TMA issue, exchange stores, publish
+constexpr int kConsWarps = 8;                       // warps 24-31: drain this CTA's bucket
+constexpr int kDecodeThreads = kDecodeWarps * 32;
+constexpr int kConsThreads = kConsWarps * 32;
+constexpr int kConsBase = (kCtrlWarp + 1) * 32;
+constexpr int kDecodeRecs = kPartChunk / kDecodeThreads;   // records per decode thread per chunk
 constexpr int kRing = 2;                           // TMA ring depth (input chunks)
 constexpr int kInbox = 3;                          // consumer inbox depth (exchange chunks)
+constexpr int kStage = 3;                          // staging buffers (decode k+1 never waits for chunk k's store)
 constexpr int kTrash = 32;                         // lane-distinct sink for dropped keys / padding
 constexpr uint32_t kLocalBits = 13;                // key = local bin (13 bits) | count (3 bits)
 constexpr uint32_t kMaxKeyCount = 7;
 constexpr uint64_t kWrapGuard = (uint64_t)kPartMaxCtas * kPartCap * kMaxKeyCount;   // max samples per chunk
-static_assert(kPartChunk % (2 * kProdThreads) == 0, "whole record pairs per producer thread");
+static_assert(kPartChunk % (2 * kDecodeThreads) == 0, "whole record pairs per decode thread");
 static_assert((kPartCap * 2) % 16 == 0, "slots must be whole 16-byte units for bulk copies");
+static_assert(kConsBase + kConsThreads == kPartThreads, "warp roles cover the CTA");
 
 __device__ __forceinline__ void named_bar(uint32_t id, uint32_t threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 
 __device__ __forceinline__ uint64_t evict_first_policy() {
@@ -226,6 +236,7 @@ __device__ __forceinline__ void tma_bulk_load_ef(void *dst, const void *src, uin
       "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
       : "memory");
 }
+
 // shared -> global bulk copy (async proxy), tracked by this thread's bulk async-groups
 __device__ __forceinline__ void tma_bulk_store(void *gdst, const void *ssrc, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst), "r"(smem_addr(ssrc)),
@@ -250,23 +261,31 @@ __device__ __forceinline__ void tma_tile_load_2d(void *dst, const CUtensorMap *t
 
 __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, const __grid_constant__ CUtensorMap xmap) {
   extern __shared__ __align__(128) uint8_t sm[];
-  const uint32_t tid = threadIdx.x;
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t G = gridDim.x, me = blockIdx.x;
   const uint32_t slot_keys = G * kPartCap;                                       // keys per staging / inbox buffer
+  const uint32_t ibuf_keys = ((slot_keys * 2 + 127) & ~127u) / 2;             // 128-B aligned buffers (TMA)
   uint2 *ring = reinterpret_cast<uint2 *>(sm);                                   // [kRing][chunk] records
-  const uint32_t ibuf_keys = ((slot_keys * 2 + 127) & ~127u) / 2;             // inbox buffers 128-B aligned (TMA tile)
   uint16_t *inbox = reinterpret_cast<uint16_t *>(sm + kRing * kPartChunk * 8); // [kInbox][G src][cap]
-  uint16_t *stag = inbox + kInbox * ibuf_keys;                                  // [2][G dst][cap]
-  uint32_t *trash = reinterpret_cast<uint32_t *>(stag + 2 * slot_keys);         // [kTrash]
-  uint32_t *cnt = trash + kTrash;                                                // [kPartMaxCtas + 8]
-  unsigned long long *ctotal = reinterpret_cast<unsigned long long *>(cnt + kPartMaxCtas + 8);   // [2]
-  uint64_t *bars = reinterpret_cast<uint64_t *>(ctotal + 2);                    // [kRing + kInbox]
-  uint32_t *tab = reinterpret_cast<uint32_t *>(bars + kRing + kInbox);          // [bpb + kTrash]
+  uint16_t *stag = inbox + kInbox * ibuf_keys;                                  // [kStage][G dst][cap]
+  uint32_t *trash = reinterpret_cast<uint32_t *>(stag + kStage * ibuf_keys);    // [kTrash]
+  uint32_t *cnt = trash + kTrash;                                                // [kStage][kPartMaxCtas + 8]
+  unsigned long long *ctotal = reinterpret_cast<unsigned long long *>(cnt + kStage * (kPartMaxCtas + 8));   // [2]
+  uint64_t *ring_full = reinterpret_cast<uint64_t *>(ctotal + 2);                // [kRing]   TMA -> decoders
+  uint64_t *buf_ready = ring_full + kRing;                                       // [kStage]  control -> decoders
+  uint64_t *decoded = buf_ready + kStage;                                        // [kStage]  decoders -> control
+  uint64_t *inbox_full = decoded + kStage;                                       // [kInbox]  TMA -> consumers
+  uint32_t *tab = reinterpret_cast<uint32_t *>(inbox_full + kInbox);            // [bpb + kTrash]
   for (uint32_t i = tid; i < a.bpb + kTrash; i += kPartThreads) tab[i] = 0;
-  for (uint32_t i = tid; i < slot_keys; i += kPartThreads) reinterpret_cast<uint32_t *>(stag)[i] = 0;   // both buffers
-  for (uint32_t i = tid; i < kPartMaxCtas + 8; i += kPartThreads) cnt[i] = 0;
+  for (uint32_t i = tid; i < kStage * ibuf_keys / 2; i += kPartThreads) reinterpret_cast<uint32_t *>(stag)[i] = 0;
+  for (uint32_t i = tid; i < kStage * (kPartMaxCtas + 8); i += kPartThreads) cnt[i] = 0;
   if (tid == 0) {
-    for (int r = 0; r < kRing + kInbox; ++r) mbar_init(&bars[r], 1);
+    for (int r = 0; r < kRing; ++r) mbar_init(&ring_full[r], 1);
+    for (int r = 0; r < kStage; ++r) {
+      mbar_init(&buf_ready[r], 1);
+      mbar_init(&decoded[r], kDecodeWarps);
+    }
+    for (int r = 0; r < kInbox; ++r) mbar_init(&inbox_full[r], 1);
     ctotal[0] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -286,43 +305,29 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
   };
   const uint32_t twoR = 2 * a.R;
   IngestStats st{0, 0, 0};
-  if (tid < kProdThreads) {
-    // ======================= producers: TMA ring -> decode + slot-shaped scatter (2-byte keys)
-    //                         -> one bulk store of my exchange row; chunk k published during k+1
-    const uint32_t ptid = tid, lane = tid & 31;
-    const uint64_t pol = evict_first_policy();
+  if (warp < kDecodeWarps) {
+    // ======================= decoders: wait only on data (ring_full) and on a clean staging
+    //                         buffer (buf_ready); decode + scatter; signal decoded
+    const uint32_t dtid = tid;
     const uint32_t n_instr = a.n_instr, R = a.R, mg = a.mg;
     const uint32_t trash_addr = smem_addr(trash + lane);
-    const uint32_t cnt_addr = smem_addr(cnt), stag_addr = smem_addr(stag);
-    auto issue = [&](uint32_t k) {
-      uint64_t s0;
-      const uint32_t len = slice_len(k, s0);
-      if (len) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(&bars[k % kRing], len * 8);
-        tma_bulk_load_ef(ring + (k % kRing) * kPartChunk, a.rec + s0, len * 8, &bars[k % kRing], pol);
-      }
-    };
-    if (ptid == 0)
-      for (uint32_t k = 0; k + 1 < (uint32_t)kRing && k < n_chunks; ++k) issue(k);
     for (uint32_t k = 0; k < n_chunks; ++k) {
       uint64_t s0;
       const uint32_t len = slice_len(k, s0);
-      const uint32_t buf = k % kPartBufs;
-      const uint32_t sg_addr = stag_addr + (k & 1) * slot_keys * 2;
-      if (ptid == 0 && k + kRing - 1 < n_chunks) issue(k + kRing - 1);   // slot held chunk k-1
-      if (len) mbar_wait(&bars[k % kRing], (k / kRing) & 1);
-      named_bar(1, kProdThreads);   // cnt zeroed and staging buffer k&1 cleared (iteration k-1)
-      // ---- decode + scatter, branch-free: bucket = pc mod G (interleaved PCs balance the load),
-      //      key = local bin (pc / G) * 2R + class * R + reason | count << 13, stored at position
-      //      cnt[b]++ of bucket b's zero-padded slot (invalid records count in the dummy bucket G,
-      //      dropped keys go to a trash word; counts > 7 and slot overflow go through L2 atomics)
+      const uint32_t sb = k % kStage;
+      const uint32_t sg_addr = smem_addr(stag + sb * ibuf_keys), cnt_addr = smem_addr(cnt + sb * (kPartMaxCtas + 8));
+      mbar_wait(&buf_ready[sb], (k / kStage) & 1);       // staging buffer + counters clean
+      if (len) mbar_wait(&ring_full[k % kRing], (k / kRing) & 1);
+      // ---- branch-free decode: bucket = pc mod G (interleaved PCs balance the load), key = local
+      //      bin (pc / G) * 2R + class * R + reason | count << 13, stored at position cnt[b]++ of
+      //      bucket b's zero-padded slot (invalid and padding records count in the dummy bucket G
+      //      and land in a trash word; counts > 7 and slot overflow go through L2 atomics)
       const uint4 *rs = reinterpret_cast<const uint4 *>(ring + (k % kRing) * kPartChunk);
       uint32_t csum = 0, bads = 0, badr = 0;
       const bool full = len == (uint32_t)kPartChunk;
 #pragma unroll
-      for (int u = 0; u < kProdRecs / 2; ++u) {
-        const uint32_t pair = u * kProdThreads + ptid;
+      for (int u = 0; u < kDecodeRecs / 2; ++u) {
+        const uint32_t pair = u * kDecodeThreads + dtid;
         const bool in = full || 2 * pair < len;   // len is even: both records of the pair or neither
         const uint4 v = in ? rs[pair] : make_uint4(0xffffffffu, 0, 0xffffffffu, 0);
 #pragma unroll
@@ -333,7 +338,7 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
           const uint32_t q = __umulhi(pc, mg), b = pc - q * G;
           const uint32_t local = q * twoR + (t >> 8) * R + reason;
           const bool small = c <= kMaxKeyCount;
-          const uint32_t be = ok && small ? b : G;   // invalid, padding, big-count records -> bucket G
+          const uint32_t be = ok && small ? b : G;
           uint32_t pos;
           asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(pos) : "r"(cnt_addr + be * 4) : "memory");
           const bool keep = ok && small && pos < (uint32_t)kPartCap;
@@ -350,53 +355,79 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
       st.valid += csum - bads;
       st.bad_samples += bads;
       st.bad_records += badr;
-      // every thread that wrote the staging buffer orders its generic-proxy writes before the
-      // async-proxy bulk stores issued after the barrier
+      // generic-proxy staging writes must be ordered before the control warp's bulk store
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      named_bar(1, kProdThreads);
-      if (ptid == 0) {
-        // exchange buffer k%NBUF is free once every CTA drained chunk k-NBUF
-        if (k >= (uint32_t)kPartBufs) spin_until(&a.sync[kPartBufs + buf], G * (k / kPartBufs));
-        tma_bulk_store(xrow(buf, me), stag + (k & 1) * slot_keys, slot_keys * 2);   // my row, all G slots
-        bulk_commit();
-        if (k > 0) {   // chunk k-1's store (one iteration ago) is complete: publish it
-          asm volatile("cp.async.bulk.wait_group 1;" ::: "memory");
-          fence_proxy_async_global();
-          __threadfence();
-          atomicAdd(&a.sync[(k - 1) % kPartBufs], 1u);   // this CTA produced chunk k-1
-        }
-      }
-      named_bar(1, kProdThreads);   // chunk k-1's staging buffer is free again
-      for (uint32_t i = ptid; i <= G; i += kProdThreads) cnt[i] = 0;
-      if (k + 1 < n_chunks) {   // clear the buffer chunk k+1 will use (it held chunk k-1)
-        uint4 *z = reinterpret_cast<uint4 *>(stag + ((k + 1) & 1) * slot_keys);
-        for (uint32_t i = ptid; i < slot_keys / 8; i += kProdThreads) z[i] = make_uint4(0, 0, 0, 0);
-      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&decoded[sb]);          // ring slot and staging buffer handed over
     }
-    if (n_chunks && ptid == 0) {
-      bulk_wait_all();
+  } else if (warp == kCtrlWarp) {
+    // ======================= control: TMA ring refills, exchange stores, publication, recycling
+    const uint64_t pol = evict_first_policy();
+    auto issue = [&](uint32_t k) {
+      uint64_t s0;
+      const uint32_t len = slice_len(k, s0);
+      if (len) {
+        mbar_expect_tx(&ring_full[k % kRing], len * 8);
+        tma_bulk_load_ef(ring + (k % kRing) * kPartChunk, a.rec + s0, len * 8, &ring_full[k % kRing], pol);
+      }
+    };
+    auto publish = [&](uint32_t k) {
       fence_proxy_async_global();
       __threadfence();
-      atomicAdd(&a.sync[(n_chunks - 1) % kPartBufs], 1u);
+      atomicAdd(&a.sync[k % kPartBufs], 1u);   // this CTA produced chunk k
+    };
+    if (lane == 0) {
+      for (uint32_t k = 0; k < (uint32_t)kRing && k < n_chunks; ++k) issue(k);
+      for (int r = 0; r < kStage; ++r) mbar_arrive(&buf_ready[r]);
+    }
+    for (uint32_t k = 0; k < n_chunks; ++k) {
+      const uint32_t sb = k % kStage, buf = k % kPartBufs;
+      mbar_wait(&decoded[sb], (k / kStage) & 1);        // all decoders finished chunk k
+      if (lane == 0) {
+        if (k + kRing < n_chunks) {                       // ring slot k%kRing is free again
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue(k + kRing);
+        }
+        // exchange buffer k%NBUF is free once every CTA drained chunk k-NBUF
+        if (k >= (uint32_t)kPartBufs) spin_until(&a.sync[kPartBufs + buf], G * (k / kPartBufs));
+        tma_bulk_store(xrow(buf, me), stag + sb * ibuf_keys, slot_keys * 2);   // my row, all G slots
+        bulk_commit();
+        if (k > 0) {   // chunk k-1's store is complete: publish it
+          asm volatile("cp.async.bulk.wait_group 1;" ::: "memory");
+          publish(k - 1);
+        }
+      }
+      __syncwarp();
+      if (k > 0 && k + kStage - 1 < n_chunks) {   // recycle chunk k-1's staging buffer for chunk k+kStage-1
+        const uint32_t ob = (k - 1) % kStage;
+        uint4 *z = reinterpret_cast<uint4 *>(stag + ob * ibuf_keys);
+        for (uint32_t i = lane; i < slot_keys / 8; i += 32) z[i] = make_uint4(0, 0, 0, 0);
+        for (uint32_t i = lane; i <= G; i += 32) cnt[ob * (kPartMaxCtas + 8) + i] = 0;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&buf_ready[ob]);
+      }
+    }
+    if (n_chunks && lane == 0) {
+      bulk_wait_all();
+      publish(n_chunks - 1);
     }
   } else {
     // ======================= consumers: my column of the exchange buffer -> smem inbox (one 2-D
     //                         TMA tile load per chunk, kInbox deep) -> table
-    const uint32_t ctid = tid - kProdThreads;
+    const uint32_t ctid = tid - kConsBase;
     const uint32_t tab_addr = smem_addr(tab), dummy_addr = smem_addr(tab + a.bpb + (ctid & 31));
-    uint64_t *ibars = bars + kRing;
     auto fetch = [&](uint32_t j) {   // ctid 0: wait for chunk j everywhere, then load my column
       spin_until(&a.sync[j % kPartBufs], G * (j / kPartBufs + 1));
       fence_proxy_async_global();
-      mbar_expect_tx(&ibars[j % kInbox], slot_keys * 2);
+      mbar_expect_tx(&inbox_full[j % kInbox], slot_keys * 2);
       tma_tile_load_2d(inbox + (j % kInbox) * ibuf_keys, &xmap, me * kPartCap, (j % kPartBufs) * kPartMaxCtas,
-                       &ibars[j % kInbox]);
+                       &inbox_full[j % kInbox]);
     };
     if (ctid == 0)
       for (uint32_t j = 0; j + 1 < (uint32_t)kInbox && j < n_chunks; ++j) fetch(j);
     for (uint32_t j = 0; j < n_chunks; ++j) {
       if (ctid == 0 && j + kInbox - 1 < n_chunks) fetch(j + kInbox - 1);   // inbox slot freed at end of j-1
-      mbar_wait(&ibars[j % kInbox], (j / kInbox) & 1);
+      mbar_wait(&inbox_full[j % kInbox], (j / kInbox) & 1);
       const uint4 *in4 = reinterpret_cast<const uint4 *>(inbox + (j % kInbox) * ibuf_keys);
       uint32_t tot = 0;
       for (uint32_t v = ctid; v < slot_keys / 8; v += kConsThreads) {
@@ -480,9 +511,9 @@ static cudaError_t make_exchange_map(CUtensorMap *tm, void *X, uint32_t G) {
 }
 
 size_t part_smem_bytes(uint32_t bpb, uint32_t G) {
-  return (size_t)kRing * kPartChunk * 8 + (size_t)kInbox * ((G * kPartCap * 2 + 127) & ~127u) +
-         (size_t)2 * G * kPartCap * 2 + kTrash * 4 + (kPartMaxCtas + 8) * 4 + 16 + (kRing + kInbox) * 8 +
-         (size_t)(bpb + kTrash) * 4;
+  const size_t ibuf = ((size_t)G * kPartCap * 2 + 127) & ~(size_t)127;
+  return (size_t)kRing * kPartChunk * 8 + (kInbox + kStage) * ibuf + kTrash * 4 + kStage * (kPartMaxCtas + 8) * 4 + 16 +
+         (kRing + 2 * kStage + kInbox) * 8 + (size_t)(bpb + kTrash) * 4;
 }
 
 static uint32_t part_grid(int n_sms) { return (uint32_t)std::min(n_sms, kPartMaxCtas); }

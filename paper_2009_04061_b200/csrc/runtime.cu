@@ -545,6 +545,8 @@ gpa_status gpa_program_create(const gpa_program_desc *d, void *d_workspace, size
 
 gpa_status gpa_program_destroy(gpa_program *p) {
   if (!p) return GPA_OK;
+  if (p->analyze_exec) cudaGraphExecDestroy(p->analyze_exec);
+  if (p->capture_stream) cudaStreamDestroy(p->capture_stream);
   if (p->staging) cudaFree(p->staging);
   if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
   for (int i = 0; i < 2; ++i) {
@@ -669,6 +671,38 @@ gpa_status gpa_estimate(gpa_program *p, void *stream) {
   if (!(p->state & ST_PATTERNS)) return fail(GPA_ERR_BAD_STATE, "gpa_estimate before gpa_set_patterns");
   cudaError_t e = launch_estimate(p->d, p->ep, p->n_sms, (cudaStream_t)stream, &p->launches);
   if (e != cudaSuccess) return cuda_fail(e, "estimate launch");
+  return GPA_OK;
+}
+
+gpa_status gpa_analyze(gpa_program *p, void *stream) {
+  gpa_status st = check_prog(p);
+  if (st) return st;
+  if (!(p->state & ST_COUNTS)) return fail(GPA_ERR_BAD_STATE, "gpa_analyze before gpa_reset_counts/gpa_ingest_samples");
+  const uint32_t npat = (p->state & ST_PATTERNS) ? p->ep.n_pat : 0;
+  if (!p->analyze_exec || p->analyze_npat != npat) {
+    if (p->analyze_exec) {
+      cudaGraphExecDestroy(p->analyze_exec);
+      p->analyze_exec = nullptr;
+    }
+    if (!p->capture_stream) CUDA_TRY(cudaStreamCreateWithFlags(&p->capture_stream, cudaStreamNonBlocking));
+    cudaGraph_t g = nullptr;
+    uint64_t n = 0;
+    CUDA_TRY(cudaStreamBeginCapture(p->capture_stream, cudaStreamCaptureModeThreadLocal));
+    cudaError_t e = launch_blame(p->d, p->n_sms, p->capture_stream, &n);
+    if (e == cudaSuccess) e = launch_rollup(p->d, p->rp, p->n_sms, p->capture_stream, &n);
+    if (e == cudaSuccess && npat) e = launch_estimate(p->d, p->ep, p->n_sms, p->capture_stream, &n);
+    cudaError_t e2 = cudaStreamEndCapture(p->capture_stream, &g);
+    if (e != cudaSuccess) return cuda_fail(e, "analyze capture");
+    if (e2 != cudaSuccess) return cuda_fail(e2, "analyze end capture");
+    e = cudaGraphInstantiate(&p->analyze_exec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return cuda_fail(e, "analyze instantiate");
+    p->analyze_npat = npat;
+    p->analyze_launches = n;
+  }
+  CUDA_TRY(cudaGraphLaunch(p->analyze_exec, (cudaStream_t)stream));
+  p->launches += p->analyze_launches;
+  p->state |= ST_BLAMED | ST_AGGREGATED;
   return GPA_OK;
 }
 

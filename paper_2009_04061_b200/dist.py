@@ -34,7 +34,8 @@ def sharded_step(program, records, group=None, stream=None, estimate=True):
     program.ingest(records, stream=stream)
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
         allreduce_counts(program.view("counts"), program.view("stats"), group)
-    program.blame(stream)
-    program.aggregate(stream)
-    if estimate and program.n_patterns:
-        program.estimate(stream)
+    if estimate:
+        program.analyze(stream)      # blame + aggregate + estimate as one CUDA graph
+    else:
+        program.blame(stream)
+        program.aggregate(stream)

@@ -56,7 +56,7 @@ EXPORTS = ["gpa_validate_program", "gpa_workspace_size", "gpa_program_create", "
            "gpa_reset_counts", "gpa_ingest_samples", "gpa_ingest_samples_host", "gpa_blame",
            "gpa_aggregate", "gpa_set_patterns", "gpa_estimate", "gpa_read_estimates", "gpa_get_stats",
            "gpa_view", "gpa_instr_vector", "gpa_program_info", "gpa_ingest_variant",
-           "gpa_set_ingest_variant", "gpa_launch_count", "gpa_last_error", "gpa_version"]
+           "gpa_set_ingest_variant", "gpa_launch_count", "gpa_last_error", "gpa_version", "gpa_analyze"]
 
 _lib = None
 
@@ -80,6 +80,7 @@ def lib():
             "gpa_view": [vp, ctypes.c_int, vp, vp], "gpa_instr_vector": [vp, vp, vp],
             "gpa_program_info": [vp, vp], "gpa_ingest_variant": [vp, vp],
             "gpa_set_ingest_variant": [vp, ctypes.c_int], "gpa_launch_count": [vp, vp],
+            "gpa_analyze": [vp, vp],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -212,14 +213,15 @@ class Program:
     def estimate(self, stream=None):
         _check(lib().gpa_estimate(self.handle, self._s(stream)), "gpa_estimate")
 
-    def step(self, samples, stream=None, estimate=True):
+    def analyze(self, stream=None):
+        """blame + aggregate + estimate (if patterns are set) replayed as one CUDA graph."""
+        _check(lib().gpa_analyze(self.handle, self._s(stream)), "gpa_analyze")
+
+    def step(self, samples, stream=None):
         """One pass of the whole hot path over one batch of device-resident records."""
         self.reset(stream)
         self.ingest(samples, stream=stream)
-        self.blame(stream)
-        self.aggregate(stream)
-        if estimate and self.n_patterns:
-            self.estimate(stream)
+        self.analyze(stream)
 
     # -------------------------------------------------------------- results
     def read_estimates(self, stream=None):

@@ -173,3 +173,29 @@ def test_call_order_errors():
         P.estimate()
     with pytest.raises(GpaError):
         P.ingest(torch.zeros(65, dtype=torch.uint8, device="cuda")[1:])  # 8 records, misaligned pointer
+
+
+def test_analyze_graph_equals_separate_calls():
+    """gpa_analyze (one CUDA graph) gives bit-identical results to blame + aggregate + estimate."""
+    import torch
+    from paper_2009_04061_b200 import Program
+    prog = gp.config_program(2)
+    recs = config_stream(prog, 2).host(0, 2_000_000)
+    d = torch.from_numpy(recs.view(np.int64)).cuda()
+    P = Program(prog)
+    P.set_patterns(table2())
+    outs = []
+    for mode in ("calls", "graph", "graph"):
+        P.reset()
+        P.ingest(d)
+        if mode == "calls":
+            P.blame(); P.aggregate(); P.estimate()
+        else:
+            P.analyze()
+        torch.cuda.synchronize()
+        outs.append((P.instr_vector(), P.view("line").clone(), P.view("kernel").clone(),
+                     bytes(P.view("estimates").cpu().numpy())))
+    for other in outs[1:]:
+        for a, b in zip(outs[0][:3], other[:3]):
+            assert torch.equal(a, b)
+        assert outs[0][3] == other[3]
