@@ -33,6 +33,20 @@ def _compile(src: str, verbose: bool) -> str:
     return obj
 
 
+def build_variant(out: str, defines: list[str]) -> str:
+    """Extra build with -D flags into build/ (tuning instrumentation; not the product library)."""
+    obj_dir = os.path.join(ROOT, "build", "obj_" + os.path.basename(out).replace(".so", ""))
+    os.makedirs(obj_dir, exist_ok=True)
+    objs = []
+    for src in SOURCES:
+        obj = os.path.join(obj_dir, src.replace(".cu", ".o"))
+        subprocess.check_call(["nvcc", *ARCH, *FLAGS, *["-D" + d for d in defines], "-c", os.path.join(CSRC, src), "-o", obj],
+                              stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        objs.append(obj)
+    subprocess.check_call(["nvcc", *ARCH, "-shared", "-o", out, *objs])
+    return out
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= _newest_dep():
         return LIB

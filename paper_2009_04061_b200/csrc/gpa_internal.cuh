@@ -17,9 +17,9 @@ constexpr int kMaxIngestCtas = 256;         // per-CTA partial tables reserved (
 constexpr size_t kSmemTableMax = 224 * 1024;// largest CTA-private table (bytes; sm_100a opt-in is 227 KB)
 // partitioned ingest (variant P): bucket exchange through L2
 constexpr int kPartThreads = 1024;
-constexpr int kPartChunk = 5888;            // records per CTA per chunk (46 KB, one TMA bulk copy)
-constexpr int kPartBufs = 8;                // exchange buffers in flight
-constexpr int kPartCap = 56;                // keys per (src, dst) slot per chunk (mean 39.8 at G=148);
+constexpr int kPartChunk = 5632;            // records per CTA per chunk (44 KB, one TMA bulk copy)
+constexpr int kPartBufs = 16;               // exchange buffers in flight
+constexpr int kPartCap = 56;                // keys per (src, dst) slot per chunk (mean 38.1 at G=148);
                                             // excess -> L2 atomics
 constexpr int kPartMaxCtas = 160;           // < 255: bucket ids fit a byte
 size_t part_smem_bytes(uint32_t bpb, uint32_t G);

@@ -186,6 +186,21 @@ __device__ __forceinline__ void spin_until(const unsigned int *ctr, unsigned int
   }
 }
 
+#ifdef GPA_PART_TIMING
+// phase timers (cycles, summed over CTAs) for tuning: read with tools/part_timing.py
+__device__ unsigned long long g_part_timing[16];
+#define PT_DECL unsigned long long _pt0 = clock64(), _pt1;
+#define PT_MARK(slot)                                                     \
+  do {                                                                    \
+    _pt1 = clock64();                                                     \
+    if ((threadIdx.x & 31) == 0) atomicAdd(&g_part_timing[slot], _pt1 - _pt0); \
+    _pt0 = _pt1;                                                          \
+  } while (0)
+#else
+#define PT_DECL
+#define PT_MARK(slot) do {} while (0)
+#endif
+
 struct PartArgs {
   const uint2 *rec;       // 16-byte aligned body
   uint64_t n_even;        // records in the body (even)
@@ -197,12 +212,16 @@ struct PartArgs {
 };
 
 // warp roles of the 1024-thread CTA
-constexpr int kDecodeWarps = 23;                    // warps 0-22: decode + scatter records
-constexpr int kCtrlWarp = 23;                       // warp 23: TMA issue, exchange stores, publish
+constexpr int kDecodeWarps = 22;                    // warps 0-21: decode + scatter records
+constexpr int kCtrlWarp = 22;                       // warp 22: TMA issue, exchange stores, recycling
+constexpr int kPubWarp = 23;                        // warp 23: publication of stored chunks
 constexpr int kConsWarps = 8;                       // warps 24-31: drain this CTA's bucket
+constexpr int kLoaderWarp = kPubWarp + 1;           //   warp 24: exchange -> inbox TMA loads
+constexpr int kProcBase = (kLoaderWarp + 1) * 32;   //   warps 25-31: inbox -> table
+constexpr int kProcThreads = (kConsWarps - 1) * 32;
 constexpr int kDecodeThreads = kDecodeWarps * 32;
 constexpr int kConsThreads = kConsWarps * 32;
-constexpr int kConsBase = (kCtrlWarp + 1) * 32;
+constexpr int kConsBase = (kPubWarp + 1) * 32;
 constexpr int kDecodeRecs = kPartChunk / kDecodeThreads;   // records per decode thread per chunk
 constexpr int kRing = 2;                           // TMA ring depth (input chunks)
 constexpr int kInbox = 3;                          // consumer inbox depth (exchange chunks)
@@ -217,6 +236,9 @@ static_assert(kConsBase + kConsThreads == kPartThreads, "warp roles cover the CT
 
 __device__ __forceinline__ void named_bar(uint32_t id, uint32_t threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+__device__ __forceinline__ void red_release_add(unsigned int *p, unsigned int v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
@@ -275,17 +297,23 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
   uint64_t *buf_ready = ring_full + kRing;                                       // [kStage]  control -> decoders
   uint64_t *decoded = buf_ready + kStage;                                        // [kStage]  decoders -> control
   uint64_t *inbox_full = decoded + kStage;                                       // [kInbox]  TMA -> consumers
-  uint32_t *tab = reinterpret_cast<uint32_t *>(inbox_full + kInbox);            // [bpb + kTrash]
+  uint64_t *inbox_free = inbox_full + kInbox;                                    // [kInbox]  consumers -> loader
+  uint64_t *stored = inbox_free + kInbox;                                        // [kStage]  control -> publisher
+  uint32_t *tab = reinterpret_cast<uint32_t *>(stored + kStage);                // [bpb + kTrash]
   for (uint32_t i = tid; i < a.bpb + kTrash; i += kPartThreads) tab[i] = 0;
   for (uint32_t i = tid; i < kStage * ibuf_keys / 2; i += kPartThreads) reinterpret_cast<uint32_t *>(stag)[i] = 0;
   for (uint32_t i = tid; i < kStage * (kPartMaxCtas + 8); i += kPartThreads) cnt[i] = 0;
   if (tid == 0) {
     for (int r = 0; r < kRing; ++r) mbar_init(&ring_full[r], 1);
     for (int r = 0; r < kStage; ++r) {
+      mbar_init(&stored[r], 1);
       mbar_init(&buf_ready[r], 1);
       mbar_init(&decoded[r], kDecodeWarps);
     }
-    for (int r = 0; r < kInbox; ++r) mbar_init(&inbox_full[r], 1);
+    for (int r = 0; r < kInbox; ++r) {
+      mbar_init(&inbox_full[r], 1);
+      mbar_init(&inbox_free[r], 1);
+    }
     ctotal[0] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -316,8 +344,11 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
       const uint32_t len = slice_len(k, s0);
       const uint32_t sb = k % kStage;
       const uint32_t sg_addr = smem_addr(stag + sb * ibuf_keys), cnt_addr = smem_addr(cnt + sb * (kPartMaxCtas + 8));
+      PT_DECL
       mbar_wait(&buf_ready[sb], (k / kStage) & 1);       // staging buffer + counters clean
+      PT_MARK(0);
       if (len) mbar_wait(&ring_full[k % kRing], (k / kRing) & 1);
+      PT_MARK(1);
       // ---- branch-free decode: bucket = pc mod G (interleaved PCs balance the load), key = local
       //      bin (pc / G) * 2R + class * R + reason | count << 13, stored at position cnt[b]++ of
       //      bucket b's zero-padded slot (invalid and padding records count in the dummy bucket G
@@ -359,6 +390,7 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(&decoded[sb]);          // ring slot and staging buffer handed over
+      PT_MARK(2);
     }
   } else if (warp == kCtrlWarp) {
     // ======================= control: TMA ring refills, exchange stores, publication, recycling
@@ -371,18 +403,15 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
         tma_bulk_load_ef(ring + (k % kRing) * kPartChunk, a.rec + s0, len * 8, &ring_full[k % kRing], pol);
       }
     };
-    auto publish = [&](uint32_t k) {
-      fence_proxy_async_global();
-      __threadfence();
-      atomicAdd(&a.sync[k % kPartBufs], 1u);   // this CTA produced chunk k
-    };
     if (lane == 0) {
       for (uint32_t k = 0; k < (uint32_t)kRing && k < n_chunks; ++k) issue(k);
       for (int r = 0; r < kStage; ++r) mbar_arrive(&buf_ready[r]);
     }
     for (uint32_t k = 0; k < n_chunks; ++k) {
       const uint32_t sb = k % kStage, buf = k % kPartBufs;
+      PT_DECL
       mbar_wait(&decoded[sb], (k / kStage) & 1);        // all decoders finished chunk k
+      PT_MARK(3);
       if (lane == 0) {
         if (k + kRing < n_chunks) {                       // ring slot k%kRing is free again
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -390,11 +419,14 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
         }
         // exchange buffer k%NBUF is free once every CTA drained chunk k-NBUF
         if (k >= (uint32_t)kPartBufs) spin_until(&a.sync[kPartBufs + buf], G * (k / kPartBufs));
+        PT_MARK(4);
         tma_bulk_store(xrow(buf, me), stag + sb * ibuf_keys, slot_keys * 2);   // my row, all G slots
         bulk_commit();
-        if (k > 0) {   // chunk k-1's store is complete: publish it
+        if (k > 0) {   // chunk k-1's store is complete: hand it to the publisher warp
           asm volatile("cp.async.bulk.wait_group 1;" ::: "memory");
-          publish(k - 1);
+          fence_proxy_async_global();
+          mbar_arrive(&stored[(k - 1) % kStage]);
+          PT_MARK(5);
         }
       }
       __syncwarp();
@@ -405,57 +437,80 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
         for (uint32_t i = lane; i <= G; i += 32) cnt[ob * (kPartMaxCtas + 8) + i] = 0;
         __syncwarp();
         if (lane == 0) mbar_arrive(&buf_ready[ob]);
+        PT_MARK(7);
       }
     }
     if (n_chunks && lane == 0) {
       bulk_wait_all();
-      publish(n_chunks - 1);
+      fence_proxy_async_global();
+      mbar_arrive(&stored[(n_chunks - 1) % kStage]);
+    }
+  } else if (warp == kPubWarp) {
+    // ======================= publisher: release each stored chunk to the other CTAs
+    if (lane == 0) {
+      for (uint32_t k = 0; k < n_chunks; ++k) {
+        mbar_wait(&stored[k % kStage], (k / kStage) & 1);
+        fence_proxy_async_global();
+        red_release_add(&a.sync[k % kPartBufs], 1u);   // this CTA produced chunk k
+      }
     }
   } else {
-    // ======================= consumers: my column of the exchange buffer -> smem inbox (one 2-D
-    //                         TMA tile load per chunk, kInbox deep) -> table
-    const uint32_t ctid = tid - kConsBase;
-    const uint32_t tab_addr = smem_addr(tab), dummy_addr = smem_addr(tab + a.bpb + (ctid & 31));
-    auto fetch = [&](uint32_t j) {   // ctid 0: wait for chunk j everywhere, then load my column
-      spin_until(&a.sync[j % kPartBufs], G * (j / kPartBufs + 1));
-      fence_proxy_async_global();
-      mbar_expect_tx(&inbox_full[j % kInbox], slot_keys * 2);
-      tma_tile_load_2d(inbox + (j % kInbox) * ibuf_keys, &xmap, me * kPartCap, (j % kPartBufs) * kPartMaxCtas,
-                       &inbox_full[j % kInbox]);
-    };
-    if (ctid == 0)
-      for (uint32_t j = 0; j + 1 < (uint32_t)kInbox && j < n_chunks; ++j) fetch(j);
-    for (uint32_t j = 0; j < n_chunks; ++j) {
-      if (ctid == 0 && j + kInbox - 1 < n_chunks) fetch(j + kInbox - 1);   // inbox slot freed at end of j-1
-      mbar_wait(&inbox_full[j % kInbox], (j / kInbox) & 1);
-      const uint4 *in4 = reinterpret_cast<const uint4 *>(inbox + (j % kInbox) * ibuf_keys);
-      uint32_t tot = 0;
-      for (uint32_t v = ctid; v < slot_keys / 8; v += kConsThreads) {
-        const uint4 kv = in4[v];
-        const uint32_t w4[4] = {kv.x, kv.y, kv.z, kv.w};
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const uint32_t key = (w4[e >> 1] >> ((e & 1) * 16)) & 0xffffu;
-          const uint32_t c = key >> kLocalBits;
-          const uint32_t addr = c ? tab_addr + (key & ((1u << kLocalBits) - 1)) * 4 : dummy_addr;   // padding -> dummy
-          asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(c) : "memory");
-          tot += c;
+    // ======================= consumers: warp kLoaderWarp fetches my column of each exchange
+    //                         buffer into the kInbox-deep smem inbox (one 2-D TMA tile load per
+    //                         chunk, as soon as every producer published it and the slot is free);
+    //                         the other warps only wait on their data and add keys to the table
+    if (warp == kLoaderWarp) {
+      if (lane == 0) {
+        for (uint32_t j = 0; j < n_chunks; ++j) {
+          if (j >= (uint32_t)kInbox) mbar_wait(&inbox_free[j % kInbox], ((j / kInbox) + 1) & 1);
+          spin_until(&a.sync[j % kPartBufs], G * (j / kPartBufs + 1));
+          fence_proxy_async_global();
+          mbar_expect_tx(&inbox_full[j % kInbox], slot_keys * 2);
+          tma_tile_load_2d(inbox + (j % kInbox) * ibuf_keys, &xmap, me * kPartCap, (j % kPartBufs) * kPartMaxCtas,
+                           &inbox_full[j % kInbox]);
         }
       }
+    } else {
+      const uint32_t ctid = tid - kProcBase;
+      const uint32_t tab_addr = smem_addr(tab), dummy_addr = smem_addr(tab + a.bpb + (ctid & 31));
+      for (uint32_t j = 0; j < n_chunks; ++j) {
+        PT_DECL
+        mbar_wait(&inbox_full[j % kInbox], (j / kInbox) & 1);
+        PT_MARK(9);
+        const uint4 *in4 = reinterpret_cast<const uint4 *>(inbox + (j % kInbox) * ibuf_keys);
+        uint32_t tot = 0;
+        for (uint32_t v = ctid; v < slot_keys / 8; v += kProcThreads) {
+          const uint4 kv = in4[v];
+          const uint32_t w4[4] = {kv.x, kv.y, kv.z, kv.w};
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-      if ((ctid & 31) == 0) atomicAdd(&ctotal[0], (unsigned long long)tot);
-      named_bar(2, kConsThreads);   // inbox slot j%kInbox fully read
-      if (ctid == 0) atomicAdd(&a.sync[kPartBufs + j % kPartBufs], 1u);   // this CTA drained chunk j
-      if (ctotal[0] + kWrapGuard >= 0xffffffffull) {   // rare: flush the table to global and restart
-        for (uint32_t i = ctid; i < a.bpb; i += kConsThreads) {
-          const uint32_t bin = ((i / twoR) * G + me) * twoR + i % twoR;
-          if (tab[i]) atomicAdd((unsigned long long *)&a.C[bin], (unsigned long long)tab[i]);
-          tab[i] = 0;
+          for (int e = 0; e < 8; ++e) {
+            const uint32_t key = (w4[e >> 1] >> ((e & 1) * 16)) & 0xffffu;
+            const uint32_t c = key >> kLocalBits;
+            const uint32_t addr = c ? tab_addr + (key & ((1u << kLocalBits) - 1)) * 4 : dummy_addr;   // padding -> dummy
+            asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(c) : "memory");
+            tot += c;
+          }
         }
-        named_bar(2, kConsThreads);
-        if (ctid == 0) ctotal[0] = 0;
-        named_bar(2, kConsThreads);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        if ((ctid & 31) == 0) atomicAdd(&ctotal[0], (unsigned long long)tot);
+        PT_MARK(10);
+        named_bar(2, kProcThreads);   // inbox slot j%kInbox fully read
+        PT_MARK(11);
+        if (ctid == 0) {
+          mbar_arrive(&inbox_free[j % kInbox]);
+          red_release_add(&a.sync[kPartBufs + j % kPartBufs], 1u);   // this CTA drained chunk j
+        }
+        if (ctotal[0] + kWrapGuard >= 0xffffffffull) {   // rare: flush the table to global and restart
+          for (uint32_t i = ctid; i < a.bpb; i += kProcThreads) {
+            const uint32_t bin = ((i / twoR) * G + me) * twoR + i % twoR;
+            if (tab[i]) atomicAdd((unsigned long long *)&a.C[bin], (unsigned long long)tab[i]);
+            tab[i] = 0;
+          }
+          named_bar(2, kProcThreads);
+          if (ctid == 0) ctotal[0] = 0;
+          named_bar(2, kProcThreads);
+        }
       }
     }
   }
@@ -510,10 +565,17 @@ static cudaError_t make_exchange_map(CUtensorMap *tm, void *X, uint32_t G) {
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+#ifdef GPA_PART_TIMING
+extern "C" int gpa_debug_read_timing(unsigned long long *out) {
+  cudaDeviceSynchronize();
+  return (int)cudaMemcpyFromSymbol(out, g_part_timing, sizeof(g_part_timing));
+}
+#endif
+
 size_t part_smem_bytes(uint32_t bpb, uint32_t G) {
   const size_t ibuf = ((size_t)G * kPartCap * 2 + 127) & ~(size_t)127;
   return (size_t)kRing * kPartChunk * 8 + (kInbox + kStage) * ibuf + kTrash * 4 + kStage * (kPartMaxCtas + 8) * 4 + 16 +
-         (kRing + 2 * kStage + kInbox) * 8 + (size_t)(bpb + kTrash) * 4;
+         (kRing + 3 * kStage + 2 * kInbox) * 8 + (size_t)(bpb + kTrash) * 4;
 }
 
 static uint32_t part_grid(int n_sms) { return (uint32_t)std::min(n_sms, kPartMaxCtas); }

@@ -302,7 +302,7 @@ Offsets layout(const gpa_program_desc *d, const HostPlan &h) {
   {
     const bool part = n * 2 * R * 4 > kSmemTableMax && n <= (size_t)kPartMaxCtas * 4095;  // see part_feasible
     const size_t pairs = (size_t)kPartBufs * kPartMaxCtas * kPartMaxCtas;
-    o.part_x = a.take(part ? pairs * kPartCap * 4 : 0);
+    o.part_x = a.take(part ? pairs * kPartCap * 2 : 0);   // 2-byte keys
     o.part_n = a.take(part ? pairs * 4 : 0);
     o.part_sync = a.take(part ? 64 : 0);
     o.part_reserved = part;

@@ -169,7 +169,10 @@ class Program:
     def __del__(self):
         h = getattr(self, "handle", None)
         if h is not None and h.value:
-            lib().gpa_program_destroy(h)
+            try:
+                lib().gpa_program_destroy(h)
+            except Exception:   # interpreter shutdown
+                pass
             self.handle = None
 
     def _s(self, stream):
