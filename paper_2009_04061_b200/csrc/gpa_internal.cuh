@@ -17,12 +17,19 @@ constexpr int kMaxIngestCtas = 256;         // per-CTA partial tables reserved (
 constexpr size_t kSmemTableMax = 224 * 1024;// largest CTA-private table (bytes; sm_100a opt-in is 227 KB)
 // partitioned ingest (variant P): bucket exchange through L2
 constexpr int kPartThreads = 1024;
-constexpr int kPartChunk = 5632;            // records per CTA per chunk (44 KB, one TMA bulk copy)
+#ifndef GPA_PART_CHUNK
+#define GPA_PART_CHUNK 6400
+#endif
+constexpr int kPartChunk = GPA_PART_CHUNK;  // largest exchange chunk: records per CTA per round (50 KB)
 constexpr int kPartBufs = 16;               // exchange buffers in flight
-constexpr int kPartCap = 56;                // keys per (src, dst) slot per chunk (mean 38.1 at G=148);
+#ifndef GPA_PART_CAP
+#define GPA_PART_CAP 56
+#endif
+constexpr int kPartCap = GPA_PART_CAP;                // keys per (src, dst) slot per chunk (mean 38.1 at G=148);
                                             // excess -> L2 atomics
 constexpr int kPartMaxCtas = 160;           // < 255: bucket ids fit a byte
-size_t part_smem_bytes(uint32_t bpb, uint32_t G);
+constexpr int kPartZeroBytes = kPartMaxCtas * kPartCap * 2 + 128 + (kPartMaxCtas + 8) * 4;   // >= one staging buffer + counters
+size_t part_smem_bytes(uint32_t bpb, uint32_t G, int chunk);
 
 // stall reasons
 constexpr uint32_t R_NONE = 0, R_MEM = 1, R_EXEC = 2, R_SYNC = 3;
@@ -54,8 +61,8 @@ struct DevProgram {
   uint64_t *C, *stats, *AL;
   uint32_t *partials;               // [kMaxIngestCtas][n*2R] per-CTA tables (smem variant)
   uint32_t *part_x;                 // [kPartBufs][kPartMaxCtas dst][G src][kPartCap] 2-byte exchange keys
-  uint32_t *part_n;                 // [kPartBufs][kPartMaxCtas][kPartMaxCtas] keys per (dst, src)
   unsigned int *part_sync;          // [2*kPartBufs]: per exchange buffer, CTAs that produced / consumed it
+  const uint8_t *part_zero;         // [kPartZeroBytes] zeros (TMA source that clears staging buffers)
   uint8_t *cand, *selfm;
   double *share, *B;
 };

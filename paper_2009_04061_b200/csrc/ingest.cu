@@ -189,16 +189,25 @@ __device__ __forceinline__ void spin_until(const unsigned int *ctr, unsigned int
 #ifdef GPA_PART_TIMING
 // phase timers (cycles, summed over CTAs) for tuning: read with tools/part_timing.py
 __device__ unsigned long long g_part_timing[16];
-#define PT_DECL unsigned long long _pt0 = clock64(), _pt1;
-#define PT_MARK(slot)                                                     \
-  do {                                                                    \
-    _pt1 = clock64();                                                     \
-    if ((threadIdx.x & 31) == 0) atomicAdd(&g_part_timing[slot], _pt1 - _pt0); \
-    _pt0 = _pt1;                                                          \
+#define PT_DECL unsigned long long _pt0 = 0, _pt1, _pta[16] = {0};
+#define PT_START _pt0 = clock64()
+#define PT_MARK(slot)    \
+  do {                   \
+    _pt1 = clock64();    \
+    _pta[slot] += _pt1 - _pt0; \
+    _pt0 = _pt1;         \
+  } while (0)
+#define PT_FLUSH                                                                       \
+  do {                                                                                 \
+    if ((threadIdx.x & 31) == 0)                                                       \
+      for (int _i = 0; _i < 16; ++_i)                                                  \
+        if (_pta[_i]) atomicAdd(&g_part_timing[_i], _pta[_i]);                         \
   } while (0)
 #else
 #define PT_DECL
+#define PT_START do {} while (0)
 #define PT_MARK(slot) do {} while (0)
+#define PT_FLUSH do {} while (0)
 #endif
 
 struct PartArgs {
@@ -208,29 +217,43 @@ struct PartArgs {
   uint32_t mg;            // ceil(2^32 / G): pc / G = umulhi(pc, mg), exact for pc < 2^32 / G
   uint64_t *C, *stats;
   uint16_t *X;            // [kPartBufs][src < kPartMaxCtas][dst < G][kPartCap] 2-byte keys, zero-padded
+  const uint8_t *zero;    // kPartZeroBytes of zeros in global memory (L2-resident)
   unsigned int *sync;     // [kPartBufs] produced, [kPartBufs] consumed
 };
 
 // warp roles of the 1024-thread CTA
-constexpr int kDecodeWarps = 22;                    // warps 0-21: decode + scatter records
-constexpr int kCtrlWarp = 22;                       // warp 22: TMA issue, exchange stores, recycling
-constexpr int kPubWarp = 23;                        // warp 23: publication of stored chunks
-constexpr int kConsWarps = 8;                       // warps 24-31: drain this CTA's bucket
+#ifndef GPA_PART_DECODE_WARPS
+#define GPA_PART_DECODE_WARPS 20
+#endif
+constexpr int kDecodeWarps = GPA_PART_DECODE_WARPS;  // warps 0..D-1: decode + scatter records
+constexpr int kCtrlWarp = kDecodeWarps;              // warp D: TMA issue, exchange stores, recycling
+constexpr int kPubWarp = kDecodeWarps + 1;           // warp D+1: publication of stored chunks
+constexpr int kConsWarps = 32 - kDecodeWarps - 2;    // warps D+2..31: drain this CTA's bucket
 constexpr int kLoaderWarp = kPubWarp + 1;           //   warp 24: exchange -> inbox TMA loads
 constexpr int kProcBase = (kLoaderWarp + 1) * 32;   //   warps 25-31: inbox -> table
 constexpr int kProcThreads = (kConsWarps - 1) * 32;
 constexpr int kDecodeThreads = kDecodeWarps * 32;
 constexpr int kConsThreads = kConsWarps * 32;
 constexpr int kConsBase = (kPubWarp + 1) * 32;
-constexpr int kDecodeRecs = kPartChunk / kDecodeThreads;   // records per decode thread per chunk
 constexpr int kRing = 2;                           // TMA ring depth (input chunks)
-constexpr int kInbox = 3;                          // consumer inbox depth (exchange chunks)
-constexpr int kStage = 3;                          // staging buffers (decode k+1 never waits for chunk k's store)
+#ifndef GPA_PART_INBOX
+#define GPA_PART_INBOX 3
+#endif
+constexpr int kInbox = GPA_PART_INBOX;                          // consumer inbox depth (exchange chunks)
+#ifndef GPA_PART_STAGE
+#define GPA_PART_STAGE 3
+#endif
+constexpr int kStage = GPA_PART_STAGE;                          // staging buffers (decode k+1 never waits for chunk k's store)
 constexpr int kTrash = 32;                         // lane-distinct sink for dropped keys / padding
 constexpr uint32_t kLocalBits = 13;                // key = local bin (13 bits) | count (3 bits)
 constexpr uint32_t kMaxKeyCount = 7;
 constexpr uint64_t kWrapGuard = (uint64_t)kPartMaxCtas * kPartCap * kMaxKeyCount;   // max samples per chunk
-static_assert(kPartChunk % (2 * kDecodeThreads) == 0, "whole record pairs per decode thread");
+// exchange chunk sizes (records per CTA per round), largest first: the launch takes the largest
+// whose shared-memory footprint fits next to the program's table
+constexpr int kChunkStep = 2 * kDecodeThreads;     // whole record pairs per decode thread
+constexpr int kNumChunkSizes = 4;
+__host__ __device__ constexpr int chunk_size(int i) { return kPartChunk - i * kChunkStep; }
+static_assert(kPartChunk % kChunkStep == 0 && chunk_size(kNumChunkSizes - 1) > 0, "chunk sizes");
 static_assert((kPartCap * 2) % 16 == 0, "slots must be whole 16-byte units for bulk copies");
 static_assert(kConsBase + kConsThreads == kPartThreads, "warp roles cover the CTA");
 
@@ -248,6 +271,13 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
   uint64_t pol;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   return pol;
+}
+
+__device__ __forceinline__ void tma_bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
 }
 
 __device__ __forceinline__ void tma_bulk_load_ef(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
@@ -281,14 +311,16 @@ __device__ __forceinline__ void tma_tile_load_2d(void *dst, const CUtensorMap *t
       : "memory");
 }
 
+template <int CHUNK>
 __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, const __grid_constant__ CUtensorMap xmap) {
+  constexpr int kDecodeRecs = CHUNK / kDecodeThreads;   // records per decode thread per chunk
   extern __shared__ __align__(128) uint8_t sm[];
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t G = gridDim.x, me = blockIdx.x;
   const uint32_t slot_keys = G * kPartCap;                                       // keys per staging / inbox buffer
   const uint32_t ibuf_keys = ((slot_keys * 2 + 127) & ~127u) / 2;             // 128-B aligned buffers (TMA)
   uint2 *ring = reinterpret_cast<uint2 *>(sm);                                   // [kRing][chunk] records
-  uint16_t *inbox = reinterpret_cast<uint16_t *>(sm + kRing * kPartChunk * 8); // [kInbox][G src][cap]
+  uint16_t *inbox = reinterpret_cast<uint16_t *>(sm + kRing * CHUNK * 8); // [kInbox][G src][cap]
   uint16_t *stag = inbox + kInbox * ibuf_keys;                                  // [kStage][G dst][cap]
   uint32_t *trash = reinterpret_cast<uint32_t *>(stag + kStage * ibuf_keys);    // [kTrash]
   uint32_t *cnt = trash + kTrash;                                                // [kStage][kPartMaxCtas + 8]
@@ -298,15 +330,15 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
   uint64_t *decoded = buf_ready + kStage;                                        // [kStage]  decoders -> control
   uint64_t *inbox_full = decoded + kStage;                                       // [kInbox]  TMA -> consumers
   uint64_t *inbox_free = inbox_full + kInbox;                                    // [kInbox]  consumers -> loader
-  uint64_t *stored = inbox_free + kInbox;                                        // [kStage]  control -> publisher
-  uint32_t *tab = reinterpret_cast<uint32_t *>(stored + kStage);                // [bpb + kTrash]
+  uint64_t *stored = inbox_free + kInbox;   // [kPartBufs] control -> publisher (control runs at most
+                                            // kPartBufs-1 chunks ahead: see the cons-counter wait)
+  uint32_t *tab = reinterpret_cast<uint32_t *>(stored + kPartBufs);                // [bpb + kTrash]
   for (uint32_t i = tid; i < a.bpb + kTrash; i += kPartThreads) tab[i] = 0;
   for (uint32_t i = tid; i < kStage * ibuf_keys / 2; i += kPartThreads) reinterpret_cast<uint32_t *>(stag)[i] = 0;
   for (uint32_t i = tid; i < kStage * (kPartMaxCtas + 8); i += kPartThreads) cnt[i] = 0;
   if (tid == 0) {
     for (int r = 0; r < kRing; ++r) mbar_init(&ring_full[r], 1);
     for (int r = 0; r < kStage; ++r) {
-      mbar_init(&stored[r], 1);
       mbar_init(&buf_ready[r], 1);
       mbar_init(&decoded[r], kDecodeWarps);
     }
@@ -314,16 +346,17 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
       mbar_init(&inbox_full[r], 1);
       mbar_init(&inbox_free[r], 1);
     }
+    for (int r = 0; r < kPartBufs; ++r) mbar_init(&stored[r], 1);
     ctotal[0] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const uint64_t per_chunk = (uint64_t)kPartChunk * G;
+  const uint64_t per_chunk = (uint64_t)CHUNK * G;
   const uint32_t n_chunks = (uint32_t)((a.n_even + per_chunk - 1) / per_chunk);
   auto slice_len = [&](uint32_t k, uint64_t &start) -> uint32_t {
-    start = (uint64_t)k * per_chunk + (uint64_t)me * kPartChunk;
+    start = (uint64_t)k * per_chunk + (uint64_t)me * CHUNK;
     return start >= a.n_even ? 0u
-                             : (uint32_t)(a.n_even - start < (uint64_t)kPartChunk ? a.n_even - start : (uint64_t)kPartChunk);
+                             : (uint32_t)(a.n_even - start < (uint64_t)CHUNK ? a.n_even - start : (uint64_t)CHUNK);
   };
   // row (buf, src) of the exchange: G slots of kPartCap keys, one per destination; a producer
   // writes its row with one bulk store, a consumer reads its column (x = dst * cap) with one
@@ -332,6 +365,7 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
     return a.X + ((uint64_t)buf * kPartMaxCtas + src) * G * kPartCap;
   };
   const uint32_t twoR = 2 * a.R;
+  const uint32_t zero_keys_bytes = (slot_keys * 2 + 15) & ~15u, zero_cnt_bytes = ((G + 1) * 4 + 15) & ~15u;
   IngestStats st{0, 0, 0};
   if (warp < kDecodeWarps) {
     // ======================= decoders: wait only on data (ring_full) and on a clean staging
@@ -339,12 +373,13 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
     const uint32_t dtid = tid;
     const uint32_t n_instr = a.n_instr, R = a.R, mg = a.mg;
     const uint32_t trash_addr = smem_addr(trash + lane);
+    PT_DECL
     for (uint32_t k = 0; k < n_chunks; ++k) {
       uint64_t s0;
       const uint32_t len = slice_len(k, s0);
       const uint32_t sb = k % kStage;
       const uint32_t sg_addr = smem_addr(stag + sb * ibuf_keys), cnt_addr = smem_addr(cnt + sb * (kPartMaxCtas + 8));
-      PT_DECL
+      PT_START;
       mbar_wait(&buf_ready[sb], (k / kStage) & 1);       // staging buffer + counters clean
       PT_MARK(0);
       if (len) mbar_wait(&ring_full[k % kRing], (k / kRing) & 1);
@@ -353,9 +388,9 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
       //      bin (pc / G) * 2R + class * R + reason | count << 13, stored at position cnt[b]++ of
       //      bucket b's zero-padded slot (invalid and padding records count in the dummy bucket G
       //      and land in a trash word; counts > 7 and slot overflow go through L2 atomics)
-      const uint4 *rs = reinterpret_cast<const uint4 *>(ring + (k % kRing) * kPartChunk);
+      const uint4 *rs = reinterpret_cast<const uint4 *>(ring + (k % kRing) * CHUNK);
       uint32_t csum = 0, bads = 0, badr = 0;
-      const bool full = len == (uint32_t)kPartChunk;
+      const bool full = len == (uint32_t)CHUNK;
 #pragma unroll
       for (int u = 0; u < kDecodeRecs / 2; ++u) {
         const uint32_t pair = u * kDecodeThreads + dtid;
@@ -392,6 +427,7 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
       if (lane == 0) mbar_arrive(&decoded[sb]);          // ring slot and staging buffer handed over
       PT_MARK(2);
     }
+    PT_FLUSH;
   } else if (warp == kCtrlWarp) {
     // ======================= control: TMA ring refills, exchange stores, publication, recycling
     const uint64_t pol = evict_first_policy();
@@ -400,16 +436,17 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
       const uint32_t len = slice_len(k, s0);
       if (len) {
         mbar_expect_tx(&ring_full[k % kRing], len * 8);
-        tma_bulk_load_ef(ring + (k % kRing) * kPartChunk, a.rec + s0, len * 8, &ring_full[k % kRing], pol);
+        tma_bulk_load_ef(ring + (k % kRing) * CHUNK, a.rec + s0, len * 8, &ring_full[k % kRing], pol);
       }
     };
     if (lane == 0) {
       for (uint32_t k = 0; k < (uint32_t)kRing && k < n_chunks; ++k) issue(k);
       for (int r = 0; r < kStage; ++r) mbar_arrive(&buf_ready[r]);
     }
+    PT_DECL
     for (uint32_t k = 0; k < n_chunks; ++k) {
       const uint32_t sb = k % kStage, buf = k % kPartBufs;
-      PT_DECL
+      PT_START;
       mbar_wait(&decoded[sb], (k / kStage) & 1);        // all decoders finished chunk k
       PT_MARK(3);
       if (lane == 0) {
@@ -425,35 +462,53 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
         if (k > 0) {   // chunk k-1's store is complete: hand it to the publisher warp
           asm volatile("cp.async.bulk.wait_group 1;" ::: "memory");
           fence_proxy_async_global();
-          mbar_arrive(&stored[(k - 1) % kStage]);
+          mbar_arrive(&stored[(k - 1) % kPartBufs]);
           PT_MARK(5);
+#ifdef GPA_PART_TMA_ZERO
+          if (k + kStage - 1 < n_chunks) {   // recycle chunk k-1's staging buffer + counters for chunk
+            const uint32_t ob = (k - 1) % kStage;   // k+kStage-1: the TMA engine copies zeros over them
+            mbar_expect_tx(&buf_ready[ob], zero_keys_bytes + zero_cnt_bytes);
+            tma_bulk_load(stag + ob * ibuf_keys, a.zero, zero_keys_bytes, &buf_ready[ob]);
+            tma_bulk_load(cnt + ob * (kPartMaxCtas + 8), a.zero + zero_keys_bytes, zero_cnt_bytes, &buf_ready[ob]);
+            PT_MARK(7);
+          }
+#endif
         }
       }
       __syncwarp();
-      if (k > 0 && k + kStage - 1 < n_chunks) {   // recycle chunk k-1's staging buffer for chunk k+kStage-1
-        const uint32_t ob = (k - 1) % kStage;
+    }
+    PT_FLUSH;
+    if (n_chunks && lane == 0) {
+      bulk_wait_all();
+      fence_proxy_async_global();
+      mbar_arrive(&stored[(n_chunks - 1) % kPartBufs]);
+    }
+  } else if (warp == kPubWarp) {
+    // ======================= publisher: release each stored chunk to the other CTAs, then clear
+    //                         its staging buffer and counters for chunk k+kStage
+    PT_DECL
+    for (uint32_t k = 0; k < n_chunks; ++k) {
+      PT_START;
+      mbar_wait(&stored[k % kPartBufs], (k / kPartBufs) & 1);   // chunk k's store has completed
+      PT_MARK(14);
+      if (lane == 0) {
+        fence_proxy_async_global();
+        red_release_add(&a.sync[k % kPartBufs], 1u);   // this CTA produced chunk k
+      }
+      PT_MARK(15);
+#ifndef GPA_PART_TMA_ZERO
+      if (k + kStage < n_chunks) {
+        const uint32_t ob = k % kStage;
         uint4 *z = reinterpret_cast<uint4 *>(stag + ob * ibuf_keys);
         for (uint32_t i = lane; i < slot_keys / 8; i += 32) z[i] = make_uint4(0, 0, 0, 0);
         for (uint32_t i = lane; i <= G; i += 32) cnt[ob * (kPartMaxCtas + 8) + i] = 0;
         __syncwarp();
         if (lane == 0) mbar_arrive(&buf_ready[ob]);
-        PT_MARK(7);
       }
+      PT_MARK(7);
+#endif
     }
-    if (n_chunks && lane == 0) {
-      bulk_wait_all();
-      fence_proxy_async_global();
-      mbar_arrive(&stored[(n_chunks - 1) % kStage]);
-    }
-  } else if (warp == kPubWarp) {
-    // ======================= publisher: release each stored chunk to the other CTAs
-    if (lane == 0) {
-      for (uint32_t k = 0; k < n_chunks; ++k) {
-        mbar_wait(&stored[k % kStage], (k / kStage) & 1);
-        fence_proxy_async_global();
-        red_release_add(&a.sync[k % kPartBufs], 1u);   // this CTA produced chunk k
-      }
-    }
+    PT_FLUSH;
   } else {
     // ======================= consumers: warp kLoaderWarp fetches my column of each exchange
     //                         buffer into the kInbox-deep smem inbox (one 2-D TMA tile load per
@@ -461,33 +516,49 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
     //                         the other warps only wait on their data and add keys to the table
     if (warp == kLoaderWarp) {
       if (lane == 0) {
+        PT_DECL
         for (uint32_t j = 0; j < n_chunks; ++j) {
+          PT_START;
           if (j >= (uint32_t)kInbox) mbar_wait(&inbox_free[j % kInbox], ((j / kInbox) + 1) & 1);
+          PT_MARK(12);
           spin_until(&a.sync[j % kPartBufs], G * (j / kPartBufs + 1));
+          PT_MARK(13);
           fence_proxy_async_global();
           mbar_expect_tx(&inbox_full[j % kInbox], slot_keys * 2);
           tma_tile_load_2d(inbox + (j % kInbox) * ibuf_keys, &xmap, me * kPartCap, (j % kPartBufs) * kPartMaxCtas,
                            &inbox_full[j % kInbox]);
         }
+        PT_FLUSH;
       }
     } else {
       const uint32_t ctid = tid - kProcBase;
       const uint32_t tab_addr = smem_addr(tab), dummy_addr = smem_addr(tab + a.bpb + (ctid & 31));
+      PT_DECL
       for (uint32_t j = 0; j < n_chunks; ++j) {
-        PT_DECL
+        PT_START;
         mbar_wait(&inbox_full[j % kInbox], (j / kInbox) & 1);
         PT_MARK(9);
         const uint4 *in4 = reinterpret_cast<const uint4 *>(inbox + (j % kInbox) * ibuf_keys);
         uint32_t tot = 0;
         for (uint32_t v = ctid; v < slot_keys / 8; v += kProcThreads) {
           const uint4 kv = in4[v];
+#ifndef GPA_PART_NO_SKIP
+          if ((kv.x | kv.y | kv.z | kv.w) == 0) continue;   // all padding (slot tails): no work
+#endif
           const uint32_t w4[4] = {kv.x, kv.y, kv.z, kv.w};
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             const uint32_t key = (w4[e >> 1] >> ((e & 1) * 16)) & 0xffffu;
             const uint32_t c = key >> kLocalBits;
+#ifndef GPA_PART_PRED_RED
             const uint32_t addr = c ? tab_addr + (key & ((1u << kLocalBits) - 1)) * 4 : dummy_addr;   // padding -> dummy
             asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(c) : "memory");
+#else
+            const uint32_t addr = tab_addr + (key & ((1u << kLocalBits) - 1)) * 4;   // padding (c = 0) skipped
+            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t@p red.shared.add.u32 [%0], %1;\n\t}" ::"r"(addr),
+                         "r"(c)
+                         : "memory");
+#endif
             tot += c;
           }
         }
@@ -512,6 +583,7 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
           named_bar(2, kProcThreads);
         }
       }
+      PT_FLUSH;
     }
   }
   __syncthreads();
@@ -572,10 +644,10 @@ extern "C" int gpa_debug_read_timing(unsigned long long *out) {
 }
 #endif
 
-size_t part_smem_bytes(uint32_t bpb, uint32_t G) {
+size_t part_smem_bytes(uint32_t bpb, uint32_t G, int chunk) {
   const size_t ibuf = ((size_t)G * kPartCap * 2 + 127) & ~(size_t)127;
-  return (size_t)kRing * kPartChunk * 8 + (kInbox + kStage) * ibuf + kTrash * 4 + kStage * (kPartMaxCtas + 8) * 4 + 16 +
-         (kRing + 3 * kStage + 2 * kInbox) * 8 + (size_t)(bpb + kTrash) * 4;
+  return (size_t)kRing * chunk * 8 + (kInbox + kStage) * ibuf + kTrash * 4 + kStage * (kPartMaxCtas + 8) * 4 + 16 +
+         (kRing + 2 * kStage + kPartBufs + 2 * kInbox) * 8 + (size_t)(bpb + kTrash) * 4;
 }
 
 static uint32_t part_grid(int n_sms) { return (uint32_t)std::min(n_sms, kPartMaxCtas); }
@@ -589,9 +661,17 @@ static bool part_shape(const DevProgram &p, int n_sms, uint32_t &G, uint32_t &pp
   return ppb < 4096 && bpb < (1u << kLocalBits) && G <= 256;   // 2-byte keys: 13-bit local bins; TMA box <= 256
 }
 
-bool part_feasible(const DevProgram &p, int n_sms, size_t smem_optin) {
+// index of the largest exchange chunk that fits, or -1
+static int part_chunk_index(const DevProgram &p, int n_sms, size_t smem_optin) {
   uint32_t G, ppb, bpb;
-  return part_shape(p, n_sms, G, ppb, bpb) && part_smem_bytes(bpb, G) + 256 <= smem_optin;
+  if (!part_shape(p, n_sms, G, ppb, bpb)) return -1;
+  for (int i = 0; i < kNumChunkSizes; ++i)
+    if (part_smem_bytes(bpb, G, chunk_size(i)) + 256 <= smem_optin) return i;
+  return -1;
+}
+
+bool part_feasible(const DevProgram &p, int n_sms, size_t smem_optin) {
+  return part_chunk_index(p, n_sms, smem_optin) >= 0;
 }
 
 size_t ingest_smem_bytes(const DevProgram &p) { return (size_t)p.n * 2 * p.R * 4; }
@@ -623,7 +703,8 @@ cudaError_t launch_ingest(const DevProgram &p, int variant, const void *records,
     return cudaGetLastError();
   }
   if (variant == VAR_PART) {
-    if (!part_feasible(p, n_sms, smem_optin)) return cudaErrorInvalidValue;
+    const int ci = part_chunk_index(p, n_sms, smem_optin);
+    if (ci < 0) return cudaErrorInvalidValue;
     uint32_t G, ppb, bpb;
     part_shape(p, n_sms, G, ppb, bpb);
     PartArgs a;
@@ -639,8 +720,15 @@ cudaError_t launch_ingest(const DevProgram &p, int variant, const void *records,
     a.stats = p.stats;
     a.X = reinterpret_cast<uint16_t *>(p.part_x);
     a.sync = p.part_sync;
-    const size_t smem = part_smem_bytes(a.bpb, G);
-    cudaError_t e = cudaFuncSetAttribute(k_ingest_part, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    a.zero = p.part_zero;
+    static const void *const kernels[kNumChunkSizes] = {(const void *)k_ingest_part<chunk_size(0)>,
+                                                         (const void *)k_ingest_part<chunk_size(1)>,
+                                                         (const void *)k_ingest_part<chunk_size(2)>,
+                                                         (const void *)k_ingest_part<chunk_size(3)>};
+    static_assert(kNumChunkSizes == 4, "kernel table");
+    const void *kern = kernels[ci];
+    const size_t smem = part_smem_bytes(a.bpb, G, chunk_size(ci));
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(p.part_sync, 0, 2 * kPartBufs * sizeof(unsigned int), s);
     if (e != cudaSuccess) return e;
@@ -654,7 +742,7 @@ cudaError_t launch_ingest(const DevProgram &p, int variant, const void *records,
     e = make_exchange_map(&xmap, p.part_x, G);
     if (e != cudaSuccess) return e;
     void *args[] = {&a, &xmap};
-    return cudaLaunchCooperativeKernel((const void *)k_ingest_part, dim3(G), dim3(kPartThreads), args, smem, s);
+    return cudaLaunchCooperativeKernel(kern, dim3(G), dim3(kPartThreads), args, smem, s);
   }
   return cudaErrorNotSupported;
 }

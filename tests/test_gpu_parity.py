@@ -82,6 +82,18 @@ def test_part_ragged_and_small_streams(n_rec, offset):
     compare(g, run_oracle(prog, recs), rel=REL)
 
 
+@pytest.mark.parametrize("n_instr,R", [(65_000, 9), (37_000, 16)])
+def test_part_large_tables_smaller_chunk(n_instr, R):
+    """Per-CTA tables of 7920 / 8000 bins (13-bit local keys, near the limit): the 6400-record
+    exchange chunk no longer fits next to the table in shared memory and the launch takes the
+    5120-record instantiation."""
+    prog = gp.random_program(n_instr, 8, 40, 6, seed=51, n_reasons=R)
+    recs = StreamSpec(prog, seed=52, count_max=5, invalid_ppm=1_000).host(0, 3_000_001)
+    g = run_gpu(prog, recs, offset_records=1)
+    assert g["program"].variant == "part"
+    compare(g, run_oracle(prog, recs), rel=REL)
+
+
 def test_part_skewed_stream_overflow():
     """A hot PC takes half the samples: its bucket overflows the exchange slots and the excess
     goes through L2 atomics; counts stay exact."""

@@ -1,29 +1,35 @@
-"""Build a GPA_PART_TIMING variant of the library, run the config-3 ingest once, print phase cycles."""
-import ctypes, os, subprocess, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+"""Build-variant probe: run the config-3 ingest with the GPA_PART_TIMING library (build/libgpa_timing.so,
+built by paper_2009_04061_b200.build.build_variant) and print the per-role phase cycles.
+Each thread accumulates its phases in registers and adds them to the global timers once."""
+import ctypes, os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-import numpy as np, torch
+sys.path.insert(0, ROOT)
+import torch
 import gpagen
 from paper_2009_04061_b200 import gpa as G
-lib_path = os.path.join(ROOT, "build", "libgpa_timing.so")
-G.LIB_PATH = lib_path
+
+G.LIB_PATH = os.path.join(ROOT, "build", "libgpa_timing.so")
 lib = G.lib()
 prog = gpagen.config_program(3)
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 200_000_000
 recs = gpagen.config_stream(prog, 3).device(0, n)
 P = G.Program(prog)
-for it in range(2):
-    P.reset(); P.ingest(recs); torch.cuda.synchronize()
-# read the device symbol via cudaMemcpyFromSymbol through a tiny helper: use cuda-python-free route
-cudart = ctypes.CDLL("libcudart.so") if False else None
-names = ["dec:wait_buf", "dec:wait_ring", "dec:decode", "ctl:wait_decoded", "ctl:spin_cons+tma", "ctl:wait_store",
-         "ctl:publish", "ctl:recycle", "con:fetch(spin)", "con:wait_inbox", "con:process", "con:barrier"]
 buf = (ctypes.c_ulonglong * 16)()
 lib.gpa_debug_read_timing.argtypes = [ctypes.c_void_p]
-lib.gpa_debug_read_timing(buf)
-tot_dec = sum(buf[i] for i in range(3)) or 1
-tot_ctl = sum(buf[i] for i in range(3, 8)) or 1
-tot_con = sum(buf[i] for i in range(8, 12)) or 1
-for i, nm in enumerate(names):
-    grp = tot_dec if i < 3 else tot_ctl if i < 8 else tot_con
-    print(f"{nm:22s} {buf[i]/1e9:10.3f} Gcyc  {100*buf[i]/grp:5.1f}% of role")
+for it in range(2):      # the second pass is the measured one
+    lib.gpa_debug_read_timing(buf)
+    before = list(buf)
+    P.reset(); P.ingest(recs); torch.cuda.synchronize()
+    lib.gpa_debug_read_timing(buf)
+delta = [buf[i] - before[i] for i in range(16)]
+roles = {
+    "decoders (per warp)": ([0, 1, 2], ["wait_buf", "wait_ring", "decode"]),
+    "control": ([3, 4, 5, 7], ["wait_decoded", "tma+spin_cons", "store+wait_group", "recycle"]),
+    "processors (per warp)": ([9, 10, 11], ["wait_inbox", "process", "barrier"]),
+    "loader": ([12, 13], ["wait_inbox_free", "spin_prod"]),
+    "publisher": ([14, 15], ["wait_stored", "publish"]),
+}
+for role, (slots, names) in roles.items():
+    tot = sum(delta[s] for s in slots) or 1
+    print(role + ": " + ", ".join(f"{nm} {100 * delta[s] / tot:.1f}%" for s, nm in zip(slots, names))
+          + f"  (total {tot / 1e9:.2f} Gcyc)")
