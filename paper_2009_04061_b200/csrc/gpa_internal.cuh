@@ -28,8 +28,7 @@ constexpr int kPartBufs = 16;               // exchange buffers in flight
 constexpr int kPartCap = GPA_PART_CAP;                // keys per (src, dst) slot per chunk (mean 38.1 at G=148);
                                             // excess -> L2 atomics
 constexpr int kPartMaxCtas = 160;           // < 255: bucket ids fit a byte
-constexpr int kPartZeroBytes = kPartMaxCtas * kPartCap * 2 + 128 + (kPartMaxCtas + 8) * 4;   // >= one staging buffer + counters
-size_t part_smem_bytes(uint32_t bpb, uint32_t G, int chunk);
+size_t part_smem_bytes(uint32_t bpb, uint32_t G);
 
 // stall reasons
 constexpr uint32_t R_NONE = 0, R_MEM = 1, R_EXEC = 2, R_SYNC = 3;
@@ -62,7 +61,6 @@ struct DevProgram {
   uint32_t *partials;               // [kMaxIngestCtas][n*2R] per-CTA tables (smem variant)
   uint32_t *part_x;                 // [kPartBufs][kPartMaxCtas dst][G src][kPartCap] 2-byte exchange keys
   unsigned int *part_sync;          // [2*kPartBufs]: per exchange buffer, CTAs that produced / consumed it
-  const uint8_t *part_zero;         // [kPartZeroBytes] zeros (TMA source that clears staging buffers)
   uint8_t *cand, *selfm;
   double *share, *B;
 };

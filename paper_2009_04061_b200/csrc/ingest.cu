@@ -217,7 +217,6 @@ struct PartArgs {
   uint32_t mg;            // ceil(2^32 / G): pc / G = umulhi(pc, mg), exact for pc < 2^32 / G
   uint64_t *C, *stats;
   uint16_t *X;            // [kPartBufs][src < kPartMaxCtas][dst < G][kPartCap] 2-byte keys, zero-padded
-  const uint8_t *zero;    // kPartZeroBytes of zeros in global memory (L2-resident)
   unsigned int *sync;     // [kPartBufs] produced, [kPartBufs] consumed
 };
 
@@ -235,7 +234,6 @@ constexpr int kProcThreads = (kConsWarps - 1) * 32;
 constexpr int kDecodeThreads = kDecodeWarps * 32;
 constexpr int kConsThreads = kConsWarps * 32;
 constexpr int kConsBase = (kPubWarp + 1) * 32;
-constexpr int kRing = 2;                           // TMA ring depth (input chunks)
 #ifndef GPA_PART_INBOX
 #define GPA_PART_INBOX 3
 #endif
@@ -247,13 +245,10 @@ constexpr int kStage = GPA_PART_STAGE;                          // staging buffe
 constexpr int kTrash = 32;                         // lane-distinct sink for dropped keys / padding
 constexpr uint32_t kLocalBits = 13;                // key = local bin (13 bits) | count (3 bits)
 constexpr uint32_t kMaxKeyCount = 7;
-constexpr uint64_t kWrapGuard = (uint64_t)kPartMaxCtas * kPartCap * kMaxKeyCount;   // max samples per chunk
-// exchange chunk sizes (records per CTA per round), largest first: the launch takes the largest
-// whose shared-memory footprint fits next to the program's table
-constexpr int kChunkStep = 2 * kDecodeThreads;     // whole record pairs per decode thread
-constexpr int kNumChunkSizes = 4;
-__host__ __device__ constexpr int chunk_size(int i) { return kPartChunk - i * kChunkStep; }
-static_assert(kPartChunk % kChunkStep == 0 && chunk_size(kNumChunkSizes - 1) > 0, "chunk sizes");
+// a chunk adds at most G * cap * 7 samples to any one table entry: flushing the u32 table every
+// kFlushEvery chunks keeps every entry below 2^32
+constexpr uint32_t kFlushEvery = (uint32_t)(0xffffffffull / ((uint64_t)kPartMaxCtas * kPartCap * kMaxKeyCount));
+static_assert(kPartChunk % (2 * kDecodeThreads) == 0, "whole record pairs per decode thread");
 static_assert((kPartCap * 2) % 16 == 0, "slots must be whole 16-byte units for bulk copies");
 static_assert(kConsBase + kConsThreads == kPartThreads, "warp roles cover the CTA");
 
@@ -265,28 +260,6 @@ __device__ __forceinline__ void red_release_add(unsigned int *p, unsigned int v)
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
-}
-
-__device__ __forceinline__ uint64_t evict_first_policy() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-
-__device__ __forceinline__ void tma_bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_addr(dst)),
-               "l"(src), "r"(bytes), "r"(smem_addr(bar))
-               : "memory");
-}
-
-__device__ __forceinline__ void tma_bulk_load_ef(void *dst, const void *src, uint32_t bytes, uint64_t *bar,
-                                                 uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-          smem_addr(dst)),
-      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
-      : "memory");
 }
 
 // shared -> global bulk copy (async proxy), tracked by this thread's bulk async-groups
@@ -311,22 +284,19 @@ __device__ __forceinline__ void tma_tile_load_2d(void *dst, const CUtensorMap *t
       : "memory");
 }
 
-template <int CHUNK>
 __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, const __grid_constant__ CUtensorMap xmap) {
+  constexpr int CHUNK = kPartChunk;
   constexpr int kDecodeRecs = CHUNK / kDecodeThreads;   // records per decode thread per chunk
   extern __shared__ __align__(128) uint8_t sm[];
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t G = gridDim.x, me = blockIdx.x;
   const uint32_t slot_keys = G * kPartCap;                                       // keys per staging / inbox buffer
   const uint32_t ibuf_keys = ((slot_keys * 2 + 127) & ~127u) / 2;             // 128-B aligned buffers (TMA)
-  uint2 *ring = reinterpret_cast<uint2 *>(sm);                                   // [kRing][chunk] records
-  uint16_t *inbox = reinterpret_cast<uint16_t *>(sm + kRing * CHUNK * 8); // [kInbox][G src][cap]
+  uint16_t *inbox = reinterpret_cast<uint16_t *>(sm);                            // [kInbox][G src][cap]
   uint16_t *stag = inbox + kInbox * ibuf_keys;                                  // [kStage][G dst][cap]
   uint32_t *trash = reinterpret_cast<uint32_t *>(stag + kStage * ibuf_keys);    // [kTrash]
   uint32_t *cnt = trash + kTrash;                                                // [kStage][kPartMaxCtas + 8]
-  unsigned long long *ctotal = reinterpret_cast<unsigned long long *>(cnt + kStage * (kPartMaxCtas + 8));   // [2]
-  uint64_t *ring_full = reinterpret_cast<uint64_t *>(ctotal + 2);                // [kRing]   TMA -> decoders
-  uint64_t *buf_ready = ring_full + kRing;                                       // [kStage]  control -> decoders
+  uint64_t *buf_ready = reinterpret_cast<uint64_t *>(cnt + kStage * (kPartMaxCtas + 8));   // [kStage] publisher -> decoders
   uint64_t *decoded = buf_ready + kStage;                                        // [kStage]  decoders -> control
   uint64_t *inbox_full = decoded + kStage;                                       // [kInbox]  TMA -> consumers
   uint64_t *inbox_free = inbox_full + kInbox;                                    // [kInbox]  consumers -> loader
@@ -337,7 +307,6 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
   for (uint32_t i = tid; i < kStage * ibuf_keys / 2; i += kPartThreads) reinterpret_cast<uint32_t *>(stag)[i] = 0;
   for (uint32_t i = tid; i < kStage * (kPartMaxCtas + 8); i += kPartThreads) cnt[i] = 0;
   if (tid == 0) {
-    for (int r = 0; r < kRing; ++r) mbar_init(&ring_full[r], 1);
     for (int r = 0; r < kStage; ++r) {
       mbar_init(&buf_ready[r], 1);
       mbar_init(&decoded[r], kDecodeWarps);
@@ -347,7 +316,6 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
       mbar_init(&inbox_free[r], 1);
     }
     for (int r = 0; r < kPartBufs; ++r) mbar_init(&stored[r], 1);
-    ctotal[0] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -365,7 +333,6 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
     return a.X + ((uint64_t)buf * kPartMaxCtas + src) * G * kPartCap;
   };
   const uint32_t twoR = 2 * a.R;
-  const uint32_t zero_keys_bytes = (slot_keys * 2 + 15) & ~15u, zero_cnt_bytes = ((G + 1) * 4 + 15) & ~15u;
   IngestStats st{0, 0, 0};
   if (warp < kDecodeWarps) {
     // ======================= decoders: wait only on data (ring_full) and on a clean staging
@@ -379,23 +346,26 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
       const uint32_t len = slice_len(k, s0);
       const uint32_t sb = k % kStage;
       const uint32_t sg_addr = smem_addr(stag + sb * ibuf_keys), cnt_addr = smem_addr(cnt + sb * (kPartMaxCtas + 8));
+      const uint4 *rs = reinterpret_cast<const uint4 *>(a.rec + s0);
+      const bool full = len == (uint32_t)CHUNK;
       PT_START;
+      uint4 vv[kDecodeRecs / 2];   // 16-byte streaming loads, in flight while waiting for the buffer
+#pragma unroll
+      for (int u = 0; u < kDecodeRecs / 2; ++u) {
+        const uint32_t pair = u * kDecodeThreads + dtid;   // len is even: both records of a pair or neither
+        vv[u] = (full || 2 * pair < len) ? ld_stream(rs + pair) : make_uint4(0xffffffffu, 0, 0xffffffffu, 0);
+      }
       mbar_wait(&buf_ready[sb], (k / kStage) & 1);       // staging buffer + counters clean
       PT_MARK(0);
-      if (len) mbar_wait(&ring_full[k % kRing], (k / kRing) & 1);
-      PT_MARK(1);
       // ---- branch-free decode: bucket = pc mod G (interleaved PCs balance the load), key = local
       //      bin (pc / G) * 2R + class * R + reason | count << 13, stored at position cnt[b]++ of
       //      bucket b's zero-padded slot (invalid and padding records count in the dummy bucket G
       //      and land in a trash word; counts > 7 and slot overflow go through L2 atomics)
-      const uint4 *rs = reinterpret_cast<const uint4 *>(ring + (k % kRing) * CHUNK);
       uint32_t csum = 0, bads = 0, badr = 0;
-      const bool full = len == (uint32_t)CHUNK;
 #pragma unroll
       for (int u = 0; u < kDecodeRecs / 2; ++u) {
-        const uint32_t pair = u * kDecodeThreads + dtid;
-        const bool in = full || 2 * pair < len;   // len is even: both records of the pair or neither
-        const uint4 v = in ? rs[pair] : make_uint4(0xffffffffu, 0, 0xffffffffu, 0);
+        const bool in = full || 2 * (u * kDecodeThreads + dtid) < len;
+        const uint4 v = vv[u];
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const uint32_t pc = h ? v.z : v.x, w = h ? v.w : v.y;
@@ -424,25 +394,15 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
       // generic-proxy staging writes must be ordered before the control warp's bulk store
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(&decoded[sb]);          // ring slot and staging buffer handed over
+      if (lane == 0) mbar_arrive(&decoded[sb]);          // staging buffer handed over
       PT_MARK(2);
     }
     PT_FLUSH;
   } else if (warp == kCtrlWarp) {
-    // ======================= control: TMA ring refills, exchange stores, publication, recycling
-    const uint64_t pol = evict_first_policy();
-    auto issue = [&](uint32_t k) {
-      uint64_t s0;
-      const uint32_t len = slice_len(k, s0);
-      if (len) {
-        mbar_expect_tx(&ring_full[k % kRing], len * 8);
-        tma_bulk_load_ef(ring + (k % kRing) * CHUNK, a.rec + s0, len * 8, &ring_full[k % kRing], pol);
-      }
-    };
-    if (lane == 0) {
-      for (uint32_t k = 0; k < (uint32_t)kRing && k < n_chunks; ++k) issue(k);
+    // ======================= control: one bulk store of the CTA's row per chunk, completed
+    //                         stores handed to the publisher
+    if (lane == 0)
       for (int r = 0; r < kStage; ++r) mbar_arrive(&buf_ready[r]);
-    }
     PT_DECL
     for (uint32_t k = 0; k < n_chunks; ++k) {
       const uint32_t sb = k % kStage, buf = k % kPartBufs;
@@ -450,10 +410,6 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
       mbar_wait(&decoded[sb], (k / kStage) & 1);        // all decoders finished chunk k
       PT_MARK(3);
       if (lane == 0) {
-        if (k + kRing < n_chunks) {                       // ring slot k%kRing is free again
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          issue(k + kRing);
-        }
         // exchange buffer k%NBUF is free once every CTA drained chunk k-NBUF
         if (k >= (uint32_t)kPartBufs) spin_until(&a.sync[kPartBufs + buf], G * (k / kPartBufs));
         PT_MARK(4);
@@ -464,15 +420,6 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
           fence_proxy_async_global();
           mbar_arrive(&stored[(k - 1) % kPartBufs]);
           PT_MARK(5);
-#ifdef GPA_PART_TMA_ZERO
-          if (k + kStage - 1 < n_chunks) {   // recycle chunk k-1's staging buffer + counters for chunk
-            const uint32_t ob = (k - 1) % kStage;   // k+kStage-1: the TMA engine copies zeros over them
-            mbar_expect_tx(&buf_ready[ob], zero_keys_bytes + zero_cnt_bytes);
-            tma_bulk_load(stag + ob * ibuf_keys, a.zero, zero_keys_bytes, &buf_ready[ob]);
-            tma_bulk_load(cnt + ob * (kPartMaxCtas + 8), a.zero + zero_keys_bytes, zero_cnt_bytes, &buf_ready[ob]);
-            PT_MARK(7);
-          }
-#endif
         }
       }
       __syncwarp();
@@ -496,7 +443,6 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
         red_release_add(&a.sync[k % kPartBufs], 1u);   // this CTA produced chunk k
       }
       PT_MARK(15);
-#ifndef GPA_PART_TMA_ZERO
       if (k + kStage < n_chunks) {
         const uint32_t ob = k % kStage;
         uint4 *z = reinterpret_cast<uint4 *>(stag + ob * ibuf_keys);
@@ -506,7 +452,6 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
         if (lane == 0) mbar_arrive(&buf_ready[ob]);
       }
       PT_MARK(7);
-#endif
     }
     PT_FLUSH;
   } else {
@@ -539,32 +484,19 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
         mbar_wait(&inbox_full[j % kInbox], (j / kInbox) & 1);
         PT_MARK(9);
         const uint4 *in4 = reinterpret_cast<const uint4 *>(inbox + (j % kInbox) * ibuf_keys);
-        uint32_t tot = 0;
         for (uint32_t v = ctid; v < slot_keys / 8; v += kProcThreads) {
           const uint4 kv = in4[v];
-#ifndef GPA_PART_NO_SKIP
-          if ((kv.x | kv.y | kv.z | kv.w) == 0) continue;   // all padding (slot tails): no work
-#endif
           const uint32_t w4[4] = {kv.x, kv.y, kv.z, kv.w};
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             const uint32_t key = (w4[e >> 1] >> ((e & 1) * 16)) & 0xffffu;
             const uint32_t c = key >> kLocalBits;
-#ifndef GPA_PART_PRED_RED
-            const uint32_t addr = c ? tab_addr + (key & ((1u << kLocalBits) - 1)) * 4 : dummy_addr;   // padding -> dummy
+            // padding keys (c = 0) add 0 to a lane-distinct dummy word: cheaper on the shared-memory
+            // pipe than a predicated (branching) update, measured
+            const uint32_t addr = c ? tab_addr + (key & ((1u << kLocalBits) - 1)) * 4 : dummy_addr;
             asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(c) : "memory");
-#else
-            const uint32_t addr = tab_addr + (key & ((1u << kLocalBits) - 1)) * 4;   // padding (c = 0) skipped
-            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t@p red.shared.add.u32 [%0], %1;\n\t}" ::"r"(addr),
-                         "r"(c)
-                         : "memory");
-#endif
-            tot += c;
           }
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-        if ((ctid & 31) == 0) atomicAdd(&ctotal[0], (unsigned long long)tot);
         PT_MARK(10);
         named_bar(2, kProcThreads);   // inbox slot j%kInbox fully read
         PT_MARK(11);
@@ -572,14 +504,12 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
           mbar_arrive(&inbox_free[j % kInbox]);
           red_release_add(&a.sync[kPartBufs + j % kPartBufs], 1u);   // this CTA drained chunk j
         }
-        if (ctotal[0] + kWrapGuard >= 0xffffffffull) {   // rare: flush the table to global and restart
+        if ((j + 1) % kFlushEvery == 0) {   // u32 table entries cannot wrap: flush every kFlushEvery chunks
           for (uint32_t i = ctid; i < a.bpb; i += kProcThreads) {
             const uint32_t bin = ((i / twoR) * G + me) * twoR + i % twoR;
             if (tab[i]) atomicAdd((unsigned long long *)&a.C[bin], (unsigned long long)tab[i]);
             tab[i] = 0;
           }
-          named_bar(2, kProcThreads);
-          if (ctid == 0) ctotal[0] = 0;
           named_bar(2, kProcThreads);
         }
       }
@@ -644,10 +574,10 @@ extern "C" int gpa_debug_read_timing(unsigned long long *out) {
 }
 #endif
 
-size_t part_smem_bytes(uint32_t bpb, uint32_t G, int chunk) {
+size_t part_smem_bytes(uint32_t bpb, uint32_t G) {
   const size_t ibuf = ((size_t)G * kPartCap * 2 + 127) & ~(size_t)127;
-  return (size_t)kRing * chunk * 8 + (kInbox + kStage) * ibuf + kTrash * 4 + kStage * (kPartMaxCtas + 8) * 4 + 16 +
-         (kRing + 2 * kStage + kPartBufs + 2 * kInbox) * 8 + (size_t)(bpb + kTrash) * 4;
+  return (kInbox + kStage) * ibuf + kTrash * 4 + kStage * (kPartMaxCtas + 8) * 4 +
+         (2 * kStage + kPartBufs + 2 * kInbox) * 8 + (size_t)(bpb + kTrash) * 4;
 }
 
 static uint32_t part_grid(int n_sms) { return (uint32_t)std::min(n_sms, kPartMaxCtas); }
@@ -661,17 +591,9 @@ static bool part_shape(const DevProgram &p, int n_sms, uint32_t &G, uint32_t &pp
   return ppb < 4096 && bpb < (1u << kLocalBits) && G <= 256;   // 2-byte keys: 13-bit local bins; TMA box <= 256
 }
 
-// index of the largest exchange chunk that fits, or -1
-static int part_chunk_index(const DevProgram &p, int n_sms, size_t smem_optin) {
-  uint32_t G, ppb, bpb;
-  if (!part_shape(p, n_sms, G, ppb, bpb)) return -1;
-  for (int i = 0; i < kNumChunkSizes; ++i)
-    if (part_smem_bytes(bpb, G, chunk_size(i)) + 256 <= smem_optin) return i;
-  return -1;
-}
-
 bool part_feasible(const DevProgram &p, int n_sms, size_t smem_optin) {
-  return part_chunk_index(p, n_sms, smem_optin) >= 0;
+  uint32_t G, ppb, bpb;
+  return part_shape(p, n_sms, G, ppb, bpb) && part_smem_bytes(bpb, G) + 256 <= smem_optin;
 }
 
 size_t ingest_smem_bytes(const DevProgram &p) { return (size_t)p.n * 2 * p.R * 4; }
@@ -703,8 +625,7 @@ cudaError_t launch_ingest(const DevProgram &p, int variant, const void *records,
     return cudaGetLastError();
   }
   if (variant == VAR_PART) {
-    const int ci = part_chunk_index(p, n_sms, smem_optin);
-    if (ci < 0) return cudaErrorInvalidValue;
+    if (!part_feasible(p, n_sms, smem_optin)) return cudaErrorInvalidValue;
     uint32_t G, ppb, bpb;
     part_shape(p, n_sms, G, ppb, bpb);
     PartArgs a;
@@ -720,14 +641,8 @@ cudaError_t launch_ingest(const DevProgram &p, int variant, const void *records,
     a.stats = p.stats;
     a.X = reinterpret_cast<uint16_t *>(p.part_x);
     a.sync = p.part_sync;
-    a.zero = p.part_zero;
-    static const void *const kernels[kNumChunkSizes] = {(const void *)k_ingest_part<chunk_size(0)>,
-                                                         (const void *)k_ingest_part<chunk_size(1)>,
-                                                         (const void *)k_ingest_part<chunk_size(2)>,
-                                                         (const void *)k_ingest_part<chunk_size(3)>};
-    static_assert(kNumChunkSizes == 4, "kernel table");
-    const void *kern = kernels[ci];
-    const size_t smem = part_smem_bytes(a.bpb, G, chunk_size(ci));
+    const void *kern = (const void *)k_ingest_part;
+    const size_t smem = part_smem_bytes(a.bpb, G);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(p.part_sync, 0, 2 * kPartBufs * sizeof(unsigned int), s);

@@ -280,7 +280,7 @@ struct Offsets {
       part_al, rows_v, rows_al, vbuf;
   size_t pats, mval, mrow, loop_items, loop_item_ptr, pre_perm, pre_begin, pre_end, kloop_ptr, kloops,
       loop_func, lM_excl, lM_incl, fM, kM, est;
-  size_t C, stats, AL, cand, selfm, share, B, partials, part_x, part_sync, part_zero;
+  size_t C, stats, AL, cand, selfm, share, B, partials, part_x, part_sync;
   bool part_reserved = false;
   size_t total;
 };
@@ -304,7 +304,6 @@ Offsets layout(const gpa_program_desc *d, const HostPlan &h) {
     const size_t pairs = (size_t)kPartBufs * kPartMaxCtas * kPartMaxCtas;
     o.part_x = a.take(part ? pairs * kPartCap * 2 : 0);   // 2-byte keys
     o.part_sync = a.take(part ? 2 * kPartBufs * 4 : 0);   // producer + consumer counters per buffer
-    o.part_zero = a.take(part ? kPartZeroBytes : 0);       // never written: TMA source for recycling
     o.part_reserved = part;
   }
   o.opclass = a.take(n);
@@ -444,7 +443,6 @@ gpa_status gpa_program_create(const gpa_program_desc *d, void *d_workspace, size
   UP(o.kloops, h.kloops.data(), h.kloops.size());
   UP(o.loop_func, h.loop_func.data(), h.loop_func.size());
   CUDA_TRY(cudaMemsetAsync(ws + o.C, 0, o.partials - o.C, s));   // outputs zeroed
-  if (o.part_reserved) CUDA_TRY(cudaMemsetAsync(ws + o.part_zero, 0, kPartZeroBytes, s));
   CUDA_TRY(cudaStreamSynchronize(s));
 
   gpa_program *p = new gpa_program();
@@ -472,7 +470,6 @@ gpa_status gpa_program_create(const gpa_program_desc *d, void *d_workspace, size
   DP(cand, uint8_t *, cand); DP(selfm, uint8_t *, selfm); DP(share, double *, share);
   DP(B, double *, B); DP(partials, uint32_t *, partials);
   DP(part_x, uint32_t *, part_x); DP(part_sync, unsigned int *, part_sync);
-  DP(part_zero, const uint8_t *, part_zero);
 #undef DP
   RollupPlan &rp = p->rp;
   rp.order = (const uint32_t *)(ws + o.order);

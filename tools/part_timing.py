@@ -23,11 +23,11 @@ for it in range(2):      # the second pass is the measured one
     lib.gpa_debug_read_timing(buf)
 delta = [buf[i] - before[i] for i in range(16)]
 roles = {
-    "decoders (per warp)": ([0, 1, 2], ["wait_buf", "wait_ring", "decode"]),
-    "control": ([3, 4, 5, 7], ["wait_decoded", "tma+spin_cons", "store+wait_group", "recycle"]),
-    "processors (per warp)": ([9, 10, 11], ["wait_inbox", "process", "barrier"]),
-    "loader": ([12, 13], ["wait_inbox_free", "spin_prod"]),
-    "publisher": ([14, 15], ["wait_stored", "publish"]),
+    "decoders (per warp)": ([0, 2], ["load+wait_buf", "decode"]),
+    "control": ([3, 4, 5], ["wait_decoded", "spin_cons", "store+wait_group"]),
+    "publisher": ([14, 15, 7], ["wait_stored", "publish", "recycle"]),
+    "loader": ([12, 13], ["wait_inbox_full(+spin_prod)", "wait_processors"]),
+    "processors (per warp)": ([9, 10, 11], ["wait_full", "process", "flush"]),
 }
 for role, (slots, names) in roles.items():
     tot = sum(delta[s] for s in slots) or 1
