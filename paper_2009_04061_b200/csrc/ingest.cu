@@ -287,6 +287,10 @@ __device__ __forceinline__ void tma_tile_load_2d(void *dst, const CUtensorMap *t
 __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, const __grid_constant__ CUtensorMap xmap) {
   constexpr int CHUNK = kPartChunk;
   constexpr int kDecodeRecs = CHUNK / kDecodeThreads;   // records per decode thread per chunk
+#ifndef GPA_PART_BATCH
+#define GPA_PART_BATCH 1
+#endif
+  constexpr int kDecodeBatch = GPA_PART_BATCH;
   extern __shared__ __align__(128) uint8_t sm[];
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t G = gridDim.x, me = blockIdx.x;
@@ -362,30 +366,44 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
       //      bucket b's zero-padded slot (invalid and padding records count in the dummy bucket G
       //      and land in a trash word; counts > 7 and slot overflow go through L2 atomics)
       uint32_t csum = 0, bads = 0, badr = 0;
+      // records are processed in batches of kDecodeBatch pairs: all slot allocations (atomics) of a
+      // batch are issued before its key stores, so their latencies overlap
 #pragma unroll
-      for (int u = 0; u < kDecodeRecs / 2; ++u) {
-        const bool in = full || 2 * (u * kDecodeThreads + dtid) < len;
-        const uint4 v = vv[u];
+      for (int u0 = 0; u0 < kDecodeRecs / 2; u0 += kDecodeBatch) {
+        constexpr int kB = 2 * kDecodeBatch;
+        uint32_t pos[kB], slot[kB], bin[kB], cnts[kB];
+        unsigned short key[kB];
+        bool okk[kB];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int i = 0; i < kB; ++i) {
+          const int u = u0 + i / 2, h = i & 1;
+          if (u >= kDecodeRecs / 2) break;
+          const bool in = full || 2 * (u * kDecodeThreads + dtid) < len;
+          const uint4 v = vv[u];
           const uint32_t pc = h ? v.z : v.x, w = h ? v.w : v.y;
           const uint32_t t = w >> 16, reason = t & 0xffu, c = w & 0xffffu;
           const bool ok = pc < n_instr && reason < R && t < 0x200u && t != 0x100u;
           const uint32_t q = __umulhi(pc, mg), b = pc - q * G;
-          const uint32_t local = q * twoR + (t >> 8) * R + reason;
           const bool small = c <= kMaxKeyCount;
           const uint32_t be = ok && small ? b : G;
-          uint32_t pos;
-          asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(pos) : "r"(cnt_addr + be * 4) : "memory");
-          const bool keep = ok && small && pos < (uint32_t)kPartCap;
-          const uint32_t dst = keep ? sg_addr + (be * kPartCap + pos) * 2 : trash_addr;
-          asm volatile("st.shared.u16 [%0], %1;" ::"r"(dst), "h"((unsigned short)(local | (c << kLocalBits)))
-                       : "memory");
-          if (ok && !keep)   // count > 7 or slot overflow (skew): exact via L2 atomics
-            atomicAdd((unsigned long long *)&a.C[(uint64_t)pc * twoR + (t >> 8) * R + reason], (unsigned long long)c);
+          key[i] = (unsigned short)((q * twoR + (t >> 8) * R + reason) | (c << kLocalBits));
+          bin[i] = pc * twoR + (t >> 8) * R + reason;
+          slot[i] = ok && small ? sg_addr + be * kPartCap * 2 : 0u;   // 0: never kept
+          okk[i] = ok;
+          cnts[i] = c;
+          asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(pos[i]) : "r"(cnt_addr + be * 4) : "memory");
           csum += c;        // padding records have count 0
           bads += ok ? 0u : c;
           badr += (in && !ok) ? 1u : 0u;
+        }
+#pragma unroll
+        for (int i = 0; i < kB; ++i) {
+          if (u0 + i / 2 >= kDecodeRecs / 2) break;
+          const bool keep = slot[i] != 0u && pos[i] < (uint32_t)kPartCap;
+          const uint32_t dst = keep ? slot[i] + pos[i] * 2 : trash_addr;
+          asm volatile("st.shared.u16 [%0], %1;" ::"r"(dst), "h"(key[i]) : "memory");
+          if (okk[i] && !keep)   // count > 7 or slot overflow (skew): exact via L2 atomics
+            atomicAdd((unsigned long long *)&a.C[bin[i]], (unsigned long long)cnts[i]);
         }
       }
       st.valid += csum - bads;
