@@ -21,7 +21,10 @@ constexpr int kPartThreads = 1024;
 #define GPA_PART_CHUNK 6400
 #endif
 constexpr int kPartChunk = GPA_PART_CHUNK;  // largest exchange chunk: records per CTA per round (50 KB)
-constexpr int kPartBufs = 16;               // exchange buffers in flight
+#ifndef GPA_PART_BUFS
+#define GPA_PART_BUFS 16
+#endif
+constexpr int kPartBufs = GPA_PART_BUFS;    // exchange buffers in flight
 #ifndef GPA_PART_CAP
 #define GPA_PART_CAP 56
 #endif
