@@ -8,17 +8,18 @@
 //   CTA tables are written out coalesced and summed per bin by k_ingest_reduce (no global
 //   atomics on the hot path, deterministic).
 // Variant P (k_ingest_part): tables larger than one SM's shared memory (config 3: 50k PCs x 18
-//   bins = 3.6 MB).  The bin space is split into G = #SM contiguous buckets, one per CTA of a
-//   persistent cooperative grid, each held in that CTA's shared memory.  Every CTA streams
-//   64 KB chunks of records into a double-buffered shared-memory ring with TMA bulk copies
-//   (cp.async.bulk + mbarrier), counting-sorts each chunk by bucket in shared memory, and
-//   writes each bucket's run of 4-byte keys {local bin:16 | count:16} coalesced into an
-//   L2-resident exchange buffer slot (dst, src).  One chunk later the owning CTA drains its
-//   slots into its table with shared-memory atomics.  Producer/consumer hand-off uses monotonic
-//   per-buffer global counters (split-phase: arrive after producing chunk k, wait before
-//   consuming it one iteration later), with 3 exchange buffers in flight, so HBM sees each
-//   record once and the keys never leave L2.  Keys beyond a slot's capacity (extreme skew)
-//   fall back to L2 atomics, so the result is exact for any distribution.
+//   bins = 3.6 MB).  The bin space is split over the G = #SM CTAs of a persistent cooperative
+//   grid by pc mod G, each CTA holding its bins in shared memory.  Per round every CTA streams
+//   kPartChunk records (direct 16-byte loads), counting-sorts them by destination CTA into
+//   zero-padded slots of 2-byte keys {local bin:13 | count:3} in shared memory, and writes its
+//   whole row of slots into an L2-resident exchange buffer with one bulk store; each CTA then
+//   fetches its column of every producer's row with one 2-D TMA tile load and adds the keys into
+//   its table with shared-memory atomics.  Warp-specialised (decoders / control / publisher /
+//   loader / processors) with mbarrier hand-offs inside the CTA and monotonic
+//   per-buffer release/acquire counters between CTAs (16 exchange buffers in flight), so HBM
+//   sees each record once and the keys stay in L2.  Counts > 7, slot overflow (extreme skew)
+//   and malformed records go through L2 atomics / the stats, so the result is exact for any
+//   distribution.
 // Variant L (k_ingest_l2): tables larger than shared memory; one RED.E.ADD.64 per record into
 //   the L2-resident u64 table.
 #include <algorithm>
