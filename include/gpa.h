@@ -174,6 +174,22 @@ gpa_status gpa_ingest_samples(gpa_program *prog, const gpa_sample *d_samples, ui
 gpa_status gpa_ingest_samples_host(gpa_program *prog, const gpa_sample *h_samples, uint64_t n,
                                    void *stream);
 
+/* Histogram a stream grouped by kernel launch (enqueue; accumulates).  GPA's profiler collects
+ * the PC samples of each kernel launch and the blamer analyses each invocation,
+ * so a whole-application batch (BASELINE config 4) arrives as per-launch segments:
+ *   segment s = records [d_seg_begin[s], d_seg_begin[s+1]) of d_samples, drawn from kernel
+ *   d_seg_kernel[s] of this program (any value >= n_kernels: unknown kernel).
+ * d_seg_begin: DEVICE u64 [n_segments + 1], non-decreasing (offsets past n_samples are clipped;
+ * records outside [d_seg_begin[0], d_seg_begin[n_segments]) are not ingested).
+ * d_seg_kernel: DEVICE u32 [n_segments].  pc_base is subtracted from every record's pc before
+ * decoding (a program holding a slice of an application's kernels).
+ * Counts and stats are identical to gpa_ingest_samples over the same records (with pc - pc_base):
+ * records outside their segment's kernel are still counted, only more slowly.  Non-monotone
+ * offsets are memory-safe but give unspecified counts.  n_segments = 0 is a no-op. */
+gpa_status gpa_ingest_segments(gpa_program *prog, const gpa_sample *d_samples, uint64_t n_samples,
+                               const uint64_t *d_seg_begin, const uint32_t *d_seg_kernel,
+                               uint32_t n_segments, uint32_t pc_base, void *stream);
+
 /* Rules 1-3, Eq. 1 (all and latency samples), self flags, Fig. 6 classes, def-side
  * reduction (enqueue).  GPA_ERR_BAD_STATE before any reset/ingest. */
 gpa_status gpa_blame(gpa_program *prog, void *stream);

@@ -115,6 +115,9 @@ cudaError_t launch_rollup(const DevProgram &p, const RollupPlan &rp, int n_sms, 
 cudaError_t launch_estimate(const DevProgram &p, const EstimatePlan &ep, int n_sms,
                             cudaStream_t s, uint64_t *launches);
 cudaError_t launch_vrows(const DevProgram &p, double *vbuf, int n_sms, cudaStream_t s);
+cudaError_t launch_ingest_segments(const DevProgram &p, const void *records, uint64_t n, const uint64_t *seg_begin,
+                                   const uint32_t *seg_kernel, uint32_t n_seg, uint32_t pc_base, uint32_t max_tab_bins,
+                                   int n_sms, cudaStream_t s);
 size_t ingest_smem_bytes(const DevProgram &p);
 bool part_feasible(const DevProgram &p, int n_sms, size_t smem_optin);
 
@@ -157,6 +160,7 @@ struct gpa_program {
   int state = 0;
   int variant = gpa::VAR_SMEM;
   bool part_ok = false;
+  uint32_t seg_tab_bins = 0;        // shared-memory table of the segment ingest (bins)
   uint64_t launches = 0;
   uint64_t view_off[GPA_VIEW_COUNT_] = {};
   uint64_t view_bytes[GPA_VIEW_COUNT_] = {};

@@ -568,6 +568,88 @@ __global__ void k_ingest_edges(const uint2 *rec, uint64_t n_rec, uint32_t head, 
   flush_stats(st, stats);
 }
 
+// ----------------------------------------------------------------------------- variant K
+// Streams grouped by kernel launch (gpa_ingest_segments): segment s = records
+// [seg_begin[s], seg_begin[s+1]) of kernel seg_kernel[s].  The record index space is cut into
+// tiles of kSegTile records, tiles are dealt to the CTAs round-robin, and every (tile, segment)
+// piece is counted in a shared-memory table covering only that kernel's PCs (config 4: <= 2048
+// instructions x 2R bins), which is then added to C with one coalesced u64 atomic per nonzero
+// bin.  Records whose pc lies outside the segment's kernel, segments of unknown kernels
+// (seg_kernel >= n_kernels) and kernels too large for the table take L2 atomics: exact for any
+// input.  A piece holds at most kSegTile records of count <= 65535, so u32 bins cannot wrap.
+constexpr uint32_t kSegTile = 16384;
+constexpr uint32_t kSegThreads = 1024;
+
+__global__ void __launch_bounds__(kSegThreads, 1)
+k_ingest_seg(const uint2 *__restrict__ rec, uint64_t n_rec, const uint64_t *__restrict__ seg_begin,
+             const uint32_t *__restrict__ seg_kernel, uint32_t n_seg, uint32_t pc_base,
+             const uint32_t *__restrict__ func_begin, const uint32_t *__restrict__ kernel_func_begin,
+             uint32_t n_kernels, uint32_t n_instr, uint32_t R, uint32_t max_tab_bins,
+             uint64_t *__restrict__ C, uint64_t *__restrict__ stats) {
+  extern __shared__ uint32_t tab[];
+  const uint32_t twoR = 2 * R;
+  auto clampr = [&](uint64_t x) { return x < n_rec ? x : n_rec; };
+  const uint64_t r0 = clampr(seg_begin[0]), r1 = clampr(seg_begin[n_seg]);
+  const uint64_t n_tiles = r1 > r0 ? (r1 - r0 + kSegTile - 1) / kSegTile : 0;
+  IngestStats st{0, 0, 0};
+  for (uint64_t t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    const uint64_t t0 = r0 + t * kSegTile, t1 = t0 + kSegTile < r1 ? t0 + kSegTile : r1;
+    // first segment overlapping the tile: the last s with seg_begin[s] <= t0
+    uint32_t lo = 0, hi = n_seg;
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (clampr(seg_begin[mid]) <= t0) lo = mid; else hi = mid;
+    }
+    for (uint32_t s = lo; s < n_seg; ++s) {
+      const uint64_t b = clampr(seg_begin[s]) > t0 ? clampr(seg_begin[s]) : t0;
+      const uint64_t e = clampr(seg_begin[s + 1]) < t1 ? clampr(seg_begin[s + 1]) : t1;
+      if (clampr(seg_begin[s]) >= t1) break;
+      if (b >= e) continue;
+      const uint32_t k = seg_kernel[s];
+      uint32_t p0 = 0, np = 0;
+      if (k < n_kernels) {
+        p0 = func_begin[kernel_func_begin[k]];
+        np = func_begin[kernel_func_begin[k + 1]] - p0;
+      }
+      const bool use_tab = np > 0 && np * twoR <= max_tab_bins;
+      const uint32_t nb = use_tab ? np * twoR : 0;
+      __syncthreads();                                   // previous piece's flush read the table
+      for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) tab[i] = 0;
+      __syncthreads();
+      auto add = [&](uint32_t pc, uint32_t w) {
+        uint32_t bin, cnt;
+        if (decode(pc - pc_base, w, n_instr, R, bin, cnt)) {
+          st.valid += cnt;
+          const uint32_t lb = bin - p0 * twoR;           // wraps past nb when pc < p0
+          if (lb < nb) atomicAdd(&tab[lb], cnt);
+          else atomicAdd((unsigned long long *)&C[bin], (unsigned long long)cnt);
+        } else {
+          st.bad_records += 1;
+          st.bad_samples += cnt;
+        }
+      };
+      // 16-byte pairs over the aligned body of [b, e); a head / odd tail record by thread 0
+      const uint64_t hb = ((uintptr_t)(rec + b) & 15u) ? 1 : 0;
+      const uint64_t body = (e - b - hb) >> 1;
+      const uint4 *r16 = reinterpret_cast<const uint4 *>(rec + b + hb);
+      for (uint64_t i = threadIdx.x; i < body; i += blockDim.x) {
+        const uint4 v = ld_stream(r16 + i);
+        add(v.x, v.y);
+        add(v.z, v.w);
+      }
+      if (threadIdx.x == 0) {
+        if (hb) { const uint2 v = ld_stream8(rec + b); add(v.x, v.y); }
+        if ((e - b - hb) & 1) { const uint2 v = ld_stream8(rec + e - 1); add(v.x, v.y); }
+      }
+      __syncthreads();
+      uint64_t *dst = C + (uint64_t)p0 * twoR;
+      for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x)
+        if (tab[i]) atomicAdd((unsigned long long *)&dst[i], (unsigned long long)tab[i]);
+    }
+  }
+  flush_stats(st, stats);
+}
+
 }  // namespace
 
 // 2-D view of the exchange buffers for the consumers' column loads: element = 2-byte key,
@@ -683,6 +765,19 @@ cudaError_t launch_ingest(const DevProgram &p, int variant, const void *records,
     return cudaLaunchCooperativeKernel(kern, dim3(G), dim3(kPartThreads), args, smem, s);
   }
   return cudaErrorNotSupported;
+}
+
+cudaError_t launch_ingest_segments(const DevProgram &p, const void *records, uint64_t n, const uint64_t *seg_begin,
+                                   const uint32_t *seg_kernel, uint32_t n_seg, uint32_t pc_base, uint32_t max_tab_bins,
+                                   int n_sms, cudaStream_t s) {
+  const size_t smem = (size_t)max_tab_bins * 4;
+  cudaError_t e = cudaFuncSetAttribute(k_ingest_seg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const uint32_t grid = (uint32_t)std::max(1, n_sms);
+  k_ingest_seg<<<grid, kSegThreads, smem, s>>>((const uint2 *)records, n, seg_begin, seg_kernel, n_seg, pc_base,
+                                               p.func_begin, p.kernel_func_begin, p.n_kernels, p.n, p.R,
+                                               max_tab_bins, p.C, p.stats);
+  return cudaGetLastError();
 }
 
 }  // namespace gpa

@@ -538,6 +538,15 @@ gpa_status gpa_program_create(const gpa_program_desc *d, void *d_workspace, size
   p->variant = VAR_SMEM;
   p->part_ok = o.part_reserved && part_feasible(dp, p->n_sms, p->smem_optin);
   if (ingest_smem_bytes(dp) > std::min(p->smem_optin, kSmemTableMax)) p->variant = p->part_ok ? VAR_PART : VAR_L2;
+  // segment ingest: a shared-memory table sized for the largest kernel that fits
+  {
+    uint32_t max_np = 0;
+    for (uint32_t k = 0; k < d->n_kernels; ++k)
+      max_np = std::max(max_np, d->func_begin[d->kernel_func_begin[k + 1]] - d->func_begin[d->kernel_func_begin[k]]);
+    const uint64_t cap = std::min<uint64_t>(p->smem_optin, kSmemTableMax) / 4;
+    const uint64_t want = (uint64_t)max_np * 2 * d->n_reasons;
+    p->seg_tab_bins = (uint32_t)std::min(want, cap);
+  }
   *out = p;
   return GPA_OK;
 }
@@ -578,6 +587,26 @@ gpa_status gpa_ingest_samples(gpa_program *p, const gpa_sample *d_samples, uint6
   cudaError_t e = launch_ingest(p->d, p->variant, d_samples, n, p->n_sms, p->smem_optin, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "ingest launch");
   p->launches += (p->variant == VAR_L2) ? 1 : 2;
+  p->state = (p->state | ST_COUNTS) & ~(ST_BLAMED | ST_AGGREGATED);
+  return GPA_OK;
+}
+
+gpa_status gpa_ingest_segments(gpa_program *p, const gpa_sample *d_samples, uint64_t n, const uint64_t *d_seg_begin,
+                               const uint32_t *d_seg_kernel, uint32_t n_seg, uint32_t pc_base, void *stream) {
+  gpa_status st = check_prog(p);
+  if (st) return st;
+  if (n_seg == 0 || n == 0) {
+    p->state = (p->state | ST_COUNTS) & ~(ST_BLAMED | ST_AGGREGATED);
+    return GPA_OK;
+  }
+  if (!d_samples || !d_seg_begin || !d_seg_kernel) return fail(GPA_ERR_INVALID_ARGUMENT, "NULL samples or segment table");
+  if (((uintptr_t)d_samples & 7u) != 0) return fail(GPA_ERR_INVALID_ARGUMENT, "d_samples not 8-byte aligned");
+  if (((uintptr_t)d_seg_begin & 7u) != 0 || ((uintptr_t)d_seg_kernel & 3u) != 0)
+    return fail(GPA_ERR_INVALID_ARGUMENT, "segment table misaligned");
+  cudaError_t e = launch_ingest_segments(p->d, d_samples, n, d_seg_begin, d_seg_kernel, n_seg, pc_base, p->seg_tab_bins,
+                                         p->n_sms, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "segment ingest launch");
+  p->launches += 1;
   p->state = (p->state | ST_COUNTS) & ~(ST_BLAMED | ST_AGGREGATED);
   return GPA_OK;
 }

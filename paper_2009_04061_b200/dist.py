@@ -39,3 +39,99 @@ def sharded_step(program, records, group=None, stream=None, estimate=True):
     else:
         program.blame(stream)
         program.aggregate(stream)
+
+
+# ----------------------------------------------------------------------------- DP-2
+# Kernel partition: the blame of a kernel depends only on its own
+# instructions, edges and samples (every def-use edge, line, loop and function lies inside one
+# kernel), so a batch of kernels splits into contiguous kernel ranges that ranks analyse
+# independently; only the (kernel x pattern) estimates travel back.
+
+def partition_kernels(kernel_samples, world: int):
+    """Contiguous kernel ranges [k_r, k_{r+1}) with balanced sample counts (each rank gets at
+    least one kernel while there are kernels left).  Returns the world + 1 boundaries."""
+    import numpy as np
+    w = np.asarray(kernel_samples, np.float64)
+    K = len(w)
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    cum = np.concatenate([[0.0], np.cumsum(w)])
+    bounds = [0]
+    for r in range(1, world):
+        lo = min(bounds[-1] + 1, K)                         # every rank gets a kernel while any remain
+        hi = max(lo, K - (world - r))
+        target = cum[-1] * r / world
+        ks = np.arange(lo, hi + 1)
+        bounds.append(int(ks[np.argmin(np.abs(cum[ks] - target))]))
+    bounds.append(K)
+    return bounds
+
+
+def slice_program(prog, k0: int, k1: int):
+    """The sub-program of kernels [k0, k1): instruction, edge, line, loop and function ids are
+    renumbered from 0; returns (sub_program, maps) where maps holds the global ids of the slice's
+    instructions ('pc_base', 'n_instr'), lines, loops, functions and kernels, for reassembling
+    per-rank results.  Works on any object with the gpa_program_desc arrays (gpagen.Program)."""
+    import dataclasses
+    import numpy as np
+    kfb = np.asarray(prog.kernel_func_begin, np.int64)
+    fb = np.asarray(prog.func_begin, np.int64)
+    if not 0 <= k0 < k1 <= len(kfb) - 1:
+        raise ValueError(f"bad kernel range [{k0}, {k1})")
+    f0, f1 = int(kfb[k0]), int(kfb[k1])
+    i0, i1 = int(fb[f0]), int(fb[f1])
+    rp = np.asarray(prog.row_ptr, np.int64)
+    e0, e1 = int(rp[i0]), int(rp[i1])
+    edef = np.asarray(prog.edge_def, np.int64)[e0:e1]
+    if len(edef) and (edef.min() < i0 or edef.max() >= i1):
+        raise ValueError("an edge crosses the kernel range")
+    dom = np.asarray(prog.edge_dom_k, np.int64)[e0:e1]
+    lines = np.asarray(prog.line_id, np.int64)[i0:i1]
+    line_ids, line_new = np.unique(lines, return_inverse=True)
+    lid = np.asarray(prog.loop_id, np.int64)[i0:i1]
+    parent = np.asarray(prog.loop_parent, np.int64)
+    used = set(int(x) for x in np.unique(lid[lid >= 0]))
+    for l in list(used):                                  # close over enclosing loops
+        p = int(parent[l])
+        while p >= 0 and p not in used:
+            used.add(p)
+            p = int(parent[p])
+    loop_ids = np.array(sorted(used), np.int64)
+    remap = {int(l): r for r, l in enumerate(loop_ids)}
+    new_lid = np.array([remap[int(l)] if l >= 0 else -1 for l in lid], np.int32) if len(lid) else lid.astype(np.int32)
+    new_parent = np.array([remap[int(parent[l])] if parent[l] >= 0 else -1 for l in loop_ids], np.int32)
+    fields = {f.name: getattr(prog, f.name) for f in dataclasses.fields(prog)}
+    sl = slice(i0, i1)
+    fields.update(
+        opclass=np.asarray(prog.opclass)[sl].copy(), iflags=np.asarray(prog.iflags)[sl].copy(),
+        latency=np.asarray(prog.latency)[sl].copy(), line_id=line_new.astype(np.uint32),
+        loop_id=new_lid, loop_parent=new_parent,
+        func_begin=(fb[f0:f1 + 1] - i0).astype(np.uint32),
+        kernel_func_begin=(kfb[k0:k1 + 1] - f0).astype(np.uint32),
+        kernel_grid_blocks=np.asarray(prog.kernel_grid_blocks)[k0:k1].copy(),
+        row_ptr=(rp[i0:i1 + 1] - e0).astype(np.uint32),
+        edge_def=(edef - i0).astype(np.uint32), edge_kind=np.asarray(prog.edge_kind)[e0:e1].copy(),
+        edge_min_len=np.asarray(prog.edge_min_len)[e0:e1].copy(),
+        edge_max_len=np.asarray(prog.edge_max_len)[e0:e1].copy(),
+        edge_dom_k=np.where(dom >= 0, dom - i0, -1).astype(np.int32),
+        n_lines=int(len(line_ids)))
+    for opt in ("pc_weight", "pc_profile"):
+        if fields.get(opt) is not None:
+            fields[opt] = np.asarray(fields[opt])[sl].copy()
+    sub = type(prog)(**fields)
+    maps = {"pc_base": i0, "n_instr": i1 - i0, "edge_base": e0, "lines": line_ids, "loops": loop_ids,
+            "funcs": np.arange(f0, f1), "kernels": np.arange(k0, k1)}
+    return sub, maps
+
+
+def gather_estimates(local_est, group=None):
+    """Concatenate every rank's estimate rows (numpy structured/byte arrays, kernel-major) on all
+    ranks, in rank order (= kernel order for partition_kernels ranges)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return local_est
+    parts = [None] * dist.get_world_size(group)
+    dist.all_gather_object(parts, local_est, group=group)
+    return np.concatenate(parts) if isinstance(local_est, np.ndarray) else sum(parts, [])

@@ -56,7 +56,8 @@ EXPORTS = ["gpa_validate_program", "gpa_workspace_size", "gpa_program_create", "
            "gpa_reset_counts", "gpa_ingest_samples", "gpa_ingest_samples_host", "gpa_blame",
            "gpa_aggregate", "gpa_set_patterns", "gpa_estimate", "gpa_read_estimates", "gpa_get_stats",
            "gpa_view", "gpa_instr_vector", "gpa_program_info", "gpa_ingest_variant",
-           "gpa_set_ingest_variant", "gpa_launch_count", "gpa_last_error", "gpa_version", "gpa_analyze"]
+           "gpa_set_ingest_variant", "gpa_launch_count", "gpa_last_error", "gpa_version", "gpa_analyze",
+           "gpa_ingest_segments"]
 
 _lib = None
 
@@ -81,6 +82,7 @@ def lib():
             "gpa_program_info": [vp, vp], "gpa_ingest_variant": [vp, vp],
             "gpa_set_ingest_variant": [vp, ctypes.c_int], "gpa_launch_count": [vp, vp],
             "gpa_analyze": [vp, vp],
+            "gpa_ingest_segments": [vp, vp, u64, vp, vp, u32, u32, vp],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -190,6 +192,23 @@ class Program:
             raise GpaError("ingest() takes a device tensor; use ingest_host() for host memory")
         nrec = int(t.numel() * t.element_size() // 8) if n is None else int(n)
         _check(lib().gpa_ingest_samples(self.handle, t.data_ptr(), nrec, self._s(stream)), "gpa_ingest_samples")
+
+    def ingest_segments(self, samples, seg_begin, seg_kernel, pc_base=0, n=None, stream=None):
+        """Stream grouped by kernel launch (gpa_ingest_segments): samples as in ingest();
+        seg_begin: CUDA int64/uint64 tensor [S+1] of record offsets; seg_kernel: CUDA int32/uint32
+        tensor [S] of kernel ids; pc_base subtracted from every pc."""
+        for t in (samples, seg_begin, seg_kernel):
+            if not t.is_cuda:
+                raise GpaError("ingest_segments() takes device tensors")
+        if seg_begin.element_size() != 8 or seg_kernel.element_size() != 4:
+            raise GpaError("seg_begin must hold 8-byte and seg_kernel 4-byte integers")
+        n_seg = int(seg_kernel.numel())
+        if int(seg_begin.numel()) != n_seg + 1:
+            raise GpaError("seg_begin needs len(seg_kernel) + 1 entries")
+        nrec = int(samples.numel() * samples.element_size() // 8) if n is None else int(n)
+        _check(lib().gpa_ingest_segments(self.handle, samples.data_ptr(), nrec, seg_begin.data_ptr(),
+                                         seg_kernel.data_ptr(), n_seg, int(pc_base), self._s(stream)),
+               "gpa_ingest_segments")
 
     def ingest_host(self, samples, n=None, stream=None):
         """samples: host numpy array / CPU tensor of 8-byte records (pinned memory overlaps)."""

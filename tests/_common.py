@@ -28,9 +28,10 @@ def run_oracle(prog, records, patterns=None, chunk=None):
     return {"C": C, "stats": stats, **b, **r, "est": est}
 
 
-def run_gpu(prog, records, patterns=None, variant=None, host=False, offset_records=0):
+def run_gpu(prog, records, patterns=None, variant=None, host=False, offset_records=0, segments=None):
     """records: numpy uint64 array.  offset_records: place the stream at an 8-byte (not 16-byte)
-    aligned address to exercise the unaligned head."""
+    aligned address to exercise the unaligned head.  segments: (seg_begin, seg_kernel, pc_base)
+    to ingest through gpa_ingest_segments (records grouped by kernel launch)."""
     import torch
     from paper_2009_04061_b200 import Program
     patterns = table2(prog.n_reasons) if patterns is None else patterns
@@ -45,7 +46,14 @@ def run_gpu(prog, records, patterns=None, variant=None, host=False, offset_recor
         buf = torch.empty(len(records) + offset_records + 1, dtype=torch.int64, device="cuda")
         if len(records):
             buf[offset_records:offset_records + len(records)] = torch.from_numpy(records.view(np.int64)).cuda()
-        P.ingest(buf[offset_records:offset_records + len(records)])
+        view = buf[offset_records:offset_records + len(records)]
+        if segments is None:
+            P.ingest(view)
+        else:
+            seg_begin, seg_kernel, pc_base = segments
+            P.ingest_segments(view, torch.from_numpy(np.asarray(seg_begin).astype(np.int64)).cuda(),
+                              torch.from_numpy(np.asarray(seg_kernel).astype(np.uint32).view(np.int32)).cuda(),
+                              pc_base=pc_base)
     P.blame()
     P.aggregate()
     P.estimate()

@@ -1,0 +1,79 @@
+"""Config 4 on the GPU: gpa_ingest_segments (streams grouped by kernel launch) and
+DP-2 kernel slices, against the CPU oracle on the same records.  Counts, stats, candidate masks
+and self flags bit-exact; fp64 within 1e-9 relative (BASELINE.json north_star)."""
+import numpy as np
+import pytest
+
+from gpagen import batch
+from gpagen.streams import StreamSpec
+from paper_2009_04061_b200.dist import slice_program
+from tests._common import compare, run_gpu, run_oracle
+
+pytestmark = pytest.mark.gpu
+REL = 1e-9
+
+
+@pytest.fixture(autouse=True)
+def _need_cuda(cuda_available):
+    if not cuda_available:
+        pytest.skip("no CUDA device")
+
+
+def _grouped(prog, recs, seed=0, split=False):
+    pcs = batch.record_pcs(recs)
+    order = np.random.default_rng(seed).permutation(prog.n_kernels)
+    perm, seg_begin, seg_kernel = batch.grouped_order(pcs, prog, kernel_order=order)
+    if split:   # every launch delivered in two buffers (the same kernel in consecutive segments)
+        mid = (seg_begin[:-1] + seg_begin[1:]) // 2
+        seg_begin = np.stack([seg_begin[:-1], mid], 1).reshape(-1)
+        seg_begin = np.concatenate([seg_begin, [len(recs)]]).astype(np.uint64)
+        seg_kernel = np.repeat(seg_kernel, 2)
+    return recs[perm], seg_begin, seg_kernel
+
+
+@pytest.mark.parametrize("split,offset", [(False, 0), (True, 1)])
+def test_segment_ingest_matches_oracle(split, offset):
+    prog = batch.batch_program(300, seed=61)
+    recs = StreamSpec(prog, seed=62, count_max=5, invalid_ppm=2_000).host(0, 2_000_001)
+    g, sb, sk = _grouped(prog, recs, seed=1, split=split)
+    o = run_oracle(prog, recs)
+    compare(run_gpu(prog, g, segments=(sb, sk, 0), offset_records=offset), o, rel=REL)
+
+
+def test_segment_ingest_mislabelled_and_unknown_segments():
+    """Records outside their segment's kernel and segments of unknown kernels are still counted
+    (L2 path); records outside [seg_begin[0], seg_begin[-1]) are not ingested."""
+    prog = batch.batch_program(200, seed=63)
+    recs = StreamSpec(prog, seed=64, count_max=3, invalid_ppm=0).host(0, 600_000)
+    g, sb, sk = _grouped(prog, recs, seed=2)
+    sk = sk.copy()
+    sk[::3] = (sk[::3] + 1) % prog.n_kernels          # wrong kernel
+    sk[1::7] = 0xFFFFFFFF                              # unknown kernel
+    lo, hi = int(sb[1]), int(sb[-2])                   # drop the first and last segments
+    sub_b = sb[1:-1].copy()
+    o = run_oracle(prog, g[lo:hi])
+    compare(run_gpu(prog, g, segments=(sub_b, sk[1:-1], 0)), o, rel=REL)
+
+
+def test_kernel_slice_with_pc_base():
+    """DP-2: a rank's program holds kernels [k0, k1); its records keep the application's PCs and
+    the segment ingest subtracts pc_base."""
+    prog = batch.batch_program(150, seed=65)
+    recs = StreamSpec(prog, seed=66, count_max=2, invalid_ppm=1_000).host(0, 1_000_000)
+    sub, maps = slice_program(prog, 40, 97)
+    pcs = batch.record_pcs(recs)
+    sel = (pcs >= maps["pc_base"]) & (pcs < maps["pc_base"] + maps["n_instr"])
+    mine = recs[sel]
+    perm, sb, sk = batch.grouped_order(batch.record_pcs(batch.rebase_records(mine, maps["pc_base"])), sub)
+    o = run_oracle(sub, batch.rebase_records(mine, maps["pc_base"]))
+    compare(run_gpu(sub, mine[perm], segments=(sb, sk, maps["pc_base"])), o, rel=REL)
+
+
+def test_config4_full_batch_reduced_stream():
+    """BASELINE config 4's program (10^4 kernels, ~4.5 M instructions) on a 10^7-record prefix of
+    its stream grouped by kernel launch."""
+    prog = batch.config4_program()
+    recs = batch.config4_stream(prog).host(0, 10_000_000)
+    g, sb, sk = _grouped(prog, recs, seed=3)
+    o = run_oracle(prog, recs)
+    compare(run_gpu(prog, g, segments=(sb, sk, 0)), o, rel=REL)
