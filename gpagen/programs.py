@@ -325,7 +325,7 @@ CONFIG_SEED_BASE = 0x2009040610
 
 
 def config_program(cfg: int) -> Program:
-    """Programs of BASELINE.json configs 1-3 (config 5 reuses config 3's program)."""
+    """Programs of BASELINE.json configs 1-4 (config 5 reuses config 3's program)."""
     seed = CONFIG_SEED_BASE + cfg
     if cfg == 1:
         return tiny_fixture()
@@ -336,6 +336,9 @@ def config_program(cfg: int) -> Program:
                CONSTANT: .03, CONVERT: .03, SYNC: .02, CONTROL: .08, MISC: .09, TEXTURE: .01}
         return random_program(50000, 64, 200, 6, CONFIG_SEED_BASE + 3, depth_bias=1.5,
                               weight_sigma=0.75, class_mix=mix, name="large")
+    if cfg == 4:
+        from .batch import config4_program
+        return config4_program()
     raise ValueError(f"no program for config {cfg}")
 
 

@@ -2,7 +2,7 @@
 // P:457-460) and the estimators of §5.2: Eq. 2, Eq. 3, Eq. 4
 // (P:496-503), Eq. 5 (Q16), Eqs. 6-10 (Q18), per kernel.
 //
-//   k_est_rows    one thread per (use row j, pattern): the matched samples of each
+//   k_est_rows    one thread per (use row j, pattern group): the matched samples of each
 //                 in-edge (blamed at the def, scope loop = lca(def, use)) and of j itself
 //                 (self / pass-through columns, scope loop = loop of j); row totals mrow[q][j]
 //                 and, for loop-scoped patterns, per-item values for the loop reduction.
@@ -28,59 +28,96 @@ __device__ __forceinline__ bool passes(const gpa_pattern &q, uint32_t cls, uint3
   return ((q.class_mask >> cls) & 1u) && (!q.flag_filter || (flags & q.flag_filter));
 }
 
-// one thread per (use row j, pattern q), pattern-major so a warp shares q (uniform control flow)
+// one thread per (use row j, group of kEstGroup patterns): the row's counts and in-edges are read
+// once per group and every pattern of the group is evaluated from registers; consecutive threads
+// take consecutive rows (coalesced).  Per (j, pattern) the sum runs over the row's edges in CSR
+// order, then adds j's own part -- the oracle's order.
+constexpr int kEstGroup = 8;
+
 __global__ void k_est_rows(DevProgram p, EstimatePlan ep) {
   __shared__ gpa_pattern sp[kPatternsMax];
-  for (uint32_t q = threadIdx.x; q < ep.n_pat; q += blockDim.x) sp[q] = ep.pats[q];
+  __shared__ int8_t sslot[kPatternsMax];
+  for (uint32_t q = threadIdx.x; q < ep.n_pat; q += blockDim.x) {
+    sp[q] = ep.pats[q];
+    sslot[q] = ep.loop_slot[q];
+  }
   __syncthreads();
   const uint64_t stride_items = (uint64_t)p.E + p.n;
-  const uint32_t rows_pad = (p.n + 31) & ~31u;
-  const uint64_t total = (uint64_t)rows_pad * ep.n_pat;
+  const uint32_t n_groups = (ep.n_pat + kEstGroup - 1) / kEstGroup;
+  const uint64_t total = (uint64_t)p.n * n_groups;
   for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total; t += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t qi = (uint32_t)(t / rows_pad), j = (uint32_t)(t % rows_pad);
-    if (j >= p.n) continue;
-    const gpa_pattern &q = sp[qi];
-    const int slot = ep.loop_slot[qi];
-    if (q.model == 5) {
-      ep.mrow[(uint64_t)qi * p.n + j] = 0.0;
-      continue;
-    }
+    const uint32_t grp = (uint32_t)(t / p.n), j = (uint32_t)(t % p.n);
+    const uint32_t q0 = grp * kEstGroup;
+    const uint32_t nq = min((uint32_t)kEstGroup, ep.n_pat - q0);
     const uint64_t *row = p.C + (uint64_t)j * 2 * p.R;
-    const bool L = q.sample_class != 0;
-    double X[4];
+    double XA[4], XL[4];   // all / latency samples of the dependency reasons at j
 #pragma unroll
-    for (int r = 1; r <= 3; ++r) X[r] = (double)(row[p.R + r] + (L ? 0ull : row[r]));
+    for (int r = 1; r <= 3; ++r) {
+      const uint64_t lat = row[p.R + r];
+      XL[r] = (double)lat;
+      XA[r] = (double)(lat + row[r]);
+    }
     const uint32_t e0 = p.row_ptr[j], e1 = p.row_ptr[j + 1];
     const int32_t loop_j = p.loop_id[j];
-    double sum = 0.0;
+    double sum[kEstGroup];
+#pragma unroll
+    for (int k = 0; k < kEstGroup; ++k) sum[k] = 0.0;
     for (uint32_t e = e0; e < e1; ++e) {
       const uint32_t m = p.cand[e];
-      const uint32_t d = p.edge_def[e];
-      double me = 0.0;
+      uint32_t cls = 0, flags = 0, kind = 0;
+      bool same = false;
+      double sh0 = 0.0, sh1 = 0.0, sh2 = 0.0;
       if (m) {
-        const uint32_t cls = p.opclass[d];
-        if (passes(q, cls, p.iflags[d]) && (!q.same_loop || (p.loop_id[d] >= 0 && p.loop_id[d] == loop_j))) {
-          const uint32_t kind = p.edge_kind[e];
-          const double *sh = p.share + 3 * (uint64_t)e;
-          if ((m & 1u) && ((q.column_mask >> classify(R_MEM, cls, kind)) & 1u)) me = __dadd_rn(me, __dmul_rn(X[1], sh[0]));
-          if ((m & 2u) && ((q.column_mask >> classify(R_EXEC, cls, kind)) & 1u)) me = __dadd_rn(me, __dmul_rn(X[2], sh[1]));
-          if ((m & 4u) && ((q.column_mask >> COL_SYNC) & 1u)) me = __dadd_rn(me, __dmul_rn(X[3], sh[2]));
-        }
+        const uint32_t d = p.edge_def[e];
+        cls = p.opclass[d];
+        flags = p.iflags[d];
+        kind = p.edge_kind[e];
+        same = p.loop_id[d] >= 0 && p.loop_id[d] == loop_j;
+        const double *sh = p.share + 3 * (uint64_t)e;
+        sh0 = sh[0]; sh1 = sh[1]; sh2 = sh[2];
       }
-      if (slot >= 0) ep.mval[(uint64_t)slot * stride_items + e] = me;
-      sum = __dadd_rn(sum, me);
+      const uint32_t c_mem = classify(R_MEM, cls, kind), c_exec = classify(R_EXEC, cls, kind);
+#pragma unroll
+      for (int k = 0; k < kEstGroup; ++k) {
+        if ((uint32_t)k >= nq) break;
+        const gpa_pattern &q = sp[q0 + k];
+        if (q.model == 5) continue;
+        const double *X = q.sample_class ? XL : XA;
+        double me = 0.0;
+        if (m && passes(q, cls, flags) && (!q.same_loop || same)) {
+          if ((m & 1u) && ((q.column_mask >> c_mem) & 1u)) me = __dadd_rn(me, __dmul_rn(X[1], sh0));
+          if ((m & 2u) && ((q.column_mask >> c_exec) & 1u)) me = __dadd_rn(me, __dmul_rn(X[2], sh1));
+          if ((m & 4u) && ((q.column_mask >> COL_SYNC) & 1u)) me = __dadd_rn(me, __dmul_rn(X[3], sh2));
+        }
+        const int slot = sslot[q0 + k];
+        if (slot >= 0) ep.mval[(uint64_t)slot * stride_items + e] = me;
+        sum[k] = __dadd_rn(sum[k], me);
+      }
     }
-    double mi = 0.0;
-    if (passes(q, p.opclass[j], p.iflags[j]) && (!q.same_loop || loop_j >= 0)) {
-      const uint32_t self_j = p.selfm[j];
-      for (uint32_t r = R_MEM; r <= R_SYNC; ++r)
-        if (((self_j >> (r - 1)) & 1u) && ((q.column_mask >> (COL_MEM_SELF + r - 1)) & 1u)) mi = __dadd_rn(mi, X[r]);
-      for (uint32_t r = 4; r < p.R; ++r)
-        if ((q.column_mask >> (COL_PASS0 + r - 4)) & 1u)
-          mi = __dadd_rn(mi, (double)(row[p.R + r] + (L ? 0ull : row[r])));
+    const uint32_t cls_j = p.opclass[j], flags_j = p.iflags[j], self_j = p.selfm[j];
+#pragma unroll
+    for (int k = 0; k < kEstGroup; ++k) {
+      if ((uint32_t)k >= nq) break;
+      const uint32_t qi = q0 + k;
+      const gpa_pattern &q = sp[qi];
+      if (q.model == 5) {
+        ep.mrow[(uint64_t)qi * p.n + j] = 0.0;
+        continue;
+      }
+      const bool L = q.sample_class != 0;
+      const double *X = L ? XL : XA;
+      double mi = 0.0;
+      if (passes(q, cls_j, flags_j) && (!q.same_loop || loop_j >= 0)) {
+        for (uint32_t r = R_MEM; r <= R_SYNC; ++r)
+          if (((self_j >> (r - 1)) & 1u) && ((q.column_mask >> (COL_MEM_SELF + r - 1)) & 1u)) mi = __dadd_rn(mi, X[r]);
+        for (uint32_t r = 4; r < p.R; ++r)
+          if ((q.column_mask >> (COL_PASS0 + r - 4)) & 1u)
+            mi = __dadd_rn(mi, (double)(row[p.R + r] + (L ? 0ull : row[r])));
+      }
+      const int slot = sslot[qi];
+      if (slot >= 0) ep.mval[(uint64_t)slot * stride_items + p.E + j] = mi;
+      ep.mrow[(uint64_t)qi * p.n + j] = __dadd_rn(sum[k], mi);
     }
-    if (slot >= 0) ep.mval[(uint64_t)slot * stride_items + p.E + j] = mi;
-    ep.mrow[(uint64_t)qi * p.n + j] = __dadd_rn(sum, mi);
   }
 }
 
@@ -220,7 +257,7 @@ __global__ void k_est_final(DevProgram p, EstimatePlan ep) {
 cudaError_t launch_estimate(const DevProgram &p, const EstimatePlan &ep, int n_sms, cudaStream_t s,
                             uint64_t *launches) {
   const uint32_t threads = 128;
-  const uint64_t work = (uint64_t)((p.n + 31) & ~31u) * ep.n_pat;
+  const uint64_t work = (uint64_t)p.n * ((ep.n_pat + kEstGroup - 1) / kEstGroup);
   const uint32_t g = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((work + threads - 1) / threads, (uint64_t)n_sms * 32));
   k_est_rows<<<g, threads, 0, s>>>(p, ep);
   SegLaunch a{};

@@ -3,8 +3,8 @@
 //
 // Hand-written segmented reductions (no CUB), deterministic: every sum has a fixed order.
 //   k_vrows            V[i] = {NCOL x (all, lat)} for every instruction, one
-//                      warp per (32 instructions, value slot) so control flow is warp-uniform;
-//                      this is also the instruction level of the rollup (gpa_instr_vector).
+//                      warp per instruction row, stores coalesced; this is also the instruction
+//                      level of the rollup (gpa_instr_vector).
 //   k_rollup_chunks    one warp per <=128-instruction chunk of a create-time order (line-major |
 //                      loop-major | function ranges); member ids are loaded once and broadcast by
 //                      shuffles, lane s owns value slot s (and s+32) of the row, so each member
@@ -21,15 +21,13 @@
 namespace gpa {
 namespace {
 
-// one warp per (32 instructions, slot): uniform control flow across the warp
+// one warp per instruction row (lane = value slot): the row's loads are shared by the warp and
+// V is written coalesced
 __global__ void k_vrows(DevProgram p, double *__restrict__ vbuf) {
   const uint32_t nv = 2 * p.ncol, lane = threadIdx.x & 31;
-  const uint64_t groups = (uint64_t)((p.n + 31) / 32) * nv;
-  const uint64_t warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  for (uint64_t w = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < groups; w += warps) {
-    const uint32_t s = (uint32_t)(w % nv), i = (uint32_t)(w / nv) * 32 + lane;
-    if (i < p.n) vbuf[(uint64_t)i * nv + s] = vvalue(p, i, s >> 1, s & 1);
-  }
+  const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < p.n; i += warps)
+    for (uint32_t s = lane; s < nv; s += 32) vbuf[(uint64_t)i * nv + s] = vvalue(p, i, s >> 1, s & 1);
 }
 
 // sum over positions [b, e) of rows it(pos): slot s < nv from vals, slots nv, nv+1 from al
@@ -133,7 +131,7 @@ inline uint32_t warp_grid(uint64_t warps, int n_sms) {
 }  // namespace
 
 cudaError_t launch_vrows(const DevProgram &p, double *vbuf, int n_sms, cudaStream_t s) {
-  const uint64_t total = (uint64_t)((p.n + 31) / 32) * 32 * 2 * p.ncol;
+  const uint64_t total = (uint64_t)p.n * 32;
   const uint32_t g = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, (uint64_t)n_sms * 32));
   k_vrows<<<g, 256, 0, s>>>(p, vbuf);
   return cudaGetLastError();

@@ -1,7 +1,3 @@
-for rep in 1 2; do
-for v in product build/libv_*.so; do timeout 120 python tools/variant_time.py $v 2>&1 | grep -v Warn | tail -1; done
-done
-rm -f gpurun_out/counts_*
-for v in build/libv_el.so build/libv_plain_el.so; do
-GPA_LIB=$v timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:k_ingest_part -c 1 python tools/variant_time.py $v 2>&1 | grep -E "dram__|gpu__time"
-done
+timeout 600 python tools/batch_probe.py 2>&1 | grep -v Warn | tail -4
+timeout 300 python bench.py --steps 5 --warmup 3 --e2e-steps 0 --no-cpu-baseline 2>&1 | tail -1 | grep -o '"value": [0-9.e+]*\|"ingest_ms": [0-9.]*\|"blame_rollup_estimate_ms": [0-9.]*'
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/batch_launches.csv python tools/batch_profile.py > /dev/null 2>&1
