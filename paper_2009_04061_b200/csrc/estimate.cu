@@ -28,11 +28,47 @@ __device__ __forceinline__ bool passes(const gpa_pattern &q, uint32_t cls, uint3
   return ((q.class_mask >> cls) & 1u) && (!q.flag_filter || (flags & q.flag_filter));
 }
 
+// matched samples of edge e (def d -> use j) under pattern q: X = all / latency samples of j
+struct EdgeInfo {
+  uint32_t m, cls, flags, c_mem, c_exec;
+  bool same;
+  double sh0, sh1, sh2;
+};
+__device__ __forceinline__ EdgeInfo edge_info(const DevProgram &p, uint32_t e, int32_t loop_j) {
+  EdgeInfo x{};
+  x.m = p.cand[e];
+  uint32_t kind = 0;
+  if (x.m) {
+    const uint32_t d = p.edge_def[e];
+    x.cls = p.opclass[d];
+    x.flags = p.iflags[d];
+    kind = p.edge_kind[e];
+    x.same = p.loop_id[d] >= 0 && p.loop_id[d] == loop_j;
+    const double *sh = p.share + 3 * (uint64_t)e;
+    x.sh0 = sh[0]; x.sh1 = sh[1]; x.sh2 = sh[2];
+  }
+  x.c_mem = classify(R_MEM, x.cls, kind);
+  x.c_exec = classify(R_EXEC, x.cls, kind);
+  return x;
+}
+__device__ __forceinline__ double edge_match(const gpa_pattern &q, const EdgeInfo &x, const double *X) {
+  double me = 0.0;
+  if (x.m && passes(q, x.cls, x.flags) && (!q.same_loop || x.same)) {
+    if ((x.m & 1u) && ((q.column_mask >> x.c_mem) & 1u)) me = __dadd_rn(me, __dmul_rn(X[1], x.sh0));
+    if ((x.m & 2u) && ((q.column_mask >> x.c_exec) & 1u)) me = __dadd_rn(me, __dmul_rn(X[2], x.sh1));
+    if ((x.m & 4u) && ((q.column_mask >> COL_SYNC) & 1u)) me = __dadd_rn(me, __dmul_rn(X[3], x.sh2));
+  }
+  return me;
+}
+
 // one thread per (use row j, group of kEstGroup patterns): the row's counts and in-edges are read
 // once per group and every pattern of the group is evaluated from registers; consecutive threads
 // take consecutive rows (coalesced).  Per (j, pattern) the sum runs over the row's edges in CSR
 // order, then adds j's own part -- the oracle's order.
-constexpr int kEstGroup = 8;
+#ifndef GPA_EST_GROUP
+#define GPA_EST_GROUP 4
+#endif
+constexpr int kEstGroup = GPA_EST_GROUP;
 
 __global__ void k_est_rows(DevProgram p, EstimatePlan ep) {
   __shared__ gpa_pattern sp[kPatternsMax];
@@ -62,36 +98,14 @@ __global__ void k_est_rows(DevProgram p, EstimatePlan ep) {
     double sum[kEstGroup];
 #pragma unroll
     for (int k = 0; k < kEstGroup; ++k) sum[k] = 0.0;
-    for (uint32_t e = e0; e < e1; ++e) {
-      const uint32_t m = p.cand[e];
-      uint32_t cls = 0, flags = 0, kind = 0;
-      bool same = false;
-      double sh0 = 0.0, sh1 = 0.0, sh2 = 0.0;
-      if (m) {
-        const uint32_t d = p.edge_def[e];
-        cls = p.opclass[d];
-        flags = p.iflags[d];
-        kind = p.edge_kind[e];
-        same = p.loop_id[d] >= 0 && p.loop_id[d] == loop_j;
-        const double *sh = p.share + 3 * (uint64_t)e;
-        sh0 = sh[0]; sh1 = sh[1]; sh2 = sh[2];
-      }
-      const uint32_t c_mem = classify(R_MEM, cls, kind), c_exec = classify(R_EXEC, cls, kind);
+    for (uint32_t e = e0; e < e1; ++e) {   // loads only: per-edge values go to k_est_edges
+      const EdgeInfo x = edge_info(p, e, loop_j);
 #pragma unroll
       for (int k = 0; k < kEstGroup; ++k) {
         if ((uint32_t)k >= nq) break;
         const gpa_pattern &q = sp[q0 + k];
         if (q.model == 5) continue;
-        const double *X = q.sample_class ? XL : XA;
-        double me = 0.0;
-        if (m && passes(q, cls, flags) && (!q.same_loop || same)) {
-          if ((m & 1u) && ((q.column_mask >> c_mem) & 1u)) me = __dadd_rn(me, __dmul_rn(X[1], sh0));
-          if ((m & 2u) && ((q.column_mask >> c_exec) & 1u)) me = __dadd_rn(me, __dmul_rn(X[2], sh1));
-          if ((m & 4u) && ((q.column_mask >> COL_SYNC) & 1u)) me = __dadd_rn(me, __dmul_rn(X[3], sh2));
-        }
-        const int slot = sslot[q0 + k];
-        if (slot >= 0) ep.mval[(uint64_t)slot * stride_items + e] = me;
-        sum[k] = __dadd_rn(sum[k], me);
+        sum[k] = __dadd_rn(sum[k], edge_match(q, x, q.sample_class ? XL : XA));
       }
     }
     const uint32_t cls_j = p.opclass[j], flags_j = p.iflags[j], self_j = p.selfm[j];
@@ -117,6 +131,42 @@ __global__ void k_est_rows(DevProgram p, EstimatePlan ep) {
       const int slot = sslot[qi];
       if (slot >= 0) ep.mval[(uint64_t)slot * stride_items + p.E + j] = mi;
       ep.mrow[(uint64_t)qi * p.n + j] = __dadd_rn(sum[k], mi);
+    }
+  }
+}
+
+// per-edge matched samples of the loop-scoped patterns (mval[slot][e]), edge-parallel and
+// coalesced; the same arithmetic as k_est_rows, so the item values and the row sums agree
+__global__ void k_est_edges(DevProgram p, EstimatePlan ep) {
+  __shared__ gpa_pattern sp[kPatternsMax];
+  __shared__ int8_t sslot[kPatternsMax];
+  __shared__ uint32_t slot_q[kPatternsMax], n_slot_q;
+  if (threadIdx.x == 0) {
+    uint32_t c = 0;
+    for (uint32_t q = 0; q < ep.n_pat; ++q)
+      if (ep.loop_slot[q] >= 0 && ep.pats[q].model != 5) slot_q[c++] = q;
+    n_slot_q = c;
+  }
+  for (uint32_t q = threadIdx.x; q < ep.n_pat; q += blockDim.x) {
+    sp[q] = ep.pats[q];
+    sslot[q] = ep.loop_slot[q];
+  }
+  __syncthreads();
+  const uint64_t stride_items = (uint64_t)p.E + p.n;
+  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < p.E; e += gridDim.x * blockDim.x) {
+    const uint32_t j = p.edge_use[e];
+    const uint64_t *row = p.C + (uint64_t)j * 2 * p.R;
+    double XA[4], XL[4];
+#pragma unroll
+    for (int r = 1; r <= 3; ++r) {
+      const uint64_t lat = row[p.R + r];
+      XL[r] = (double)lat;
+      XA[r] = (double)(lat + row[r]);
+    }
+    const EdgeInfo x = edge_info(p, e, p.loop_id[j]);
+    for (uint32_t k = 0; k < n_slot_q; ++k) {
+      const gpa_pattern &q = sp[slot_q[k]];
+      ep.mval[(uint64_t)sslot[slot_q[k]] * stride_items + e] = edge_match(q, x, q.sample_class ? XL : XA);
     }
   }
 }
@@ -260,6 +310,13 @@ cudaError_t launch_estimate(const DevProgram &p, const EstimatePlan &ep, int n_s
   const uint64_t work = (uint64_t)p.n * ((ep.n_pat + kEstGroup - 1) / kEstGroup);
   const uint32_t g = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((work + threads - 1) / threads, (uint64_t)n_sms * 32));
   k_est_rows<<<g, threads, 0, s>>>(p, ep);
+  bool any_slot = false;
+  for (uint32_t q = 0; q < ep.n_pat; ++q) any_slot |= ep.loop_slot[q] >= 0;
+  if (any_slot && p.E) {
+    const uint32_t ge = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(((uint64_t)p.E + 255) / 256, (uint64_t)n_sms * 16));
+    k_est_edges<<<ge, 256, 0, s>>>(p, ep);
+    *launches += 1;
+  }
   SegLaunch a{};
   a.n_pat = ep.n_pat;
   a.n_fam = 2;

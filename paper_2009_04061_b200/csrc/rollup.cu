@@ -3,8 +3,8 @@
 //
 // Hand-written segmented reductions (no CUB), deterministic: every sum has a fixed order.
 //   k_vrows            V[i] = {NCOL x (all, lat)} for every instruction, one
-//                      warp per instruction row, stores coalesced; this is also the instruction
-//                      level of the rollup (gpa_instr_vector).
+//                      thread per instruction with independent vector loads and 16-byte (all, lat)
+//                      stores; this is also the instruction level of the rollup (gpa_instr_vector).
 //   k_rollup_chunks    one warp per <=128-instruction chunk of a create-time order (line-major |
 //                      loop-major | function ranges); member ids are loaded once and broadcast by
 //                      shuffles, lane s owns value slot s (and s+32) of the row, so each member
@@ -21,13 +21,39 @@
 namespace gpa {
 namespace {
 
-// one warp per instruction row (lane = value slot): the row's loads are shared by the warp and
-// V is written coalesced
+// one thread per instruction: the B row (64 B), the C row (16R B), class and self flags are
+// loaded with independent (vector) loads, and the row of V is written as one (all, lat) pair per
+// column (16-byte stores) -- many rows in flight per SM.  Same values as vvalue().
 __global__ void k_vrows(DevProgram p, double *__restrict__ vbuf) {
-  const uint32_t nv = 2 * p.ncol, lane = threadIdx.x & 31;
-  const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < p.n; i += warps)
-    for (uint32_t s = lane; s < nv; s += 32) vbuf[(uint64_t)i * nv + s] = vvalue(p, i, s >> 1, s & 1);
+  const uint32_t ncol = p.ncol, R = p.R;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += gridDim.x * blockDim.x) {
+    const double2 *b2 = reinterpret_cast<const double2 *>(p.B + 8 * (uint64_t)i);
+    const double2 bm = b2[BG_MEM], be = b2[BG_EXEC], bw = b2[BG_WAR], bs = b2[BG_SYNC];
+    const uint32_t cls = p.opclass[i], sf = p.selfm[i];
+    const uint64_t *row = p.C + (uint64_t)i * 2 * R;
+    // all loads before the first store (V may alias nothing, but the compiler cannot know)
+    uint64_t act[kReasonsMax], lat[kReasonsMax];
+#pragma unroll
+    for (uint32_t r = 1; r < kReasonsMax; ++r) {
+      act[r] = r < R ? row[r] : 0ull;
+      lat[r] = r < R ? row[R + r] : 0ull;
+    }
+    double2 *out = reinterpret_cast<double2 *>(vbuf + (uint64_t)i * 2 * ncol);
+    const double2 z = make_double2(0.0, 0.0);
+    out[COL_MEM_GLOBAL] = (cls != OC_LOCAL && cls != OC_CONSTANT) ? bm : z;
+    out[COL_MEM_LOCAL] = cls == OC_LOCAL ? bm : z;
+    out[COL_MEM_CONSTANT] = cls == OC_CONSTANT ? bm : z;
+    out[COL_EXEC_SHARED] = cls == OC_SHARED ? be : z;
+    out[COL_EXEC_ARITH] = cls != OC_SHARED ? be : z;
+    out[COL_EXEC_WAR] = bw;
+    out[COL_SYNC] = bs;
+#pragma unroll
+    for (uint32_t r = 1; r < kReasonsMax; ++r) {
+      if (r >= R) break;
+      const bool on = r > R_SYNC || ((sf >> (r - 1)) & 1u);
+      out[6 + r] = on ? make_double2((double)(act[r] + lat[r]), (double)lat[r]) : z;
+    }
+  }
 }
 
 // sum over positions [b, e) of rows it(pos): slot s < nv from vals, slots nv, nv+1 from al
@@ -57,6 +83,11 @@ __device__ __forceinline__ void warp_sum_rows(uint32_t lane, uint32_t nv, uint32
   }
 }
 
+#ifndef GPA_ROLL_MEMBERS
+#define GPA_ROLL_MEMBERS 8
+#endif
+constexpr int kRollMembers = GPA_ROLL_MEMBERS;   // members (row loads) in flight per lane
+
 // chunk of <= 128 members: member ids are loaded once (4 per lane) and broadcast by shuffles, so
 // the row loads of consecutive members are independent and stay in flight together
 __global__ void __launch_bounds__(128) k_rollup_chunks(RollupPlan rp, uint32_t nv, const double *__restrict__ vbuf,
@@ -70,36 +101,31 @@ __global__ void __launch_bounds__(128) k_rollup_chunks(RollupPlan rp, uint32_t n
     for (int t = 0; t < kChunk / 32; ++t) ids[t] = (lane + 32 * t < len) ? rp.order[b + lane + 32 * t] : 0u;
     for (uint32_t s0 = 0; s0 < nv + 2; s0 += 32) {   // uniform trip count: shuffles need all lanes
       const uint32_t s = s0 + lane;
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      uint64_t al = 0;
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};   // member u adds into acc[u % 4]: the order of the
+      uint64_t al = 0;                          // four-accumulator scheme (a0..a3) is unchanged
       const bool is_v = s < nv, is_al = s >= nv && s < nv + 2;
 #pragma unroll
       for (int t = 0; t < kChunk / 32; ++t) {
         const uint32_t m_end = len > 32u * t ? min(32u, len - 32u * t) : 0u;
-        for (uint32_t m = 0; m < m_end; m += 4) {
-          const uint32_t i0 = __shfl_sync(0xffffffffu, ids[t], m);
-          const uint32_t i1 = __shfl_sync(0xffffffffu, ids[t], m + 1 < 32 ? m + 1 : 31);
-          const uint32_t i2 = __shfl_sync(0xffffffffu, ids[t], m + 2 < 32 ? m + 2 : 31);
-          const uint32_t i3 = __shfl_sync(0xffffffffu, ids[t], m + 3 < 32 ? m + 3 : 31);
+        for (uint32_t m = 0; m < m_end; m += kRollMembers) {
+          uint32_t id[kRollMembers];
+#pragma unroll
+          for (int u = 0; u < kRollMembers; ++u) id[u] = __shfl_sync(0xffffffffu, ids[t], (m + u) & 31);
           if (is_v) {
-            const double x0 = vbuf[(uint64_t)i0 * nv + s];
-            const double x1 = m + 1 < m_end ? vbuf[(uint64_t)i1 * nv + s] : 0.0;
-            const double x2 = m + 2 < m_end ? vbuf[(uint64_t)i2 * nv + s] : 0.0;
-            const double x3 = m + 3 < m_end ? vbuf[(uint64_t)i3 * nv + s] : 0.0;
-            a0 = __dadd_rn(a0, x0);
-            a1 = __dadd_rn(a1, x1);
-            a2 = __dadd_rn(a2, x2);
-            a3 = __dadd_rn(a3, x3);
+            double x[kRollMembers];
+#pragma unroll
+            for (int u = 0; u < kRollMembers; ++u) x[u] = m + u < m_end ? vbuf[(uint64_t)id[u] * nv + s] : 0.0;
+#pragma unroll
+            for (int u = 0; u < kRollMembers; ++u) acc[u & 3] = __dadd_rn(acc[u & 3], x[u]);
           } else if (is_al) {
             const uint32_t c = s - nv;
-            al += AL[2 * (uint64_t)i0 + c];
-            if (m + 1 < m_end) al += AL[2 * (uint64_t)i1 + c];
-            if (m + 2 < m_end) al += AL[2 * (uint64_t)i2 + c];
-            if (m + 3 < m_end) al += AL[2 * (uint64_t)i3 + c];
+#pragma unroll
+            for (int u = 0; u < kRollMembers; ++u)
+              if (m + u < m_end) al += AL[2 * (uint64_t)id[u] + c];
           }
         }
       }
-      if (is_v) rp.part_v[(uint64_t)ch * nv + s] = __dadd_rn(__dadd_rn(a0, a1), __dadd_rn(a2, a3));
+      if (is_v) rp.part_v[(uint64_t)ch * nv + s] = __dadd_rn(__dadd_rn(acc[0], acc[1]), __dadd_rn(acc[2], acc[3]));
       else if (is_al) rp.part_al[2 * (uint64_t)ch + (s - nv)] = al;
     }
   }
@@ -131,8 +157,8 @@ inline uint32_t warp_grid(uint64_t warps, int n_sms) {
 }  // namespace
 
 cudaError_t launch_vrows(const DevProgram &p, double *vbuf, int n_sms, cudaStream_t s) {
-  const uint64_t total = (uint64_t)p.n * 32;
-  const uint32_t g = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, (uint64_t)n_sms * 32));
+  const uint64_t total = (uint64_t)p.n;
+  const uint32_t g = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, (uint64_t)n_sms * 8));
   k_vrows<<<g, 256, 0, s>>>(p, vbuf);
   return cudaGetLastError();
 }

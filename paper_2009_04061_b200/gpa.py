@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgpa_b200.so")
+LIB_PATH = os.environ.get("GPA_LIB_PATH") or os.path.join(_HERE, "libgpa_b200.so")   # override: tuning builds
 
 VIEW = {
     "counts": 0, "stats": 1, "instr_al": 2, "cand": 3, "self": 4, "share": 5, "instr_blame": 6,
