@@ -241,8 +241,8 @@ def run_batch(args):
     ms_per_step = ms / args.steps
     st = P.stats()
     assert st[0] + st[1] == n_mine, (st, n_mine)
-    est = P.read_estimates()
-    allest = gather_estimates(np.array([[e.speedup for e in row] for row in est], np.float64))
+    est = P.read_estimates_array()
+    allest = gather_estimates(np.ascontiguousarray(est["speedup"]))
     assert allest.shape[0] == prog.n_kernels
 
     # end to end: pinned host -> device copy of this rank's grouped records inside the timed region
@@ -258,7 +258,7 @@ def run_batch(args):
         P.reset()
         P.ingest_segments(dbuf, seg_begin, seg_kernel, pc_base=lo)
         P.analyze()
-        P.read_estimates()
+        P.read_estimates_array()
     eb.record(stream)
     torch.cuda.synchronize()
     e_ms = ea.elapsed_time(eb)
@@ -409,7 +409,7 @@ def main():
         host.copy_(recs)
         est_bytes = P.n_kernels * P.n_patterns * 56
         for _ in range(1):
-            P.reset(); P.ingest_host(host); P.analyze(); P.read_estimates()
+            P.reset(); P.ingest_host(host); P.analyze(); P.read_estimates_array()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -423,7 +423,7 @@ def main():
                 dist.all_reduce(counts, op=dist.ReduceOp.SUM)
                 dist.all_reduce(stats, op=dist.ReduceOp.SUM)
             P.analyze()
-            P.read_estimates()
+            P.read_estimates_array()
         eb.record(stream)
         torch.cuda.synchronize()
         e_ms = ea.elapsed_time(eb)

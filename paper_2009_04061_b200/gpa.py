@@ -251,6 +251,13 @@ class Program:
         _check(lib().gpa_read_estimates(self.handle, ctypes.addressof(out), self._s(stream)), "gpa_read_estimates")
         return [[out[k * self.n_patterns + q] for q in range(self.n_patterns)] for k in range(self.n_kernels)]
 
+    def read_estimates_array(self, stream=None):
+        """Same as read_estimates() as a numpy structured array [n_kernels, n_patterns] (fields of
+        gpa_estimate_out), without building Python objects per entry."""
+        out = (EstimateOut * (self.n_kernels * self.n_patterns))()
+        _check(lib().gpa_read_estimates(self.handle, ctypes.addressof(out), self._s(stream)), "gpa_read_estimates")
+        return np.ctypeslib.as_array(out).reshape(self.n_kernels, self.n_patterns)
+
     def stats(self, stream=None):
         out = (ctypes.c_uint64 * 4)()
         _check(lib().gpa_get_stats(self.handle, out, self._s(stream)), "gpa_get_stats")

@@ -211,3 +211,23 @@ def test_analyze_graph_equals_separate_calls():
         for a, b in zip(outs[0][:3], other[:3]):
             assert torch.equal(a, b)
         assert outs[0][3] == other[3]
+
+
+def test_read_estimates_array_matches_struct_list():
+    prog = gp.config_program(2)
+    recs = config_stream(prog, 2).host(0, 500_000)
+    import torch
+    from paper_2009_04061_b200 import Program
+    P = Program(prog)
+    P.set_patterns(table2())
+    P.reset()
+    P.ingest(torch.from_numpy(recs.view(np.int64)).cuda())
+    P.analyze()
+    rows = P.read_estimates()
+    arr = P.read_estimates_array()
+    assert arr.shape == (len(rows), len(rows[0]))
+    for k, row in enumerate(rows):
+        for q, e in enumerate(row):
+            for f in ("speedup", "M", "eq3", "eq4", "T", "A", "best_scope", "unbounded", "matched", "model"):
+                a, b = getattr(e, f), arr[k, q][f]
+                assert a == b or (np.isnan(a) and np.isnan(b))
