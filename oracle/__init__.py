@@ -54,6 +54,11 @@ class Estimate(ctypes.Structure):
                 ("matched", ctypes.c_uint8), ("model", ctypes.c_uint8), ("pad", ctypes.c_uint8)]
 
 
+class Hotspot(ctypes.Structure):
+    _fields_ = [("def_pc", ctypes.c_uint32), ("use_pc", ctypes.c_uint32), ("distance", ctypes.c_uint32),
+                ("item", ctypes.c_uint32), ("samples", ctypes.c_double)]
+
+
 _lib = None
 
 
@@ -66,6 +71,9 @@ def lib():
         L.or_blame.argtypes = [vp, vp, vp, vp, vp, vp]
         L.or_rollup.argtypes = [vp] * 13
         L.or_estimate_all.argtypes = [vp, vp, vp, vp, vp, vp, ctypes.c_uint32, vp]
+        L.or_hotspots.argtypes = [vp, vp, vp, vp, vp, vp, ctypes.c_uint32, ctypes.c_uint32, vp, vp]
+        L.or_rank.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint32, vp]
+        L.or_coverage.argtypes = [vp, vp, vp, vp]
         for f in ("or_eq2", "or_eq4", "or_eq5", "or_eq10"):
             getattr(L, f).restype = ctypes.c_double
         L.or_eq2.argtypes = [ctypes.c_double] * 2
@@ -168,6 +176,26 @@ class OracleProgram:
         return {"C": C, "stats": stats, **b, **r, "est": est}
 
 
+    # --- after the path: advice (hotspots, ranking, single dependency coverage)
+    def hotspots(self, C, blame, patterns, top_k):
+        """(list [K][Q] of lists of Hotspot) for the pattern list."""
+        K, Q = self.n_kernels, len(patterns)
+        pats = (Pattern * Q)(*patterns)
+        out = (Hotspot * (K * Q * top_k))()
+        n_out = np.zeros(K * Q, np.uint32)
+        lib().or_hotspots(self.ref, C.ctypes.data, blame["cand"].ctypes.data, blame["self"].ctypes.data,
+                          blame["share"].ctypes.data, ctypes.addressof(pats), Q, top_k,
+                          ctypes.addressof(out), n_out.ctypes.data)
+        return [[[out[(k * Q + q) * top_k + t] for t in range(int(n_out[k * Q + q]))] for q in range(Q)]
+                for k in range(K)]
+
+    def coverage(self, C, cand):
+        """uint64 [K, 3]: nodes, single-dependency nodes before pruning, after pruning."""
+        out = np.zeros((self.n_kernels, 3), np.uint64)
+        lib().or_coverage(self.ref, C.ctypes.data, cand.ctypes.data, out.ctypes.data)
+        return out
+
+
 def eq2(T, M):
     return lib().or_eq2(T, M)
 
@@ -182,3 +210,11 @@ def eq5(T, A_nested, ML):
 
 def eq10(W, W_new, R_I, f):
     return lib().or_eq10(W, W_new, R_I, f)
+
+def rank(est):
+    """est: list [K][Q] of Estimate -> uint32 [K, Q] pattern order by speedup (or_rank)."""
+    K, Q = len(est), len(est[0]) if est else 0
+    flat = (Estimate * (K * Q))(*[e for row in est for e in row])
+    order = np.zeros((K, Q), np.uint32)
+    lib().or_rank(ctypes.addressof(flat), K, Q, order.ctypes.data)
+    return order

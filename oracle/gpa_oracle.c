@@ -466,3 +466,109 @@ int or_estimate_all(const or_program *p, const uint64_t *C, const uint8_t *cand,
   free(loopM); free(loopA); free(funcM); free(funcA); free(loop_func);
   return 0;
 }
+
+/* ---------------------------------------------------------------- after the path: advice */
+
+/* Hotspots ("Each optimizer ... lists several hotspots to focus on.  Each hotspot
+ * consists of the def and use locations and their distance"; "the top five hotspots").
+ * The items of a kernel are its edges (def -> use, matched samples of match_edge) and its
+ * instructions (own self / pass-through samples, match_instr); Q30. */
+static int hot_before(double sa, uint32_t ia, double sb, uint32_t ib) {
+  return sa > sb || (sa == sb && ia < ib);
+}
+
+int or_hotspots(const or_program *p, const uint64_t *C, const uint8_t *cand,
+                const uint8_t *self_flags, const double *share, const or_pattern *pats,
+                uint32_t n_pat, uint32_t top_k, or_hotspot *out, uint32_t *n_out) {
+  const uint32_t E = p->row_ptr[p->n_instr];
+  uint32_t k, qi, j, e;
+  for (k = 0; k < p->n_kernels; ++k) {
+    uint32_t i0 = p->func_begin[p->kernel_func_begin[k]], i1 = p->func_begin[p->kernel_func_begin[k + 1]];
+    for (qi = 0; qi < n_pat; ++qi) {
+      const or_pattern *q = &pats[qi];
+      or_hotspot *h = &out[((uint64_t)k * n_pat + qi) * top_k];
+      uint32_t n = 0;
+      if (q->model != 5) {
+        for (j = i0; j < i1; ++j) {
+          for (e = p->row_ptr[j]; e <= p->row_ptr[j + 1]; ++e) {
+            or_hotspot x;
+            uint32_t t;
+            if (e < p->row_ptr[j + 1]) {   /* an in-edge of j */
+              x.def_pc = p->edge_def[e]; x.use_pc = j; x.distance = p->edge_max_len[e]; x.item = e;
+              x.samples = match_edge(p, C, cand, share, q, e, j);
+            } else {                       /* j's own samples */
+              x.def_pc = j; x.use_pc = j; x.distance = 0; x.item = E + j;
+              x.samples = match_instr(p, C, self_flags, q, j);
+            }
+            if (!(x.samples > 0.0)) continue;
+            /* insertion into the sorted top list */
+            if (n == top_k && !hot_before(x.samples, x.item, h[n - 1].samples, h[n - 1].item)) continue;
+            t = n < top_k ? n++ : n - 1;
+            while (t > 0 && hot_before(x.samples, x.item, h[t - 1].samples, h[t - 1].item)) {
+              h[t] = h[t - 1];
+              --t;
+            }
+            h[t] = x;
+          }
+        }
+      }
+      n_out[(uint64_t)k * n_pat + qi] = n;
+    }
+  }
+  return 0;
+}
+
+/* P:261 "an advice report that contains suggestions from its top optimizers sorted by their
+ * estimated speedups"; Q31. */
+int or_rank(const or_estimate *est, uint32_t n_kernels, uint32_t n_pat, uint32_t *order) {
+  uint32_t k, a, b;
+  for (k = 0; k < n_kernels; ++k) {
+    uint32_t *o = &order[(uint64_t)k * n_pat];
+    const or_estimate *x = &est[(uint64_t)k * n_pat];
+    for (a = 0; a < n_pat; ++a) o[a] = a;
+    for (a = 1; a < n_pat; ++a) {          /* stable insertion sort, descending speedup */
+      uint32_t v = o[a];
+      b = a;
+      while (b > 0 && x[o[b - 1]].speedup < x[v].speedup) {
+        o[b] = o[b - 1];
+        --b;
+      }
+      o[b] = v;
+    }
+  }
+  return 0;
+}
+
+/* P:658-659 "a node is a single dependency node if the node does not have any incoming edge,
+ * or each incoming edge represents a different dependency.  ... single dependency coverage as
+ * the ratio of single dependency nodes to the total number of nodes."  Q32: nodes are the
+ * instructions with dependency-stall samples; before pruning every in-edge may represent each
+ * dependency, after pruning an edge represents the reasons of its candidate mask (rules 1-3). */
+int or_coverage(const or_program *p, const uint64_t *C, const uint8_t *cand, uint64_t *out) {
+  uint32_t k, j, e, r;
+  for (k = 0; k < p->n_kernels; ++k) {
+    uint32_t i0 = p->func_begin[p->kernel_func_begin[k]], i1 = p->func_begin[p->kernel_func_begin[k + 1]];
+    uint64_t nodes = 0, before = 0, after = 0;
+    for (j = i0; j < i1; ++j) {
+      int live = 0, single_b = 1, single_a = 1;
+      uint32_t deg = p->row_ptr[j + 1] - p->row_ptr[j];
+      for (r = R_MEM; r <= R_SYNC; ++r) {
+        uint32_t n_r = 0;
+        if (cnt(p, C, j, 0, r) + cnt(p, C, j, 1, r) == 0) continue;   /* no stall of this kind */
+        live = 1;
+        for (e = p->row_ptr[j]; e < p->row_ptr[j + 1]; ++e)
+          if (cand[e] & (1u << (r - 1u))) ++n_r;
+        if (deg > 1) single_b = 0;
+        if (n_r > 1) single_a = 0;
+      }
+      if (!live) continue;
+      ++nodes;
+      before += (uint64_t)single_b;
+      after += (uint64_t)single_a;
+    }
+    out[3 * (uint64_t)k] = nodes;
+    out[3 * (uint64_t)k + 1] = before;
+    out[3 * (uint64_t)k + 2] = after;
+  }
+  return 0;
+}

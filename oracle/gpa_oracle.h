@@ -97,6 +97,30 @@ int or_estimate_all(const or_program *p, const uint64_t *C, const uint8_t *cand,
                     const uint8_t *self_flags, const double *share,
                     const or_pattern *pats, uint32_t n_pat, or_estimate *out);
 
+/* ---- after the path: the advice report's data (P:261, P:658-661,
+ * P:684-686).  DESIGN.md §3.2 Q30-Q33 state the readings. */
+typedef struct {
+  uint32_t def_pc;    /* blamed instruction (def of an edge; the use itself for self/pass-through) */
+  uint32_t use_pc;    /* instruction where the samples were observed */
+  uint32_t distance;  /* max_len of the edge (instructions on the longest path), 0 for own samples */
+  uint32_t item;      /* edge index e, or E + instruction for the use's own samples */
+  double samples;     /* matched samples of the pattern carried by this item */
+} or_hotspot;
+
+/* Per (kernel k, pattern q): the top_k items with matched samples > 0, by samples descending,
+ * ties by item ascending.  out[(k*n_pat + q)*top_k + t], n_out[k*n_pat + q] = count. */
+int or_hotspots(const or_program *p, const uint64_t *C, const uint8_t *cand,
+                const uint8_t *self_flags, const double *share, const or_pattern *pats,
+                uint32_t n_pat, uint32_t top_k, or_hotspot *out, uint32_t *n_out);
+
+/* Optimizers of each kernel ranked by estimated speedup: order[k*n_pat + t] =
+ * pattern at rank t; +inf first, ties by pattern index. */
+int or_rank(const or_estimate *est, uint32_t n_kernels, uint32_t n_pat, uint32_t *order);
+
+/* Single dependency coverage per kernel, before and after pruning:
+ * out[3k] = nodes, out[3k+1] = single-dependency nodes before, out[3k+2] = after. */
+int or_coverage(const or_program *p, const uint64_t *C, const uint8_t *cand, uint64_t *out);
+
 /* Closed forms, exposed for the equation pins. */
 double or_eq2(double T, double M);
 double or_eq4(double T, double A, double ML);
