@@ -120,6 +120,22 @@ typedef struct {
   uint8_t unbounded, matched, model, pad;
 } gpa_estimate_out;
 
+/* Advice report data (after the path; DESIGN.md §3.2 Q30-Q32). */
+#define GPA_TOP_K_MAX 8
+typedef struct {
+  uint32_t def_pc;       /* blamed instruction: def of an edge, or the use for its own samples */
+  uint32_t use_pc;       /* instruction where the samples were observed */
+  uint32_t distance;     /* the edge's max_len ("their distance"); 0 for own samples */
+  uint32_t item;         /* edge index e, or E + instruction */
+  double samples;        /* matched samples of the pattern (its sample class) on this item */
+} gpa_hotspot;           /* 24 bytes */
+
+typedef struct {
+  uint64_t nodes;          /* instructions with dependency-stall samples */
+  uint64_t single_before;  /* single-dependency nodes before pruning */
+  uint64_t single_after;   /* after rules 1-3 */
+} gpa_coverage;
+
 typedef struct gpa_program gpa_program;
 
 /* Views of device results (byte ranges of the workspace), for gpa_view(): */
@@ -160,6 +176,20 @@ gpa_status gpa_workspace_size(const gpa_program_desc *desc, size_t *bytes);
 gpa_status gpa_program_create(const gpa_program_desc *desc, void *d_workspace, size_t bytes,
                               void *stream, gpa_program **out);
 gpa_status gpa_program_destroy(gpa_program *prog);
+
+/* Advice (enqueue; needs estimates of the current counts: gpa_estimate or gpa_analyze with
+ * patterns set): per (kernel, pattern) the top_k hotspots (1 <= top_k <= GPA_TOP_K_MAX; items
+ * with matched samples > 0 by samples descending, ties by item), the patterns of every kernel
+ * ranked by estimated speedup (+inf first, ties by pattern index) and the single
+ * dependency coverage before / after pruning per kernel. */
+gpa_status gpa_advise(gpa_program *prog, uint32_t top_k, void *stream);
+
+/* Copy the advice to HOST buffers (synchronizes); any pointer may be NULL to skip it:
+ *   h_hotspots [n_kernels][n_patterns][top_k], h_n_hotspots u32 [n_kernels][n_patterns],
+ *   h_rank u32 [n_kernels][n_patterns] (pattern index at each rank), h_coverage [n_kernels].
+ * GPA_ERR_BAD_STATE before gpa_advise. */
+gpa_status gpa_read_advice(gpa_program *prog, gpa_hotspot *h_hotspots, uint32_t *h_n_hotspots, uint32_t *h_rank,
+                           gpa_coverage *h_coverage, void *stream);
 
 /* Zero the count table and stats (enqueue). */
 gpa_status gpa_reset_counts(gpa_program *prog, void *stream);

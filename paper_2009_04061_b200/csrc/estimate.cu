@@ -18,49 +18,6 @@
 namespace gpa {
 namespace {
 
-__device__ __forceinline__ uint32_t classify(uint32_t r, uint32_t cls, uint32_t kind) {
-  if (r == R_MEM) return cls == OC_LOCAL ? COL_MEM_LOCAL : cls == OC_CONSTANT ? COL_MEM_CONSTANT : COL_MEM_GLOBAL;
-  if (r == R_EXEC) return (kind & K_WAR) ? COL_EXEC_WAR : cls == OC_SHARED ? COL_EXEC_SHARED : COL_EXEC_ARITH;
-  return COL_SYNC;
-}
-
-__device__ __forceinline__ bool passes(const gpa_pattern &q, uint32_t cls, uint32_t flags) {
-  return ((q.class_mask >> cls) & 1u) && (!q.flag_filter || (flags & q.flag_filter));
-}
-
-// matched samples of edge e (def d -> use j) under pattern q: X = all / latency samples of j
-struct EdgeInfo {
-  uint32_t m, cls, flags, c_mem, c_exec;
-  bool same;
-  double sh0, sh1, sh2;
-};
-__device__ __forceinline__ EdgeInfo edge_info(const DevProgram &p, uint32_t e, int32_t loop_j) {
-  EdgeInfo x{};
-  x.m = p.cand[e];
-  uint32_t kind = 0;
-  if (x.m) {
-    const uint32_t d = p.edge_def[e];
-    x.cls = p.opclass[d];
-    x.flags = p.iflags[d];
-    kind = p.edge_kind[e];
-    x.same = p.loop_id[d] >= 0 && p.loop_id[d] == loop_j;
-    const double *sh = p.share + 3 * (uint64_t)e;
-    x.sh0 = sh[0]; x.sh1 = sh[1]; x.sh2 = sh[2];
-  }
-  x.c_mem = classify(R_MEM, x.cls, kind);
-  x.c_exec = classify(R_EXEC, x.cls, kind);
-  return x;
-}
-__device__ __forceinline__ double edge_match(const gpa_pattern &q, const EdgeInfo &x, const double *X) {
-  double me = 0.0;
-  if (x.m && passes(q, x.cls, x.flags) && (!q.same_loop || x.same)) {
-    if ((x.m & 1u) && ((q.column_mask >> x.c_mem) & 1u)) me = __dadd_rn(me, __dmul_rn(X[1], x.sh0));
-    if ((x.m & 2u) && ((q.column_mask >> x.c_exec) & 1u)) me = __dadd_rn(me, __dmul_rn(X[2], x.sh1));
-    if ((x.m & 4u) && ((q.column_mask >> COL_SYNC) & 1u)) me = __dadd_rn(me, __dmul_rn(X[3], x.sh2));
-  }
-  return me;
-}
-
 // one thread per (use row j, group of kEstGroup patterns): the row's counts and in-edges are read
 // once per group and every pattern of the group is evaluated from registers; consecutive threads
 // take consecutive rows (coalesced).  Per (j, pattern) the sum runs over the row's edges in CSR
@@ -118,16 +75,7 @@ __global__ void k_est_rows(DevProgram p, EstimatePlan ep) {
         ep.mrow[(uint64_t)qi * p.n + j] = 0.0;
         continue;
       }
-      const bool L = q.sample_class != 0;
-      const double *X = L ? XL : XA;
-      double mi = 0.0;
-      if (passes(q, cls_j, flags_j) && (!q.same_loop || loop_j >= 0)) {
-        for (uint32_t r = R_MEM; r <= R_SYNC; ++r)
-          if (((self_j >> (r - 1)) & 1u) && ((q.column_mask >> (COL_MEM_SELF + r - 1)) & 1u)) mi = __dadd_rn(mi, X[r]);
-        for (uint32_t r = 4; r < p.R; ++r)
-          if ((q.column_mask >> (COL_PASS0 + r - 4)) & 1u)
-            mi = __dadd_rn(mi, (double)(row[p.R + r] + (L ? 0ull : row[r])));
-      }
+      const double mi = instr_match(q, p.R, row, q.sample_class ? XL : XA, cls_j, flags_j, self_j, loop_j);
       const int slot = sslot[qi];
       if (slot >= 0) ep.mval[(uint64_t)slot * stride_items + p.E + j] = mi;
       ep.mrow[(uint64_t)qi * p.n + j] = __dadd_rn(sum[k], mi);

@@ -46,7 +46,7 @@ constexpr uint32_t COL_MEM_GLOBAL = 0, COL_MEM_LOCAL = 1, COL_MEM_CONSTANT = 2,
 // per-instruction edge-blame groups (GPA_VIEW_INSTR_BLAME)
 constexpr uint32_t BG_MEM = 0, BG_EXEC = 1, BG_WAR = 2, BG_SYNC = 3;
 
-enum : int { ST_COUNTS = 1, ST_BLAMED = 2, ST_AGGREGATED = 4, ST_PATTERNS = 8 };
+enum : int { ST_COUNTS = 1, ST_BLAMED = 2, ST_AGGREGATED = 4, ST_PATTERNS = 8, ST_ESTIMATED = 16, ST_ADVISED = 32 };
 enum : int { VAR_SMEM = 0, VAR_PART = 1, VAR_L2 = 2 };
 
 // Device-side view of a program: plain pointers into the workspace.
@@ -106,6 +106,16 @@ struct EstimatePlan {
   gpa_estimate_out *out;        // [n_kernels][n_pat]
 };
 
+// advice (NEXT #2): hotspots [n_kernels][n_pat][kTopKMax], counts, ranks, coverage
+constexpr uint32_t kTopKMax = GPA_TOP_K_MAX;
+struct AdvicePlan {
+  gpa_hotspot *hot;
+  uint32_t *n_hot;              // [n_kernels][n_pat]
+  uint32_t *rank;               // [n_kernels][n_pat] pattern at each rank
+  gpa_coverage *cov;            // [n_kernels]
+  uint32_t top_k;
+};
+
 // kernel launchers (return cudaError_t of the launch)
 cudaError_t launch_ingest(const DevProgram &p, int variant, const void *records, uint64_t n,
                           int n_sms, size_t smem_optin, cudaStream_t s);
@@ -115,6 +125,8 @@ cudaError_t launch_rollup(const DevProgram &p, const RollupPlan &rp, int n_sms, 
 cudaError_t launch_estimate(const DevProgram &p, const EstimatePlan &ep, int n_sms,
                             cudaStream_t s, uint64_t *launches);
 cudaError_t launch_vrows(const DevProgram &p, double *vbuf, int n_sms, cudaStream_t s);
+cudaError_t launch_advice(const DevProgram &p, const EstimatePlan &ep, const AdvicePlan &ap, cudaStream_t s,
+                          uint64_t *launches);
 cudaError_t launch_ingest_segments(const DevProgram &p, const void *records, uint64_t n, const uint64_t *seg_begin,
                                    const uint32_t *seg_kernel, uint32_t n_seg, uint32_t pc_base, uint32_t max_tab_bins,
                                    int n_sms, cudaStream_t s);
@@ -144,6 +156,66 @@ __device__ __forceinline__ double vvalue(const DevProgram &p, uint32_t i, uint32
   return (double)(c ? lat : row[r] + lat);
 }
 
+
+// ---- pattern matching shared by the estimate and advice kernels (Table 2)
+__device__ __forceinline__ uint32_t classify(uint32_t r, uint32_t cls, uint32_t kind) {
+  if (r == R_MEM) return cls == OC_LOCAL ? COL_MEM_LOCAL : cls == OC_CONSTANT ? COL_MEM_CONSTANT : COL_MEM_GLOBAL;
+  if (r == R_EXEC) return (kind & K_WAR) ? COL_EXEC_WAR : cls == OC_SHARED ? COL_EXEC_SHARED : COL_EXEC_ARITH;
+  return COL_SYNC;
+}
+
+__device__ __forceinline__ bool passes(const gpa_pattern &q, uint32_t cls, uint32_t flags) {
+  return ((q.class_mask >> cls) & 1u) && (!q.flag_filter || (flags & q.flag_filter));
+}
+
+// matched samples of edge e (def d -> use j) under pattern q: X = all / latency samples of j
+struct EdgeInfo {
+  uint32_t m, cls, flags, c_mem, c_exec;
+  bool same;
+  double sh0, sh1, sh2;
+};
+__device__ __forceinline__ EdgeInfo edge_info(const DevProgram &p, uint32_t e, int32_t loop_j) {
+  EdgeInfo x{};
+  x.m = p.cand[e];
+  uint32_t kind = 0;
+  if (x.m) {
+    const uint32_t d = p.edge_def[e];
+    x.cls = p.opclass[d];
+    x.flags = p.iflags[d];
+    kind = p.edge_kind[e];
+    x.same = p.loop_id[d] >= 0 && p.loop_id[d] == loop_j;
+    const double *sh = p.share + 3 * (uint64_t)e;
+    x.sh0 = sh[0]; x.sh1 = sh[1]; x.sh2 = sh[2];
+  }
+  x.c_mem = classify(R_MEM, x.cls, kind);
+  x.c_exec = classify(R_EXEC, x.cls, kind);
+  return x;
+}
+__device__ __forceinline__ double edge_match(const gpa_pattern &q, const EdgeInfo &x, const double *X) {
+  double me = 0.0;
+  if (x.m && passes(q, x.cls, x.flags) && (!q.same_loop || x.same)) {
+    if ((x.m & 1u) && ((q.column_mask >> x.c_mem) & 1u)) me = __dadd_rn(me, __dmul_rn(X[1], x.sh0));
+    if ((x.m & 2u) && ((q.column_mask >> x.c_exec) & 1u)) me = __dadd_rn(me, __dmul_rn(X[2], x.sh1));
+    if ((x.m & 4u) && ((q.column_mask >> COL_SYNC) & 1u)) me = __dadd_rn(me, __dmul_rn(X[3], x.sh2));
+  }
+  return me;
+}
+
+// the use's own matched samples (self and pass-through columns) under pattern q (k_est_rows,
+// k_hotspots): X = all / latency samples of the dependency reasons, row = C row of j
+__device__ __forceinline__ double instr_match(const gpa_pattern &q, uint32_t R, const uint64_t *row, const double *X,
+                                              uint32_t cls_j, uint32_t flags_j, uint32_t self_j, int32_t loop_j) {
+  double mi = 0.0;
+  const bool L = q.sample_class != 0;
+  if (passes(q, cls_j, flags_j) && (!q.same_loop || loop_j >= 0)) {
+    for (uint32_t r = R_MEM; r <= R_SYNC; ++r)
+      if (((self_j >> (r - 1)) & 1u) && ((q.column_mask >> (COL_MEM_SELF + r - 1)) & 1u)) mi = __dadd_rn(mi, X[r]);
+    for (uint32_t r = 4; r < R; ++r)
+      if ((q.column_mask >> (COL_PASS0 + r - 4)) & 1u) mi = __dadd_rn(mi, (double)(row[R + r] + (L ? 0ull : row[r])));
+  }
+  return mi;
+}
+
 #endif
 
 }  // namespace gpa
@@ -157,6 +229,7 @@ struct gpa_program {
   gpa::DevProgram d{};
   gpa::RollupPlan rp{};
   gpa::EstimatePlan ep{};
+  gpa::AdvicePlan ap{};
   int state = 0;
   int variant = gpa::VAR_SMEM;
   bool part_ok = false;

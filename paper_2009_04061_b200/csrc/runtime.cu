@@ -279,7 +279,7 @@ struct Offsets {
   size_t order, chunk_begin, chunk_end, seg1_begin, seg1_end, seg2_perm, seg2_begin, seg2_end, part_v,
       part_al, rows_v, rows_al, vbuf;
   size_t pats, mval, mrow, loop_items, loop_item_ptr, pre_perm, pre_begin, pre_end, kloop_ptr, kloops,
-      loop_func, lM_excl, lM_incl, fM, kM, est;
+      loop_func, lM_excl, lM_incl, fM, kM, est, hot, n_hot, rank, cov;
   size_t C, stats, AL, cand, selfm, share, B, partials, part_x, part_sync;
   bool part_reserved = false;
   size_t total;
@@ -353,6 +353,10 @@ Offsets layout(const gpa_program_desc *d, const HostPlan &h) {
   o.fM = a.take(kPatWs * nf * 8);
   o.kM = a.take(kPatWs * nk * 8);
   o.est = a.take(kPatWs * nk * sizeof(gpa_estimate_out));
+  o.hot = a.take((size_t)kPatWs * nk * kTopKMax * sizeof(gpa_hotspot));
+  o.n_hot = a.take((size_t)kPatWs * nk * 4);
+  o.rank = a.take((size_t)kPatWs * nk * 4);
+  o.cov = a.take((size_t)nk * sizeof(gpa_coverage));
   o.total = a.off;
   return o;
 }
@@ -512,6 +516,10 @@ gpa_status gpa_program_create(const gpa_program_desc *d, void *d_workspace, size
   ep.func_al = rp.rows_al + 2 * r_func;
   ep.kern_al = rp.rows_al + 2 * r_kern;
   ep.out = (gpa_estimate_out *)(ws + o.est);
+  p->ap.hot = (gpa_hotspot *)(ws + o.hot);
+  p->ap.n_hot = (uint32_t *)(ws + o.n_hot);
+  p->ap.rank = (uint32_t *)(ws + o.rank);
+  p->ap.cov = (gpa_coverage *)(ws + o.cov);
 
   auto setv = [&](int v, size_t off, size_t by) { p->view_off[v] = off; p->view_bytes[v] = by; };
   setv(GPA_VIEW_COUNTS, o.C, (size_t)n * 2 * dp.R * 8);
@@ -579,7 +587,7 @@ gpa_status gpa_ingest_samples(gpa_program *p, const gpa_sample *d_samples, uint6
   gpa_status st = check_prog(p);
   if (st) return st;
   if (n == 0) {
-    p->state = (p->state | ST_COUNTS) & ~(ST_BLAMED | ST_AGGREGATED);
+    p->state = (p->state | ST_COUNTS) & ~(ST_BLAMED | ST_AGGREGATED | ST_ESTIMATED | ST_ADVISED);
     return GPA_OK;
   }
   if (!d_samples) return fail(GPA_ERR_INVALID_ARGUMENT, "d_samples is NULL");
@@ -587,7 +595,7 @@ gpa_status gpa_ingest_samples(gpa_program *p, const gpa_sample *d_samples, uint6
   cudaError_t e = launch_ingest(p->d, p->variant, d_samples, n, p->n_sms, p->smem_optin, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "ingest launch");
   p->launches += (p->variant == VAR_L2) ? 1 : 2;
-  p->state = (p->state | ST_COUNTS) & ~(ST_BLAMED | ST_AGGREGATED);
+  p->state = (p->state | ST_COUNTS) & ~(ST_BLAMED | ST_AGGREGATED | ST_ESTIMATED | ST_ADVISED);
   return GPA_OK;
 }
 
@@ -596,7 +604,7 @@ gpa_status gpa_ingest_segments(gpa_program *p, const gpa_sample *d_samples, uint
   gpa_status st = check_prog(p);
   if (st) return st;
   if (n_seg == 0 || n == 0) {
-    p->state = (p->state | ST_COUNTS) & ~(ST_BLAMED | ST_AGGREGATED);
+    p->state = (p->state | ST_COUNTS) & ~(ST_BLAMED | ST_AGGREGATED | ST_ESTIMATED | ST_ADVISED);
     return GPA_OK;
   }
   if (!d_samples || !d_seg_begin || !d_seg_kernel) return fail(GPA_ERR_INVALID_ARGUMENT, "NULL samples or segment table");
@@ -607,7 +615,7 @@ gpa_status gpa_ingest_segments(gpa_program *p, const gpa_sample *d_samples, uint
                                          p->n_sms, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(e, "segment ingest launch");
   p->launches += 1;
-  p->state = (p->state | ST_COUNTS) & ~(ST_BLAMED | ST_AGGREGATED);
+  p->state = (p->state | ST_COUNTS) & ~(ST_BLAMED | ST_AGGREGATED | ST_ESTIMATED | ST_ADVISED);
   return GPA_OK;
 }
 
@@ -639,7 +647,7 @@ gpa_status gpa_ingest_samples_host(gpa_program *p, const gpa_sample *h, uint64_t
     if (st) return st;
     CUDA_TRY(cudaEventRecord(p->ev_done[b], s));
   }
-  if (n == 0) p->state = (p->state | ST_COUNTS) & ~(ST_BLAMED | ST_AGGREGATED);
+  if (n == 0) p->state = (p->state | ST_COUNTS) & ~(ST_BLAMED | ST_AGGREGATED | ST_ESTIMATED | ST_ADVISED);
   CUDA_TRY(cudaStreamSynchronize(s));
   return GPA_OK;
 }
@@ -651,7 +659,7 @@ gpa_status gpa_blame(gpa_program *p, void *stream) {
   cudaError_t e = launch_blame(p->d, p->n_sms, (cudaStream_t)stream, &p->launches);
   if (e != cudaSuccess) return cuda_fail(e, "blame launch");
   p->state |= ST_BLAMED;
-  p->state &= ~ST_AGGREGATED;
+  p->state &= ~(ST_AGGREGATED | ST_ESTIMATED | ST_ADVISED);
   return GPA_OK;
 }
 
@@ -662,6 +670,7 @@ gpa_status gpa_aggregate(gpa_program *p, void *stream) {
   cudaError_t e = launch_rollup(p->d, p->rp, p->n_sms, (cudaStream_t)stream, &p->launches);
   if (e != cudaSuccess) return cuda_fail(e, "rollup launch");
   p->state |= ST_AGGREGATED;
+  p->state &= ~(ST_ESTIMATED | ST_ADVISED);
   return GPA_OK;
 }
 
@@ -689,6 +698,7 @@ gpa_status gpa_set_patterns(gpa_program *p, const gpa_pattern *pats, uint32_t n_
     p->ep.loop_slot[q] = (q < n_pat && (pats[q].model == 2 || pats[q].model == 4)) ? (int8_t)slot++ : (int8_t)-1;
   p->view_bytes[GPA_VIEW_ESTIMATES] = (size_t)p->d.n_kernels * n_pat * sizeof(gpa_estimate_out);
   p->state |= ST_PATTERNS;
+  p->state &= ~(ST_ESTIMATED | ST_ADVISED);
   return GPA_OK;
 }
 
@@ -699,6 +709,7 @@ gpa_status gpa_estimate(gpa_program *p, void *stream) {
   if (!(p->state & ST_PATTERNS)) return fail(GPA_ERR_BAD_STATE, "gpa_estimate before gpa_set_patterns");
   cudaError_t e = launch_estimate(p->d, p->ep, p->n_sms, (cudaStream_t)stream, &p->launches);
   if (e != cudaSuccess) return cuda_fail(e, "estimate launch");
+  p->state = (p->state | ST_ESTIMATED) & ~ST_ADVISED;
   return GPA_OK;
 }
 
@@ -731,6 +742,36 @@ gpa_status gpa_analyze(gpa_program *p, void *stream) {
   CUDA_TRY(cudaGraphLaunch(p->analyze_exec, (cudaStream_t)stream));
   p->launches += p->analyze_launches;
   p->state |= ST_BLAMED | ST_AGGREGATED;
+  p->state = npat ? (p->state | ST_ESTIMATED) & ~ST_ADVISED : p->state & ~(ST_ESTIMATED | ST_ADVISED);
+  return GPA_OK;
+}
+
+gpa_status gpa_advise(gpa_program *p, uint32_t top_k, void *stream) {
+  gpa_status st = check_prog(p);
+  if (st) return st;
+  if (top_k < 1 || top_k > GPA_TOP_K_MAX) return fail(GPA_ERR_INVALID_ARGUMENT, "top_k %u not in [1, %u]", top_k, GPA_TOP_K_MAX);
+  if (!(p->state & ST_ESTIMATED)) return fail(GPA_ERR_BAD_STATE, "gpa_advise before gpa_estimate / gpa_analyze with patterns");
+  p->ap.top_k = top_k;
+  cudaError_t e = launch_advice(p->d, p->ep, p->ap, (cudaStream_t)stream, &p->launches);
+  if (e != cudaSuccess) return cuda_fail(e, "advice launch");
+  p->state |= ST_ADVISED;
+  return GPA_OK;
+}
+
+gpa_status gpa_read_advice(gpa_program *p, gpa_hotspot *h_hot, uint32_t *h_n_hot, uint32_t *h_rank, gpa_coverage *h_cov,
+                           void *stream) {
+  gpa_status st = check_prog(p);
+  if (st) return st;
+  if (!(p->state & ST_ADVISED)) return fail(GPA_ERR_BAD_STATE, "gpa_read_advice before gpa_advise");
+  cudaStream_t s = (cudaStream_t)stream;
+  const uint64_t nk = p->d.n_kernels, nq = p->ep.n_pat, K = p->ap.top_k;
+  if (h_hot)   // device rows hold kTopKMax entries; the caller's hold top_k
+    CUDA_TRY(cudaMemcpy2DAsync(h_hot, K * sizeof(gpa_hotspot), p->ap.hot, kTopKMax * sizeof(gpa_hotspot),
+                               K * sizeof(gpa_hotspot), nk * nq, cudaMemcpyDeviceToHost, s));
+  if (h_n_hot) CUDA_TRY(cudaMemcpyAsync(h_n_hot, p->ap.n_hot, nk * nq * 4, cudaMemcpyDeviceToHost, s));
+  if (h_rank) CUDA_TRY(cudaMemcpyAsync(h_rank, p->ap.rank, nk * nq * 4, cudaMemcpyDeviceToHost, s));
+  if (h_cov) CUDA_TRY(cudaMemcpyAsync(h_cov, p->ap.cov, nk * sizeof(gpa_coverage), cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
   return GPA_OK;
 }
 

@@ -52,12 +52,23 @@ class EstimateOut(ctypes.Structure):
                 ("matched", ctypes.c_uint8), ("model", ctypes.c_uint8), ("pad", ctypes.c_uint8)]
 
 
+class Hotspot(ctypes.Structure):
+    _fields_ = [("def_pc", ctypes.c_uint32), ("use_pc", ctypes.c_uint32), ("distance", ctypes.c_uint32),
+                ("item", ctypes.c_uint32), ("samples", ctypes.c_double)]
+
+
+class Coverage(ctypes.Structure):
+    _fields_ = [("nodes", ctypes.c_uint64), ("single_before", ctypes.c_uint64), ("single_after", ctypes.c_uint64)]
+
+
+TOP_K_MAX = 8
+
 EXPORTS = ["gpa_validate_program", "gpa_workspace_size", "gpa_program_create", "gpa_program_destroy",
            "gpa_reset_counts", "gpa_ingest_samples", "gpa_ingest_samples_host", "gpa_blame",
            "gpa_aggregate", "gpa_set_patterns", "gpa_estimate", "gpa_read_estimates", "gpa_get_stats",
            "gpa_view", "gpa_instr_vector", "gpa_program_info", "gpa_ingest_variant",
            "gpa_set_ingest_variant", "gpa_launch_count", "gpa_last_error", "gpa_version", "gpa_analyze",
-           "gpa_ingest_segments"]
+           "gpa_ingest_segments", "gpa_advise", "gpa_read_advice"]
 
 _lib = None
 
@@ -83,6 +94,7 @@ def lib():
             "gpa_set_ingest_variant": [vp, ctypes.c_int], "gpa_launch_count": [vp, vp],
             "gpa_analyze": [vp, vp],
             "gpa_ingest_segments": [vp, vp, u64, vp, vp, u32, u32, vp],
+            "gpa_advise": [vp, u32, vp], "gpa_read_advice": [vp, vp, vp, vp, vp, vp],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -257,6 +269,24 @@ class Program:
         out = (EstimateOut * (self.n_kernels * self.n_patterns))()
         _check(lib().gpa_read_estimates(self.handle, ctypes.addressof(out), self._s(stream)), "gpa_read_estimates")
         return np.ctypeslib.as_array(out).reshape(self.n_kernels, self.n_patterns)
+
+    def advise(self, top_k=5, stream=None):
+        """Hotspots, ranking and single dependency coverage (gpa_advise) of the current estimates."""
+        self._top_k = int(top_k)
+        _check(lib().gpa_advise(self.handle, self._top_k, self._s(stream)), "gpa_advise")
+
+    def read_advice(self, stream=None):
+        """dict: 'hotspots' structured [K, Q, top_k] (first n valid), 'n' u32 [K, Q],
+        'rank' u32 [K, Q] (pattern index per rank), 'coverage' structured [K]."""
+        K, Q, T = self.n_kernels, self.n_patterns, getattr(self, "_top_k", 0)
+        hot = (Hotspot * max(1, K * Q * T))()
+        cov = (Coverage * K)()
+        n = np.zeros((K, Q), np.uint32)
+        rank = np.zeros((K, Q), np.uint32)
+        _check(lib().gpa_read_advice(self.handle, ctypes.addressof(hot), n.ctypes.data, rank.ctypes.data,
+                                     ctypes.addressof(cov), self._s(stream)), "gpa_read_advice")
+        return {"hotspots": np.ctypeslib.as_array(hot)[:K * Q * T].reshape(K, Q, T), "n": n, "rank": rank,
+                "coverage": np.ctypeslib.as_array(cov).reshape(K)}
 
     def stats(self, stream=None):
         out = (ctypes.c_uint64 * 4)()

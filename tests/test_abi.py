@@ -38,6 +38,7 @@ def test_exports_every_declared_symbol(g):
 def test_struct_sizes_match_header(g):
     assert ctypes.sizeof(g.Pattern) == 48
     assert ctypes.sizeof(g.EstimateOut) == 56
+    assert ctypes.sizeof(g.gpa.Hotspot) == 24 and ctypes.sizeof(g.gpa.Coverage) == 24
     assert ctypes.sizeof(g.gpa.ProgramDesc) == 6 * 4 + 15 * 8
 
 
