@@ -16,7 +16,10 @@ constexpr int kChunk = 128;                 // rollup chunk length (instructions
 constexpr int kMaxIngestCtas = 256;         // per-CTA partial tables reserved (smem variant)
 constexpr size_t kSmemTableMax = 224 * 1024;// largest CTA-private table (bytes; sm_100a opt-in is 227 KB)
 // partitioned ingest (variant P): bucket exchange through L2
-constexpr int kPartThreads = 1024;
+#ifndef GPA_PART_THREADS
+#define GPA_PART_THREADS 1024
+#endif
+constexpr int kPartThreads = GPA_PART_THREADS;
 #ifndef GPA_PART_CHUNK
 #define GPA_PART_CHUNK 6400
 #endif

@@ -228,7 +228,7 @@ struct PartArgs {
 constexpr int kDecodeWarps = GPA_PART_DECODE_WARPS;  // warps 0..D-1: decode + scatter records
 constexpr int kCtrlWarp = kDecodeWarps;              // warp D: TMA issue, exchange stores, recycling
 constexpr int kPubWarp = kDecodeWarps + 1;           // warp D+1: publication of stored chunks
-constexpr int kConsWarps = 32 - kDecodeWarps - 2;    // warps D+2..31: drain this CTA's bucket
+constexpr int kConsWarps = kPartThreads / 32 - kDecodeWarps - 2;   // warps D+2..: drain this CTA's bucket
 constexpr int kLoaderWarp = kPubWarp + 1;           //   warp 24: exchange -> inbox TMA loads
 constexpr int kProcBase = (kLoaderWarp + 1) * 32;   //   warps 25-31: inbox -> table
 constexpr int kProcThreads = (kConsWarps - 1) * 32;

@@ -58,6 +58,11 @@ def run_gpu(prog, records, patterns=None, variant=None, host=False, offset_recor
     P.aggregate()
     P.estimate()
     torch.cuda.synchronize()
+    return collect(P)
+
+
+def collect(P):
+    """Every device result of an analysed Program, copied to host numpy (compare() layout)."""
     out = {
         "C": P.view("counts").cpu().numpy().view(np.uint64),
         "stats": np.array(P.stats(), np.uint64),
