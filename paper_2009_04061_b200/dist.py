@@ -135,3 +135,40 @@ def gather_estimates(local_est, group=None):
     parts = [None] * dist.get_world_size(group)
     dist.all_gather_object(parts, local_est, group=group)
     return np.concatenate(parts) if isinstance(local_est, np.ndarray) else sum(parts, [])
+
+
+def kernel_row_bounds(prog, kernel_bounds):
+    """Instruction-row boundaries of contiguous kernel ranges (the count-table slices of DP-2)."""
+    import numpy as np
+    fb = np.asarray(prog.func_begin, np.int64)
+    kfb = np.asarray(prog.kernel_func_begin, np.int64)
+    return [int(fb[kfb[k]]) for k in kernel_bounds]
+
+
+def reduce_scatter_counts(counts, row_bounds, out, group=None):
+    """DP-2 for an ungrouped stream: every rank histogrammed an arbitrary shard of
+    the records into the whole program's table `counts` (int64 view [n_instr, 2R]); rank r
+    receives into `out` ([rows of its slice, 2R]) the sum over ranks of rows
+    [row_bounds[r], row_bounds[r+1]) -- its kernels' slice.  NCCL: one reduce_scatter over
+    slices padded to the largest; other backends (gloo in the CPU tests): all_reduce + slice."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    b = row_bounds
+    if len(b) != world + 1 or out.shape[0] != b[rank + 1] - b[rank]:
+        raise ValueError("row_bounds / out do not match the world")
+    if dist.get_backend(group) == "nccl":
+        rows = max(b[r + 1] - b[r] for r in range(world))
+        flat = counts.reshape(counts.shape[0], -1)
+        send = torch.zeros((world, rows, flat.shape[1]), dtype=counts.dtype, device=counts.device)
+        for r in range(world):
+            send[r, : b[r + 1] - b[r]] = flat[b[r]:b[r + 1]]
+        recv = torch.empty((rows, flat.shape[1]), dtype=counts.dtype, device=counts.device)
+        dist.reduce_scatter_tensor(recv, send, op=dist.ReduceOp.SUM, group=group)
+        out.reshape(out.shape[0], -1).copy_(recv[: b[rank + 1] - b[rank]])
+    else:
+        tmp = counts.clone()
+        dist.all_reduce(tmp, op=dist.ReduceOp.SUM, group=group)
+        out.copy_(tmp[b[rank]:b[rank + 1]])
+    return out

@@ -156,3 +156,42 @@ def test_partitioned_step_gathers_whole_program_estimates(tmp_path):
         got = np.load(tmp_path / f"sp{r}.npy")
         assert got.shape == ref.shape
         assert np.array_equal(got, ref)
+
+
+def _rs_worker(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    from paper_2009_04061_b200.dist import kernel_row_bounds, reduce_scatter_counts, shard_range
+    prog = batch.batch_program(90, seed=81)
+    spec = StreamSpec(prog, seed=82, count_max=3, invalid_ppm=2_000)
+    n = 300_001
+    k0, k1 = shard_range(n, rank, world)             # ungrouped shard of the stream
+    C, _ = oracle.OracleProgram(prog).histogram(spec.host(k0, k1 - k0))
+    counts = torch.from_numpy(C.view(np.int64).reshape(prog.n_instr, -1).copy())
+    kb = batch.kernel_pc_begin(prog)
+    pcs = batch.record_pcs(spec.host(0, n))
+    ksamp = np.bincount(np.searchsorted(kb[1:-1], pcs[pcs < kb[-1]], side="right"), minlength=prog.n_kernels)
+    rb = kernel_row_bounds(prog, partition_kernels(ksamp, world))
+    out = torch.zeros((rb[rank + 1] - rb[rank], counts.shape[1]), dtype=torch.int64)
+    reduce_scatter_counts(counts, rb, out)
+    np.save(os.path.join(out_dir, f"rs{rank}.npy"), out.numpy())
+    np.save(os.path.join(out_dir, f"rb{rank}.npy"), np.array(rb))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_reduce_scatter_of_ungrouped_shards_gives_kernel_slices(tmp_path):
+    """DP-2 without grouping: ranks histogram arbitrary shards of the whole program, then each
+    receives the summed rows of its kernel slice -- equal to the single-process table's rows."""
+    import oracle
+    world = 2
+    mp.spawn(_rs_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    prog = batch.batch_program(90, seed=81)
+    C, _ = oracle.OracleProgram(prog).histogram(StreamSpec(prog, seed=82, count_max=3, invalid_ppm=2_000).host(0, 300_001))
+    full = C.view(np.int64).reshape(prog.n_instr, -1)
+    for r in range(world):
+        rb = np.load(tmp_path / f"rb{r}.npy")
+        got = np.load(tmp_path / f"rs{r}.npy")
+        assert np.array_equal(got, full[rb[r]:rb[r + 1]])

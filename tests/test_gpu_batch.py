@@ -77,3 +77,48 @@ def test_config4_full_batch_reduced_stream():
     g, sb, sk = _grouped(prog, recs, seed=3)
     o = run_oracle(prog, recs)
     compare(run_gpu(prog, g, segments=(sb, sk, 0)), o, rel=REL)
+
+
+def test_dp2_reduce_scatter_path_single_rank_nccl():
+    """DP-2 for an ungrouped stream through NCCL (world size 1 on this box): the whole program
+    histograms the records, reduce_scatter_counts hands the kernel slice to the sub-program's
+    count table, and the sub-program's analysis equals the oracle on the slice's records."""
+    import os
+    import socket
+    import torch
+    import torch.distributed as dist
+    from paper_2009_04061_b200 import Program
+    from paper_2009_04061_b200.dist import kernel_row_bounds, reduce_scatter_counts
+    from gpagen.patterns import table2
+    from tests._common import collect
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        prog = batch.batch_program(120, seed=91)
+        recs = StreamSpec(prog, seed=92, count_max=2, invalid_ppm=0).host(0, 800_000)
+        full = Program(prog)
+        full.reset()
+        full.ingest(torch.from_numpy(recs.view(np.int64)).cuda())
+        k0, k1 = 30, 77
+        sub, maps = slice_program(prog, k0, k1)
+        rb = kernel_row_bounds(prog, [k0, k1])
+        S = Program(sub)
+        S.set_patterns(table2(prog.n_reasons))
+        S.reset()
+        counts = full.view("counts").reshape(prog.n_instr, -1)
+        out = S.view("counts").reshape(sub.n_instr, -1)
+        reduce_scatter_counts(counts[rb[0]:], [0, rb[1] - rb[0]], out)
+        S.analyze()
+        torch.cuda.synchronize()
+        g = collect(S)
+        pcs = batch.record_pcs(recs)
+        mine = recs[(pcs >= maps["pc_base"]) & (pcs < maps["pc_base"] + maps["n_instr"])]
+        o = run_oracle(sub, batch.rebase_records(mine, maps["pc_base"]))
+        g["stats"] = o["stats"]          # stats stay with the whole-program histogram
+        compare(g, o, rel=REL)
+    finally:
+        dist.destroy_process_group()
