@@ -39,7 +39,9 @@ __global__ void k_est_rows(DevProgram p, EstimatePlan ep) {
   const uint32_t n_groups = (ep.n_pat + kEstGroup - 1) / kEstGroup;
   const uint64_t total = (uint64_t)p.n * n_groups;
   for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total; t += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t grp = (uint32_t)(t / p.n), j = (uint32_t)(t % p.n);
+    // row-major: the pattern groups of a row run on neighbouring threads, so its C row and edges
+    // are fetched from DRAM once and served from L1 to the other groups
+    const uint32_t j = (uint32_t)(t / n_groups), grp = (uint32_t)(t % n_groups);
     const uint32_t q0 = grp * kEstGroup;
     const uint32_t nq = min((uint32_t)kEstGroup, ep.n_pat - q0);
     const uint64_t *row = p.C + (uint64_t)j * 2 * p.R;

@@ -22,37 +22,49 @@ namespace gpa {
 namespace {
 
 // one thread per instruction: the B row (64 B), the C row (16R B), class and self flags are
-// loaded with independent (vector) loads, and the row of V is written as one (all, lat) pair per
-// column (16-byte stores) -- many rows in flight per SM.  Same values as vvalue().
-__global__ void k_vrows(DevProgram p, double *__restrict__ vbuf) {
-  const uint32_t ncol = p.ncol, R = p.R;
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += gridDim.x * blockDim.x) {
-    const double2 *b2 = reinterpret_cast<const double2 *>(p.B + 8 * (uint64_t)i);
-    const double2 bm = b2[BG_MEM], be = b2[BG_EXEC], bw = b2[BG_WAR], bs = b2[BG_SYNC];
-    const uint32_t cls = p.opclass[i], sf = p.selfm[i];
-    const uint64_t *row = p.C + (uint64_t)i * 2 * R;
-    // all loads before the first store (V may alias nothing, but the compiler cannot know)
-    uint64_t act[kReasonsMax], lat[kReasonsMax];
+// loaded with independent loads before any store; the warp's 32 rows of V are staged in shared
+// memory and written back as one contiguous, coalesced block (rows are consecutive in V).
+// Same values as vvalue().
+constexpr uint32_t kVrowsThreads = 128;
+__global__ void __launch_bounds__(kVrowsThreads) k_vrows(DevProgram p, double *__restrict__ vbuf) {
+  extern __shared__ double2 vstage[];          // [kVrowsThreads / 32][32 rows][ncol]
+  const uint32_t ncol = p.ncol, R = p.R, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double2 *ws = vstage + (size_t)warp * 32 * ncol;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t base = (blockIdx.x * blockDim.x + threadIdx.x) & ~31u; base < p.n; base += stride) {
+    const uint32_t i = base + lane;
+    if (i < p.n) {
+      const double2 *b2 = reinterpret_cast<const double2 *>(p.B + 8 * (uint64_t)i);
+      const double2 bm = b2[BG_MEM], be = b2[BG_EXEC], bw = b2[BG_WAR], bs = b2[BG_SYNC];
+      const uint32_t cls = p.opclass[i], sf = p.selfm[i];
+      const uint64_t *row = p.C + (uint64_t)i * 2 * R;
+      uint64_t act[kReasonsMax], lat[kReasonsMax];
 #pragma unroll
-    for (uint32_t r = 1; r < kReasonsMax; ++r) {
-      act[r] = r < R ? row[r] : 0ull;
-      lat[r] = r < R ? row[R + r] : 0ull;
-    }
-    double2 *out = reinterpret_cast<double2 *>(vbuf + (uint64_t)i * 2 * ncol);
-    const double2 z = make_double2(0.0, 0.0);
-    out[COL_MEM_GLOBAL] = (cls != OC_LOCAL && cls != OC_CONSTANT) ? bm : z;
-    out[COL_MEM_LOCAL] = cls == OC_LOCAL ? bm : z;
-    out[COL_MEM_CONSTANT] = cls == OC_CONSTANT ? bm : z;
-    out[COL_EXEC_SHARED] = cls == OC_SHARED ? be : z;
-    out[COL_EXEC_ARITH] = cls != OC_SHARED ? be : z;
-    out[COL_EXEC_WAR] = bw;
-    out[COL_SYNC] = bs;
+      for (uint32_t r = 1; r < kReasonsMax; ++r) {
+        act[r] = r < R ? row[r] : 0ull;
+        lat[r] = r < R ? row[R + r] : 0ull;
+      }
+      double2 *out = ws + (size_t)lane * ncol;
+      const double2 z = make_double2(0.0, 0.0);
+      out[COL_MEM_GLOBAL] = (cls != OC_LOCAL && cls != OC_CONSTANT) ? bm : z;
+      out[COL_MEM_LOCAL] = cls == OC_LOCAL ? bm : z;
+      out[COL_MEM_CONSTANT] = cls == OC_CONSTANT ? bm : z;
+      out[COL_EXEC_SHARED] = cls == OC_SHARED ? be : z;
+      out[COL_EXEC_ARITH] = cls != OC_SHARED ? be : z;
+      out[COL_EXEC_WAR] = bw;
+      out[COL_SYNC] = bs;
 #pragma unroll
-    for (uint32_t r = 1; r < kReasonsMax; ++r) {
-      if (r >= R) break;
-      const bool on = r > R_SYNC || ((sf >> (r - 1)) & 1u);
-      out[6 + r] = on ? make_double2((double)(act[r] + lat[r]), (double)lat[r]) : z;
+      for (uint32_t r = 1; r < kReasonsMax; ++r) {
+        if (r >= R) break;
+        const bool on = r > R_SYNC || ((sf >> (r - 1)) & 1u);
+        out[6 + r] = on ? make_double2((double)(act[r] + lat[r]), (double)lat[r]) : z;
+      }
     }
+    __syncwarp();
+    const uint32_t rows = min(32u, p.n - base);
+    double2 *dst = reinterpret_cast<double2 *>(vbuf + (uint64_t)base * 2 * ncol);
+    for (uint32_t x = lane; x < rows * ncol; x += 32) dst[x] = ws[x];
+    __syncwarp();
   }
 }
 
@@ -158,8 +170,12 @@ inline uint32_t warp_grid(uint64_t warps, int n_sms) {
 
 cudaError_t launch_vrows(const DevProgram &p, double *vbuf, int n_sms, cudaStream_t s) {
   const uint64_t total = (uint64_t)p.n;
-  const uint32_t g = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, (uint64_t)n_sms * 8));
-  k_vrows<<<g, 256, 0, s>>>(p, vbuf);
+  const uint32_t g = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((total + kVrowsThreads - 1) / kVrowsThreads,
+                                                                         (uint64_t)n_sms * 16));
+  const size_t smem = (size_t)kVrowsThreads * p.ncol * sizeof(double2);   // 32 rows per warp
+  cudaError_t e = cudaFuncSetAttribute(k_vrows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_vrows<<<g, kVrowsThreads, smem, s>>>(p, vbuf);
   return cudaGetLastError();
 }
 
