@@ -577,10 +577,16 @@ __global__ void k_ingest_edges(const uint2 *rec, uint64_t n_rec, uint32_t head, 
 // bin.  Records whose pc lies outside the segment's kernel, segments of unknown kernels
 // (seg_kernel >= n_kernels) and kernels too large for the table take L2 atomics: exact for any
 // input.  A piece holds at most kSegTile records of count <= 65535, so u32 bins cannot wrap.
-constexpr uint32_t kSegTile = 16384;
-constexpr uint32_t kSegThreads = 1024;
+#ifndef GPA_SEG_TILE
+#define GPA_SEG_TILE 32768
+#endif
+constexpr uint32_t kSegTile = GPA_SEG_TILE;
+#ifndef GPA_SEG_THREADS
+#define GPA_SEG_THREADS 512
+#endif
+constexpr uint32_t kSegThreads = GPA_SEG_THREADS;
 
-__global__ void __launch_bounds__(kSegThreads, 1)
+__global__ void __launch_bounds__(kSegThreads)
 k_ingest_seg(const uint2 *__restrict__ rec, uint64_t n_rec, const uint64_t *__restrict__ seg_begin,
              const uint32_t *__restrict__ seg_kernel, uint32_t n_seg, uint32_t pc_base,
              const uint32_t *__restrict__ func_begin, const uint32_t *__restrict__ kernel_func_begin,
@@ -632,7 +638,18 @@ k_ingest_seg(const uint2 *__restrict__ rec, uint64_t n_rec, const uint64_t *__re
       const uint64_t hb = ((uintptr_t)(rec + b) & 15u) ? 1 : 0;
       const uint64_t body = (e - b - hb) >> 1;
       const uint4 *r16 = reinterpret_cast<const uint4 *>(rec + b + hb);
-      for (uint64_t i = threadIdx.x; i < body; i += blockDim.x) {
+      uint64_t i = threadIdx.x;
+      for (; i + 3 * blockDim.x < body; i += 4 * blockDim.x) {   // four 16-byte loads in flight
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = ld_stream(r16 + i + u * blockDim.x);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          add(v[u].x, v[u].y);
+          add(v[u].z, v[u].w);
+        }
+      }
+      for (; i < body; i += blockDim.x) {
         const uint4 v = ld_stream(r16 + i);
         add(v.x, v.y);
         add(v.z, v.w);
@@ -773,7 +790,9 @@ cudaError_t launch_ingest_segments(const DevProgram &p, const void *records, uin
   const size_t smem = (size_t)max_tab_bins * 4;
   cudaError_t e = cudaFuncSetAttribute(k_ingest_seg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const uint32_t grid = (uint32_t)std::max(1, n_sms);
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ingest_seg, kSegThreads, smem);
+  const uint32_t grid = (uint32_t)std::max(1, n_sms * std::max(1, per_sm));
   k_ingest_seg<<<grid, kSegThreads, smem, s>>>((const uint2 *)records, n, seg_begin, seg_kernel, n_seg, pc_base,
                                                p.func_begin, p.kernel_func_begin, p.n_kernels, p.n, p.R,
                                                max_tab_bins, p.C, p.stats);

@@ -551,7 +551,10 @@ gpa_status gpa_program_create(const gpa_program_desc *d, void *d_workspace, size
     uint32_t max_np = 0;
     for (uint32_t k = 0; k < d->n_kernels; ++k)
       max_np = std::max(max_np, d->func_begin[d->kernel_func_begin[k + 1]] - d->func_begin[d->kernel_func_begin[k]]);
-    const uint64_t cap = std::min<uint64_t>(p->smem_optin, kSmemTableMax) / 4;
+#ifndef GPA_SEG_SMEM_MAX
+#define GPA_SEG_SMEM_MAX (72 * 1024)   // 3 CTAs of 512 threads per SM; kernels > 1024 instrs (R = 9) take L2 atomics
+#endif
+    const uint64_t cap = std::min<uint64_t>(std::min<uint64_t>(p->smem_optin, kSmemTableMax), GPA_SEG_SMEM_MAX) / 4;
     const uint64_t want = (uint64_t)max_np * 2 * d->n_reasons;
     p->seg_tab_bins = (uint32_t)std::min(want, cap);
   }
