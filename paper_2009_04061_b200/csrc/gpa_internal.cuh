@@ -79,9 +79,13 @@ struct RollupPlan {
   uint32_t n_chunks;
   double *part_v;               // [n_chunks][2*ncol]
   uint64_t *part_al;            // [n_chunks][2]
-  // stage 1: segments (lines, loops excl, funcs) over chunk ranges -> rows [0, n_seg1)
-  const uint32_t *seg1_begin, *seg1_end;
-  uint32_t n_seg1;
+  // stage 1: rows [0, n_rows1) = lines, loops excl, funcs.  Segments of <= kChunk positions are
+  // packed (pack p = segments [pack_seg[p], pack_seg[p+1]), positions segpos[s]..segpos[s+1]) and
+  // summed directly into their rows; longer ones (n_seg1, row seg1_id[i]) over chunk ranges
+  const uint32_t *seg1_begin, *seg1_end, *seg1_id;
+  uint32_t n_seg1, n_rows1;
+  const uint32_t *pack_seg, *segpos;
+  uint32_t n_packs;
   // stage 2: segments (loops incl, kernels) over rows via perm -> rows [n_seg1, n_seg1 + n_seg2)
   const uint32_t *seg2_perm, *seg2_begin, *seg2_end;
   uint32_t n_seg2;

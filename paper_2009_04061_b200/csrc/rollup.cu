@@ -148,16 +148,78 @@ __global__ void __launch_bounds__(128) k_rollup_segments(uint32_t nv, const doub
                                                          const uint32_t *__restrict__ perm,
                                                          const uint32_t *__restrict__ seg_begin,
                                                          const uint32_t *__restrict__ seg_end, uint32_t n_seg,
+                                                         const uint32_t *__restrict__ out_row,
                                                          double *__restrict__ out_v, uint64_t *__restrict__ out_al) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t sg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; sg < n_seg; sg += warps) {
+    const uint64_t row = out_row ? out_row[sg] : sg;
     if (perm)
       warp_sum_rows(lane, nv, seg_begin[sg], seg_end[sg], [perm](uint32_t pos) { return perm[pos]; }, in_v, in_al,
-                    out_v + (uint64_t)sg * nv, out_al + 2 * (uint64_t)sg);
+                    out_v + row * nv, out_al + 2 * row);
     else
       warp_sum_rows(lane, nv, seg_begin[sg], seg_end[sg], [](uint32_t pos) { return pos; }, in_v, in_al,
-                    out_v + (uint64_t)sg * nv, out_al + 2 * (uint64_t)sg);
+                    out_v + row * nv, out_al + 2 * row);
+  }
+}
+
+// packs of short segments (<= kChunk positions in all): one warp per pack, lane = value slot;
+// member rows are fetched kRollMembers at a time across segment boundaries and added in member
+// order into the current segment's sum, which is written to its row when the segment ends --
+// the same left-to-right order as the oracle's per-instruction accumulation
+__global__ void __launch_bounds__(128) k_rollup_packs(RollupPlan rp, uint32_t nv, const double *__restrict__ vbuf,
+                                                      const uint64_t *__restrict__ AL) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t pk = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; pk < rp.n_packs; pk += warps) {
+    const uint32_t sa = rp.pack_seg[pk], sb = rp.pack_seg[pk + 1];
+    const uint32_t P0 = rp.segpos[sa], P1 = rp.segpos[sb], len = P1 - P0;
+    if (len > (uint32_t)kChunk) continue;          // a long segment: chunked + k_rollup_segments
+    uint32_t ids[kChunk / 32];
+#pragma unroll
+    for (int t = 0; t < kChunk / 32; ++t) ids[t] = (lane + 32 * t < len) ? rp.order[P0 + lane + 32 * t] : 0u;
+    for (uint32_t s0 = 0; s0 < nv + 2; s0 += 32) {   // uniform trip count: shuffles need all lanes
+      const uint32_t s = s0 + lane;
+      const bool is_v = s < nv, is_al = s >= nv && s < nv + 2;
+      uint32_t seg = sa, seg_end = rp.segpos[sa + 1];
+      double acc = 0.0;
+      uint64_t al = 0;
+      auto flush_to = [&](uint32_t pos) {          // close every segment that ends at or before pos
+        while (seg < sb && seg_end <= pos) {
+          if (is_v) rp.rows_v[(uint64_t)seg * nv + s] = acc;
+          else if (is_al) rp.rows_al[2 * (uint64_t)seg + (s - nv)] = al;
+          acc = 0.0;
+          al = 0;
+          ++seg;
+          if (seg < sb) seg_end = rp.segpos[seg + 1];
+        }
+      };
+#pragma unroll
+      for (int t = 0; t < kChunk / 32; ++t) {
+        const uint32_t m_end = len > 32u * t ? min(32u, len - 32u * t) : 0u;
+        for (uint32_t m = 0; m < m_end; m += kRollMembers) {
+          uint32_t id[kRollMembers];
+#pragma unroll
+          for (int u = 0; u < kRollMembers; ++u) id[u] = __shfl_sync(0xffffffffu, ids[t], (m + u) & 31);
+          double x[kRollMembers];
+          uint64_t y[kRollMembers];
+#pragma unroll
+          for (int u = 0; u < kRollMembers; ++u) {
+            const bool in = m + u < m_end;
+            x[u] = (in && is_v) ? vbuf[(uint64_t)id[u] * nv + s] : 0.0;
+            y[u] = (in && is_al) ? AL[2 * (uint64_t)id[u] + (s - nv)] : 0ull;
+          }
+#pragma unroll
+          for (int u = 0; u < kRollMembers; ++u) {
+            if (m + u >= m_end) break;
+            flush_to(P0 + 32 * t + m + u);
+            acc = __dadd_rn(acc, x[u]);
+            al += y[u];
+          }
+        }
+      }
+      flush_to(P1);
+    }
   }
 }
 
@@ -185,12 +247,14 @@ cudaError_t launch_rollup(const DevProgram &p, const RollupPlan &rp, int n_sms, 
   cudaError_t e = launch_vrows(p, rp.vbuf, n_sms, s);
   if (e != cudaSuccess) return e;
   if (rp.n_chunks) k_rollup_chunks<<<warp_grid(rp.n_chunks, n_sms), 128, 0, s>>>(rp, nv, rp.vbuf, p.AL);
-  k_rollup_segments<<<warp_grid(rp.n_seg1, n_sms), 128, 0, s>>>(
-      nv, rp.part_v, rp.part_al, nullptr, rp.seg1_begin, rp.seg1_end, rp.n_seg1, rp.rows_v, rp.rows_al);
+  if (rp.n_packs) k_rollup_packs<<<warp_grid(rp.n_packs, n_sms), 128, 0, s>>>(rp, nv, rp.vbuf, p.AL);
+  if (rp.n_seg1)
+    k_rollup_segments<<<warp_grid(rp.n_seg1, n_sms), 128, 0, s>>>(
+        nv, rp.part_v, rp.part_al, nullptr, rp.seg1_begin, rp.seg1_end, rp.n_seg1, rp.seg1_id, rp.rows_v, rp.rows_al);
   k_rollup_segments<<<warp_grid(rp.n_seg2, n_sms), 128, 0, s>>>(
-      nv, rp.rows_v, rp.rows_al, rp.seg2_perm, rp.seg2_begin, rp.seg2_end, rp.n_seg2,
-      rp.rows_v + (uint64_t)rp.n_seg1 * nv, rp.rows_al + 2 * (uint64_t)rp.n_seg1);
-  *launches += rp.n_chunks ? 4 : 3;
+      nv, rp.rows_v, rp.rows_al, rp.seg2_perm, rp.seg2_begin, rp.seg2_end, rp.n_seg2, nullptr,
+      rp.rows_v + (uint64_t)rp.n_rows1 * nv, rp.rows_al + 2 * (uint64_t)rp.n_rows1);
+  *launches += 2 + (rp.n_chunks ? 1 : 0) + (rp.n_packs ? 1 : 0) + (rp.n_seg1 ? 1 : 0);
   return cudaGetLastError();
 }
 

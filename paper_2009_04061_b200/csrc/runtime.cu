@@ -128,8 +128,9 @@ struct HostPlan {
   // create-time arrays (host)
   std::vector<uint32_t> edge_use, def_ptr, def_perm;
   std::vector<int32_t> edge_lca, loop_func;
-  std::vector<uint32_t> order, chunk_begin, chunk_end, seg1_begin, seg1_end, seg2_perm, seg2_begin,
+  std::vector<uint32_t> order, chunk_begin, chunk_end, seg1_begin, seg1_end, seg1_id, seg2_perm, seg2_begin,
       seg2_end;
+  std::vector<uint32_t> pack_seg, segpos;   // small segments packed per warp: pack -> first segment; positions
   std::vector<uint32_t> loop_items, loop_item_ptr, pre_perm, pre_begin, pre_end, kloop_ptr, kloops;
   uint32_t n_rows = 0;
 };
@@ -191,19 +192,40 @@ gpa_status build_plan(const gpa_program_desc *d, HostPlan &h) {
       h.order[n + n_in_loops + i] = i;
     }
   }
-  auto add_segment = [&](uint32_t pos0, uint32_t pos1) {
-    h.seg1_begin.push_back((uint32_t)h.chunk_begin.size());
-    for (uint32_t p = pos0; p < pos1; p += kChunk) {
-      h.chunk_begin.push_back(p);
-      h.chunk_end.push_back(std::min(pos1, p + (uint32_t)kChunk));
-    }
-    h.seg1_end.push_back((uint32_t)h.chunk_begin.size());
-  };
-  for (uint32_t l = 0; l < d->n_lines; ++l) add_segment(line_ptr[l], line_ptr[l + 1]);
-  for (uint32_t l = 0; l < L; ++l) add_segment(n + loop_ptr[l], n + loop_ptr[l + 1]);
-  for (uint32_t f = 0; f < d->n_funcs; ++f)
-    add_segment(n + n_in_loops + d->func_begin[f], n + n_in_loops + d->func_begin[f + 1]);
+  // stage-1 segments in row order (lines, loops exclusive, functions) as position ranges of the
+  // order; segments of <= kChunk positions are packed, consecutive, into warps of <= kChunk
+  // positions (k_rollup_packs writes their rows directly); longer ones are cut into chunks whose
+  // partial sums k_rollup_segments adds (rows seg1_id)
+  std::vector<uint32_t> spos;
+  for (uint32_t l = 0; l <= d->n_lines; ++l) spos.push_back(line_ptr[l]);
+  for (uint32_t l = 1; l <= L; ++l) spos.push_back(n + loop_ptr[l]);
+  for (uint32_t f = 1; f <= d->n_funcs; ++f) spos.push_back(n + n_in_loops + d->func_begin[f]);
   const uint32_t n_seg1 = d->n_lines + L + d->n_funcs;
+  h.segpos = spos;   // segment s = positions [segpos[s], segpos[s+1])
+  {
+    uint32_t pack_pos = 0, pack_open = 0;
+    for (uint32_t sg = 0; sg < n_seg1; ++sg) {
+      const uint32_t pos0 = spos[sg], pos1 = spos[sg + 1], len = pos1 - pos0;
+      if (len <= (uint32_t)kChunk) {
+        if (!pack_open || pos1 - pack_pos > (uint32_t)kChunk || h.pack_seg.back() + 64 <= sg) {
+          h.pack_seg.push_back(sg);
+          pack_pos = pos0;
+          pack_open = 1;
+        }
+        continue;
+      }
+      pack_open = 0;
+      h.pack_seg.push_back(sg);          // a long segment closes the pack (its own "pack" is empty)
+      h.seg1_id.push_back(sg);
+      h.seg1_begin.push_back((uint32_t)h.chunk_begin.size());
+      for (uint32_t p = pos0; p < pos1; p += kChunk) {
+        h.chunk_begin.push_back(p);
+        h.chunk_end.push_back(std::min(pos1, p + (uint32_t)kChunk));
+      }
+      h.seg1_end.push_back((uint32_t)h.chunk_begin.size());
+    }
+    h.pack_seg.push_back(n_seg1);
+  }
   // ---- loop preorder (children visited in increasing id), subtree ranges
   std::vector<std::vector<uint32_t>> kids(L);
   std::vector<uint32_t> roots;
@@ -276,7 +298,7 @@ gpa_status build_plan(const gpa_program_desc *d, HostPlan &h) {
 struct Offsets {
   size_t opclass, iflags, latency, line_id, loop_id, func_begin, kfb, kgb, row_ptr, edge_def, edge_min,
       edge_max, edge_use, edge_dom, edge_lca, edge_kind, def_ptr, def_perm;
-  size_t order, chunk_begin, chunk_end, seg1_begin, seg1_end, seg2_perm, seg2_begin, seg2_end, part_v,
+  size_t order, chunk_begin, chunk_end, seg1_begin, seg1_end, seg1_id, pack_seg, segpos, seg2_perm, seg2_begin, seg2_end, part_v,
       part_al, rows_v, rows_al, vbuf;
   size_t pats, mval, mrow, loop_items, loop_item_ptr, pre_perm, pre_begin, pre_end, kloop_ptr, kloops,
       loop_func, lM_excl, lM_incl, fM, kM, est, hot, n_hot, rank, cov;
@@ -329,6 +351,9 @@ Offsets layout(const gpa_program_desc *d, const HostPlan &h) {
   o.chunk_end = a.take(h.chunk_end.size() * 4);
   o.seg1_begin = a.take(h.seg1_begin.size() * 4);
   o.seg1_end = a.take(h.seg1_end.size() * 4);
+  o.seg1_id = a.take(h.seg1_id.size() * 4);
+  o.pack_seg = a.take(h.pack_seg.size() * 4);
+  o.segpos = a.take(h.segpos.size() * 4);
   o.seg2_perm = a.take(h.seg2_perm.size() * 4);
   o.seg2_begin = a.take(h.seg2_begin.size() * 4);
   o.seg2_end = a.take(h.seg2_end.size() * 4);
@@ -435,6 +460,9 @@ gpa_status gpa_program_create(const gpa_program_desc *d, void *d_workspace, size
   UP(o.chunk_end, h.chunk_end.data(), h.chunk_end.size());
   UP(o.seg1_begin, h.seg1_begin.data(), h.seg1_begin.size());
   UP(o.seg1_end, h.seg1_end.data(), h.seg1_end.size());
+  UP(o.seg1_id, h.seg1_id.data(), h.seg1_id.size());
+  UP(o.pack_seg, h.pack_seg.data(), h.pack_seg.size());
+  UP(o.segpos, h.segpos.data(), h.segpos.size());
   UP(o.seg2_perm, h.seg2_perm.data(), h.seg2_perm.size());
   UP(o.seg2_begin, h.seg2_begin.data(), h.seg2_begin.size());
   UP(o.seg2_end, h.seg2_end.data(), h.seg2_end.size());
@@ -484,7 +512,12 @@ gpa_status gpa_program_create(const gpa_program_desc *d, void *d_workspace, size
   rp.part_al = (uint64_t *)(ws + o.part_al);
   rp.seg1_begin = (const uint32_t *)(ws + o.seg1_begin);
   rp.seg1_end = (const uint32_t *)(ws + o.seg1_end);
-  rp.n_seg1 = (uint32_t)h.seg1_begin.size();
+  rp.n_seg1 = (uint32_t)h.seg1_begin.size();   // long segments (chunked)
+  rp.seg1_id = (const uint32_t *)(ws + o.seg1_id);
+  rp.n_rows1 = d->n_lines + d->n_loops + d->n_funcs;
+  rp.pack_seg = (const uint32_t *)(ws + o.pack_seg);
+  rp.n_packs = (uint32_t)h.pack_seg.size() - 1;
+  rp.segpos = (const uint32_t *)(ws + o.segpos);
   rp.seg2_perm = (const uint32_t *)(ws + o.seg2_perm);
   rp.seg2_begin = (const uint32_t *)(ws + o.seg2_begin);
   rp.seg2_end = (const uint32_t *)(ws + o.seg2_end);
