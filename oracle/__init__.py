@@ -54,6 +54,21 @@ class Estimate(ctypes.Structure):
                 ("matched", ctypes.c_uint8), ("model", ctypes.c_uint8), ("pad", ctypes.c_uint8)]
 
 
+class Arch(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_uint32) for k in ("sm_count", "max_warps_per_sm", "max_blocks_per_sm", "regs_per_sm",
+                                               "smem_per_sm", "schedulers_per_sm", "warp_size", "reg_alloc_unit")]
+
+
+class Launch(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_uint32) for k in ("threads_per_block", "regs_per_thread", "smem_per_block", "pad")]
+
+
+class Occ(ctypes.Structure):
+    _fields_ = [("W", ctypes.c_double), ("W_new_block", ctypes.c_double), ("W_new_thread", ctypes.c_double),
+                ("blocks_per_sm", ctypes.c_uint32), ("limiter", ctypes.c_uint32),
+                ("match_block", ctypes.c_uint32), ("match_thread", ctypes.c_uint32)]
+
+
 class Hotspot(ctypes.Structure):
     _fields_ = [("def_pc", ctypes.c_uint32), ("use_pc", ctypes.c_uint32), ("distance", ctypes.c_uint32),
                 ("item", ctypes.c_uint32), ("samples", ctypes.c_double)]
@@ -71,6 +86,8 @@ def lib():
         L.or_blame.argtypes = [vp, vp, vp, vp, vp, vp]
         L.or_rollup.argtypes = [vp] * 13
         L.or_estimate_all.argtypes = [vp, vp, vp, vp, vp, vp, ctypes.c_uint32, vp]
+        L.or_estimate_all_occ.argtypes = [vp, vp, vp, vp, vp, vp, ctypes.c_uint32, vp, vp]
+        L.or_occupancy.argtypes = [vp, vp, vp, ctypes.c_uint32, vp]
         L.or_hotspots.argtypes = [vp, vp, vp, vp, vp, vp, ctypes.c_uint32, ctypes.c_uint32, vp, vp]
         L.or_rank.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint32, vp]
         L.or_coverage.argtypes = [vp, vp, vp, vp]
@@ -159,12 +176,14 @@ class OracleProgram:
         return out
 
     # --- step 8
-    def estimate(self, C, blame, patterns):
+    def estimate(self, C, blame, patterns, occ=None):
+        """occ: ctypes array of Occ per kernel (occupancy(...)) for parallel_rule 3 / 4, or None."""
         pats = (Pattern * len(patterns))(*patterns)
         out = (Estimate * (self.n_kernels * len(patterns)))()
-        lib().or_estimate_all(self.ref, C.ctypes.data, blame["cand"].ctypes.data,
-                              blame["self"].ctypes.data, blame["share"].ctypes.data,
-                              ctypes.addressof(pats), len(patterns), ctypes.addressof(out))
+        lib().or_estimate_all_occ(self.ref, C.ctypes.data, blame["cand"].ctypes.data,
+                                  blame["self"].ctypes.data, blame["share"].ctypes.data,
+                                  ctypes.addressof(pats), len(patterns),
+                                  None if occ is None else ctypes.addressof(occ), ctypes.addressof(out))
         return [[out[k * len(patterns) + q] for q in range(len(patterns))]
                 for k in range(self.n_kernels)]
 
@@ -218,3 +237,13 @@ def rank(est):
     order = np.zeros((K, Q), np.uint32)
     lib().or_rank(ctypes.addressof(flat), K, Q, order.ctypes.data)
     return order
+
+
+def occupancy(arch, launches, grid_blocks):
+    """arch: Arch; launches: list of Launch (one per kernel); grid_blocks: sequence -> ctypes Occ array."""
+    K = len(launches)
+    L = (Launch * K)(*launches)
+    g = np.ascontiguousarray(grid_blocks, dtype=np.uint32)
+    out = (Occ * K)()
+    lib().or_occupancy(ctypes.byref(arch), ctypes.addressof(L), g.ctypes.data, K, ctypes.addressof(out))
+    return out

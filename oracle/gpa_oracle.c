@@ -352,6 +352,12 @@ static double match_instr(const or_program *p, const uint64_t *C, const uint8_t 
 int or_estimate_all(const or_program *p, const uint64_t *C, const uint8_t *cand,
                     const uint8_t *self_flags, const double *share, const or_pattern *pats,
                     uint32_t n_pat, or_estimate *out) {
+  return or_estimate_all_occ(p, C, cand, self_flags, share, pats, n_pat, NULL, out);
+}
+
+int or_estimate_all_occ(const or_program *p, const uint64_t *C, const uint8_t *cand,
+                        const uint8_t *self_flags, const double *share, const or_pattern *pats,
+                        uint32_t n_pat, const or_occ *occ, or_estimate *out) {
   const uint32_t n = p->n_instr, R = p->n_reasons;
   uint32_t k, qi, i, r, e, l, f;
   double *loopM = (double *)calloc(p->n_loops ? p->n_loops : 1u, sizeof(double));
@@ -399,8 +405,16 @@ int or_estimate_all(const or_program *p, const uint64_t *C, const uint8_t *cand,
         int matched = q->parallel_rule == 1 ||
                       (q->parallel_rule == 2 && p->kernel_grid_blocks &&
                        p->kernel_grid_blocks[k] < q->sm_count);
+        double W = q->W, W_new = q->W_new;
+        if (q->parallel_rule == 3 || q->parallel_rule == 4) {   /* occupancy model (Q34) */
+          matched = occ && (q->parallel_rule == 3 ? occ[k].match_block : occ[k].match_thread);
+          if (matched) {
+            W = occ[k].W;
+            W_new = q->parallel_rule == 3 ? occ[k].W_new_block : occ[k].W_new_thread;
+          }
+        }
         o->matched = (uint8_t)matched;
-        o->speedup = matched ? or_eq10(q->W, q->W_new, R_I, q->f) : 1.0;
+        o->speedup = matched ? or_eq10(W, W_new, R_I, q->f) : 1.0;
         o->eq3 = o->eq4 = 1.0;
         continue;
       }
@@ -569,6 +583,53 @@ int or_coverage(const or_program *p, const uint64_t *C, const uint8_t *cand, uin
     out[3 * (uint64_t)k] = nodes;
     out[3 * (uint64_t)k + 1] = before;
     out[3 * (uint64_t)k + 2] = after;
+  }
+  return 0;
+}
+
+/* ---------------------------------------------------------------- occupancy (NEXT #4)
+ * The standard occupancy calculation (SPEC's invented plumbing; the paper names the limits,
+ * P:443-444, without a formula): blocks per SM = min over the warp, block-slot, register and
+ * shared-memory limits; W = resident warps per scheduler.  Block Increase (grid < #SM) spreads
+ * the same warps over all SMs, W_new = W * grid / #SM; Thread Increase matches when block slots
+ * bind and a full grid stays resident, W_new = the warp or register limit.  Q34. */
+int or_occupancy(const or_arch *a, const or_launch *L, const uint32_t *grid_blocks, uint32_t n_kernels,
+                 or_occ *out) {
+  uint32_t k;
+  for (k = 0; k < n_kernels; ++k) {
+    or_occ *o = &out[k];
+    const or_launch *l = &L[k];
+    uint32_t wpb, rpw, lim[4], i, grid, want, resident;
+    memset(o, 0, sizeof(*o));
+    if (!l->threads_per_block || !a->warp_size || !a->schedulers_per_sm || !a->sm_count) continue;
+    wpb = (l->threads_per_block + a->warp_size - 1) / a->warp_size;
+    rpw = l->regs_per_thread
+              ? (l->regs_per_thread * a->warp_size + a->reg_alloc_unit - 1) / a->reg_alloc_unit * a->reg_alloc_unit
+              : 0;
+    lim[0] = a->max_warps_per_sm / wpb;
+    lim[1] = a->max_blocks_per_sm;
+    lim[2] = rpw ? a->regs_per_sm / (rpw * wpb) : 0xffffffffu;
+    lim[3] = l->smem_per_block ? a->smem_per_sm / l->smem_per_block : 0xffffffffu;
+    o->blocks_per_sm = lim[0];
+    o->limiter = 0;
+    for (i = 1; i < 4; ++i)
+      if (lim[i] < o->blocks_per_sm) { o->blocks_per_sm = lim[i]; o->limiter = i; }
+    if (!o->blocks_per_sm) continue;   /* the launch cannot run */
+    grid = grid_blocks ? grid_blocks[k] : 0;
+    if (!grid) continue;
+    want = (grid + a->sm_count - 1) / a->sm_count;
+    resident = want < o->blocks_per_sm ? want : o->blocks_per_sm;
+    o->W = (double)resident * wpb / a->schedulers_per_sm;
+    if (grid < a->sm_count) {
+      o->match_block = 1;
+      o->W_new_block = o->W * grid / a->sm_count;
+    }
+    if (o->limiter == 1 && resident == o->blocks_per_sm) {
+      uint32_t warps = a->max_warps_per_sm;
+      if (rpw && a->regs_per_sm / rpw < warps) warps = a->regs_per_sm / rpw;
+      o->W_new_thread = (double)warps / a->schedulers_per_sm;
+      o->match_thread = o->W_new_thread > o->W;
+    }
   }
   return 0;
 }

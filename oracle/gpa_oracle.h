@@ -58,7 +58,9 @@ typedef struct {
   uint8_t  model;         /* 0 Eq.2, 1 Eq.4, 2 Eq.5 loops, 3 Eq.5 functions, 4 Eq.5 loops+functions, 5 Eq.10 */
   uint8_t  flag_filter;   /* nonzero: blamed instruction must have (iflags & flag_filter) != 0 */
   uint8_t  same_loop;     /* def and use in the same innermost loop */
-  uint8_t  parallel_rule; /* Eq.10 match: 0 never, 1 always, 2 grid_blocks < sm_count */
+  uint8_t  parallel_rule; /* Eq.10 match: 0 never, 1 always, 2 grid_blocks < sm_count with
+                            the caller's W / W_new; 3 Block Increase, 4 Thread Increase from the
+                            occupancy model (or_occupancy) */
   uint8_t  pad;
   uint32_t sm_count;
   double ratio, W, W_new, f;
@@ -96,6 +98,28 @@ int or_rollup(const or_program *p, const uint64_t *C, const double *V,
 int or_estimate_all(const or_program *p, const uint64_t *C, const uint8_t *cand,
                     const uint8_t *self_flags, const double *share,
                     const or_pattern *pats, uint32_t n_pat, or_estimate *out);
+
+/* ---- occupancy model feeding W, W_new of the parallel estimator
+ * for Block Increase and Thread Increase; DESIGN.md §3.2 Q34. */
+typedef struct {
+  uint32_t sm_count, max_warps_per_sm, max_blocks_per_sm, regs_per_sm, smem_per_sm,
+           schedulers_per_sm, warp_size, reg_alloc_unit;
+} or_arch;
+typedef struct { uint32_t threads_per_block, regs_per_thread, smem_per_block, pad; } or_launch;
+typedef struct {
+  double W;              /* active warps per scheduler */
+  double W_new_block;    /* Block Increase: the same warps spread over all SMs */
+  double W_new_thread;   /* Thread Increase: larger blocks up to the warp / register limit */
+  uint32_t blocks_per_sm, limiter;   /* limiter 0 warps, 1 block slots, 2 registers, 3 shared memory */
+  uint32_t match_block, match_thread;
+} or_occ;
+int or_occupancy(const or_arch *arch, const or_launch *launch, const uint32_t *grid_blocks,
+                 uint32_t n_kernels, or_occ *out);
+
+/* same, with the occupancy model per kernel for parallel_rule 3 / 4 (occ may be NULL) */
+int or_estimate_all_occ(const or_program *p, const uint64_t *C, const uint8_t *cand,
+                        const uint8_t *self_flags, const double *share,
+                        const or_pattern *pats, uint32_t n_pat, const or_occ *occ, or_estimate *out);
 
 /* ---- after the path: the advice report's data (P:261, P:658-661,
  * P:684-686).  DESIGN.md §3.2 Q30-Q33 state the readings. */
