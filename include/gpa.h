@@ -104,7 +104,9 @@ typedef struct {
                             4 Eq.5 over loops and functions, 5 Eq.10 (parallel) */
   uint8_t flag_filter;   /* nonzero: blamed instruction must have (iflags & flag_filter) */
   uint8_t same_loop;     /* def and use in the same innermost loop (Q15) */
-  uint8_t parallel_rule; /* model 5 match: 0 never, 1 always, 2 grid_blocks < sm_count */
+  uint8_t parallel_rule; /* model 5 match: 0 never, 1 always, 2 grid_blocks < sm_count (W, W_new
+                            below); 3 Block Increase, 4 Thread Increase with W,
+                            W_new from the occupancy model (gpa_set_launches) */
   uint8_t pad;
   uint32_t sm_count;
   double ratio;          /* Eq. 2 uses ratio * M (Q17); 1 = the paper's Eq. 2 */
@@ -119,6 +121,16 @@ typedef struct {
   int32_t best_scope;    /* Eq. 5: loop id, or n_loops + function id; -1 otherwise */
   uint8_t unbounded, matched, model, pad;
 } gpa_estimate_out;
+
+/* Occupancy model (DESIGN.md §3.2 Q34): the GPU the profile came from and
+ * each kernel's launch, for parallel_rule 3 / 4 of the parallel estimator (Eqs. 6-10). */
+typedef struct {
+  uint32_t sm_count, max_warps_per_sm, max_blocks_per_sm, regs_per_sm, smem_per_sm,
+           schedulers_per_sm, warp_size, reg_alloc_unit;
+} gpa_arch;
+typedef struct {
+  uint32_t threads_per_block, regs_per_thread, smem_per_block, pad;   /* 0 = unknown / none */
+} gpa_launch;
 
 /* Advice report data (after the path; DESIGN.md §3.2 Q30-Q32). */
 #define GPA_TOP_K_MAX 8
@@ -190,6 +202,13 @@ gpa_status gpa_advise(gpa_program *prog, uint32_t top_k, void *stream);
  * GPA_ERR_BAD_STATE before gpa_advise. */
 gpa_status gpa_read_advice(gpa_program *prog, gpa_hotspot *h_hotspots, uint32_t *h_n_hotspots, uint32_t *h_rank,
                            gpa_coverage *h_coverage, void *stream);
+
+/* Set the kernels' launch statistics (HOST array [n_kernels]; with the program's
+ * kernel_grid_blocks) and the GPU's limits; computes, per kernel, the resident warps per
+ * scheduler W and the W_new of Block Increase (same warps over all SMs when grid < #SM) and
+ * Thread Increase (block slots bind; larger blocks up to the warp / register limit).  Used by
+ * patterns with parallel_rule 3 / 4; without this call those never match.  Synchronizes. */
+gpa_status gpa_set_launches(gpa_program *prog, const gpa_launch *h_launches, const gpa_arch *arch, void *stream);
 
 /* Zero the count table and stats (enqueue). */
 gpa_status gpa_reset_counts(gpa_program *prog, void *stream);

@@ -195,12 +195,21 @@ __global__ void k_est_final(DevProgram p, EstimatePlan ep) {
     if (q.model == 5) {
       const double R_I = T ? Ad / Td : 0.0;
       const uint32_t gb = p.kernel_grid_blocks[k];
-      const bool matched = q.parallel_rule == 1 || (q.parallel_rule == 2 && gb != 0xffffffffu && gb < q.sm_count);
+      bool matched = q.parallel_rule == 1 || (q.parallel_rule == 2 && gb != 0xffffffffu && gb < q.sm_count);
+      double W = q.W, W_new = q.W_new;
+      if (q.parallel_rule == 3 || q.parallel_rule == 4) {   // occupancy model (gpa_set_launches)
+        const KernOcc &oc = ep.occ[k];
+        matched = q.parallel_rule == 3 ? oc.match_block != 0 : oc.match_thread != 0;
+        if (matched) {
+          W = oc.W;
+          W_new = q.parallel_rule == 3 ? oc.W_new_block : oc.W_new_thread;
+        }
+      }
       double s = 1.0;
       if (matched) {
-        const double C_W = q.W_new / q.W;
-        const double I = 1.0 - pow(1.0 - R_I, q.W);
-        const double In = 1.0 - pow(1.0 - R_I, q.W_new);
+        const double C_W = W_new / W;
+        const double I = 1.0 - pow(1.0 - R_I, W);
+        const double In = 1.0 - pow(1.0 - R_I, W_new);
         const double C_I = (I == 0.0) ? 1.0 : In / I;
         s = (1.0 / C_W) * C_I * q.f;
       }

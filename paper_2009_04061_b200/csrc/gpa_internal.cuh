@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 #include "../../include/gpa.h"
 
 namespace gpa {
@@ -94,8 +96,15 @@ struct RollupPlan {
   double *vbuf;                 // [n][2*ncol] per-instruction vectors V
 };
 
+// per-kernel occupancy (gpa_set_launches) for parallel_rule 3 / 4
+struct KernOcc {
+  double W, W_new_block, W_new_thread;
+  uint32_t match_block, match_thread;
+};
+
 struct EstimatePlan {
   const gpa_pattern *pats;
+  const KernOcc *occ;           // [n_kernels]; zeroed until gpa_set_launches
   uint32_t n_pat;
   int8_t loop_slot[kPatternsMax];   // pattern -> slot in mval (models 2, 4) or -1
   double *mval;                 // [n_pat][E + n]: edge part then instruction part
@@ -237,6 +246,8 @@ struct gpa_program {
   gpa::RollupPlan rp{};
   gpa::EstimatePlan ep{};
   gpa::AdvicePlan ap{};
+  gpa::KernOcc *occ_dev = nullptr;
+  std::vector<uint32_t> grid_host;   // kernel_grid_blocks (empty if not given)
   int state = 0;
   int variant = gpa::VAR_SMEM;
   bool part_ok = false;

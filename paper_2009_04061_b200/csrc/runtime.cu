@@ -301,7 +301,7 @@ struct Offsets {
   size_t order, chunk_begin, chunk_end, seg1_begin, seg1_end, seg1_id, pack_seg, segpos, seg2_perm, seg2_begin, seg2_end, part_v,
       part_al, rows_v, rows_al, vbuf;
   size_t pats, mval, mrow, loop_items, loop_item_ptr, pre_perm, pre_begin, pre_end, kloop_ptr, kloops,
-      loop_func, lM_excl, lM_incl, fM, kM, est, hot, n_hot, rank, cov;
+      loop_func, lM_excl, lM_incl, fM, kM, est, hot, n_hot, rank, cov, occ;
   size_t C, stats, AL, cand, selfm, share, B, partials, part_x, part_sync;
   bool part_reserved = false;
   size_t total;
@@ -382,6 +382,7 @@ Offsets layout(const gpa_program_desc *d, const HostPlan &h) {
   o.n_hot = a.take((size_t)kPatWs * nk * 4);
   o.rank = a.take((size_t)kPatWs * nk * 4);
   o.cov = a.take((size_t)nk * sizeof(gpa_coverage));
+  o.occ = a.take((size_t)nk * sizeof(KernOcc));
   o.total = a.off;
   return o;
 }
@@ -549,6 +550,10 @@ gpa_status gpa_program_create(const gpa_program_desc *d, void *d_workspace, size
   ep.func_al = rp.rows_al + 2 * r_func;
   ep.kern_al = rp.rows_al + 2 * r_kern;
   ep.out = (gpa_estimate_out *)(ws + o.est);
+  ep.occ = (const KernOcc *)(ws + o.occ);
+  p->occ_dev = (KernOcc *)(ws + o.occ);
+  p->grid_host.assign(d->kernel_grid_blocks ? d->kernel_grid_blocks : nullptr,
+                      d->kernel_grid_blocks ? d->kernel_grid_blocks + d->n_kernels : nullptr);
   p->ap.hot = (gpa_hotspot *)(ws + o.hot);
   p->ap.n_hot = (uint32_t *)(ws + o.n_hot);
   p->ap.rank = (uint32_t *)(ws + o.rank);
@@ -779,6 +784,52 @@ gpa_status gpa_analyze(gpa_program *p, void *stream) {
   p->launches += p->analyze_launches;
   p->state |= ST_BLAMED | ST_AGGREGATED;
   p->state = npat ? (p->state | ST_ESTIMATED) & ~ST_ADVISED : p->state & ~(ST_ESTIMATED | ST_ADVISED);
+  return GPA_OK;
+}
+
+// Occupancy of every kernel (DESIGN.md §3.2 Q34): the usual calculator -- blocks per SM are the
+// tightest of the warp, block-slot, register (allocation-unit rounded) and shared-memory limits.
+gpa_status gpa_set_launches(gpa_program *p, const gpa_launch *h_launch, const gpa_arch *arch, void *stream) {
+  gpa_status st = check_prog(p);
+  if (st) return st;
+  if (!h_launch || !arch) return fail(GPA_ERR_INVALID_ARGUMENT, "NULL launches or arch");
+  if (!arch->sm_count || !arch->warp_size || !arch->schedulers_per_sm || !arch->reg_alloc_unit)
+    return fail(GPA_ERR_INVALID_ARGUMENT, "arch needs sm_count, warp_size, schedulers_per_sm, reg_alloc_unit > 0");
+  const uint32_t nk = p->d.n_kernels;
+  std::vector<KernOcc> occ(nk);
+  for (uint32_t k = 0; k < nk; ++k) {
+    KernOcc &o = occ[k];
+    o = KernOcc{0.0, 0.0, 0.0, 0u, 0u};
+    const gpa_launch &l = h_launch[k];
+    const uint32_t grid = p->grid_host.empty() ? 0u : p->grid_host[k];
+    if (!l.threads_per_block || !grid || grid == 0xffffffffu) continue;
+    const uint64_t warps_per_block = (l.threads_per_block + arch->warp_size - 1) / arch->warp_size;
+    const uint64_t unit = arch->reg_alloc_unit;
+    const uint64_t regs_per_warp = l.regs_per_thread ? ((uint64_t)l.regs_per_thread * arch->warp_size + unit - 1) / unit * unit : 0;
+    const uint64_t by_warps = arch->max_warps_per_sm / warps_per_block;
+    const uint64_t by_slots = arch->max_blocks_per_sm;
+    const uint64_t by_regs = regs_per_warp ? arch->regs_per_sm / (regs_per_warp * warps_per_block) : UINT64_MAX;
+    const uint64_t by_smem = l.smem_per_block ? arch->smem_per_sm / l.smem_per_block : UINT64_MAX;
+    const uint64_t blocks = std::min(std::min(by_warps, by_slots), std::min(by_regs, by_smem));
+    if (blocks == 0) continue;   // cannot launch
+    const bool slots_bind = by_slots == blocks && by_warps > blocks;   // ties go to the warp limit
+    const uint64_t resident = std::min<uint64_t>(blocks, (grid + arch->sm_count - 1) / arch->sm_count);
+    o.W = (double)(resident * warps_per_block) / arch->schedulers_per_sm;
+    if (grid < arch->sm_count) {
+      o.match_block = 1;
+      o.W_new_block = o.W * grid / arch->sm_count;
+    }
+    if (slots_bind && resident == blocks) {
+      uint64_t warps = arch->max_warps_per_sm;
+      if (regs_per_warp) warps = std::min<uint64_t>(warps, arch->regs_per_sm / regs_per_warp);
+      o.W_new_thread = (double)warps / arch->schedulers_per_sm;
+      o.match_thread = o.W_new_thread > o.W;
+    }
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  CUDA_TRY(cudaMemcpyAsync(p->occ_dev, occ.data(), nk * sizeof(KernOcc), cudaMemcpyHostToDevice, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  p->state &= ~(ST_ESTIMATED | ST_ADVISED);
   return GPA_OK;
 }
 

@@ -61,6 +61,21 @@ class Coverage(ctypes.Structure):
     _fields_ = [("nodes", ctypes.c_uint64), ("single_before", ctypes.c_uint64), ("single_after", ctypes.c_uint64)]
 
 
+class Arch(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_uint32) for k in ("sm_count", "max_warps_per_sm", "max_blocks_per_sm", "regs_per_sm",
+                                               "smem_per_sm", "schedulers_per_sm", "warp_size", "reg_alloc_unit")]
+
+
+class Launch(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_uint32) for k in ("threads_per_block", "regs_per_thread", "smem_per_block", "pad")]
+
+
+# GPU limits for the occupancy model: the paper's profiled V100 and this B200
+ARCH_V100 = dict(sm_count=80, max_warps_per_sm=64, max_blocks_per_sm=32, regs_per_sm=65536, smem_per_sm=98304,
+                 schedulers_per_sm=4, warp_size=32, reg_alloc_unit=256)
+ARCH_B200 = dict(sm_count=148, max_warps_per_sm=64, max_blocks_per_sm=32, regs_per_sm=65536, smem_per_sm=233472,
+                 schedulers_per_sm=4, warp_size=32, reg_alloc_unit=256)
+
 TOP_K_MAX = 8
 
 EXPORTS = ["gpa_validate_program", "gpa_workspace_size", "gpa_program_create", "gpa_program_destroy",
@@ -68,7 +83,7 @@ EXPORTS = ["gpa_validate_program", "gpa_workspace_size", "gpa_program_create", "
            "gpa_aggregate", "gpa_set_patterns", "gpa_estimate", "gpa_read_estimates", "gpa_get_stats",
            "gpa_view", "gpa_instr_vector", "gpa_program_info", "gpa_ingest_variant",
            "gpa_set_ingest_variant", "gpa_launch_count", "gpa_last_error", "gpa_version", "gpa_analyze",
-           "gpa_ingest_segments", "gpa_advise", "gpa_read_advice"]
+           "gpa_ingest_segments", "gpa_advise", "gpa_read_advice", "gpa_set_launches"]
 
 _lib = None
 
@@ -95,6 +110,7 @@ def lib():
             "gpa_analyze": [vp, vp],
             "gpa_ingest_segments": [vp, vp, u64, vp, vp, u32, u32, vp],
             "gpa_advise": [vp, u32, vp], "gpa_read_advice": [vp, vp, vp, vp, vp, vp],
+            "gpa_set_launches": [vp, vp, vp, vp],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -269,6 +285,16 @@ class Program:
         out = (EstimateOut * (self.n_kernels * self.n_patterns))()
         _check(lib().gpa_read_estimates(self.handle, ctypes.addressof(out), self._s(stream)), "gpa_read_estimates")
         return np.ctypeslib.as_array(out).reshape(self.n_kernels, self.n_patterns)
+
+    def set_launches(self, launches, arch=None, stream=None):
+        """launches: per kernel (threads_per_block, regs_per_thread, smem_per_block); arch: dict of
+        gpa_arch fields (default ARCH_V100, the paper's GPU).  Enables parallel_rule 3 / 4."""
+        a = Arch(**(arch or ARCH_V100))
+        if len(launches) != self.n_kernels:
+            raise GpaError(f"need {self.n_kernels} launches")
+        L = (Launch * self.n_kernels)(*[Launch(int(t), int(r), int(m), 0) for t, r, m in launches])
+        _check(lib().gpa_set_launches(self.handle, ctypes.addressof(L), ctypes.byref(a), self._s(stream)),
+               "gpa_set_launches")
 
     def advise(self, top_k=5, stream=None):
         """Hotspots, ranking and single dependency coverage (gpa_advise) of the current estimates."""

@@ -39,6 +39,7 @@ def test_struct_sizes_match_header(g):
     assert ctypes.sizeof(g.Pattern) == 48
     assert ctypes.sizeof(g.EstimateOut) == 56
     assert ctypes.sizeof(g.gpa.Hotspot) == 24 and ctypes.sizeof(g.gpa.Coverage) == 24
+    assert ctypes.sizeof(g.gpa.Arch) == 32 and ctypes.sizeof(g.gpa.Launch) == 16
     assert ctypes.sizeof(g.gpa.ProgramDesc) == 6 * 4 + 15 * 8
 
 

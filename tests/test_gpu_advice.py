@@ -106,3 +106,41 @@ def test_advice_state_errors():
     P.reset()
     with pytest.raises(GpaError):
         P.read_advice()                  # new counts invalidate the advice
+
+
+def test_occupancy_parallel_estimates_match_oracle():
+    """parallel_rule 3 / 4 (NEXT #4): per-kernel W, W_new from gpa_set_launches equal the oracle's
+    occupancy model; the Eq. 10 estimates agree within 1e-9."""
+    import torch
+    from paper_2009_04061_b200 import Program
+    from paper_2009_04061_b200.gpa import ARCH_V100
+    prog = gp.random_program(2000, 10, 20, 3, seed=75, n_kernels=6)
+    prog.kernel_grid_blocks = np.array([16, 200, 10_000, 79, 4, 1000], np.uint32)
+    launches = [(256, 64, 0), (32, 32, 0), (32, 32, 0), (128, 33, 40960), (1024, 255, 0), (256, 32, 0)]
+    recs = StreamSpec(prog, seed=76).host(0, 300_000)
+    pats = table2(prog.n_reasons)
+    for p in pats:
+        if p["name"] == "block_increase":
+            p["parallel_rule"] = 3
+        if p["name"] == "thread_increase":
+            p["parallel_rule"] = 4
+    o = run_oracle(prog, recs, pats)
+    occ = oracle.occupancy(oracle.Arch(*ARCH_V100.values()), [oracle.Launch(*l, 0) for l in launches],
+                           prog.kernel_grid_blocks)
+    op = oracle.OracleProgram(prog)
+    est_o = op.estimate(o["C"], o, [oracle_pattern(p) for p in pats], occ)
+    P = Program(prog)
+    P.set_patterns(pats)
+    P.set_launches(launches, ARCH_V100)
+    P.reset()
+    P.ingest(torch.from_numpy(recs.view(np.int64)).cuda())
+    P.analyze()
+    est_g = P.read_estimates()
+    matched = 0
+    for k in range(prog.n_kernels):
+        for q, p in enumerate(pats):
+            a, b = est_g[k][q], est_o[k][q]
+            assert a.matched == b.matched, (k, p["name"])
+            assert abs(a.speedup - b.speedup) <= 1e-9 * abs(b.speedup), (k, p["name"], a.speedup, b.speedup)
+            matched += a.matched and p["model"] == 5
+    assert matched >= 3      # kernels 0, 3, 4 (block increase) and 1, 2 (thread increase) exercise both rules
