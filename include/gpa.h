@@ -59,7 +59,8 @@ typedef enum {
   GPA_ERR_BAD_STATE = -3,        /* call order violated (e.g. aggregate before blame) */
   GPA_ERR_CUDA = -4,             /* CUDA runtime / launch error */
   GPA_ERR_WORKSPACE = -5,        /* workspace too small or not 256-byte aligned */
-  GPA_ERR_DOMAIN = -6            /* estimator input outside its domain (W <= 0, R_I not in [0,1]) */
+  GPA_ERR_DOMAIN = -6,           /* estimator input outside its domain (W <= 0, R_I not in [0,1]) */
+  GPA_ERR_OVERFLOW = -7          /* an output capacity or search budget was exceeded (gpa_slice) */
 } gpa_status;
 
 /* One PC-sampling record: `count` identical samples of instruction `pc`
@@ -121,6 +122,21 @@ typedef struct {
   int32_t best_scope;    /* Eq. 5: loop id, or n_loops + function id; -1 otherwise */
   uint8_t unbounded, matched, model, pad;
 } gpa_estimate_out;
+
+/* SASS fields for backward slicing (Table 1) and the
+ * control flow graph.  Host pointers, read during gpa_slice only. */
+typedef struct {
+  uint32_t n_instr, n_funcs, n_blocks;
+  const uint32_t *func_begin;   /* [n_funcs+1] contiguous instruction ranges (block boundaries) */
+  const uint32_t *block_begin;  /* [n_blocks+1] contiguous basic blocks, [0] = 0, [n_blocks] = n_instr */
+  const uint32_t *succ_ptr;     /* [n_blocks+1] CSR of successor blocks */
+  const uint32_t *succ;         /* successor block ids, in the same function */
+  const uint8_t *guard;         /* [n_instr] bits 0-2 predicate P0..P6 (7 = none, '_'), bit 3 = negated (!P) */
+  const uint16_t *dst, *src;    /* [n_instr][4] operands: 0..254 R0..R254, 255 RZ (ignored),
+                                   256..262 P0..P6, 0xFFFF = none */
+  const uint8_t *wbar, *rbar;   /* [n_instr] write / read barrier masks over B0..B5 */
+  const uint8_t *wait;          /* [n_instr] wait mask over B0..B5 */
+} gpa_sass_desc;
 
 /* Occupancy model (DESIGN.md §3.2 Q34): the GPU the profile came from and
  * each kernel's launch, for parallel_rule 3 / 4 of the parallel estimator (Eqs. 6-10). */
@@ -202,6 +218,16 @@ gpa_status gpa_advise(gpa_program *prog, uint32_t top_k, void *stream);
  * GPA_ERR_BAD_STATE before gpa_advise. */
 gpa_status gpa_read_advice(gpa_program *prog, gpa_hotspot *h_hotspots, uint32_t *h_n_hotspots, uint32_t *h_rank,
                            gpa_coverage *h_coverage, void *stream);
+
+/* Backward slicing (DESIGN.md §3.2 Q35-Q39): the def-use CSR keyed by the use -- what
+ * gpa_program_desc's row_ptr / edge_* fields take -- from SASS fields and the CFG, computed on
+ * the device (one thread per use).  Host output arrays: h_row_ptr [n_instr+1] and cap_edges
+ * entries of each edge array; *n_edges receives the edge count.  GPA_ERR_OVERFLOW if cap_edges
+ * is too small (nothing but *n_edges and h_row_ptr written) or a search exceeds its state budget
+ * (4 x the longest function + 256 states).  Synchronizes. */
+gpa_status gpa_slice(const gpa_sass_desc *h_sass, uint64_t cap_edges, uint32_t *h_row_ptr, uint32_t *h_edge_def,
+                     uint8_t *h_edge_kind, uint32_t *h_edge_min_len, uint32_t *h_edge_max_len,
+                     int32_t *h_edge_dom_k, uint64_t *n_edges, void *stream);
 
 /* Set the kernels' launch statistics (HOST array [n_kernels]; with the program's
  * kernel_grid_blocks) and the GPU's limits; computes, per kernel, the resident warps per

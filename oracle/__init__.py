@@ -88,6 +88,8 @@ def lib():
         L.or_estimate_all.argtypes = [vp, vp, vp, vp, vp, vp, ctypes.c_uint32, vp]
         L.or_estimate_all_occ.argtypes = [vp, vp, vp, vp, vp, vp, ctypes.c_uint32, vp, vp]
         L.or_occupancy.argtypes = [vp, vp, vp, ctypes.c_uint32, vp]
+        L.or_slice.argtypes = [vp, ctypes.c_uint64, vp, vp, vp, vp, vp, vp]
+        L.or_slice.restype = ctypes.c_int64
         L.or_hotspots.argtypes = [vp, vp, vp, vp, vp, vp, ctypes.c_uint32, ctypes.c_uint32, vp, vp]
         L.or_rank.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint32, vp]
         L.or_coverage.argtypes = [vp, vp, vp, vp]
@@ -247,3 +249,33 @@ def occupancy(arch, launches, grid_blocks):
     out = (Occ * K)()
     lib().or_occupancy(ctypes.byref(arch), ctypes.addressof(L), g.ctypes.data, K, ctypes.addressof(out))
     return out
+
+
+class _Sass(ctypes.Structure):
+    _fields_ = [("n_instr", ctypes.c_uint32), ("n_funcs", ctypes.c_uint32), ("n_blocks", ctypes.c_uint32)] + [
+        (k, ctypes.c_void_p) for k in ("func_begin", "block_begin", "succ_ptr", "succ", "guard", "dst", "src",
+                                       "wbar", "rbar", "wait")]
+
+
+def slice_program(sass):
+    """Backward slicing (or_slice) of a SASS description (object with the or_sass arrays) ->
+    dict of the def-use CSR: row_ptr, edge_def, edge_kind, edge_min_len, edge_max_len, edge_dom_k."""
+    dt = {"func_begin": np.uint32, "block_begin": np.uint32, "succ_ptr": np.uint32, "succ": np.uint32,
+          "guard": np.uint8, "dst": np.uint16, "src": np.uint16, "wbar": np.uint8, "rbar": np.uint8, "wait": np.uint8}
+    a = {k: np.ascontiguousarray(getattr(sass, k), dtype=t) for k, t in dt.items()}
+    n = int(a["guard"].shape[0])
+    st = _Sass(n, int(a["func_begin"].shape[0] - 1), int(a["block_begin"].shape[0] - 1),
+               *[a[k].ctypes.data for k in ("func_begin", "block_begin", "succ_ptr", "succ", "guard", "dst", "src",
+                                            "wbar", "rbar", "wait")])
+    cap = 64 * max(n, 1)
+    row_ptr = np.zeros(n + 1, np.uint32)
+    out = {"edge_def": np.zeros(cap, np.uint32), "edge_kind": np.zeros(cap, np.uint8),
+           "edge_min_len": np.zeros(cap, np.uint32), "edge_max_len": np.zeros(cap, np.uint32),
+           "edge_dom_k": np.zeros(cap, np.int32)}
+    E = lib().or_slice(ctypes.byref(st), cap, row_ptr.ctypes.data, *[out[k].ctypes.data for k in (
+        "edge_def", "edge_kind", "edge_min_len", "edge_max_len", "edge_dom_k")])
+    if E < 0:
+        raise RuntimeError(f"or_slice failed ({E})")
+    res = {k: v[:E].copy() for k, v in out.items()}
+    res["row_ptr"] = row_ptr
+    return res

@@ -633,3 +633,323 @@ int or_occupancy(const or_arch *a, const or_launch *L, const uint32_t *grid_bloc
   }
   return 0;
 }
+
+/* ---------------------------------------------------------------- backward slicing (NEXT #1)
+ * P:289-321.  For every use j and every register j reads (source operands, its guard predicate,
+ * the virtual barrier registers B0-B5 of its wait mask), search backward along the
+ * control flow graph of j's function.  A search state is (instruction x about to be examined, P =
+ * union of the predicates of the defs of the register already passed on this path).  Examining x:
+ * if x defines the register (destination operand, or write / read barrier for a B register,
+ * P:301-302) it is a dependency source at path length L = steps from x to j; P grows by x's
+ * predicate and the path stops once P contains j's predicate.  Otherwise the search
+ * continues to x-1, or to the last instruction of every predecessor block.  Q35-Q39. */
+
+#define SL_ALL 0x4000u   /* '_' */
+#define SL_NONE 0xFFFFu
+
+static uint32_t sl_pbit(uint8_t g) {         /* predicate of an instruction as a P-set bit */
+  uint32_t r = g & 7u;
+  if (r == 7u) return SL_ALL;
+  return (g & 8u) ? (1u << (7u + r)) : (1u << r);
+}
+static uint32_t sl_norm(uint32_t P) {         /* {p_i} u {!p_i} = {_} */
+  uint32_t i;
+  for (i = 0; i < 7; ++i)
+    if ((P >> i & 1u) && (P >> (7 + i) & 1u)) P |= SL_ALL;
+  return P;
+}
+static int sl_contains(uint32_t P, uint32_t pbit) { return (P & SL_ALL) || (P & pbit); }
+
+/* registers read by instruction x: out[] = reg ids (0..254, 256..262, 512+b), kinds[] */
+static int sl_reads(const or_sass *s, uint32_t x, uint32_t *out, uint8_t *kinds) {
+  int n = 0, t;
+  for (t = 0; t < 4; ++t) {
+    uint16_t r = s->src[4u * x + t];
+    if (r == SL_NONE || r == 255u) continue;
+    out[n] = r; kinds[n] = r >= 256u ? 2u : 1u; ++n;
+  }
+  if ((s->guard[x] & 7u) != 7u) { out[n] = 256u + (s->guard[x] & 7u); kinds[n] = 2u; ++n; }
+  for (t = 0; t < 6; ++t)
+    if (s->wait[x] >> t & 1u) { out[n] = 512u + t; kinds[n] = 4u; ++n; }
+  return n;
+}
+static int sl_defines(const or_sass *s, uint32_t x, uint32_t r) {
+  int t;
+  if (r >= 512u) return ((s->wbar[x] | s->rbar[x]) >> (r - 512u)) & 1u;
+  for (t = 0; t < 4; ++t)
+    if (s->dst[4u * x + t] == r) return 1;
+  return 0;
+}
+static int sl_reads_reg(const or_sass *s, uint32_t x, uint32_t r) {
+  uint32_t rr[16];
+  uint8_t kk[16];
+  int n = sl_reads(s, x, rr, kk), t;
+  for (t = 0; t < n; ++t)
+    if (rr[t] == r) return 1;
+  return 0;
+}
+
+typedef struct {
+  uint32_t *x, *P, *dist, *lng, *rpo_pos, *hslot;
+  uint8_t *term;
+  uint32_t n, cap;
+  uint32_t *hkey_x, *hkey_p, *hval, hcap;   /* open-addressing index (x, P) -> state */
+} sl_graph;
+
+static uint32_t sl_hash(const sl_graph *g, uint32_t x, uint32_t P) {
+  return (x * 2654435761u ^ (P + 1u) * 40503u) & (g->hcap - 1u);
+}
+static uint32_t sl_find(const sl_graph *g, uint32_t x, uint32_t P) {
+  uint32_t h = sl_hash(g, x, P);
+  while (g->hval[h] != 0xFFFFFFFFu) {
+    if (g->hkey_x[h] == x && g->hkey_p[h] == P) return g->hval[h];
+    h = (h + 1u) & (g->hcap - 1u);
+  }
+  return 0xFFFFFFFFu;
+}
+static uint32_t sl_insert(sl_graph *g, uint32_t x, uint32_t P) {
+  uint32_t h = sl_hash(g, x, P);
+  while (g->hval[h] != 0xFFFFFFFFu) {
+    if (g->hkey_x[h] == x && g->hkey_p[h] == P) return g->hval[h];
+    h = (h + 1u) & (g->hcap - 1u);
+  }
+  g->hkey_x[h] = x; g->hkey_p[h] = P; g->hval[h] = g->n;
+  g->x[g->n] = x; g->P[g->n] = P; g->hslot[g->n] = h;
+  return g->n++;
+}
+static void sl_clear(sl_graph *g) {
+  uint32_t i;
+  for (i = 0; i < g->n; ++i) g->hval[g->hslot[i]] = 0xFFFFFFFFu;
+  g->n = 0;
+}
+
+/* predecessors of instruction x in backward order: x-1 in its block, else the last instruction
+ * of each predecessor block (ascending block id) */
+static int sl_prev(const or_sass *s, const uint32_t *blk_of, const uint32_t *pred_ptr, const uint32_t *pred,
+                   uint32_t x, uint32_t *out) {
+  uint32_t b = blk_of[x], e;
+  int n = 0;
+  if (x > s->block_begin[b]) { out[0] = x - 1; return 1; }
+  for (e = pred_ptr[b]; e < pred_ptr[b + 1] && n < 64; ++e) out[n++] = s->block_begin[pred[e] + 1] - 1;
+  return n;
+}
+
+/* the mask a state passes on to its predecessors (P grown by a def's predicate), and whether the
+ * state ends its path */
+static uint32_t sl_out_mask(const or_sass *s, uint32_t x, uint32_t P, uint32_t r, uint32_t pj, int *term) {
+  int is_def = sl_defines(s, x, r);
+  if (is_def) P = sl_norm(P | sl_pbit(s->guard[x]));
+  *term = is_def && sl_contains(P, pj);
+  return P;
+}
+
+int64_t or_slice(const or_sass *s, uint64_t cap, uint32_t *row_ptr, uint32_t *edge_def, uint8_t *edge_kind,
+                 uint32_t *edge_min, uint32_t *edge_max, int32_t *edge_dom) {
+  const uint32_t n = s->n_instr, NB = s->n_blocks;
+  uint32_t *blk_of = (uint32_t *)malloc(sizeof(uint32_t) * (n ? n : 1));
+  uint32_t *pred_ptr = (uint32_t *)calloc(NB + 1, sizeof(uint32_t));
+  uint32_t *pred = (uint32_t *)malloc(sizeof(uint32_t) * (s->succ_ptr[NB] ? s->succ_ptr[NB] : 1));
+  uint32_t *fill = (uint32_t *)calloc(NB + 1, sizeof(uint32_t));
+  uint32_t b, e, j, f, maxf = 1;
+  uint64_t E = 0;
+  int64_t ret = -1;
+  sl_graph g;
+  uint32_t *queue, *stack, *sidx, *rpo, *mark, *cands;
+  uint32_t *acc_def, *acc_min, *acc_max, *acc_last;
+  int32_t *acc_dom;
+  uint8_t *acc_kind;
+  for (b = 0; b < NB; ++b)
+    for (j = s->block_begin[b]; j < s->block_begin[b + 1]; ++j) blk_of[j] = b;
+  for (b = 0; b < NB; ++b)
+    for (e = s->succ_ptr[b]; e < s->succ_ptr[b + 1]; ++e) pred_ptr[s->succ[e] + 1]++;
+  for (b = 0; b < NB; ++b) pred_ptr[b + 1] += pred_ptr[b];
+  for (b = 0; b < NB; ++b)                       /* ascending source block id per target */
+    for (e = s->succ_ptr[b]; e < s->succ_ptr[b + 1]; ++e) {
+      uint32_t t = s->succ[e];
+      pred[pred_ptr[t] + fill[t]++] = b;
+    }
+  for (f = 0; f < s->n_funcs; ++f)
+    if (s->func_begin[f + 1] - s->func_begin[f] > maxf) maxf = s->func_begin[f + 1] - s->func_begin[f];
+  g.cap = 16u * maxf + 1024u;                    /* states per search (<= 16 P-sets per instruction) */
+  g.hcap = 1u;
+  while (g.hcap < 2u * g.cap) g.hcap <<= 1;
+  g.x = (uint32_t *)malloc(4u * g.cap); g.P = (uint32_t *)malloc(4u * g.cap);
+  g.dist = (uint32_t *)malloc(4u * g.cap); g.lng = (uint32_t *)malloc(4u * g.cap);
+  g.rpo_pos = (uint32_t *)malloc(4u * g.cap); g.hslot = (uint32_t *)malloc(4u * g.cap);
+  g.term = (uint8_t *)malloc(g.cap);
+  g.hkey_x = (uint32_t *)malloc(4u * g.hcap); g.hkey_p = (uint32_t *)malloc(4u * g.hcap);
+  g.hval = (uint32_t *)malloc(4u * g.hcap);
+  queue = (uint32_t *)malloc(4u * g.cap); stack = (uint32_t *)malloc(4u * g.cap);
+  sidx = (uint32_t *)malloc(4u * g.cap); rpo = (uint32_t *)malloc(4u * g.cap);
+  mark = (uint32_t *)malloc(4u * g.cap); cands = (uint32_t *)malloc(4u * g.cap);
+  acc_def = (uint32_t *)malloc(4u * g.cap); acc_min = (uint32_t *)malloc(4u * g.cap);
+  acc_max = (uint32_t *)malloc(4u * g.cap); acc_dom = (int32_t *)malloc(4u * g.cap);
+  acc_last = (uint32_t *)malloc(4u * g.cap);
+  acc_kind = (uint8_t *)malloc(g.cap);
+  for (e = 0; e < g.hcap; ++e) g.hval[e] = 0xFFFFFFFFu;
+  g.n = 0;
+  row_ptr[0] = 0;
+  for (j = 0; j < n; ++j) {
+    uint32_t reads[16], n_acc = 0, a, a2;
+    uint8_t kinds[16];
+    const int nr = sl_reads(s, j, reads, kinds);
+    const uint32_t pj = sl_pbit(s->guard[j]);
+    int ri;
+    for (ri = 0; ri < nr; ++ri) {
+      const uint32_t r = reads[ri];
+      uint32_t head = 0, tail = 0, i, roots[64], kids[64], n_cand = 0, sp = 0, cnt = 0;
+      int nroot, nk, q, term;
+      /* ---- BFS over states from the virtual root at j (shortest path lengths), Q36 */
+      sl_clear(&g);
+      nroot = sl_prev(s, blk_of, pred_ptr, pred, j, roots);
+      for (q = 0; q < nroot; ++q)
+        if (sl_find(&g, roots[q], 0u) == 0xFFFFFFFFu) {
+          uint32_t id = sl_insert(&g, roots[q], 0u);
+          g.dist[id] = 1u;
+          queue[tail++] = id;
+        }
+      while (head < tail) {
+        uint32_t u = queue[head++];
+        const uint32_t Pout = sl_out_mask(s, g.x[u], g.P[u], r, pj, &term);
+        g.term[u] = (uint8_t)term;
+        if (term) continue;
+        nk = sl_prev(s, blk_of, pred_ptr, pred, g.x[u], kids);
+        for (q = 0; q < nk; ++q)
+          if (sl_find(&g, kids[q], Pout) == 0xFFFFFFFFu) {
+            uint32_t v;
+            if (g.n + 1u >= g.cap) goto fail;           /* state budget */
+            v = sl_insert(&g, kids[q], Pout);
+            g.dist[v] = g.dist[u] + 1u;
+            queue[tail++] = v;
+          }
+      }
+      /* ---- DFS in the same successor order; longest paths over the edges that go forward in
+       *      the reverse postorder (the DFS back edges -- loops -- are cut), Q37 */
+      for (i = 0; i < g.n; ++i) { mark[i] = 0; g.lng[i] = 0; }
+      for (q = 0; q < nroot; ++q) {
+        const uint32_t c = sl_find(&g, roots[q], 0u);
+        if (mark[c]) continue;
+        mark[c] = 1; stack[0] = c; sidx[0] = 0; sp = 1;
+        while (sp) {
+          const uint32_t u = stack[sp - 1];
+          nk = 0;
+          if (!g.term[u]) {
+            const uint32_t Pout = sl_out_mask(s, g.x[u], g.P[u], r, pj, &term);
+            nk = sl_prev(s, blk_of, pred_ptr, pred, g.x[u], kids);
+            if ((int)sidx[sp - 1] < nk) {
+              const uint32_t v = sl_find(&g, kids[sidx[sp - 1]++], Pout);
+              if (!mark[v]) { mark[v] = 1; stack[sp] = v; sidx[sp] = 0; ++sp; }
+              continue;
+            }
+          }
+          rpo[cnt++] = u;                                /* postorder */
+          --sp;
+        }
+      }
+      for (i = 0; i < cnt; ++i) g.rpo_pos[rpo[i]] = cnt - 1 - i;
+      for (q = 0; q < nroot; ++q) g.lng[sl_find(&g, roots[q], 0u)] = 1u;
+      for (i = cnt; i-- > 0;) {                          /* reverse postorder */
+        const uint32_t u = rpo[i];
+        uint32_t Pout;
+        if (g.term[u]) continue;
+        Pout = sl_out_mask(s, g.x[u], g.P[u], r, pj, &term);
+        nk = sl_prev(s, blk_of, pred_ptr, pred, g.x[u], kids);
+        for (q = 0; q < nk; ++q) {
+          const uint32_t v = sl_find(&g, kids[q], Pout);
+          if (g.rpo_pos[v] > g.rpo_pos[u] && g.lng[u] + 1u > g.lng[v]) g.lng[v] = g.lng[u] + 1u;
+        }
+      }
+      /* ---- rule-2 candidates: unpredicated readers of r met by the search (ascending), Q38 */
+      for (i = 0; i < g.n; ++i) {
+        const uint32_t k = g.x[i];
+        if (k == j || (s->guard[k] & 7u) != 7u || !sl_reads_reg(s, k, r)) continue;
+        for (a = 0; a < n_cand && cands[a] != k; ++a) {}
+        if (a == n_cand) cands[n_cand++] = k;
+      }
+      for (a = 1; a < n_cand; ++a)
+        for (a2 = a; a2 > 0 && cands[a2 - 1] > cands[a2]; --a2) {
+          const uint32_t t0 = cands[a2]; cands[a2] = cands[a2 - 1]; cands[a2 - 1] = t0;
+        }
+      /* ---- the defs this read found */
+      for (i = 0; i < g.n; ++i) {
+        const uint32_t x = g.x[i];
+        uint8_t kind;
+        int32_t dom = -1;
+        uint32_t c;
+        if (!sl_defines(s, x, r)) continue;
+        for (a = 0; a < n_acc && acc_def[a] != x; ++a) {}
+        kind = kinds[ri];
+        if (r >= 512u && ((s->rbar[x] >> (r - 512u)) & 1u)) {   /* WAR: j overwrites what x reads */
+          int tt, uu;
+          for (tt = 0; tt < 4; ++tt)
+            for (uu = 0; uu < 4; ++uu) {
+              const uint16_t d = s->dst[4u * j + tt];
+              if (d != SL_NONE && d != 255u && d == s->src[4u * x + uu]) kind |= 8u;
+            }
+        }
+        if (a == n_acc) {                          /* first state of def x in this row */
+          acc_def[a] = x; acc_kind[a] = 0; acc_min[a] = 0xFFFFFFFFu; acc_max[a] = 0; acc_dom[a] = -2;
+          acc_last[a] = 0;
+          ++n_acc;
+        }
+        acc_kind[a] |= kind;
+        if (g.dist[i] < acc_min[a]) acc_min[a] = g.dist[i];
+        if (g.lng[i] > acc_max[a]) acc_max[a] = g.lng[i];
+        if (acc_last[a] == (uint32_t)ri + 1u) continue;   /* rule 2 already settled for (x, this read) */
+        acc_last[a] = (uint32_t)ri + 1u;
+        /* rule 2: the smallest candidate k != x on every path from j to every state of x */
+        for (c = 0; c < n_cand && dom < 0; ++c) {
+          uint32_t h2 = 0, t2 = 0, st;
+          int reach = 0;
+          const uint32_t k = cands[c];
+          if (k == x) continue;
+          for (st = 0; st < g.n; ++st) mark[st] = 0;
+          for (q = 0; q < nroot; ++q) {
+            const uint32_t cc = sl_find(&g, roots[q], 0u);
+            if (g.x[cc] != k && !mark[cc]) { mark[cc] = 1; queue[t2++] = cc; }
+          }
+          while (h2 < t2 && !reach) {
+            const uint32_t u = queue[h2++];
+            uint32_t Pout;
+            if (g.x[u] == x) { reach = 1; break; }
+            if (g.term[u]) continue;
+            Pout = sl_out_mask(s, g.x[u], g.P[u], r, pj, &term);
+            nk = sl_prev(s, blk_of, pred_ptr, pred, g.x[u], kids);
+            for (q = 0; q < nk; ++q) {
+              const uint32_t v = sl_find(&g, kids[q], Pout);
+              if (g.x[v] != k && !mark[v]) { mark[v] = 1; queue[t2++] = v; }
+            }
+          }
+          if (!reach) dom = (int32_t)k;
+        }
+        /* merged over the reads reaching x: kept only if all agree (Q38) */
+        if (acc_dom[a] == -2) acc_dom[a] = dom;
+        else if (acc_dom[a] != dom) acc_dom[a] = -1;
+      }
+    }
+    for (a = 1; a < n_acc; ++a)                          /* defs ascending */
+      for (a2 = a; a2 > 0 && acc_def[a2 - 1] > acc_def[a2]; --a2) {
+        uint32_t t0 = acc_def[a2]; acc_def[a2] = acc_def[a2 - 1]; acc_def[a2 - 1] = t0;
+        t0 = acc_min[a2]; acc_min[a2] = acc_min[a2 - 1]; acc_min[a2 - 1] = t0;
+        t0 = acc_max[a2]; acc_max[a2] = acc_max[a2 - 1]; acc_max[a2 - 1] = t0;
+        { const uint8_t t1 = acc_kind[a2]; acc_kind[a2] = acc_kind[a2 - 1]; acc_kind[a2 - 1] = t1; }
+        { const int32_t t3 = acc_dom[a2]; acc_dom[a2] = acc_dom[a2 - 1]; acc_dom[a2 - 1] = t3; }
+      }
+    for (a = 0; a < n_acc; ++a) {
+      if (E >= cap) goto fail;
+      edge_def[E] = acc_def[a]; edge_kind[E] = acc_kind[a];
+      edge_min[E] = acc_min[a]; edge_max[E] = acc_max[a];
+      edge_dom[E] = acc_dom[a] < 0 ? -1 : acc_dom[a];
+      ++E;
+    }
+    row_ptr[j + 1] = (uint32_t)E;
+  }
+  ret = (int64_t)E;
+fail:
+  free(blk_of); free(pred_ptr); free(pred); free(fill);
+  free(g.x); free(g.P); free(g.dist); free(g.lng); free(g.rpo_pos); free(g.hslot); free(g.term);
+  free(g.hkey_x); free(g.hkey_p); free(g.hval);
+  free(queue); free(stack); free(sidx); free(rpo); free(mark); free(cands);
+  free(acc_def); free(acc_min); free(acc_max); free(acc_dom); free(acc_kind); free(acc_last);
+  return ret;
+}

@@ -99,6 +99,26 @@ int or_estimate_all(const or_program *p, const uint64_t *C, const uint8_t *cand,
                     const uint8_t *self_flags, const double *share,
                     const or_pattern *pats, uint32_t n_pat, or_estimate *out);
 
+/* ---- backward slicing: the def-use CSR from SASS fields
+ * (Table 1: wait mask, write / read barrier, predicate, destination and source
+ * operands) and the CFG; DESIGN.md §3.2 Q35-Q39 state the readings. */
+typedef struct {
+  uint32_t n_instr, n_funcs, n_blocks;
+  const uint32_t *func_begin;   /* [n_funcs+1] */
+  const uint32_t *block_begin;  /* [n_blocks+1] contiguous instruction ranges inside functions */
+  const uint32_t *succ_ptr;     /* [n_blocks+1] */
+  const uint32_t *succ;         /* successor blocks, same function */
+  const uint8_t  *guard;        /* [n_instr] bits 0-2 predicate register P0..P6, 7 = none ('_'); bit 3 = negated */
+  const uint16_t *dst, *src;    /* [n_instr][4]: 0..254 R0..R254, 255 RZ (ignored), 256..262 P0..P6, 0xFFFF none */
+  const uint8_t  *wbar, *rbar, *wait;   /* [n_instr] barrier masks over B0..B5 */
+} or_sass;
+
+/* Def-use CSR keyed by the use (one edge per (def, use), defs ascending), as gpa_program_desc
+ * takes it: kind bits REG 1, PRED 2, BAR 4, WAR 8; min_len / max_len; dom_k (rule 2) or -1.
+ * cap = capacity of the edge arrays; returns the edge count, or -1 if cap is too small. */
+int64_t or_slice(const or_sass *s, uint64_t cap, uint32_t *row_ptr, uint32_t *edge_def, uint8_t *edge_kind,
+                 uint32_t *edge_min, uint32_t *edge_max, int32_t *edge_dom);
+
 /* ---- occupancy model feeding W, W_new of the parallel estimator
  * for Block Increase and Thread Increase; DESIGN.md §3.2 Q34. */
 typedef struct {

@@ -141,6 +141,9 @@ cudaError_t launch_rollup(const DevProgram &p, const RollupPlan &rp, int n_sms, 
 cudaError_t launch_estimate(const DevProgram &p, const EstimatePlan &ep, int n_sms,
                             cudaStream_t s, uint64_t *launches);
 cudaError_t launch_vrows(const DevProgram &p, double *vbuf, int n_sms, cudaStream_t s);
+cudaError_t launch_slice(const gpa_sass_desc *h, uint32_t *h_row_ptr, uint64_t cap_edges, uint32_t *h_def,
+                         uint8_t *h_kind, uint32_t *h_min, uint32_t *h_max, int32_t *h_dom, uint64_t *n_edges,
+                         int n_sms, cudaStream_t st, int *status);
 cudaError_t launch_advice(const DevProgram &p, const EstimatePlan &ep, const AdvicePlan &ap, cudaStream_t s,
                           uint64_t *launches);
 cudaError_t launch_ingest_segments(const DevProgram &p, const void *records, uint64_t n, const uint64_t *seg_begin,

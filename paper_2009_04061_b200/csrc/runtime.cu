@@ -787,6 +787,55 @@ gpa_status gpa_analyze(gpa_program *p, void *stream) {
   return GPA_OK;
 }
 
+gpa_status gpa_slice(const gpa_sass_desc *h, uint64_t cap_edges, uint32_t *h_row_ptr, uint32_t *h_def, uint8_t *h_kind,
+                     uint32_t *h_min, uint32_t *h_max, int32_t *h_dom, uint64_t *n_edges, void *stream) {
+  if (!h || !h_row_ptr || !n_edges || !h->func_begin || !h->block_begin || !h->succ_ptr || !h->guard || !h->dst ||
+      !h->src || !h->wbar || !h->rbar || !h->wait || (h->succ_ptr && h->n_blocks && h->succ_ptr[h->n_blocks] && !h->succ))
+    return fail(GPA_ERR_INVALID_ARGUMENT, "NULL SASS array or output");
+  if (cap_edges && (!h_def || !h_kind || !h_min || !h_max || !h_dom))
+    return fail(GPA_ERR_INVALID_ARGUMENT, "NULL edge output array");
+  const uint32_t n = h->n_instr, NB = h->n_blocks, NF = h->n_funcs;
+  if (n == 0 || NB == 0 || NF == 0) return fail(GPA_ERR_INVALID_PROGRAM, "empty SASS program");
+  if (h->block_begin[0] != 0 || h->block_begin[NB] != n || h->func_begin[0] != 0 || h->func_begin[NF] != n)
+    return fail(GPA_ERR_INVALID_PROGRAM, "block / function ranges must cover [0, n_instr)");
+  std::vector<uint32_t> bfunc(NB);
+  for (uint32_t b = 0, f = 0; b < NB; ++b) {
+    if (h->block_begin[b + 1] <= h->block_begin[b]) return fail(GPA_ERR_INVALID_PROGRAM, "empty or unordered block %u", b);
+    while (f < NF && h->func_begin[f + 1] <= h->block_begin[b]) ++f;
+    if (f >= NF || h->block_begin[b + 1] > h->func_begin[f + 1]) return fail(GPA_ERR_INVALID_PROGRAM, "block %u crosses a function", b);
+    bfunc[b] = f;
+  }
+  for (uint32_t f = 0; f < NF; ++f)
+    if (h->func_begin[f + 1] <= h->func_begin[f]) return fail(GPA_ERR_INVALID_PROGRAM, "empty function %u", f);
+  if (h->succ_ptr[0] != 0) return fail(GPA_ERR_INVALID_PROGRAM, "succ_ptr[0] != 0");
+  for (uint32_t b = 0; b < NB; ++b) {
+    if (h->succ_ptr[b + 1] < h->succ_ptr[b]) return fail(GPA_ERR_INVALID_PROGRAM, "succ_ptr not monotone");
+    for (uint32_t e = h->succ_ptr[b]; e < h->succ_ptr[b + 1]; ++e)
+      if (h->succ[e] >= NB || bfunc[h->succ[e]] != bfunc[b])
+        return fail(GPA_ERR_INVALID_PROGRAM, "block %u: successor outside its function", b);
+  }
+  for (uint32_t i = 0; i < n; ++i) {
+    if (h->guard[i] > 15 || h->wbar[i] > 63 || h->rbar[i] > 63 || h->wait[i] > 63)
+      return fail(GPA_ERR_INVALID_PROGRAM, "instruction %u: guard / barrier field out of range", i);
+    for (int t = 0; t < 4; ++t) {
+      const uint16_t d = h->dst[4u * i + t], sr = h->src[4u * i + t];
+      if ((d != 0xFFFF && d > 262) || (sr != 0xFFFF && sr > 262) || (d > 255 && d < 256) || (sr > 255 && sr < 256))
+        return fail(GPA_ERR_INVALID_PROGRAM, "instruction %u: operand out of range", i);
+    }
+  }
+  int dev = 0, n_sms = 148;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev));
+  int status = 0;
+  cudaError_t e = launch_slice(h, h_row_ptr, cap_edges, h_def, h_kind, h_min, h_max, h_dom, n_edges, n_sms,
+                               (cudaStream_t)stream, &status);
+  if (e != cudaSuccess) return cuda_fail(e, "slice");
+  if (status == 1) return fail(GPA_ERR_OVERFLOW, "slicing: a search exceeded its state budget");
+  if (status == 2) return fail(GPA_ERR_OVERFLOW, "slicing: %llu edges > cap_edges %llu", (unsigned long long)*n_edges,
+                               (unsigned long long)cap_edges);
+  return GPA_OK;
+}
+
 // Occupancy of every kernel (DESIGN.md §3.2 Q34): the usual calculator -- blocks per SM are the
 // tightest of the warp, block-slot, register (allocation-unit rounded) and shared-memory limits.
 gpa_status gpa_set_launches(gpa_program *p, const gpa_launch *h_launch, const gpa_arch *arch, void *stream) {

@@ -1,0 +1,411 @@
+// slice.cu -- the step before the path: backward slicing of SASS fields into
+// the def-use CSR that gpa_program_create takes (readings DESIGN.md §3.2 Q35-Q39).
+//
+// One thread per use instruction j (grid-stride), independent of all others: for every register j
+// reads (source operands, its guard predicate, the virtual barrier registers of its wait mask) it
+// explores the backward state graph of j's function -- states (instruction x about to be examined,
+// P = predicates of the defs of the register passed so far) -- breadth first (shortest path
+// lengths), orders it depth first (longest path lengths over the edges that go forward in the
+// reverse postorder), and tests rule 2 by re-running the breadth-first search with each
+// unpredicated reader blocked.  Each thread owns a slice of a scratch buffer (state arrays and an
+// open-addressing index), so the work is an irregular per-thread graph walk with no
+// communication.  Two launches: edge counts per use, then (after a host prefix sum) the edges.
+#include <algorithm>
+#include <vector>
+
+#include "gpa_internal.cuh"
+
+namespace gpa {
+namespace {
+
+constexpr uint32_t kSlNone = 0xFFFFu;
+constexpr uint32_t kSlAll = 0x4000u;   // the '_' predicate
+constexpr uint32_t kSlEmpty = 0xFFFFFFFFu;
+constexpr uint32_t kSlMaxKids = 64;
+constexpr uint32_t kSlThreads = 64;
+
+struct SliceIn {
+  uint32_t n, n_blocks;
+  const uint32_t *block_begin, *blk_of, *pred_ptr, *pred;
+  const uint8_t *guard, *wbar, *rbar, *wait;
+  const uint16_t *dst, *src;
+};
+
+struct SliceScratch {   // per-thread views into the scratch buffer
+  uint32_t *x, *P, *dist, *lng, *rpo_pos, *hslot, *queue, *stack, *sidx, *rpo, *mark, *cands;
+  uint32_t *hx, *hp, *hv;
+  uint8_t *term;
+  uint32_t cap, hcap, n;
+};
+
+__device__ __forceinline__ uint32_t pbit(uint8_t g) {
+  const uint32_t r = g & 7u;
+  if (r == 7u) return kSlAll;
+  return (g & 8u) ? (1u << (7u + r)) : (1u << r);
+}
+__device__ __forceinline__ uint32_t pnorm(uint32_t P) {
+  for (uint32_t i = 0; i < 7; ++i)
+    if (((P >> i) & 1u) && ((P >> (7 + i)) & 1u)) P |= kSlAll;
+  return P;
+}
+__device__ __forceinline__ bool pcontains(uint32_t P, uint32_t b) { return (P & kSlAll) || (P & b); }
+
+__device__ int reads_of(const SliceIn &s, uint32_t x, uint32_t *out, uint8_t *kinds) {
+  int n = 0;
+  for (int t = 0; t < 4; ++t) {
+    const uint32_t r = s.src[4u * x + t];
+    if (r == kSlNone || r == 255u) continue;
+    out[n] = r;
+    kinds[n] = r >= 256u ? 2u : 1u;
+    ++n;
+  }
+  if ((s.guard[x] & 7u) != 7u) { out[n] = 256u + (s.guard[x] & 7u); kinds[n] = 2u; ++n; }
+  for (int t = 0; t < 6; ++t)
+    if ((s.wait[x] >> t) & 1u) { out[n] = 512u + t; kinds[n] = 4u; ++n; }
+  return n;
+}
+__device__ __forceinline__ bool defines(const SliceIn &s, uint32_t x, uint32_t r) {
+  if (r >= 512u) return (((s.wbar[x] | s.rbar[x]) >> (r - 512u)) & 1u) != 0;
+  for (int t = 0; t < 4; ++t)
+    if (s.dst[4u * x + t] == r) return true;
+  return false;
+}
+__device__ bool reads_reg(const SliceIn &s, uint32_t x, uint32_t r) {
+  uint32_t rr[16];
+  uint8_t kk[16];
+  const int n = reads_of(s, x, rr, kk);
+  for (int t = 0; t < n; ++t)
+    if (rr[t] == r) return true;
+  return false;
+}
+__device__ int prev_of(const SliceIn &s, uint32_t x, uint32_t *out) {
+  const uint32_t b = s.blk_of[x];
+  if (x > s.block_begin[b]) { out[0] = x - 1; return 1; }
+  int n = 0;
+  for (uint32_t e = s.pred_ptr[b]; e < s.pred_ptr[b + 1] && n < (int)kSlMaxKids; ++e) out[n++] = s.block_begin[s.pred[e] + 1] - 1;
+  return n;
+}
+__device__ __forceinline__ uint32_t out_mask(const SliceIn &s, uint32_t x, uint32_t P, uint32_t r, uint32_t pj, bool &term) {
+  const bool d = defines(s, x, r);
+  if (d) P = pnorm(P | pbit(s.guard[x]));
+  term = d && pcontains(P, pj);
+  return P;
+}
+__device__ __forceinline__ uint32_t hhash(const SliceScratch &g, uint32_t x, uint32_t P) {
+  return (x * 2654435761u ^ (P + 1u) * 40503u) & (g.hcap - 1u);
+}
+__device__ uint32_t hfind(const SliceScratch &g, uint32_t x, uint32_t P) {
+  uint32_t h = hhash(g, x, P);
+  while (g.hv[h] != kSlEmpty) {
+    if (g.hx[h] == x && g.hp[h] == P) return g.hv[h];
+    h = (h + 1u) & (g.hcap - 1u);
+  }
+  return kSlEmpty;
+}
+__device__ uint32_t hinsert(SliceScratch &g, uint32_t x, uint32_t P) {
+  uint32_t h = hhash(g, x, P);
+  while (g.hv[h] != kSlEmpty) {
+    if (g.hx[h] == x && g.hp[h] == P) return g.hv[h];
+    h = (h + 1u) & (g.hcap - 1u);
+  }
+  g.hx[h] = x; g.hp[h] = P; g.hv[h] = g.n;
+  g.x[g.n] = x; g.P[g.n] = P; g.hslot[g.n] = h;
+  return g.n++;
+}
+
+struct RowAcc {
+  uint32_t def, mn, mx, last;
+  int32_t dom;
+  uint8_t kind;
+};
+
+// the edges of use j, defs ascending, into out[] (when non-null); returns the count, or -1 when
+// the per-search state budget or the row capacity is exceeded
+__device__ int slice_row(const SliceIn &s, SliceScratch &g, RowAcc *acc, uint32_t acc_cap, uint32_t j,
+                         uint32_t *o_def, uint8_t *o_kind, uint32_t *o_min, uint32_t *o_max, int32_t *o_dom) {
+  uint32_t reads[16];
+  uint8_t kinds[16];
+  const int nr = reads_of(s, j, reads, kinds);
+  const uint32_t pj = pbit(s.guard[j]);
+  uint32_t n_acc = 0;
+  uint32_t roots[kSlMaxKids], kids[kSlMaxKids];
+  for (int ri = 0; ri < nr; ++ri) {
+    const uint32_t r = reads[ri];
+    bool term;
+    // ---- breadth first from the root at j
+    for (uint32_t i = 0; i < g.n; ++i) g.hv[g.hslot[i]] = kSlEmpty;
+    g.n = 0;
+    uint32_t head = 0, tail = 0;
+    const int nroot = prev_of(s, j, roots);
+    for (int q = 0; q < nroot; ++q)
+      if (hfind(g, roots[q], 0u) == kSlEmpty) {
+        const uint32_t id = hinsert(g, roots[q], 0u);
+        g.dist[id] = 1u;
+        g.queue[tail++] = id;
+      }
+    while (head < tail) {
+      const uint32_t u = g.queue[head++];
+      const uint32_t Pout = out_mask(s, g.x[u], g.P[u], r, pj, term);
+      g.term[u] = term;
+      if (term) continue;
+      const int nk = prev_of(s, g.x[u], kids);
+      for (int q = 0; q < nk; ++q)
+        if (hfind(g, kids[q], Pout) == kSlEmpty) {
+          if (g.n + 1u >= g.cap) return -1;
+          const uint32_t v = hinsert(g, kids[q], Pout);
+          g.dist[v] = g.dist[u] + 1u;
+          g.queue[tail++] = v;
+        }
+    }
+    // ---- depth first (same successor order): reverse postorder; longest paths forward in it
+    for (uint32_t i = 0; i < g.n; ++i) { g.mark[i] = 0; g.lng[i] = 0; }
+    uint32_t cnt = 0;
+    for (int q = 0; q < nroot; ++q) {
+      const uint32_t c = hfind(g, roots[q], 0u);
+      if (g.mark[c]) continue;
+      g.mark[c] = 1; g.stack[0] = c; g.sidx[0] = 0;
+      uint32_t sp = 1;
+      while (sp) {
+        const uint32_t u = g.stack[sp - 1];
+        if (!g.term[u]) {
+          const uint32_t Pout = out_mask(s, g.x[u], g.P[u], r, pj, term);
+          const int nk = prev_of(s, g.x[u], kids);
+          if ((int)g.sidx[sp - 1] < nk) {
+            const uint32_t v = hfind(g, kids[g.sidx[sp - 1]++], Pout);
+            if (!g.mark[v]) { g.mark[v] = 1; g.stack[sp] = v; g.sidx[sp] = 0; ++sp; }
+            continue;
+          }
+        }
+        g.rpo[cnt++] = u;
+        --sp;
+      }
+    }
+    for (uint32_t i = 0; i < cnt; ++i) g.rpo_pos[g.rpo[i]] = cnt - 1 - i;
+    for (int q = 0; q < nroot; ++q) g.lng[hfind(g, roots[q], 0u)] = 1u;
+    for (uint32_t i = cnt; i-- > 0;) {
+      const uint32_t u = g.rpo[i];
+      if (g.term[u]) continue;
+      const uint32_t Pout = out_mask(s, g.x[u], g.P[u], r, pj, term);
+      const int nk = prev_of(s, g.x[u], kids);
+      for (int q = 0; q < nk; ++q) {
+        const uint32_t v = hfind(g, kids[q], Pout);
+        if (g.rpo_pos[v] > g.rpo_pos[u] && g.lng[u] + 1u > g.lng[v]) g.lng[v] = g.lng[u] + 1u;
+      }
+    }
+    // ---- rule-2 candidates: unpredicated readers of r met by the search, ascending
+    uint32_t n_cand = 0;
+    for (uint32_t i = 0; i < g.n; ++i) {
+      const uint32_t k = g.x[i];
+      if (k == j || (s.guard[k] & 7u) != 7u || !reads_reg(s, k, r)) continue;
+      uint32_t a = 0;
+      while (a < n_cand && g.cands[a] != k) ++a;
+      if (a == n_cand) g.cands[n_cand++] = k;
+    }
+    for (uint32_t a = 1; a < n_cand; ++a)
+      for (uint32_t b = a; b > 0 && g.cands[b - 1] > g.cands[b]; --b) {
+        const uint32_t t = g.cands[b]; g.cands[b] = g.cands[b - 1]; g.cands[b - 1] = t;
+      }
+    // ---- the defs this read found
+    for (uint32_t i = 0; i < g.n; ++i) {
+      const uint32_t x = g.x[i];
+      if (!defines(s, x, r)) continue;
+      uint32_t a = 0;
+      while (a < n_acc && acc[a].def != x) ++a;
+      uint8_t kind = kinds[ri];
+      if (r >= 512u && ((s.rbar[x] >> (r - 512u)) & 1u)) {   // WAR
+        for (int tt = 0; tt < 4; ++tt)
+          for (int uu = 0; uu < 4; ++uu) {
+            const uint16_t d = s.dst[4u * j + tt];
+            if (d != kSlNone && d != 255u && d == s.src[4u * x + uu]) kind |= 8u;
+          }
+      }
+      if (a == n_acc) {
+        if (n_acc >= acc_cap) return -1;
+        acc[a] = RowAcc{x, 0xFFFFFFFFu, 0u, 0u, -2, 0};
+        ++n_acc;
+      }
+      acc[a].kind |= kind;
+      acc[a].mn = min(acc[a].mn, g.dist[i]);
+      acc[a].mx = max(acc[a].mx, g.lng[i]);
+      if (acc[a].last == (uint32_t)ri + 1u) continue;
+      acc[a].last = (uint32_t)ri + 1u;
+      int32_t dom = -1;
+      for (uint32_t c = 0; c < n_cand && dom < 0; ++c) {
+        const uint32_t k = g.cands[c];
+        if (k == x) continue;
+        for (uint32_t st = 0; st < g.n; ++st) g.mark[st] = 0;
+        uint32_t h2 = 0, t2 = 0;
+        bool reach = false;
+        for (int q = 0; q < nroot; ++q) {
+          const uint32_t cc = hfind(g, roots[q], 0u);
+          if (g.x[cc] != k && !g.mark[cc]) { g.mark[cc] = 1; g.queue[t2++] = cc; }
+        }
+        while (h2 < t2 && !reach) {
+          const uint32_t u = g.queue[h2++];
+          if (g.x[u] == x) { reach = true; break; }
+          if (g.term[u]) continue;
+          const uint32_t Pout = out_mask(s, g.x[u], g.P[u], r, pj, term);
+          const int nk = prev_of(s, g.x[u], kids);
+          for (int q = 0; q < nk; ++q) {
+            const uint32_t v = hfind(g, kids[q], Pout);
+            if (g.x[v] != k && !g.mark[v]) { g.mark[v] = 1; g.queue[t2++] = v; }
+          }
+        }
+        if (!reach) dom = (int32_t)k;
+      }
+      if (acc[a].dom == -2) acc[a].dom = dom;
+      else if (acc[a].dom != dom) acc[a].dom = -1;
+    }
+  }
+  for (uint32_t a = 1; a < n_acc; ++a)
+    for (uint32_t b = a; b > 0 && acc[b - 1].def > acc[b].def; --b) {
+      const RowAcc t = acc[b]; acc[b] = acc[b - 1]; acc[b - 1] = t;
+    }
+  if (o_def)
+    for (uint32_t a = 0; a < n_acc; ++a) {
+      o_def[a] = acc[a].def; o_kind[a] = acc[a].kind; o_min[a] = acc[a].mn; o_max[a] = acc[a].mx;
+      o_dom[a] = acc[a].dom < 0 ? -1 : acc[a].dom;
+    }
+  return (int)n_acc;
+}
+
+// pass 1 (row_ptr == nullptr): counts[j]; pass 2: edges at row_ptr[j]
+__global__ void __launch_bounds__(kSlThreads) k_slice(SliceIn s, uint8_t *scratch, size_t per_thread, uint32_t cap,
+                                                      uint32_t hcap, uint32_t *counts, const uint32_t *row_ptr,
+                                                      uint32_t *e_def, uint8_t *e_kind, uint32_t *e_min,
+                                                      uint32_t *e_max, int32_t *e_dom, int *error) {
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+  uint8_t *base = scratch + (size_t)tid * per_thread;
+  SliceScratch g;
+  uint32_t *w = reinterpret_cast<uint32_t *>(base);
+  g.cap = cap;
+  g.hcap = hcap;
+  g.x = w; w += cap; g.P = w; w += cap; g.dist = w; w += cap; g.lng = w; w += cap; g.rpo_pos = w; w += cap;
+  g.hslot = w; w += cap; g.queue = w; w += cap; g.stack = w; w += cap; g.sidx = w; w += cap; g.rpo = w; w += cap;
+  g.mark = w; w += cap; g.cands = w; w += cap;
+  g.hx = w; w += hcap; g.hp = w; w += hcap; g.hv = w; w += hcap;
+  RowAcc *acc = reinterpret_cast<RowAcc *>(w);
+  g.term = reinterpret_cast<uint8_t *>(acc + cap);
+  for (uint32_t h = 0; h < hcap; ++h) g.hv[h] = kSlEmpty;
+  g.n = 0;
+  for (uint32_t j = tid; j < s.n; j += gridDim.x * blockDim.x) {
+    int c;
+    if (!row_ptr) {
+      c = slice_row(s, g, acc, cap, j, nullptr, nullptr, nullptr, nullptr, nullptr);
+      if (c >= 0) counts[j] = (uint32_t)c;
+    } else {
+      const uint32_t o = row_ptr[j];
+      c = slice_row(s, g, acc, cap, j, e_def + o, e_kind + o, e_min + o, e_max + o, e_dom + o);
+      if (c >= 0 && (uint32_t)c != row_ptr[j + 1] - o) c = -1;
+    }
+    if (c < 0) atomicExch(error, 1);
+  }
+}
+
+}  // namespace
+
+size_t slice_scratch_per_thread(uint32_t cap, uint32_t hcap) {
+  return (size_t)cap * (12 * 4 + sizeof(RowAcc) + 1) + (size_t)hcap * 12 + 64;
+}
+
+cudaError_t launch_slice(const gpa_sass_desc *h, uint32_t *h_row_ptr, uint64_t cap_edges, uint32_t *h_def,
+                         uint8_t *h_kind, uint32_t *h_min, uint32_t *h_max, int32_t *h_dom, uint64_t *n_edges,
+                         int n_sms, cudaStream_t st, int *status) {
+  const uint32_t n = h->n_instr, NB = h->n_blocks;
+  *status = 0;
+  // host-side CFG helpers: block of each instruction, predecessor CSR (ascending source block)
+  std::vector<uint32_t> blk_of(std::max<uint32_t>(n, 1)), pred_ptr(NB + 1, 0), pred(std::max<uint32_t>(h->succ_ptr[NB], 1));
+  for (uint32_t b = 0; b < NB; ++b)
+    for (uint32_t j = h->block_begin[b]; j < h->block_begin[b + 1]; ++j) blk_of[j] = b;
+  for (uint32_t b = 0; b < NB; ++b)
+    for (uint32_t e = h->succ_ptr[b]; e < h->succ_ptr[b + 1]; ++e) pred_ptr[h->succ[e] + 1]++;
+  for (uint32_t b = 0; b < NB; ++b) pred_ptr[b + 1] += pred_ptr[b];
+  {
+    std::vector<uint32_t> fill(NB, 0);
+    for (uint32_t b = 0; b < NB; ++b)
+      for (uint32_t e = h->succ_ptr[b]; e < h->succ_ptr[b + 1]; ++e) {
+        const uint32_t t = h->succ[e];
+        pred[pred_ptr[t] + fill[t]++] = b;
+      }
+  }
+  uint32_t maxf = 1;
+  for (uint32_t f = 0; f < h->n_funcs; ++f) maxf = std::max(maxf, h->func_begin[f + 1] - h->func_begin[f]);
+  const uint32_t cap = 4u * maxf + 256u;   // states per search (Q39)
+  uint32_t hcap = 1;
+  while (hcap < 2u * cap) hcap <<= 1;
+  const size_t per_thread = (slice_scratch_per_thread(cap, hcap) + 255) & ~(size_t)255;
+  // device copies
+  auto up = [&](const void *src, size_t bytes, void **dst) -> cudaError_t {
+    cudaError_t e = cudaMallocAsync(dst, std::max<size_t>(bytes, 16), st);
+    if (e != cudaSuccess) return e;
+    return bytes ? cudaMemcpyAsync(*dst, src, bytes, cudaMemcpyHostToDevice, st) : cudaSuccess;
+  };
+  void *d_bb, *d_blk, *d_pp, *d_pr, *d_g, *d_wb, *d_rb, *d_wt, *d_dst, *d_src;
+  cudaError_t e;
+  if ((e = up(h->block_begin, (NB + 1) * 4, &d_bb))) return e;
+  if ((e = up(blk_of.data(), (size_t)n * 4, &d_blk))) return e;
+  if ((e = up(pred_ptr.data(), (NB + 1) * 4, &d_pp))) return e;
+  if ((e = up(pred.data(), (size_t)pred_ptr[NB] * 4, &d_pr))) return e;
+  if ((e = up(h->guard, n, &d_g))) return e;
+  if ((e = up(h->wbar, n, &d_wb))) return e;
+  if ((e = up(h->rbar, n, &d_rb))) return e;
+  if ((e = up(h->wait, n, &d_wt))) return e;
+  if ((e = up(h->dst, (size_t)n * 8, &d_dst))) return e;
+  if ((e = up(h->src, (size_t)n * 8, &d_src))) return e;
+  SliceIn s{n, NB, (const uint32_t *)d_bb, (const uint32_t *)d_blk, (const uint32_t *)d_pp, (const uint32_t *)d_pr,
+            (const uint8_t *)d_g, (const uint8_t *)d_wb, (const uint8_t *)d_rb, (const uint8_t *)d_wt,
+            (const uint16_t *)d_dst, (const uint16_t *)d_src};
+  // threads: enough for the GPU, bounded by a ~2 GB scratch
+  uint64_t threads = std::min<uint64_t>((uint64_t)std::max(n_sms, 1) * 8 * kSlThreads, ((uint64_t)n + kSlThreads - 1) / kSlThreads * kSlThreads);
+  threads = std::min<uint64_t>(threads, std::max<uint64_t>(kSlThreads, ((2ull << 30) / per_thread) / kSlThreads * kSlThreads));
+  threads = std::max<uint64_t>(threads, kSlThreads);
+  void *d_scr, *d_cnt, *d_rp, *d_err, *d_def, *d_kind, *d_min, *d_max, *d_dom;
+  if ((e = cudaMallocAsync(&d_scr, threads * per_thread, st))) return e;
+  if ((e = cudaMallocAsync(&d_cnt, (size_t)std::max<uint32_t>(n, 1) * 4, st))) return e;
+  if ((e = cudaMallocAsync(&d_err, 4, st))) return e;
+  if ((e = cudaMemsetAsync(d_err, 0, 4, st))) return e;
+  const uint32_t grid = (uint32_t)(threads / kSlThreads);
+  k_slice<<<grid, kSlThreads, 0, st>>>(s, (uint8_t *)d_scr, per_thread, cap, hcap, (uint32_t *)d_cnt, nullptr, nullptr,
+                                       nullptr, nullptr, nullptr, nullptr, (int *)d_err);
+  if ((e = cudaGetLastError())) return e;
+  std::vector<uint32_t> cnt(std::max<uint32_t>(n, 1));
+  int err = 0;
+  if ((e = cudaMemcpyAsync(cnt.data(), d_cnt, (size_t)n * 4, cudaMemcpyDeviceToHost, st))) return e;
+  if ((e = cudaMemcpyAsync(&err, d_err, 4, cudaMemcpyDeviceToHost, st))) return e;
+  if ((e = cudaStreamSynchronize(st))) return e;
+  uint64_t E = 0;
+  h_row_ptr[0] = 0;
+  for (uint32_t j = 0; j < n; ++j) {
+    E += cnt[j];
+    h_row_ptr[j + 1] = (uint32_t)E;
+  }
+  *n_edges = E;
+  if (err) *status = 1;                    // state budget exceeded
+  else if (E > cap_edges) *status = 2;     // caller's edge arrays too small
+  if (!*status && E) {
+    if ((e = up(h_row_ptr, ((size_t)n + 1) * 4, &d_rp))) return e;
+    if ((e = cudaMallocAsync(&d_def, E * 4, st))) return e;
+    if ((e = cudaMallocAsync(&d_kind, E, st))) return e;
+    if ((e = cudaMallocAsync(&d_min, E * 4, st))) return e;
+    if ((e = cudaMallocAsync(&d_max, E * 4, st))) return e;
+    if ((e = cudaMallocAsync(&d_dom, E * 4, st))) return e;
+    k_slice<<<grid, kSlThreads, 0, st>>>(s, (uint8_t *)d_scr, per_thread, cap, hcap, (uint32_t *)d_cnt,
+                                         (const uint32_t *)d_rp, (uint32_t *)d_def, (uint8_t *)d_kind, (uint32_t *)d_min,
+                                         (uint32_t *)d_max, (int32_t *)d_dom, (int *)d_err);
+    if ((e = cudaGetLastError())) return e;
+    if ((e = cudaMemcpyAsync(h_def, d_def, E * 4, cudaMemcpyDeviceToHost, st))) return e;
+    if ((e = cudaMemcpyAsync(h_kind, d_kind, E, cudaMemcpyDeviceToHost, st))) return e;
+    if ((e = cudaMemcpyAsync(h_min, d_min, E * 4, cudaMemcpyDeviceToHost, st))) return e;
+    if ((e = cudaMemcpyAsync(h_max, d_max, E * 4, cudaMemcpyDeviceToHost, st))) return e;
+    if ((e = cudaMemcpyAsync(h_dom, d_dom, E * 4, cudaMemcpyDeviceToHost, st))) return e;
+    if ((e = cudaMemcpyAsync(&err, d_err, 4, cudaMemcpyDeviceToHost, st))) return e;
+    if ((e = cudaStreamSynchronize(st))) return e;
+    if (err) *status = 1;
+    for (void *ptr : {d_rp, d_def, d_kind, d_min, d_max, d_dom}) cudaFreeAsync(ptr, st);
+  }
+  for (void *ptr : {d_bb, d_blk, d_pp, d_pr, d_g, d_wb, d_rb, d_wt, d_dst, d_src, d_scr, d_cnt, d_err})
+    cudaFreeAsync(ptr, st);
+  return cudaStreamSynchronize(st);
+}
+
+}  // namespace gpa

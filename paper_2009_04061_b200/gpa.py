@@ -61,6 +61,12 @@ class Coverage(ctypes.Structure):
     _fields_ = [("nodes", ctypes.c_uint64), ("single_before", ctypes.c_uint64), ("single_after", ctypes.c_uint64)]
 
 
+class SassDesc(ctypes.Structure):
+    _fields_ = [("n_instr", ctypes.c_uint32), ("n_funcs", ctypes.c_uint32), ("n_blocks", ctypes.c_uint32)] + [
+        (k, ctypes.c_void_p) for k in ("func_begin", "block_begin", "succ_ptr", "succ", "guard", "dst", "src",
+                                       "wbar", "rbar", "wait")]
+
+
 class Arch(ctypes.Structure):
     _fields_ = [(k, ctypes.c_uint32) for k in ("sm_count", "max_warps_per_sm", "max_blocks_per_sm", "regs_per_sm",
                                                "smem_per_sm", "schedulers_per_sm", "warp_size", "reg_alloc_unit")]
@@ -83,7 +89,7 @@ EXPORTS = ["gpa_validate_program", "gpa_workspace_size", "gpa_program_create", "
            "gpa_aggregate", "gpa_set_patterns", "gpa_estimate", "gpa_read_estimates", "gpa_get_stats",
            "gpa_view", "gpa_instr_vector", "gpa_program_info", "gpa_ingest_variant",
            "gpa_set_ingest_variant", "gpa_launch_count", "gpa_last_error", "gpa_version", "gpa_analyze",
-           "gpa_ingest_segments", "gpa_advise", "gpa_read_advice", "gpa_set_launches"]
+           "gpa_ingest_segments", "gpa_advise", "gpa_read_advice", "gpa_set_launches", "gpa_slice"]
 
 _lib = None
 
@@ -111,6 +117,7 @@ def lib():
             "gpa_ingest_segments": [vp, vp, u64, vp, vp, u32, u32, vp],
             "gpa_advise": [vp, u32, vp], "gpa_read_advice": [vp, vp, vp, vp, vp, vp],
             "gpa_set_launches": [vp, vp, vp, vp],
+            "gpa_slice": [vp, u64, vp, vp, vp, vp, vp, vp, vp, vp],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -120,6 +127,40 @@ def lib():
         L.gpa_version.restype = ctypes.c_char_p
         _lib = L
     return _lib
+
+
+def slice_sass(sass, stream=None):
+    """Backward slicing on the GPU (gpa_slice): SASS fields + CFG (an object with the gpa_sass_desc
+    arrays, e.g. gpagen.sass.Sass) -> dict of the def-use CSR (numpy): row_ptr, edge_def,
+    edge_kind, edge_min_len, edge_max_len, edge_dom_k."""
+    dt = {"func_begin": np.uint32, "block_begin": np.uint32, "succ_ptr": np.uint32, "succ": np.uint32,
+          "guard": np.uint8, "dst": np.uint16, "src": np.uint16, "wbar": np.uint8, "rbar": np.uint8, "wait": np.uint8}
+    a = {k: np.ascontiguousarray(getattr(sass, k), dtype=t) for k, t in dt.items()}
+    n = int(a["guard"].shape[0])
+    desc = SassDesc(n, int(a["func_begin"].shape[0] - 1), int(a["block_begin"].shape[0] - 1),
+                    *[a[k].ctypes.data for k in ("func_begin", "block_begin", "succ_ptr", "succ", "guard", "dst",
+                                                 "src", "wbar", "rbar", "wait")])
+    row_ptr = np.zeros(n + 1, np.uint32)
+    ne = ctypes.c_uint64(0)
+    cap = 0
+    out = None
+    for _ in range(2):   # the first call may only report the edge count
+        out = {"edge_def": np.zeros(max(cap, 1), np.uint32), "edge_kind": np.zeros(max(cap, 1), np.uint8),
+               "edge_min_len": np.zeros(max(cap, 1), np.uint32), "edge_max_len": np.zeros(max(cap, 1), np.uint32),
+               "edge_dom_k": np.zeros(max(cap, 1), np.int32)}
+        rc = lib().gpa_slice(ctypes.byref(desc), cap, row_ptr.ctypes.data,
+                             *[out[k].ctypes.data for k in ("edge_def", "edge_kind", "edge_min_len", "edge_max_len",
+                                                            "edge_dom_k")], ctypes.byref(ne),
+                             None if stream is None else ctypes.c_void_p(stream.cuda_stream))
+        if rc == 0:
+            break
+        if rc == -7 and ne.value > cap:
+            cap = int(ne.value)
+            continue
+        _check(rc, "gpa_slice")
+    res = {k: v[: ne.value].copy() for k, v in out.items()}
+    res["row_ptr"] = row_ptr
+    return res
 
 
 def _check(rc: int, what: str):

@@ -1,0 +1,62 @@
+"""Backward slicing on the GPU (gpa_slice) against the oracle: the def-use CSR
+(defs, kinds, path lengths, rule-2 interposers) bit-exact on the hand-derived fixture and on random
+SASS programs; then the whole path on a program whose graph came from the GPU slicer."""
+import numpy as np
+import pytest
+
+import oracle
+from gpagen import sass
+from gpagen import programs as gp
+from gpagen.streams import StreamSpec
+from tests._common import compare, run_gpu, run_oracle
+
+pytestmark = pytest.mark.gpu
+KEYS = ("row_ptr", "edge_def", "edge_kind", "edge_min_len", "edge_max_len", "edge_dom_k")
+
+
+@pytest.fixture(autouse=True)
+def _need_cuda(cuda_available):
+    if not cuda_available:
+        pytest.skip("no CUDA device")
+
+
+def _same(a, b):
+    for k in KEYS:
+        assert np.array_equal(a[k], b[k]), k
+
+
+def test_fixture_slicing_bit_exact():
+    from paper_2009_04061_b200 import slice_sass
+    S = sass.slice_fixture()
+    _same(slice_sass(S), oracle.slice_program(S))
+
+
+@pytest.mark.parametrize("n_funcs,seed", [(4, 11), (12, 12), (40, 13)])
+def test_random_sass_slicing_bit_exact(n_funcs, seed):
+    from paper_2009_04061_b200 import slice_sass
+    S = sass.random_sass(n_funcs, seed)
+    _same(slice_sass(S), oracle.slice_program(S))
+
+
+def test_path_on_gpu_sliced_program():
+    """SASS -> gpa_slice -> gpa_program_create -> ingest / blame / rollup / estimate, against the oracle
+    fed the oracle's own slicing of the same SASS (identical graphs, so identical programs)."""
+    from paper_2009_04061_b200 import slice_sass
+    S = sass.random_sass(8, 14)
+    csr = slice_sass(S)
+    n = S.n_instr
+    rows = [[] for _ in range(n)]
+    rp = csr["row_ptr"]
+    for j in range(n):
+        for e in range(rp[j], rp[j + 1]):
+            rows[j].append((int(csr["edge_def"][e]), int(csr["edge_kind"][e]), int(csr["edge_min_len"][e]),
+                            int(csr["edge_max_len"][e]), int(csr["edge_dom_k"][e])))
+    prog = gp._finalize(9, S.opclass, np.zeros(n, np.uint8), S.latency, np.arange(n), np.full(n, -1), [],
+                        S.func_begin, [0, len(S.func_begin) - 1], [16], rows, n_lines=n)
+    prog.pc_weight = np.ones(n)
+    prog.pc_profile = np.zeros(n, np.uint8)
+    recs = StreamSpec(prog, seed=15, count_max=3).host(0, 200_000)
+    o = run_oracle(prog, recs)
+    oc = oracle.slice_program(S)
+    assert np.array_equal(oc["edge_def"], prog.edge_def) and np.array_equal(oc["edge_max_len"], prog.edge_max_len)
+    compare(run_gpu(prog, recs), o, rel=1e-9)
