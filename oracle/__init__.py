@@ -90,6 +90,8 @@ def lib():
         L.or_occupancy.argtypes = [vp, vp, vp, ctypes.c_uint32, vp]
         L.or_slice.argtypes = [vp, ctypes.c_uint64, vp, vp, vp, vp, vp, vp]
         L.or_slice.restype = ctypes.c_int64
+        L.or_simulate.argtypes = [vp, vp, vp, ctypes.c_uint32, vp, ctypes.c_uint32, ctypes.c_uint64, vp, vp]
+        L.or_simulate.restype = ctypes.c_int64
         L.or_hotspots.argtypes = [vp, vp, vp, vp, vp, vp, ctypes.c_uint32, ctypes.c_uint32, vp, vp]
         L.or_rank.argtypes = [vp, ctypes.c_uint32, ctypes.c_uint32, vp]
         L.or_coverage.argtypes = [vp, vp, vp, vp]
@@ -279,3 +281,28 @@ def slice_program(sass):
     res = {k: v[:E].copy() for k, v in out.items()}
     res["row_ptr"] = row_ptr
     return res
+
+
+class SimCfg(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_uint32) for k in ("schedulers", "warps_per_scheduler", "period", "trip_count",
+                                               "rbar_latency", "max_cycles")] + [("seed", ctypes.c_uint64)]
+
+
+def simulate(sass, cfg, sm=0, func=0, cap=1 << 22):
+    """or_simulate: (records uint64 [n], truth int32 [n]) of SM `sm` running function `func`."""
+    dt = {"func_begin": np.uint32, "block_begin": np.uint32, "succ_ptr": np.uint32, "succ": np.uint32,
+          "guard": np.uint8, "dst": np.uint16, "src": np.uint16, "wbar": np.uint8, "rbar": np.uint8, "wait": np.uint8}
+    a = {k: np.ascontiguousarray(getattr(sass, k), dtype=t) for k, t in dt.items()}
+    n = int(a["guard"].shape[0])
+    st = _Sass(n, int(a["func_begin"].shape[0] - 1), int(a["block_begin"].shape[0] - 1),
+               *[a[k].ctypes.data for k in ("func_begin", "block_begin", "succ_ptr", "succ", "guard", "dst", "src",
+                                            "wbar", "rbar", "wait")])
+    cls = np.ascontiguousarray(sass.opclass, np.uint8)
+    lat = np.ascontiguousarray(sass.latency, np.uint32)
+    rec = np.zeros(cap, np.uint64)
+    truth = np.zeros(cap, np.int32)
+    m = lib().or_simulate(ctypes.byref(st), cls.ctypes.data, lat.ctypes.data, func, ctypes.byref(cfg), sm, cap,
+                          rec.ctypes.data, truth.ctypes.data)
+    if m < 0:
+        raise RuntimeError(f"or_simulate failed ({m})")
+    return rec[:m].copy(), truth[:m].copy()

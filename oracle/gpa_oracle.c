@@ -953,3 +953,178 @@ fail:
   free(acc_def); free(acc_min); free(acc_max); free(acc_dom); free(acc_kind); free(acc_last);
   return ret;
 }
+
+/* ---------------------------------------------------------------- sampling simulator (NEXT #3)
+ * each SM has warp schedulers with active warps; every sampling period the SM records
+ * a sample for one of its schedulers, cycling round-robin: an active sample if that scheduler is
+ * issuing, a latency sample otherwise, with the sampled warp's stall reason if any.  The model
+ * (SPEC's invented plumbing; Q40-Q44): in-order issue, one instruction per scheduler per cycle,
+ * loose round-robin among ready warps; a register is ready `latency` cycles after its producer
+ * issues, a write barrier clears `latency` cycles after, a read barrier `rbar_latency` after; a
+ * warp waits for its sources and the barriers of its wait mask.  Predicated-off instructions issue
+ * as no-ops.  Loops (self-loop blocks) run trip_count times; a two-way branch goes to successor
+ * (warp mod 2). */
+
+#define SIM_REGS 263u    /* R0-R254, RZ, P0-P6 */
+#define R_NOTSEL 7u
+
+static uint64_t sim_mix(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+typedef struct {
+  uint32_t pc, done, loop_count, last_pc;
+  int64_t last_issue;
+  int64_t ready[SIM_REGS];  int32_t prod[SIM_REGS];
+  int64_t bclear[6];        int32_t bprod[6];
+  uint32_t predv;           /* bit k = value of P_k */
+} sim_warp;
+
+static int sim_is_mem(uint8_t c) { return c == 0 || c == 1 || c == 3 || c == 4; }   /* GLOBAL LOCAL CONSTANT TEXTURE */
+
+/* blocking requirement of the warp's next instruction at cycle t: returns 1 if ready; else the
+ * reason (MEM / EXEC / SYNC) and the producing instruction via *why / *who */
+static int sim_ready(const or_sass *s, const uint8_t *opclass, const sim_warp *w, int64_t t, uint32_t *why, int32_t *who) {
+  const uint32_t j = w->pc;
+  int64_t worst = -1;
+  int32_t p = -1;
+  int t2, bar = 0;
+  uint32_t b;
+  for (b = 0; b < 6; ++b)
+    if ((s->wait[j] >> b & 1u) && w->bclear[b] > t && w->bclear[b] > worst) { worst = w->bclear[b]; p = w->bprod[b]; bar = 1; }
+  for (t2 = 0; t2 < 4; ++t2) {
+    const uint16_t r = s->src[4u * j + t2];
+    if (r == 0xFFFFu || r == 255u) continue;
+    if (w->ready[r] > t && w->ready[r] > worst) { worst = w->ready[r]; p = w->prod[r]; bar = 0; }
+  }
+  if ((s->guard[j] & 7u) != 7u) {
+    const uint32_t r = 256u + (s->guard[j] & 7u);
+    if (w->ready[r] > t && w->ready[r] > worst) { worst = w->ready[r]; p = w->prod[r]; bar = 0; }
+  }
+  (void)bar;
+  if (worst < 0) return 1;
+  *who = p;
+  *why = p < 0 ? R_EXEC : (opclass[p] == 9 ? R_SYNC : sim_is_mem(opclass[p]) ? R_MEM : R_EXEC);
+  return 0;
+}
+
+int64_t or_simulate(const or_sass *s, const uint8_t *opclass, const uint32_t *latency, uint32_t func,
+                    const or_simcfg *cfg, uint32_t sm, uint64_t cap, uint64_t *records, int32_t *truth) {
+  const uint32_t S = cfg->schedulers, WP = cfg->warps_per_scheduler, W = S * WP;
+  const uint32_t f0 = s->func_begin[func];
+  uint32_t *blk_of = (uint32_t *)malloc(4u * s->n_instr);
+  sim_warp *w = (sim_warp *)calloc(W, sizeof(sim_warp));
+  uint32_t *rr = (uint32_t *)calloc(S, 4), *srr = (uint32_t *)calloc(S, 4);
+  int32_t *issued = (int32_t *)malloc(4u * S);
+  uint32_t b, k, live = W;
+  uint64_t n_rec = 0;
+  int64_t c, ret = -2;
+  for (b = 0; b < s->n_blocks; ++b)
+    for (k = s->block_begin[b]; k < s->block_begin[b + 1]; ++k) blk_of[k] = b;
+  for (k = 0; k < W; ++k) {
+    uint32_t r, q;
+    w[k].pc = f0;
+    w[k].last_issue = -1;
+    for (r = 0; r < SIM_REGS; ++r) { w[k].ready[r] = 0; w[k].prod[r] = -1; }
+    for (r = 0; r < 6; ++r) { w[k].bclear[r] = 0; w[k].bprod[r] = -1; }
+    for (q = 0; q < 7; ++q)
+      w[k].predv |= (uint32_t)(sim_mix(cfg->seed ^ ((uint64_t)(sm * W + k) << 8) ^ q) & 1u) << q;
+  }
+  for (c = 0; live > 0; ++c) {
+    uint32_t sc;
+    if (c >= (int64_t)cfg->max_cycles) goto out;
+    /* ---- issue: per scheduler the first ready warp from its round-robin pointer */
+    for (sc = 0; sc < S; ++sc) {
+      uint32_t i;
+      issued[sc] = -1;
+      for (i = 0; i < WP; ++i) {
+        const uint32_t lw = (rr[sc] + i) % WP, wi = lw * S + sc;   /* warp wi belongs to scheduler wi % S */
+        sim_warp *x = &w[wi];
+        uint32_t why;
+        int32_t who;
+        if (x->done || x->last_issue == c || !sim_ready(s, opclass, x, c, &why, &who)) continue;
+        {
+          const uint32_t j = x->pc;
+          const uint32_t g = s->guard[j];
+          const int on = (g & 7u) == 7u || ((((x->predv >> (g & 7u)) & 1u) != 0) != ((g & 8u) != 0));
+          int t2;
+          if (on) {
+            for (t2 = 0; t2 < 4; ++t2) {
+              const uint16_t d = s->dst[4u * j + t2];
+              if (d == 0xFFFFu || d == 255u) continue;
+              x->ready[d] = c + latency[j];
+              x->prod[d] = (int32_t)j;
+            }
+            for (t2 = 0; t2 < 6; ++t2) {
+              if (s->wbar[j] >> t2 & 1u) { x->bclear[t2] = c + latency[j]; x->bprod[t2] = (int32_t)j; }
+              else if (s->rbar[j] >> t2 & 1u) { x->bclear[t2] = c + cfg->rbar_latency; x->bprod[t2] = (int32_t)j; }
+            }
+          }
+          x->last_issue = c;
+          x->last_pc = j;
+          issued[sc] = (int32_t)wi;
+          rr[sc] = (lw + 1u) % WP;
+          /* advance the pc: next instruction, or the next block by the control policy */
+          if (j + 1 < s->block_begin[blk_of[j] + 1]) {
+            x->pc = j + 1;
+          } else {
+            const uint32_t bb = blk_of[j], e0 = s->succ_ptr[bb], e1 = s->succ_ptr[bb + 1];
+            uint32_t e, self = 0, other = 0xFFFFFFFFu, n_other = 0, first_other = 0xFFFFFFFFu;
+            for (e = e0; e < e1; ++e) {
+              if (s->succ[e] == bb) self = 1;
+              else { if (first_other == 0xFFFFFFFFu) first_other = s->succ[e]; ++n_other; }
+            }
+            if (self && x->loop_count + 1 < cfg->trip_count) {
+              ++x->loop_count;
+              other = bb;
+            } else {
+              x->loop_count = 0;
+              if (n_other == 1 || (self && n_other >= 1)) other = first_other;
+              else if (n_other >= 2) {
+                uint32_t pick = wi % 2u, cnt = 0;
+                for (e = e0; e < e1; ++e)
+                  if (s->succ[e] != bb) { if (cnt == pick) { other = s->succ[e]; break; } ++cnt; }
+              }
+            }
+            if (other == 0xFFFFFFFFu) { x->done = 1; --live; }
+            else x->pc = s->block_begin[other];
+          }
+        }
+        break;
+      }
+    }
+    /* ---- sample at c = period, 2 period, ...: scheduler (c/period - 1) mod S, its warps in turn */
+    if (c > 0 && c % cfg->period == 0) {
+      const uint32_t sc2 = (uint32_t)((c / cfg->period - 1) % S);
+      uint32_t i;
+      for (i = 0; i < WP; ++i) {
+        const uint32_t lw = (srr[sc2] + i) % WP, wi = lw * S + sc2;
+        sim_warp *x = &w[wi];
+        uint32_t why = 0, pc, reason, cls;
+        int32_t who = -1;
+        if (x->done && issued[sc2] != (int32_t)wi) continue;
+        srr[sc2] = (lw + 1u) % WP;
+        cls = issued[sc2] >= 0 ? 0u : 1u;
+        if (issued[sc2] == (int32_t)wi) {          /* the issuing warp: its issued instruction */
+          pc = x->last_pc;
+          reason = R_NONE;
+        } else {
+          pc = x->pc;
+          reason = sim_ready(s, opclass, x, c, &why, &who) ? R_NOTSEL : why;
+        }
+        if (n_rec >= cap) { ret = -1; goto out; }
+        records[n_rec] = (uint64_t)pc | (1ull << 32) | ((uint64_t)reason << 48) | ((uint64_t)cls << 56);
+        truth[n_rec] = (reason == R_MEM || reason == R_EXEC || reason == R_SYNC) ? who : -1;
+        ++n_rec;
+        break;
+      }
+    }
+  }
+  ret = (int64_t)n_rec;
+out:
+  free(blk_of); free(w); free(rr); free(srr); free(issued);
+  return ret;
+}

@@ -119,6 +119,21 @@ typedef struct {
 int64_t or_slice(const or_sass *s, uint64_t cap, uint32_t *row_ptr, uint32_t *edge_def, uint8_t *edge_kind,
                  uint32_t *edge_min, uint32_t *edge_max, int32_t *edge_dom);
 
+/* ---- sampling simulator (P:119-142 PC sampling model, DESIGN.md §3.2
+ * Q40-Q44): one SM running warps of one SASS function with an in-order scoreboard, loose
+ * round-robin warp schedulers, and a sample every `period` cycles from the schedulers in turn. */
+typedef struct {
+  uint32_t schedulers, warps_per_scheduler, period, trip_count, rbar_latency, max_cycles;
+  uint64_t seed;          /* predicate values: P_k of warp w = bit 0 of mix(seed, w, k) */
+} or_simcfg;
+
+/* Simulate SM `sm` (its warps are sm*W .. sm*W+W-1 globally) running function `func`; writes up to
+ * cap records (8 bytes: pc | count 1 | reason | class) and truth[] (the instruction that produced
+ * the value a dependency-stalled sample waits for, else -1).  Returns the record count, -1 if cap is
+ * too small, -2 on a scheduling deadlock or max_cycles. */
+int64_t or_simulate(const or_sass *s, const uint8_t *opclass, const uint32_t *latency, uint32_t func,
+                    const or_simcfg *cfg, uint32_t sm, uint64_t cap, uint64_t *records, int32_t *truth);
+
 /* ---- occupancy model feeding W, W_new of the parallel estimator
  * for Block Increase and Thread Increase; DESIGN.md §3.2 Q34. */
 typedef struct {
