@@ -167,3 +167,52 @@ def random_sass(n_funcs: int, seed: int, func_len=(24, 160), n_regs: int = 24) -
         blocks[b][1] = len(instrs)
         funcs.append(len(instrs))
     return _build(instrs, [tuple(x) for x in blocks], succs, funcs)
+
+
+def single_source_sass(n: int, seed: int) -> Sass:
+    """Straight-line function where every instruction reads exactly one register, produced by one
+    of the previous 5 instructions (so each stall has a single true source): loads (GLOBAL, 400
+    cycles, a write barrier its consumers wait on), long (20-cycle) and short (4-6-cycle) arithmetic."""
+    rng = np.random.default_rng(seed)
+    instrs, n_loads = [], 0
+    for i in range(n):
+        ins = dict(dst=[i % 250])
+        if i > 0:
+            p = i - int(rng.integers(1, min(5, i) + 1))
+            ins["src"] = [p % 250]
+            if instrs[p].get("wbar"):
+                ins["wait"] = instrs[p]["wbar"]
+        u = rng.random()
+        if u < 0.25:
+            ins.update(wbar=1 << (n_loads % 6), cls=0, lat=400)
+            n_loads += 1
+        elif u < 0.4:
+            ins.update(cls=6, lat=20)
+        else:
+            ins.update(cls=5, lat=int(rng.integers(4, 7)))
+        instrs.append(ins)
+    return _build(instrs, [(0, n)], [[]])
+
+
+def program_from_sass(S: Sass, csr: dict, n_reasons: int = 9):
+    """A gpa Program (gpagen.programs.Program) for a sliced SASS program: lines = instructions,
+    one loop per self-loop block, the functions of S, one kernel."""
+    from .programs import _finalize
+    n = S.n_instr
+    loop_id = np.full(n, -1, np.int32)
+    n_loops = 0
+    for b in range(len(S.block_begin) - 1):
+        if b in set(int(x) for x in S.succ[S.succ_ptr[b]:S.succ_ptr[b + 1]]):
+            loop_id[S.block_begin[b]:S.block_begin[b + 1]] = n_loops
+            n_loops += 1
+    rows = [[] for _ in range(n)]
+    rp = csr["row_ptr"]
+    for j in range(n):
+        for e in range(rp[j], rp[j + 1]):
+            rows[j].append((int(csr["edge_def"][e]), int(csr["edge_kind"][e]), int(csr["edge_min_len"][e]),
+                            int(csr["edge_max_len"][e]), int(csr["edge_dom_k"][e])))
+    prog = _finalize(n_reasons, S.opclass, np.zeros(n, np.uint8), S.latency, np.arange(n), loop_id,
+                     [-1] * n_loops, S.func_begin, [0, len(S.func_begin) - 1], [16], rows, n_lines=n)
+    prog.pc_weight = np.ones(n)
+    prog.pc_profile = np.zeros(n, np.uint8)
+    return prog

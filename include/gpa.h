@@ -138,6 +138,16 @@ typedef struct {
   const uint8_t *wait;          /* [n_instr] wait mask over B0..B5 */
 } gpa_sass_desc;
 
+/* PC-sampling simulator (DESIGN.md §3.2 Q40-Q44). */
+typedef struct {
+  uint32_t schedulers, warps_per_scheduler;  /* warps of one simulated SM */
+  uint32_t period;                           /* a sample every `period` cycles, schedulers in turn */
+  uint32_t trip_count;                       /* iterations of every self-loop block */
+  uint32_t rbar_latency;                     /* cycles until a read barrier clears */
+  uint32_t max_cycles;                       /* per SM; exceeding it is an error */
+  uint64_t seed;                             /* predicate values per warp */
+} gpa_simcfg;
+
 /* Occupancy model (DESIGN.md §3.2 Q34): the GPU the profile came from and
  * each kernel's launch, for parallel_rule 3 / 4 of the parallel estimator (Eqs. 6-10). */
 typedef struct {
@@ -228,6 +238,16 @@ gpa_status gpa_read_advice(gpa_program *prog, gpa_hotspot *h_hotspots, uint32_t 
 gpa_status gpa_slice(const gpa_sass_desc *h_sass, uint64_t cap_edges, uint32_t *h_row_ptr, uint32_t *h_edge_def,
                      uint8_t *h_edge_kind, uint32_t *h_edge_min_len, uint32_t *h_edge_max_len,
                      int32_t *h_edge_dom_k, uint64_t *n_edges, void *stream);
+
+/* Simulate n_sm SMs (one GPU thread each) running function `func` of a SASS program and write each
+ * SM's PC samples to DEVICE d_records + sm * cap_per_sm (gpa_sample: pc within the program, count
+ * 1, reason, class) and, if d_truth is not NULL, the ground truth (the instruction whose result a
+ * dependency-stalled sample waits for, else -1) at the same positions.  h_counts[sm] receives the
+ * SM's record count.  h_opclass / h_latency: HOST [n_instr].  GPA_ERR_OVERFLOW if an SM exceeds
+ * cap_per_sm records or cfg.max_cycles.  Synchronizes. */
+gpa_status gpa_simulate(const gpa_sass_desc *h_sass, const uint8_t *h_opclass, const uint32_t *h_latency,
+                        uint32_t func, const gpa_simcfg *cfg, uint32_t n_sm, uint64_t cap_per_sm,
+                        gpa_sample *d_records, int32_t *d_truth, uint64_t *h_counts, void *stream);
 
 /* Set the kernels' launch statistics (HOST array [n_kernels]; with the program's
  * kernel_grid_blocks) and the GPU's limits; computes, per kernel, the resident warps per

@@ -3,8 +3,8 @@
 PC-sample histogram -> stall blame over a pruned def-use graph -> rollup -> speedup estimates,
 as hand-written sm_100a CUDA behind the C ABI in include/gpa.h.  See DESIGN.md.
 """
-from .gpa import (GpaError, Program, Pattern, EstimateOut, VIEW, VARIANT, lib, validate, slice_sass,
+from .gpa import (GpaError, Program, Pattern, EstimateOut, VIEW, VARIANT, lib, validate, slice_sass, simulate_sass,
                   workspace_size, EXPORTS)
 
-__all__ = ["GpaError", "Program", "Pattern", "EstimateOut", "VIEW", "VARIANT", "lib", "validate", "slice_sass",
+__all__ = ["GpaError", "Program", "Pattern", "EstimateOut", "VIEW", "VARIANT", "lib", "validate", "slice_sass", "simulate_sass",
            "workspace_size", "EXPORTS"]

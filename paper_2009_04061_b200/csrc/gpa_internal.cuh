@@ -144,6 +144,9 @@ cudaError_t launch_vrows(const DevProgram &p, double *vbuf, int n_sms, cudaStrea
 cudaError_t launch_slice(const gpa_sass_desc *h, uint32_t *h_row_ptr, uint64_t cap_edges, uint32_t *h_def,
                          uint8_t *h_kind, uint32_t *h_min, uint32_t *h_max, int32_t *h_dom, uint64_t *n_edges,
                          int n_sms, cudaStream_t st, int *status);
+cudaError_t launch_simulate(const gpa_sass_desc *h, const uint8_t *h_cls, const uint32_t *h_lat, uint32_t func,
+                            const gpa_simcfg &cfg, uint32_t n_sm, uint64_t cap, gpa_sample *d_out, int32_t *d_truth,
+                            uint64_t *h_counts, cudaStream_t st);
 cudaError_t launch_advice(const DevProgram &p, const EstimatePlan &ep, const AdvicePlan &ap, cudaStream_t s,
                           uint64_t *launches);
 cudaError_t launch_ingest_segments(const DevProgram &p, const void *records, uint64_t n, const uint64_t *seg_begin,

@@ -787,13 +787,7 @@ gpa_status gpa_analyze(gpa_program *p, void *stream) {
   return GPA_OK;
 }
 
-gpa_status gpa_slice(const gpa_sass_desc *h, uint64_t cap_edges, uint32_t *h_row_ptr, uint32_t *h_def, uint8_t *h_kind,
-                     uint32_t *h_min, uint32_t *h_max, int32_t *h_dom, uint64_t *n_edges, void *stream) {
-  if (!h || !h_row_ptr || !n_edges || !h->func_begin || !h->block_begin || !h->succ_ptr || !h->guard || !h->dst ||
-      !h->src || !h->wbar || !h->rbar || !h->wait || (h->succ_ptr && h->n_blocks && h->succ_ptr[h->n_blocks] && !h->succ))
-    return fail(GPA_ERR_INVALID_ARGUMENT, "NULL SASS array or output");
-  if (cap_edges && (!h_def || !h_kind || !h_min || !h_max || !h_dom))
-    return fail(GPA_ERR_INVALID_ARGUMENT, "NULL edge output array");
+static gpa_status validate_sass(const gpa_sass_desc *h) {
   const uint32_t n = h->n_instr, NB = h->n_blocks, NF = h->n_funcs;
   if (n == 0 || NB == 0 || NF == 0) return fail(GPA_ERR_INVALID_PROGRAM, "empty SASS program");
   if (h->block_begin[0] != 0 || h->block_begin[NB] != n || h->func_begin[0] != 0 || h->func_begin[NF] != n)
@@ -823,6 +817,18 @@ gpa_status gpa_slice(const gpa_sass_desc *h, uint64_t cap_edges, uint32_t *h_row
         return fail(GPA_ERR_INVALID_PROGRAM, "instruction %u: operand out of range", i);
     }
   }
+  return GPA_OK;
+}
+
+gpa_status gpa_slice(const gpa_sass_desc *h, uint64_t cap_edges, uint32_t *h_row_ptr, uint32_t *h_def, uint8_t *h_kind,
+                     uint32_t *h_min, uint32_t *h_max, int32_t *h_dom, uint64_t *n_edges, void *stream) {
+  if (!h || !h_row_ptr || !n_edges || !h->func_begin || !h->block_begin || !h->succ_ptr || !h->guard || !h->dst ||
+      !h->src || !h->wbar || !h->rbar || !h->wait || (h->succ_ptr && h->n_blocks && h->succ_ptr[h->n_blocks] && !h->succ))
+    return fail(GPA_ERR_INVALID_ARGUMENT, "NULL SASS array or output");
+  if (cap_edges && (!h_def || !h_kind || !h_min || !h_max || !h_dom))
+    return fail(GPA_ERR_INVALID_ARGUMENT, "NULL edge output array");
+  gpa_status vst = validate_sass(h);
+  if (vst) return vst;
   int dev = 0, n_sms = 148;
   CUDA_TRY(cudaGetDevice(&dev));
   CUDA_TRY(cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, dev));
@@ -833,6 +839,27 @@ gpa_status gpa_slice(const gpa_sass_desc *h, uint64_t cap_edges, uint32_t *h_row
   if (status == 1) return fail(GPA_ERR_OVERFLOW, "slicing: a search exceeded its state budget");
   if (status == 2) return fail(GPA_ERR_OVERFLOW, "slicing: %llu edges > cap_edges %llu", (unsigned long long)*n_edges,
                                (unsigned long long)cap_edges);
+  return GPA_OK;
+}
+
+gpa_status gpa_simulate(const gpa_sass_desc *h, const uint8_t *h_cls, const uint32_t *h_lat, uint32_t func,
+                        const gpa_simcfg *cfg, uint32_t n_sm, uint64_t cap, gpa_sample *d_records, int32_t *d_truth,
+                        uint64_t *h_counts, void *stream) {
+  if (!h || !h_cls || !h_lat || !cfg || !d_records || !h_counts || !h->func_begin || !h->block_begin || !h->succ_ptr ||
+      !h->guard || !h->dst || !h->src || !h->wbar || !h->rbar || !h->wait)
+    return fail(GPA_ERR_INVALID_ARGUMENT, "NULL argument");
+  gpa_status vst = validate_sass(h);
+  if (vst) return vst;
+  if (func >= h->n_funcs) return fail(GPA_ERR_INVALID_ARGUMENT, "func %u >= n_funcs", func);
+  if (!cfg->schedulers || !cfg->warps_per_scheduler || !cfg->period || !cfg->trip_count || !n_sm || !cap)
+    return fail(GPA_ERR_INVALID_ARGUMENT, "schedulers, warps, period, trip_count, n_sm and cap must be > 0");
+  if ((uint64_t)cfg->schedulers * cfg->warps_per_scheduler > 64)
+    return fail(GPA_ERR_INVALID_ARGUMENT, "at most 64 warps per simulated SM");
+  cudaError_t e = launch_simulate(h, h_cls, h_lat, func, *cfg, n_sm, cap, d_records, d_truth, h_counts,
+                                  (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(e, "simulate");
+  for (uint32_t i = 0; i < n_sm; ++i)
+    if (h_counts[i] == ~0ull) return fail(GPA_ERR_OVERFLOW, "SM %u exceeded cap_per_sm or max_cycles", i);
   return GPA_OK;
 }
 

@@ -67,6 +67,11 @@ class SassDesc(ctypes.Structure):
                                        "wbar", "rbar", "wait")]
 
 
+class SimCfg(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_uint32) for k in ("schedulers", "warps_per_scheduler", "period", "trip_count",
+                                               "rbar_latency", "max_cycles")] + [("seed", ctypes.c_uint64)]
+
+
 class Arch(ctypes.Structure):
     _fields_ = [(k, ctypes.c_uint32) for k in ("sm_count", "max_warps_per_sm", "max_blocks_per_sm", "regs_per_sm",
                                                "smem_per_sm", "schedulers_per_sm", "warp_size", "reg_alloc_unit")]
@@ -89,7 +94,7 @@ EXPORTS = ["gpa_validate_program", "gpa_workspace_size", "gpa_program_create", "
            "gpa_aggregate", "gpa_set_patterns", "gpa_estimate", "gpa_read_estimates", "gpa_get_stats",
            "gpa_view", "gpa_instr_vector", "gpa_program_info", "gpa_ingest_variant",
            "gpa_set_ingest_variant", "gpa_launch_count", "gpa_last_error", "gpa_version", "gpa_analyze",
-           "gpa_ingest_segments", "gpa_advise", "gpa_read_advice", "gpa_set_launches", "gpa_slice"]
+           "gpa_ingest_segments", "gpa_advise", "gpa_read_advice", "gpa_set_launches", "gpa_slice", "gpa_simulate"]
 
 _lib = None
 
@@ -118,6 +123,7 @@ def lib():
             "gpa_advise": [vp, u32, vp], "gpa_read_advice": [vp, vp, vp, vp, vp, vp],
             "gpa_set_launches": [vp, vp, vp, vp],
             "gpa_slice": [vp, u64, vp, vp, vp, vp, vp, vp, vp, vp],
+            "gpa_simulate": [vp, vp, vp, u32, vp, u32, u64, vp, vp, vp, vp],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -161,6 +167,37 @@ def slice_sass(sass, stream=None):
     res = {k: v[: ne.value].copy() for k, v in out.items()}
     res["row_ptr"] = row_ptr
     return res
+
+
+def _sass_desc(sass):
+    dt = {"func_begin": np.uint32, "block_begin": np.uint32, "succ_ptr": np.uint32, "succ": np.uint32,
+          "guard": np.uint8, "dst": np.uint16, "src": np.uint16, "wbar": np.uint8, "rbar": np.uint8, "wait": np.uint8}
+    a = {k: np.ascontiguousarray(getattr(sass, k), dtype=t) for k, t in dt.items()}
+    n = int(a["guard"].shape[0])
+    desc = SassDesc(n, int(a["func_begin"].shape[0] - 1), int(a["block_begin"].shape[0] - 1),
+                    *[a[k].ctypes.data for k in ("func_begin", "block_begin", "succ_ptr", "succ", "guard", "dst",
+                                                 "src", "wbar", "rbar", "wait")])
+    return desc, a
+
+
+def simulate_sass(sass, n_sm, cap_per_sm, func=0, schedulers=4, warps_per_scheduler=4, period=4, trip_count=4,
+                  rbar_latency=2, max_cycles=10_000_000, seed=1, truth=True, stream=None):
+    """PC-sampling simulator on the GPU (gpa_simulate): n_sm simulated SMs running `func`.  Returns
+    (records: CUDA int64 tensor [n_sm * cap_per_sm], zero-filled past each SM's count -- a zero record
+    is a valid no-op sample of count 0 --, truth: CUDA int32 tensor or None, counts: numpy [n_sm])."""
+    import torch
+    desc, keep = _sass_desc(sass)
+    cls = np.ascontiguousarray(sass.opclass, np.uint8)
+    lat = np.ascontiguousarray(sass.latency, np.uint32)
+    cfg = SimCfg(schedulers, warps_per_scheduler, period, trip_count, rbar_latency, max_cycles, seed)
+    rec = torch.zeros(n_sm * cap_per_sm, dtype=torch.int64, device="cuda")
+    tr = torch.full((n_sm * cap_per_sm,), -1, dtype=torch.int32, device="cuda") if truth else None
+    counts = np.zeros(n_sm, np.uint64)
+    s = torch.cuda.current_stream() if stream is None else stream
+    _check(lib().gpa_simulate(ctypes.byref(desc), cls.ctypes.data, lat.ctypes.data, int(func), ctypes.byref(cfg),
+                              int(n_sm), int(cap_per_sm), rec.data_ptr(), tr.data_ptr() if truth else None,
+                              counts.ctypes.data, ctypes.c_void_p(s.cuda_stream)), "gpa_simulate")
+    return rec, tr, counts
 
 
 def _check(rc: int, what: str):
