@@ -18,6 +18,9 @@ constexpr int kChunk = 128;                 // rollup chunk length (instructions
 constexpr int kMaxIngestCtas = 256;         // per-CTA partial tables reserved (smem variant)
 constexpr size_t kSmemTableMax = 224 * 1024;// largest CTA-private table (bytes; sm_100a opt-in is 227 KB)
 // partitioned ingest (variant P): bucket exchange through L2
+// GPA_* macros below (and in ingest.cu / rollup.cu / estimate.cu / runtime.cu) are tuning knobs:
+// tools/variant_build.py builds alternative libraries with other values for A/B timing on the GPU
+// (tools/variant_time.py, tools/seg_time.py); the defaults are the measured best.
 #ifndef GPA_PART_THREADS
 #define GPA_PART_THREADS 1024
 #endif
@@ -33,7 +36,7 @@ constexpr int kPartBufs = GPA_PART_BUFS;    // exchange buffers in flight
 #ifndef GPA_PART_CAP
 #define GPA_PART_CAP 56
 #endif
-constexpr int kPartCap = GPA_PART_CAP;                // keys per (src, dst) slot per chunk (mean 38.1 at G=148);
+constexpr int kPartCap = GPA_PART_CAP;                // keys per (src, dst) slot per chunk (mean 43 at G=148);
                                             // excess -> L2 atomics
 constexpr int kPartMaxCtas = 160;           // < 255: bucket ids fit a byte
 size_t part_smem_bytes(uint32_t bpb, uint32_t G);
