@@ -248,6 +248,7 @@ constexpr uint32_t kLocalBits = 13;                // key = local bin (13 bits) 
 constexpr uint32_t kMaxKeyCount = 7;
 // a chunk adds at most G * cap * 7 samples to any one table entry: flushing the u32 table every
 // kFlushEvery chunks keeps every entry below 2^32
+constexpr uint32_t kBarProc = 2;   // named barrier of the processor warps (0 is __syncthreads)
 constexpr uint32_t kFlushEvery = (uint32_t)(0xffffffffull / ((uint64_t)kPartMaxCtas * kPartCap * kMaxKeyCount));
 static_assert(kPartChunk % (2 * kDecodeThreads) == 0, "whole record pairs per decode thread");
 static_assert((kPartCap * 2) % 16 == 0, "slots must be whole 16-byte units for bulk copies");
@@ -262,6 +263,7 @@ __device__ __forceinline__ void red_release_add(unsigned int *p, unsigned int v)
 __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
+
 
 // shared -> global bulk copy (async proxy), tracked by this thread's bulk async-groups
 // (evict-last: the exchange rows are read back by the consumers and the buffers are reused, so
@@ -311,7 +313,7 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
   uint64_t *inbox_free = inbox_full + kInbox;                                    // [kInbox]  consumers -> loader
   uint64_t *stored = inbox_free + kInbox;   // [kPartBufs] control -> publisher (control runs at most
                                             // kPartBufs-1 chunks ahead: see the cons-counter wait)
-  uint32_t *tab = reinterpret_cast<uint32_t *>(stored + kPartBufs);                // [bpb + kTrash]
+  uint32_t *tab = reinterpret_cast<uint32_t *>(stored + kPartBufs);              // [bpb + kTrash]
   for (uint32_t i = tid; i < a.bpb + kTrash; i += kPartThreads) tab[i] = 0;
   for (uint32_t i = tid; i < kStage * ibuf_keys / 2; i += kPartThreads) reinterpret_cast<uint32_t *>(stag)[i] = 0;
   for (uint32_t i = tid; i < kStage * (kPartMaxCtas + 8); i += kPartThreads) cnt[i] = 0;
@@ -364,7 +366,7 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
         const uint32_t pair = u * kDecodeThreads + dtid;   // len is even: both records of a pair or neither
         vv[u] = (full || 2 * pair < len) ? ld_stream(rs + pair) : make_uint4(0xffffffffu, 0, 0xffffffffu, 0);
       }
-      mbar_wait(&buf_ready[sb], (k / kStage) & 1);       // staging buffer + counters clean
+      mbar_wait(&buf_ready[sb], (k / kStage) & 1);
       PT_MARK(0);
       // ---- branch-free decode: bucket = pc mod G (interleaved PCs balance the load), key = local
       //      bin (pc / G) * 2R + class * R + reason | count << 13, stored at position cnt[b]++ of
@@ -372,43 +374,58 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
       //      and land in a trash word; counts > 7 and slot overflow go through L2 atomics)
       uint32_t csum = 0, bads = 0, badr = 0;
       // records are processed in batches of kDecodeBatch pairs: all slot allocations (atomics) of a
-      // batch are issued before its key stores, so their latencies overlap
+      // batch are issued before its key stores, so their latencies overlap.  Validity (Q12): t =
+      // flags:reason is valid iff t < R (ACT) or 0x101 <= t < 0x100 + R (LAT with a reason); then
+      // class * R + reason = t - (t >> 8) * (256 - R).  The rare cases -- invalid records, counts
+      // > 7, slot overflow -- share one branch.
 #pragma unroll
       for (int u0 = 0; u0 < kDecodeRecs / 2; u0 += kDecodeBatch) {
         constexpr int kB = 2 * kDecodeBatch;
-        uint32_t pos[kB], slot[kB], bin[kB], cnts[kB];
+        uint32_t pos[kB], slot[kB], pcs[kB], tls[kB], cnts[kB];
         unsigned short key[kB];
-        bool okk[kB];
 #pragma unroll
         for (int i = 0; i < kB; ++i) {
           const int u = u0 + i / 2, h = i & 1;
           if (u >= kDecodeRecs / 2) break;
-          const bool in = full || 2 * (u * kDecodeThreads + dtid) < len;
           const uint4 v = vv[u];
           const uint32_t pc = h ? v.z : v.x, w = h ? v.w : v.y;
-          const uint32_t t = w >> 16, reason = t & 0xffu, c = w & 0xffffu;
-          const bool ok = pc < n_instr && reason < R && t < 0x200u && t != 0x100u;
+          const uint32_t t = w >> 16, c = w & 0xffffu;
+          const uint32_t tl = t - (t >> 8) * (256u - R);
+          const bool ok = pc < n_instr && (t < R || t - 0x101u < R - 1u);
           const uint32_t q = __umulhi(pc, mg), b = pc - q * G;
-          const bool small = c <= kMaxKeyCount;
-          const uint32_t be = ok && small ? b : G;
-          key[i] = (unsigned short)((q * twoR + (t >> 8) * R + reason) | (c << kLocalBits));
-          bin[i] = pc * twoR + (t >> 8) * R + reason;
-          slot[i] = ok && small ? sg_addr + be * kPartCap * 2 : 0u;   // 0: never kept
-          okk[i] = ok;
+          const bool fast = ok && c <= kMaxKeyCount;
+          const uint32_t be = fast ? b : G;
+          key[i] = (unsigned short)((q * twoR + tl) | (c << kLocalBits));
+          slot[i] = fast ? sg_addr + be * (kPartCap * 2) : 0u;   // 0: never kept
+          pcs[i] = ok ? pc : 0xFFFFFFFFu;                        // invalid marker for the rare branch
+          tls[i] = tl;
           cnts[i] = c;
+#ifndef GPA_ABLATE_DEC_ATOM
           asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(pos[i]) : "r"(cnt_addr + be * 4) : "memory");
+#else
+          pos[i] = (dtid + i) % 40u + (cnt_addr == 0xFFFFFFFFu ? be : 0u);
+#endif
           csum += c;        // padding records have count 0
-          bads += ok ? 0u : c;
-          badr += (in && !ok) ? 1u : 0u;
         }
 #pragma unroll
         for (int i = 0; i < kB; ++i) {
-          if (u0 + i / 2 >= kDecodeRecs / 2) break;
+          const int u = u0 + i / 2;
+          if (u >= kDecodeRecs / 2) break;
           const bool keep = slot[i] != 0u && pos[i] < (uint32_t)kPartCap;
           const uint32_t dst = keep ? slot[i] + pos[i] * 2 : trash_addr;
+#ifndef GPA_ABLATE_DEC_STS
           asm volatile("st.shared.u16 [%0], %1;" ::"r"(dst), "h"(key[i]) : "memory");
-          if (okk[i] && !keep)   // count > 7 or slot overflow (skew): exact via L2 atomics
-            atomicAdd((unsigned long long *)&a.C[bin[i]], (unsigned long long)cnts[i]);
+#else
+          if (dst == 0xFFFFFFFFu) asm volatile("st.shared.u16 [%0], %1;" ::"r"(dst), "h"(key[i]) : "memory");
+#endif
+          if (!keep) {       // rare: an invalid record, a count > 7 or slot overflow (skew)
+            if (pcs[i] != 0xFFFFFFFFu) {
+              atomicAdd((unsigned long long *)&a.C[(uint64_t)pcs[i] * twoR + tls[i]], (unsigned long long)cnts[i]);
+            } else {
+              bads += cnts[i];
+              badr += (full || 2 * (u * kDecodeThreads + dtid) < len) ? 1u : 0u;   // padding is not a record
+            }
+          }
         }
       }
       st.valid += csum - bads;
@@ -424,8 +441,7 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
   } else if (warp == kCtrlWarp) {
     // ======================= control: one bulk store of the CTA's row per chunk, completed
     //                         stores handed to the publisher
-    if (lane == 0)
-      for (int r = 0; r < kStage; ++r) mbar_arrive(&buf_ready[r]);
+
     PT_DECL
     for (uint32_t k = 0; k < n_chunks; ++k) {
       const uint32_t sb = k % kStage, buf = k % kPartBufs;
@@ -457,6 +473,9 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
     // ======================= publisher: release each stored chunk to the other CTAs, then clear
     //                         its staging buffer and counters for chunk k+kStage
     PT_DECL
+    for (uint32_t r = 0; r < (uint32_t)kStage && r < n_chunks; ++r) {   // the staging buffers start clean
+      if (lane == 0) mbar_arrive(&buf_ready[r]);
+    }
     for (uint32_t k = 0; k < n_chunks; ++k) {
       PT_START;
       mbar_wait(&stored[k % kPartBufs], (k / kPartBufs) & 1);   // chunk k's store has completed
@@ -483,21 +502,33 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
     //                         chunk, as soon as every producer published it and the slot is free);
     //                         the other warps only wait on their data and add keys to the table
     if (warp == kLoaderWarp) {
-      if (lane == 0) {
-        PT_DECL
-        for (uint32_t j = 0; j < n_chunks; ++j) {
-          PT_START;
-          if (j >= (uint32_t)kInbox) mbar_wait(&inbox_free[j % kInbox], ((j / kInbox) + 1) & 1);
-          PT_MARK(12);
-          spin_until(&a.sync[j % kPartBufs], G * (j / kPartBufs + 1));
-          PT_MARK(13);
-          fence_proxy_async_global();
-          mbar_expect_tx(&inbox_full[j % kInbox], slot_keys * 2);
-          tma_tile_load_2d(inbox + (j % kInbox) * ibuf_keys, &xmap, me * kPartCap, (j % kPartBufs) * kPartMaxCtas,
-                           &inbox_full[j % kInbox]);
+      // loads run kInbox chunks ahead; the loader alone polls the TMA completion and releases the
+      // processor warps through a named barrier
+      auto load = [&](uint32_t j) {
+        spin_until(&a.sync[j % kPartBufs], G * (j / kPartBufs + 1));   // every producer published j
+        fence_proxy_async_global();
+        mbar_expect_tx(&inbox_full[j % kInbox], slot_keys * 2);
+        tma_tile_load_2d(inbox + (j % kInbox) * ibuf_keys, &xmap, me * kPartCap, (j % kPartBufs) * kPartMaxCtas,
+                         &inbox_full[j % kInbox]);
+      };
+      PT_DECL
+      if (lane == 0)
+        for (uint32_t j = 0; j < (uint32_t)kInbox && j < n_chunks; ++j) load(j);
+      for (uint32_t j = 0; j < n_chunks; ++j) {
+        PT_START;
+        if (lane == 0) mbar_wait(&inbox_full[j % kInbox], (j / kInbox) & 1);
+        __syncwarp();
+        PT_MARK(12);
+        if (j >= 1 && j - 1 + kInbox < n_chunks) {   // slot of chunk j-1 (processed already) -> chunk j-1+kInbox
+          if (lane == 0) {
+            mbar_wait(&inbox_free[(j - 1) % kInbox], ((j - 1) / kInbox) & 1);
+            load(j - 1 + kInbox);
+          }
+          __syncwarp();
         }
-        PT_FLUSH;
+        PT_MARK(13);
       }
+      PT_FLUSH;
     } else {
       const uint32_t ctid = tid - kProcBase;
       const uint32_t tab_addr = smem_addr(tab), dummy_addr = smem_addr(tab + a.bpb + (ctid & 31));
@@ -517,11 +548,15 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
             // padding keys (c = 0) add 0 to a lane-distinct dummy word: cheaper on the shared-memory
             // pipe than a predicated (branching) update, measured
             const uint32_t addr = c ? tab_addr + (key & ((1u << kLocalBits) - 1)) * 4 : dummy_addr;
+#ifndef GPA_ABLATE_PROC_RED
             asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(c) : "memory");
+#else
+            if (addr == 0xFFFFFFFFu) asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(c) : "memory");
+#endif
           }
         }
         PT_MARK(10);
-        named_bar(2, kProcThreads);   // inbox slot j%kInbox fully read
+        named_bar(kBarProc, kProcThreads);   // inbox slot j%kInbox fully read
         PT_MARK(11);
         if (ctid == 0) {
           mbar_arrive(&inbox_free[j % kInbox]);
@@ -533,7 +568,7 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
             if (tab[i]) atomicAdd((unsigned long long *)&a.C[bin], (unsigned long long)tab[i]);
             tab[i] = 0;
           }
-          named_bar(2, kProcThreads);
+          named_bar(kBarProc, kProcThreads);
         }
       }
       PT_FLUSH;
