@@ -334,78 +334,74 @@ cudaError_t launch_slice(const gpa_sass_desc *h, uint32_t *h_row_ptr, uint64_t c
   uint32_t hcap = 1;
   while (hcap < 2u * cap) hcap <<= 1;
   const size_t per_thread = (slice_scratch_per_thread(cap, hcap) + 255) & ~(size_t)255;
-  // device copies
-  auto up = [&](const void *src, size_t bytes, void **dst) -> cudaError_t {
-    cudaError_t e = cudaMallocAsync(dst, std::max<size_t>(bytes, 16), st);
-    if (e != cudaSuccess) return e;
-    return bytes ? cudaMemcpyAsync(*dst, src, bytes, cudaMemcpyHostToDevice, st) : cudaSuccess;
+  // device copies (every allocation is released on every path)
+  std::vector<void *> owned;
+  cudaError_t e = cudaSuccess;
+  auto alloc = [&](size_t bytes) -> void * {
+    void *d = nullptr;
+    if (e == cudaSuccess) e = cudaMallocAsync(&d, std::max<size_t>(bytes, 16), st);
+    if (d) owned.push_back(d);
+    return d;
   };
-  void *d_bb, *d_blk, *d_pp, *d_pr, *d_g, *d_wb, *d_rb, *d_wt, *d_dst, *d_src;
-  cudaError_t e;
-  if ((e = up(h->block_begin, (NB + 1) * 4, &d_bb))) return e;
-  if ((e = up(blk_of.data(), (size_t)n * 4, &d_blk))) return e;
-  if ((e = up(pred_ptr.data(), (NB + 1) * 4, &d_pp))) return e;
-  if ((e = up(pred.data(), (size_t)pred_ptr[NB] * 4, &d_pr))) return e;
-  if ((e = up(h->guard, n, &d_g))) return e;
-  if ((e = up(h->wbar, n, &d_wb))) return e;
-  if ((e = up(h->rbar, n, &d_rb))) return e;
-  if ((e = up(h->wait, n, &d_wt))) return e;
-  if ((e = up(h->dst, (size_t)n * 8, &d_dst))) return e;
-  if ((e = up(h->src, (size_t)n * 8, &d_src))) return e;
-  SliceIn s{n, NB, (const uint32_t *)d_bb, (const uint32_t *)d_blk, (const uint32_t *)d_pp, (const uint32_t *)d_pr,
-            (const uint8_t *)d_g, (const uint8_t *)d_wb, (const uint8_t *)d_rb, (const uint8_t *)d_wt,
-            (const uint16_t *)d_dst, (const uint16_t *)d_src};
+  auto up = [&](const void *src, size_t bytes) -> void * {
+    void *d = alloc(bytes);
+    if (e == cudaSuccess && bytes) e = cudaMemcpyAsync(d, src, bytes, cudaMemcpyHostToDevice, st);
+    return d;
+  };
+  SliceIn s{n, NB, (const uint32_t *)up(h->block_begin, (NB + 1) * 4), (const uint32_t *)up(blk_of.data(), (size_t)n * 4),
+            (const uint32_t *)up(pred_ptr.data(), (NB + 1) * 4), (const uint32_t *)up(pred.data(), (size_t)pred_ptr[NB] * 4),
+            (const uint8_t *)up(h->guard, n), (const uint8_t *)up(h->wbar, n), (const uint8_t *)up(h->rbar, n),
+            (const uint8_t *)up(h->wait, n), (const uint16_t *)up(h->dst, (size_t)n * 8),
+            (const uint16_t *)up(h->src, (size_t)n * 8)};
   // threads: enough for the GPU, bounded by a ~2 GB scratch
   uint64_t threads = std::min<uint64_t>((uint64_t)std::max(n_sms, 1) * 8 * kSlThreads, ((uint64_t)n + kSlThreads - 1) / kSlThreads * kSlThreads);
   threads = std::min<uint64_t>(threads, std::max<uint64_t>(kSlThreads, ((2ull << 30) / per_thread) / kSlThreads * kSlThreads));
   threads = std::max<uint64_t>(threads, kSlThreads);
-  void *d_scr, *d_cnt, *d_rp, *d_err, *d_def, *d_kind, *d_min, *d_max, *d_dom;
-  if ((e = cudaMallocAsync(&d_scr, threads * per_thread, st))) return e;
-  if ((e = cudaMallocAsync(&d_cnt, (size_t)std::max<uint32_t>(n, 1) * 4, st))) return e;
-  if ((e = cudaMallocAsync(&d_err, 4, st))) return e;
-  if ((e = cudaMemsetAsync(d_err, 0, 4, st))) return e;
+  void *d_scr = alloc(threads * per_thread), *d_cnt = alloc((size_t)std::max<uint32_t>(n, 1) * 4), *d_err = alloc(4);
+  if (e == cudaSuccess) e = cudaMemsetAsync(d_err, 0, 4, st);
   const uint32_t grid = (uint32_t)(threads / kSlThreads);
-  k_slice<<<grid, kSlThreads, 0, st>>>(s, (uint8_t *)d_scr, per_thread, cap, hcap, (uint32_t *)d_cnt, nullptr, nullptr,
-                                       nullptr, nullptr, nullptr, nullptr, (int *)d_err);
-  if ((e = cudaGetLastError())) return e;
   std::vector<uint32_t> cnt(std::max<uint32_t>(n, 1));
   int err = 0;
-  if ((e = cudaMemcpyAsync(cnt.data(), d_cnt, (size_t)n * 4, cudaMemcpyDeviceToHost, st))) return e;
-  if ((e = cudaMemcpyAsync(&err, d_err, 4, cudaMemcpyDeviceToHost, st))) return e;
-  if ((e = cudaStreamSynchronize(st))) return e;
+  if (e == cudaSuccess) {
+    k_slice<<<grid, kSlThreads, 0, st>>>(s, (uint8_t *)d_scr, per_thread, cap, hcap, (uint32_t *)d_cnt, nullptr, nullptr,
+                                         nullptr, nullptr, nullptr, nullptr, (int *)d_err);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess) e = cudaMemcpyAsync(cnt.data(), d_cnt, (size_t)n * 4, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&err, d_err, 4, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   uint64_t E = 0;
-  h_row_ptr[0] = 0;
-  for (uint32_t j = 0; j < n; ++j) {
-    E += cnt[j];
-    h_row_ptr[j + 1] = (uint32_t)E;
+  if (e == cudaSuccess) {
+    h_row_ptr[0] = 0;
+    for (uint32_t j = 0; j < n; ++j) {
+      E += cnt[j];
+      h_row_ptr[j + 1] = (uint32_t)E;
+    }
+    *n_edges = E;
+    if (err) *status = 1;                    // state budget exceeded
+    else if (E > cap_edges) *status = 2;     // caller's edge arrays too small
   }
-  *n_edges = E;
-  if (err) *status = 1;                    // state budget exceeded
-  else if (E > cap_edges) *status = 2;     // caller's edge arrays too small
-  if (!*status && E) {
-    if ((e = up(h_row_ptr, ((size_t)n + 1) * 4, &d_rp))) return e;
-    if ((e = cudaMallocAsync(&d_def, E * 4, st))) return e;
-    if ((e = cudaMallocAsync(&d_kind, E, st))) return e;
-    if ((e = cudaMallocAsync(&d_min, E * 4, st))) return e;
-    if ((e = cudaMallocAsync(&d_max, E * 4, st))) return e;
-    if ((e = cudaMallocAsync(&d_dom, E * 4, st))) return e;
-    k_slice<<<grid, kSlThreads, 0, st>>>(s, (uint8_t *)d_scr, per_thread, cap, hcap, (uint32_t *)d_cnt,
-                                         (const uint32_t *)d_rp, (uint32_t *)d_def, (uint8_t *)d_kind, (uint32_t *)d_min,
-                                         (uint32_t *)d_max, (int32_t *)d_dom, (int *)d_err);
-    if ((e = cudaGetLastError())) return e;
-    if ((e = cudaMemcpyAsync(h_def, d_def, E * 4, cudaMemcpyDeviceToHost, st))) return e;
-    if ((e = cudaMemcpyAsync(h_kind, d_kind, E, cudaMemcpyDeviceToHost, st))) return e;
-    if ((e = cudaMemcpyAsync(h_min, d_min, E * 4, cudaMemcpyDeviceToHost, st))) return e;
-    if ((e = cudaMemcpyAsync(h_max, d_max, E * 4, cudaMemcpyDeviceToHost, st))) return e;
-    if ((e = cudaMemcpyAsync(h_dom, d_dom, E * 4, cudaMemcpyDeviceToHost, st))) return e;
-    if ((e = cudaMemcpyAsync(&err, d_err, 4, cudaMemcpyDeviceToHost, st))) return e;
-    if ((e = cudaStreamSynchronize(st))) return e;
-    if (err) *status = 1;
-    for (void *ptr : {d_rp, d_def, d_kind, d_min, d_max, d_dom}) cudaFreeAsync(ptr, st);
+  if (e == cudaSuccess && !*status && E) {
+    void *d_rp = up(h_row_ptr, ((size_t)n + 1) * 4);
+    void *d_def = alloc(E * 4), *d_kind = alloc(E), *d_min = alloc(E * 4), *d_max = alloc(E * 4), *d_dom = alloc(E * 4);
+    if (e == cudaSuccess) {
+      k_slice<<<grid, kSlThreads, 0, st>>>(s, (uint8_t *)d_scr, per_thread, cap, hcap, (uint32_t *)d_cnt,
+                                           (const uint32_t *)d_rp, (uint32_t *)d_def, (uint8_t *)d_kind, (uint32_t *)d_min,
+                                           (uint32_t *)d_max, (int32_t *)d_dom, (int *)d_err);
+      e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h_def, d_def, E * 4, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h_kind, d_kind, E, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h_min, d_min, E * 4, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h_max, d_max, E * 4, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h_dom, d_dom, E * 4, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&err, d_err, 4, cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess && err) *status = 1;
   }
-  for (void *ptr : {d_bb, d_blk, d_pp, d_pr, d_g, d_wb, d_rb, d_wt, d_dst, d_src, d_scr, d_cnt, d_err})
-    cudaFreeAsync(ptr, st);
-  return cudaStreamSynchronize(st);
+  for (void *ptr : owned) cudaFreeAsync(ptr, st);
+  const cudaError_t e2 = cudaStreamSynchronize(st);
+  return e != cudaSuccess ? e : e2;
 }
 
 }  // namespace gpa
