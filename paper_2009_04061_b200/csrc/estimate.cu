@@ -37,11 +37,11 @@ __global__ void k_est_rows(DevProgram p, EstimatePlan ep) {
   __syncthreads();
   const uint64_t stride_items = (uint64_t)p.E + p.n;
   const uint32_t n_groups = (ep.n_pat + kEstGroup - 1) / kEstGroup;
-  const uint64_t total = (uint64_t)p.n * n_groups;
-  for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total; t += (uint64_t)gridDim.x * blockDim.x) {
+  const uint32_t total = p.n * n_groups;          // < 2^32 (checked by the launcher)
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
     // row-major: the pattern groups of a row run on neighbouring threads, so its C row and edges
     // are fetched from DRAM once and served from L1 to the other groups
-    const uint32_t j = (uint32_t)(t / n_groups), grp = (uint32_t)(t % n_groups);
+    const uint32_t j = t / n_groups, grp = t - j * n_groups;
     const uint32_t q0 = grp * kEstGroup;
     const uint32_t nq = min((uint32_t)kEstGroup, ep.n_pat - q0);
     const uint64_t *row = p.C + (uint64_t)j * 2 * p.R;
@@ -59,6 +59,7 @@ __global__ void k_est_rows(DevProgram p, EstimatePlan ep) {
     for (int k = 0; k < kEstGroup; ++k) sum[k] = 0.0;
     for (uint32_t e = e0; e < e1; ++e) {   // loads only: per-edge values go to k_est_edges
       const EdgeInfo x = edge_info(p, e, loop_j);
+      if (!x.m) continue;                  // no candidate reason: adds 0 to every pattern
 #pragma unroll
       for (int k = 0; k < kEstGroup; ++k) {
         if ((uint32_t)k >= nq) break;
@@ -267,6 +268,7 @@ cudaError_t launch_estimate(const DevProgram &p, const EstimatePlan &ep, int n_s
                             uint64_t *launches) {
   const uint32_t threads = 128;
   const uint64_t work = (uint64_t)p.n * ((ep.n_pat + kEstGroup - 1) / kEstGroup);
+  if (work >= (1ull << 32)) return cudaErrorInvalidValue;   // k_est_rows indexes (row, group) in 32 bits
   const uint32_t g = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((work + threads - 1) / threads, (uint64_t)n_sms * 32));
   k_est_rows<<<g, threads, 0, s>>>(p, ep);
   bool any_slot = false;

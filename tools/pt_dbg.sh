@@ -1,8 +1,2 @@
-for v in product build/libv_*.so; do timeout 120 python tools/variant_time.py $v 2>&1 | grep -v Warn | tail -1; done
-python - <<'P'
-import numpy as np, glob
-ref = np.load("gpurun_out/counts_product.npy")
-for f in sorted(glob.glob("gpurun_out/counts_libv*.npy")):
-    print(f, "identical" if np.array_equal(np.load(f), ref) else "DIFFERENT")
-P
-rm -f gpurun_out/counts_*
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_advice.py -x -q 2>&1 | tail -1
+for v in "" build/libv_eg8.so build/libv_eg2.so; do echo "lib=$v"; GPA_LIB_PATH=$v timeout 600 python tools/batch_probe.py 2>&1 | grep -v Warn | grep "^reset " | tail -1; done
