@@ -8,7 +8,7 @@ import torch
 import gpagen
 from paper_2009_04061_b200 import gpa as G
 
-G.LIB_PATH = os.path.join(ROOT, "build", "libgpa_timing.so")
+G.LIB_PATH = os.path.join(ROOT, os.environ.get("PT_LIB", "build/libgpa_timing.so"))
 lib = G.lib()
 prog = gpagen.config_program(3)
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 200_000_000
