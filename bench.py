@@ -91,13 +91,16 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def _traffic_from_profile(workload):
-    """dram bytes per ingest launch from the committed ncu --set full summary, if present."""
+def _traffic_from_profile(workload, records):
+    """dram bytes per ingest launch from the committed ncu --set full summary, if it was captured
+    at this launch size (else None: the figure is per launch, not per record)."""
     path = os.path.join(ROOT, "profiles", "ncu_ingest_summary.json")
     try:
         with open(path) as fh:
             d = json.load(fh)
         e = d.get(workload, {})
+        if e.get("records_per_launch") != records:
+            return None
         return e.get("dram_bytes_per_launch")
     except Exception:
         return None
@@ -150,6 +153,24 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+
+def _local_device() -> int:
+    """This rank's GPU: LOCAL_RANK.  GPA_BENCH_ONE_GPU=1 (test knob, never used for a reported
+    number) puts every rank on GPU 0 so the multi-rank code path can be exercised on one GPU."""
+    if os.environ.get("GPA_BENCH_ONE_GPU") == "1":
+        return 0
+    return int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def _init_dist(dist, dev):
+    """NCCL over NVLink; GPA_BENCH_BACKEND=gloo (test knob, with GPA_BENCH_ONE_GPU) runs the same
+    collectives through host memory, since NCCL refuses two ranks on one GPU."""
+    backend = os.environ.get("GPA_BENCH_BACKEND", "nccl")
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group(backend)
+
 def run_batch(args):
     """--workload batch: BASELINE config 4 -- 10^4 kernels (~4.5 M instructions), 10^8 records
     grouped by kernel launch.  N > 1: DP-2 -- contiguous kernel ranges balanced by sample count,
@@ -164,11 +185,11 @@ def run_batch(args):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = _local_device()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        _init_dist(dist, dev)
     n_total = args.records or WORKLOADS["batch"][1]
     prog = batch.config4_program()
     spec = batch.config4_stream(prog)
@@ -327,11 +348,11 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = _local_device()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        _init_dist(dist, dev)
     cfg, n_per = WORKLOADS[args.workload]
     if args.records:
         n_per = args.records
@@ -459,7 +480,7 @@ def main():
                        "parallelism": f"dp{world} (sample-stream shards + NCCL all-reduce of counts)",
                        "ingest_variant": P.variant},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": _traffic_from_profile(args.workload),
+                         "frac": achieved / peak, "traffic": _traffic_from_profile(args.workload, n_per),
                          "kernel": "ingest", "peak_kind": peak_kind, "alg_bytes_per_launch": alg_bytes,
                          "ingest_ms": ingest_ms, "ingest_share_of_step": ingest_ms / ms_per_step,
                          "blame_rollup_estimate_ms": analyze_ms},
