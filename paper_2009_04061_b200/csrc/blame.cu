@@ -118,12 +118,24 @@ inline uint32_t grid_for(uint64_t items, uint32_t threads, int n_sms) {
 
 }  // namespace
 
-cudaError_t launch_blame(const DevProgram &p, int n_sms, cudaStream_t s, uint64_t *launches) {
+// summaries + candidates / shares / self flags (rows a2-a4): everything the estimate step reads
+cudaError_t launch_blame_rows(const DevProgram &p, int n_sms, cudaStream_t s, uint64_t *launches) {
   k_summaries<<<grid_for(p.n, 256, n_sms), 256, 0, s>>>(p.C, p.n, p.R, p.AL);
   k_blame_rows<<<grid_for(p.n, 128, n_sms), 128, 0, s>>>(p);
-  k_def_reduce<<<grid_for(p.n, 128, n_sms), 128, 0, s>>>(p);
-  *launches += 3;
+  *launches += 2;
   return cudaGetLastError();
+}
+
+// def-side reduction (rows a5-a6): B, read by the rollup only
+cudaError_t launch_def_reduce(const DevProgram &p, int n_sms, cudaStream_t s, uint64_t *launches) {
+  k_def_reduce<<<grid_for(p.n, 128, n_sms), 128, 0, s>>>(p);
+  *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_blame(const DevProgram &p, int n_sms, cudaStream_t s, uint64_t *launches) {
+  cudaError_t e = launch_blame_rows(p, n_sms, s, launches);
+  return e != cudaSuccess ? e : launch_def_reduce(p, n_sms, s, launches);
 }
 
 }  // namespace gpa

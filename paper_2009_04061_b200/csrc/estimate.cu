@@ -264,8 +264,10 @@ __global__ void k_est_final(DevProgram p, EstimatePlan ep) {
 
 }  // namespace
 
-cudaError_t launch_estimate(const DevProgram &p, const EstimatePlan &ep, int n_sms, cudaStream_t s,
-                            uint64_t *launches) {
+// matched samples per item, loop / function / kernel sums: reads only the blame rows' outputs
+// (cand, share, selfm) and C, so it can run beside the def reduction and the rollup
+cudaError_t launch_estimate_sums(const DevProgram &p, const EstimatePlan &ep, int n_sms, cudaStream_t s,
+                                 uint64_t *launches) {
   const uint32_t threads = 128;
   const uint64_t work = (uint64_t)p.n * ((ep.n_pat + kEstGroup - 1) / kEstGroup);
   if (work >= (1ull << 32)) return cudaErrorInvalidValue;   // k_est_rows indexes (row, group) in 32 bits
@@ -304,10 +306,23 @@ cudaError_t launch_estimate(const DevProgram &p, const EstimatePlan &ep, int n_s
   const uint64_t w2 = std::max<uint64_t>((uint64_t)p.n_loops, p.n_kernels) * ep.n_pat;
   dim3 g2((uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((w2 + 3) / 4, (uint64_t)n_sms * 32)), 2);
   k_segsum<<<g2, 128, 0, s>>>(b);
+  *launches += 3;
+  return cudaGetLastError();
+}
+
+// Eqs. 2-5 / 10 per (kernel, pattern): needs the sums above and the rollup's A sums
+cudaError_t launch_estimate_final(const DevProgram &p, const EstimatePlan &ep, int n_sms, cudaStream_t s,
+                                  uint64_t *launches) {
   const uint32_t total = p.n_kernels * ep.n_pat;
   k_est_final<<<std::max<uint32_t>(1, std::min<uint32_t>((total + 3) / 4, n_sms * 32)), 128, 0, s>>>(p, ep);
-  *launches += 4;
+  *launches += 1;
   return cudaGetLastError();
+}
+
+cudaError_t launch_estimate(const DevProgram &p, const EstimatePlan &ep, int n_sms, cudaStream_t s,
+                            uint64_t *launches) {
+  cudaError_t e = launch_estimate_sums(p, ep, n_sms, s, launches);
+  return e != cudaSuccess ? e : launch_estimate_final(p, ep, n_sms, s, launches);
 }
 
 }  // namespace gpa

@@ -139,6 +139,12 @@ struct AdvicePlan {
 cudaError_t launch_ingest(const DevProgram &p, int variant, const void *records, uint64_t n,
                           int n_sms, size_t smem_optin, cudaStream_t s);
 cudaError_t launch_blame(const DevProgram &p, int n_sms, cudaStream_t s, uint64_t *launches);
+cudaError_t launch_blame_rows(const DevProgram &p, int n_sms, cudaStream_t s, uint64_t *launches);
+cudaError_t launch_def_reduce(const DevProgram &p, int n_sms, cudaStream_t s, uint64_t *launches);
+cudaError_t launch_estimate_sums(const DevProgram &p, const EstimatePlan &ep, int n_sms, cudaStream_t s,
+                                 uint64_t *launches);
+cudaError_t launch_estimate_final(const DevProgram &p, const EstimatePlan &ep, int n_sms, cudaStream_t s,
+                                  uint64_t *launches);
 cudaError_t launch_rollup(const DevProgram &p, const RollupPlan &rp, int n_sms, cudaStream_t s,
                           uint64_t *launches);
 cudaError_t launch_estimate(const DevProgram &p, const EstimatePlan &ep, int n_sms,
@@ -272,6 +278,8 @@ struct gpa_program {
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr};
   // blame + aggregate + estimate captured once as a CUDA graph (gpa_analyze)
   cudaStream_t capture_stream = nullptr;
+  cudaStream_t side_stream = nullptr;          // analyze graph: the estimate branch
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaGraphExec_t analyze_exec = nullptr;
   uint32_t analyze_npat = 0xffffffffu;
   uint64_t analyze_launches = 0;

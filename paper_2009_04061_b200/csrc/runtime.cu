@@ -604,6 +604,9 @@ gpa_status gpa_program_destroy(gpa_program *p) {
   if (!p) return GPA_OK;
   if (p->analyze_exec) cudaGraphExecDestroy(p->analyze_exec);
   if (p->capture_stream) cudaStreamDestroy(p->capture_stream);
+  if (p->side_stream) cudaStreamDestroy(p->side_stream);
+  if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+  if (p->ev_join) cudaEventDestroy(p->ev_join);
   if (p->staging) cudaFree(p->staging);
   if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
   for (int i = 0; i < 2; ++i) {
@@ -765,12 +768,28 @@ gpa_status gpa_analyze(gpa_program *p, void *stream) {
       p->analyze_exec = nullptr;
     }
     if (!p->capture_stream) CUDA_TRY(cudaStreamCreateWithFlags(&p->capture_stream, cudaStreamNonBlocking));
+    if (!p->side_stream) CUDA_TRY(cudaStreamCreateWithFlags(&p->side_stream, cudaStreamNonBlocking));
+    if (!p->ev_fork) CUDA_TRY(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+    if (!p->ev_join) CUDA_TRY(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
     cudaGraph_t g = nullptr;
     uint64_t n = 0;
+    // two branches after the blame rows: def reduction -> rollup, and the estimate sums (which read
+    // only cand / share / selfm and C); they join before Eqs. 2-5 / 10, which need the rollup's A sums
     CUDA_TRY(cudaStreamBeginCapture(p->capture_stream, cudaStreamCaptureModeThreadLocal));
-    cudaError_t e = launch_blame(p->d, p->n_sms, p->capture_stream, &n);
-    if (e == cudaSuccess) e = launch_rollup(p->d, p->rp, p->n_sms, p->capture_stream, &n);
-    if (e == cudaSuccess && npat) e = launch_estimate(p->d, p->ep, p->n_sms, p->capture_stream, &n);
+    cudaStream_t cs = p->capture_stream, ss = p->side_stream;
+    cudaError_t e = launch_blame_rows(p->d, p->n_sms, cs, &n);
+    if (e == cudaSuccess && npat) {
+      e = cudaEventRecord(p->ev_fork, cs);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(ss, p->ev_fork, 0);
+      if (e == cudaSuccess) e = launch_estimate_sums(p->d, p->ep, p->n_sms, ss, &n);
+      if (e == cudaSuccess) e = cudaEventRecord(p->ev_join, ss);
+    }
+    if (e == cudaSuccess) e = launch_def_reduce(p->d, p->n_sms, cs, &n);
+    if (e == cudaSuccess) e = launch_rollup(p->d, p->rp, p->n_sms, cs, &n);
+    if (e == cudaSuccess && npat) {
+      e = cudaStreamWaitEvent(cs, p->ev_join, 0);
+      if (e == cudaSuccess) e = launch_estimate_final(p->d, p->ep, p->n_sms, cs, &n);
+    }
     cudaError_t e2 = cudaStreamEndCapture(p->capture_stream, &g);
     if (e != cudaSuccess) return cuda_fail(e, "analyze capture");
     if (e2 != cudaSuccess) return cuda_fail(e2, "analyze end capture");
