@@ -150,6 +150,8 @@ cudaError_t launch_rollup(const DevProgram &p, const RollupPlan &rp, int n_sms, 
 cudaError_t launch_estimate(const DevProgram &p, const EstimatePlan &ep, int n_sms,
                             cudaStream_t s, uint64_t *launches);
 cudaError_t launch_vrows(const DevProgram &p, double *vbuf, int n_sms, cudaStream_t s);
+cudaError_t launch_rollup_fork(const DevProgram &p, const RollupPlan &rp, int n_sms, cudaStream_t s,
+                               cudaStream_t side, cudaEvent_t fork, cudaEvent_t join, uint64_t *launches);
 cudaError_t launch_slice(const gpa_sass_desc *h, uint32_t *h_row_ptr, uint64_t cap_edges, uint32_t *h_def,
                          uint8_t *h_kind, uint32_t *h_min, uint32_t *h_max, int32_t *h_dom, uint64_t *n_edges,
                          int n_sms, cudaStream_t st, int *status);
@@ -280,6 +282,8 @@ struct gpa_program {
   cudaStream_t capture_stream = nullptr;
   cudaStream_t side_stream = nullptr;          // analyze graph: the estimate branch
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t pack_stream = nullptr;          // analyze graph: the rollup's short-segment packs
+  cudaEvent_t ev_pfork = nullptr, ev_pjoin = nullptr;
   cudaGraphExec_t analyze_exec = nullptr;
   uint32_t analyze_npat = 0xffffffffu;
   uint64_t analyze_launches = 0;

@@ -241,21 +241,36 @@ cudaError_t launch_vrows(const DevProgram &p, double *vbuf, int n_sms, cudaStrea
   return cudaGetLastError();
 }
 
-cudaError_t launch_rollup(const DevProgram &p, const RollupPlan &rp, int n_sms, cudaStream_t s,
-                          uint64_t *launches) {
+// fork (optional, graph capture): the packs of short segments write rows disjoint from the
+// chunked long segments', so they run on stream `side` between events fork / join
+cudaError_t launch_rollup_fork(const DevProgram &p, const RollupPlan &rp, int n_sms, cudaStream_t s,
+                               cudaStream_t side, cudaEvent_t fork, cudaEvent_t join, uint64_t *launches) {
   const uint32_t nv = 2 * p.ncol;
   cudaError_t e = launch_vrows(p, rp.vbuf, n_sms, s);
   if (e != cudaSuccess) return e;
+  const bool split = side && rp.n_packs;
+  if (split) {
+    if ((e = cudaEventRecord(fork, s)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(side, fork, 0)) != cudaSuccess) return e;
+  }
+  cudaStream_t ps = split ? side : s;
+  if (rp.n_packs) k_rollup_packs<<<warp_grid(rp.n_packs, n_sms), 128, 0, ps>>>(rp, nv, rp.vbuf, p.AL);
+  if (split && (e = cudaEventRecord(join, side)) != cudaSuccess) return e;
   if (rp.n_chunks) k_rollup_chunks<<<warp_grid(rp.n_chunks, n_sms), 128, 0, s>>>(rp, nv, rp.vbuf, p.AL);
-  if (rp.n_packs) k_rollup_packs<<<warp_grid(rp.n_packs, n_sms), 128, 0, s>>>(rp, nv, rp.vbuf, p.AL);
   if (rp.n_seg1)
     k_rollup_segments<<<warp_grid(rp.n_seg1, n_sms), 128, 0, s>>>(
         nv, rp.part_v, rp.part_al, nullptr, rp.seg1_begin, rp.seg1_end, rp.n_seg1, rp.seg1_id, rp.rows_v, rp.rows_al);
+  if (split && (e = cudaStreamWaitEvent(s, join, 0)) != cudaSuccess) return e;   // stage 2 reads the pack rows
   k_rollup_segments<<<warp_grid(rp.n_seg2, n_sms), 128, 0, s>>>(
       nv, rp.rows_v, rp.rows_al, rp.seg2_perm, rp.seg2_begin, rp.seg2_end, rp.n_seg2, nullptr,
       rp.rows_v + (uint64_t)rp.n_rows1 * nv, rp.rows_al + 2 * (uint64_t)rp.n_rows1);
   *launches += 2 + (rp.n_chunks ? 1 : 0) + (rp.n_packs ? 1 : 0) + (rp.n_seg1 ? 1 : 0);
   return cudaGetLastError();
+}
+
+cudaError_t launch_rollup(const DevProgram &p, const RollupPlan &rp, int n_sms, cudaStream_t s,
+                          uint64_t *launches) {
+  return launch_rollup_fork(p, rp, n_sms, s, nullptr, nullptr, nullptr, launches);
 }
 
 }  // namespace gpa

@@ -607,6 +607,9 @@ gpa_status gpa_program_destroy(gpa_program *p) {
   if (p->side_stream) cudaStreamDestroy(p->side_stream);
   if (p->ev_fork) cudaEventDestroy(p->ev_fork);
   if (p->ev_join) cudaEventDestroy(p->ev_join);
+  if (p->pack_stream) cudaStreamDestroy(p->pack_stream);
+  if (p->ev_pfork) cudaEventDestroy(p->ev_pfork);
+  if (p->ev_pjoin) cudaEventDestroy(p->ev_pjoin);
   if (p->staging) cudaFree(p->staging);
   if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
   for (int i = 0; i < 2; ++i) {
@@ -771,6 +774,9 @@ gpa_status gpa_analyze(gpa_program *p, void *stream) {
     if (!p->side_stream) CUDA_TRY(cudaStreamCreateWithFlags(&p->side_stream, cudaStreamNonBlocking));
     if (!p->ev_fork) CUDA_TRY(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
     if (!p->ev_join) CUDA_TRY(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
+    if (!p->pack_stream) CUDA_TRY(cudaStreamCreateWithFlags(&p->pack_stream, cudaStreamNonBlocking));
+    if (!p->ev_pfork) CUDA_TRY(cudaEventCreateWithFlags(&p->ev_pfork, cudaEventDisableTiming));
+    if (!p->ev_pjoin) CUDA_TRY(cudaEventCreateWithFlags(&p->ev_pjoin, cudaEventDisableTiming));
     cudaGraph_t g = nullptr;
     uint64_t n = 0;
     // two branches after the blame rows: def reduction -> rollup, and the estimate sums (which read
@@ -785,7 +791,7 @@ gpa_status gpa_analyze(gpa_program *p, void *stream) {
       if (e == cudaSuccess) e = cudaEventRecord(p->ev_join, ss);
     }
     if (e == cudaSuccess) e = launch_def_reduce(p->d, p->n_sms, cs, &n);
-    if (e == cudaSuccess) e = launch_rollup(p->d, p->rp, p->n_sms, cs, &n);
+    if (e == cudaSuccess) e = launch_rollup_fork(p->d, p->rp, p->n_sms, cs, p->pack_stream, p->ev_pfork, p->ev_pjoin, &n);
     if (e == cudaSuccess && npat) {
       e = cudaStreamWaitEvent(cs, p->ev_join, 0);
       if (e == cudaSuccess) e = launch_estimate_final(p->d, p->ep, p->n_sms, cs, &n);
