@@ -246,6 +246,7 @@ constexpr int kStage = GPA_PART_STAGE;                          // staging buffe
 constexpr int kTrash = 32;                         // lane-distinct sink for dropped keys / padding
 constexpr uint32_t kLocalBits = 13;                // key = local bin (13 bits) | count (3 bits)
 constexpr uint32_t kMaxKeyCount = 7;
+constexpr uint32_t kDummyCount = 1u << 30;        // dummy-bucket counter start (never < kPartCap)
 // a chunk adds at most G * cap * 7 samples to any one table entry: flushing the u32 table every
 // kFlushEvery chunks keeps every entry below 2^32
 constexpr uint32_t kBarProc = 2;   // named barrier of the processor warps (0 is __syncthreads)
@@ -316,7 +317,10 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
   uint32_t *tab = reinterpret_cast<uint32_t *>(stored + kPartBufs);              // [bpb + kTrash]
   for (uint32_t i = tid; i < a.bpb + kTrash; i += kPartThreads) tab[i] = 0;
   for (uint32_t i = tid; i < kStage * ibuf_keys / 2; i += kPartThreads) reinterpret_cast<uint32_t *>(stag)[i] = 0;
-  for (uint32_t i = tid; i < kStage * (kPartMaxCtas + 8); i += kPartThreads) cnt[i] = 0;
+  // bucket G is the dummy bucket of invalid / large-count records: its counter starts past the
+  // slot capacity, so its records always take the rare branch
+  for (uint32_t i = tid; i < kStage * (kPartMaxCtas + 8); i += kPartThreads)
+    cnt[i] = i % (kPartMaxCtas + 8) == G ? kDummyCount : 0u;
   if (tid == 0) {
     for (int r = 0; r < kStage; ++r) {
       mbar_init(&buf_ready[r], 1);
@@ -345,12 +349,34 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
   };
   const uint32_t twoR = 2 * a.R;
   IngestStats st{0, 0, 0};
+#ifndef GPA_PART_MAXNREG   // registers per decoder thread / per other thread (20*72 + 12*40 = 32*60 <= 32*64)
+#define GPA_PART_MAXNREG 72
+#define GPA_PART_LOWNREG 40
+#endif
+#if GPA_PART_MAXNREG > 0
+  // register split by warp role (setmaxnreg): the decoder warpgroups (warps 0-19) take the
+  // registers the control / publisher / loader / processor warpgroups (warps 20-31) do not need,
+  // so the decode keeps its addresses and keys in registers (measured 2.30 -> 2.26 ms on config 3)
+  static_assert(kDecodeWarps % 4 == 0, "decoders fill whole warpgroups");
+  static_assert(kDecodeWarps * GPA_PART_MAXNREG + (32 - kDecodeWarps) * GPA_PART_LOWNREG <= 32 * 64,
+                "register split exceeds the CTA's register file");
+  if (warp < kDecodeWarps) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(GPA_PART_MAXNREG));
+  else asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(GPA_PART_LOWNREG));
+#endif
   if (warp < kDecodeWarps) {
     // ======================= decoders: wait only on data (ring_full) and on a clean staging
     //                         buffer (buf_ready); decode + scatter; signal decoded
     const uint32_t dtid = tid;
-    const uint32_t n_instr = a.n_instr, R = a.R, mg = a.mg;
+    const uint32_t n_instr = a.n_instr, R = a.R, mg = a.mg, nG = 0u - G, Rm256 = R - 256u;
     const uint32_t trash_addr = smem_addr(trash + lane);
+    auto load_chunk = [&](const uint4 *rs, uint32_t len, uint4 (&v)[kDecodeRecs / 2]) {
+      const bool full = len == (uint32_t)CHUNK;
+#pragma unroll
+      for (int u = 0; u < kDecodeRecs / 2; ++u) {
+        const uint32_t pair = u * kDecodeThreads + dtid;   // len is even: both records of a pair or neither
+        v[u] = (full || 2 * pair < len) ? ld_stream(rs + pair) : make_uint4(0xffffffffu, 0, 0xffffffffu, 0);
+      }
+    };
     PT_DECL
     for (uint32_t k = 0; k < n_chunks; ++k) {
       uint64_t s0;
@@ -361,74 +387,88 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
       const bool full = len == (uint32_t)CHUNK;
       PT_START;
       uint4 vv[kDecodeRecs / 2];   // 16-byte streaming loads, in flight while waiting for the buffer
-#pragma unroll
-      for (int u = 0; u < kDecodeRecs / 2; ++u) {
-        const uint32_t pair = u * kDecodeThreads + dtid;   // len is even: both records of a pair or neither
-        vv[u] = (full || 2 * pair < len) ? ld_stream(rs + pair) : make_uint4(0xffffffffu, 0, 0xffffffffu, 0);
-      }
+      load_chunk(rs, len, vv);
       mbar_wait(&buf_ready[sb], (k / kStage) & 1);
       PT_MARK(0);
       // ---- branch-free decode: bucket = pc mod G (interleaved PCs balance the load), key = local
       //      bin (pc / G) * 2R + class * R + reason | count << 13, stored at position cnt[b]++ of
       //      bucket b's zero-padded slot (invalid and padding records count in the dummy bucket G
       //      and land in a trash word; counts > 7 and slot overflow go through L2 atomics)
-      uint32_t csum = 0, bads = 0, badr = 0;
+      uint32_t vsum = 0, bads = 0, badr = 0, rare = 0;
+      static_assert(kDecodeRecs <= 32, "one rare bit per record");
       // records are processed in batches of kDecodeBatch pairs: all slot allocations (atomics) of a
-      // batch are issued before its key stores, so their latencies overlap.  Validity (Q12): t =
-      // flags:reason is valid iff t < R (ACT) or 0x101 <= t < 0x100 + R (LAT with a reason); then
-      // class * R + reason = t - (t >> 8) * (256 - R).  The rare cases -- invalid records, counts
-      // > 7, slot overflow -- share one branch.
+      // batch are issued before its key stores, so their latencies overlap.  Record word w =
+      // flags << 24 | reason << 16 | count, t = w >> 16.  Validity (Q12): t < R (ACT) or
+      // 0x101 <= t < 0x100 + R (LAT with a reason); then class * R + reason = t + flags * (R - 256).
+      // Fast records (valid, count <= 7) get key = local bin | count << 13 = the low 16 bits of
+      // (w << 13) + q * 2R + t + flags * (R - 256) (the st.u16 drops the reason / flag bits that
+      // w << 13 carries above bit 15).  Invalid records and counts > 7 go to the dummy bucket G,
+      // whose counter never hands out a slot, so one compare (pos < cap) selects the rare path
+      // for them and for slot overflow; it runs once per chunk and re-derives each case.  Samples
+      // of fast records are summed by the processors (from the keys), not here.
+      uint32_t cnt_r, sg_r, trash_r, nG_r;   // opaque copies: kept in registers, not rematerialised per record
+      asm volatile("mov.b32 %0, %1;" : "=r"(cnt_r) : "r"(cnt_addr));
+      asm volatile("mov.b32 %0, %1;" : "=r"(sg_r) : "r"(sg_addr));
+      asm volatile("mov.b32 %0, %1;" : "=r"(trash_r) : "r"(trash_addr));
+      asm volatile("mov.b32 %0, %1;" : "=r"(nG_r) : "r"(nG));
 #pragma unroll
       for (int u0 = 0; u0 < kDecodeRecs / 2; u0 += kDecodeBatch) {
         constexpr int kB = 2 * kDecodeBatch;
-        uint32_t pos[kB], slot[kB], pcs[kB], tls[kB], cnts[kB];
-        unsigned short key[kB];
+        uint32_t pos[kB], slot[kB];
+        uint32_t key[kB];
 #pragma unroll
         for (int i = 0; i < kB; ++i) {
           const int u = u0 + i / 2, h = i & 1;
           if (u >= kDecodeRecs / 2) break;
           const uint4 v = vv[u];
           const uint32_t pc = h ? v.z : v.x, w = h ? v.w : v.y;
-          const uint32_t t = w >> 16, c = w & 0xffffu;
-          const uint32_t tl = t - (t >> 8) * (256u - R);
-          const bool ok = pc < n_instr && (t < R || t - 0x101u < R - 1u);
-          const uint32_t q = __umulhi(pc, mg), b = pc - q * G;
-          const bool fast = ok && c <= kMaxKeyCount;
+          const uint32_t t = w >> 16;
+          const bool fast = pc < n_instr && (w & 0xfff8u) == 0u && (t < R || t - 0x101u < R - 1u);
+          const uint32_t q = __umulhi(pc, mg);
+          uint32_t b;
+          asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(b) : "r"(q), "r"(nG_r), "r"(pc));   // pc mod G
           const uint32_t be = fast ? b : G;
-          key[i] = (unsigned short)((q * twoR + tl) | (c << kLocalBits));
-          slot[i] = fast ? sg_addr + be * (kPartCap * 2) : 0u;   // 0: never kept
-          pcs[i] = ok ? pc : 0xFFFFFFFFu;                        // invalid marker for the rare branch
-          tls[i] = tl;
-          cnts[i] = c;
+          key[i] = (w << kLocalBits) + q * twoR + t + (w >> 24) * Rm256;
+          slot[i] = sg_r + be * (kPartCap * 2);
 #ifndef GPA_ABLATE_DEC_ATOM
-          asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(pos[i]) : "r"(cnt_addr + be * 4) : "memory");
+          asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(pos[i]) : "r"(cnt_r + be * 4) : "memory");
 #else
-          pos[i] = (dtid + i) % 40u + (cnt_addr == 0xFFFFFFFFu ? be : 0u);
+          pos[i] = (dtid + i) % 40u + (cnt_r == 0xFFFFFFFFu ? be : 0u);
 #endif
-          csum += c;        // padding records have count 0
         }
 #pragma unroll
         for (int i = 0; i < kB; ++i) {
-          const int u = u0 + i / 2;
+          const int u = u0 + i / 2, h = i & 1;
           if (u >= kDecodeRecs / 2) break;
-          const bool keep = slot[i] != 0u && pos[i] < (uint32_t)kPartCap;
-          const uint32_t dst = keep ? slot[i] + pos[i] * 2 : trash_addr;
+          const bool keep = pos[i] < (uint32_t)kPartCap;
+          const uint32_t dst = keep ? slot[i] + pos[i] * 2 : trash_r;
 #ifndef GPA_ABLATE_DEC_STS
-          asm volatile("st.shared.u16 [%0], %1;" ::"r"(dst), "h"(key[i]) : "memory");
+          asm volatile("st.shared.u16 [%0], %1;" ::"r"(dst), "h"((unsigned short)key[i]) : "memory");
 #else
-          if (dst == 0xFFFFFFFFu) asm volatile("st.shared.u16 [%0], %1;" ::"r"(dst), "h"(key[i]) : "memory");
+          if (dst == 0xFFFFFFFFu) asm volatile("st.shared.u16 [%0], %1;" ::"r"(dst), "h"((unsigned short)key[i]) : "memory");
 #endif
-          if (!keep) {       // rare: an invalid record, a count > 7 or slot overflow (skew)
-            if (pcs[i] != 0xFFFFFFFFu) {
-              atomicAdd((unsigned long long *)&a.C[(uint64_t)pcs[i] * twoR + tls[i]], (unsigned long long)cnts[i]);
-            } else {
-              bads += cnts[i];
-              badr += (full || 2 * (u * kDecodeThreads + dtid) < len) ? 1u : 0u;   // padding is not a record
-            }
+          rare |= keep ? 0u : 1u << (2 * u + h);
+        }
+      }
+      if (rare) {   // rare: an invalid record, a count > 7 or slot overflow (skew); one branch per chunk
+#pragma unroll
+        for (int i = 0; i < kDecodeRecs; ++i) {
+          if (!((rare >> i) & 1u)) continue;
+          const int u = i / 2, h = i & 1;
+          const uint4 v = vv[u];
+          const uint32_t pc = h ? v.z : v.x, w = h ? v.w : v.y;
+          const uint32_t t = w >> 16, c = w & 0xffffu;
+          if (pc < n_instr && (t < R || t - 0x101u < R - 1u)) {
+            const uint32_t tl = t - (t >> 8) * (256u - R);
+            atomicAdd((unsigned long long *)&a.C[(uint64_t)pc * twoR + tl], (unsigned long long)c);
+            vsum += c;
+          } else {
+            bads += c;
+            badr += (full || 2 * (u * kDecodeThreads + dtid) < len) ? 1u : 0u;   // padding is not a record
           }
         }
       }
-      st.valid += csum - bads;
+      st.valid += vsum;
       st.bad_samples += bads;
       st.bad_records += badr;
       // generic-proxy staging writes must be ordered before the control warp's bulk store
@@ -489,7 +529,7 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
         const uint32_t ob = k % kStage;
         uint4 *z = reinterpret_cast<uint4 *>(stag + ob * ibuf_keys);
         for (uint32_t i = lane; i < slot_keys / 8; i += 32) z[i] = make_uint4(0, 0, 0, 0);
-        for (uint32_t i = lane; i <= G; i += 32) cnt[ob * (kPartMaxCtas + 8) + i] = 0;
+        for (uint32_t i = lane; i <= G; i += 32) cnt[ob * (kPartMaxCtas + 8) + i] = i == G ? kDummyCount : 0u;
         __syncwarp();
         if (lane == 0) mbar_arrive(&buf_ready[ob]);
       }
@@ -532,6 +572,7 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
     } else {
       const uint32_t ctid = tid - kProcBase;
       const uint32_t tab_addr = smem_addr(tab), dummy_addr = smem_addr(tab + a.bpb + (ctid & 31));
+      uint32_t psum = 0;   // < 2^32: flushed into st.valid every chunk
       PT_DECL
       for (uint32_t j = 0; j < n_chunks; ++j) {
         PT_START;
@@ -545,6 +586,7 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
           for (int e = 0; e < 8; ++e) {
             const uint32_t key = (w4[e >> 1] >> ((e & 1) * 16)) & 0xffffu;
             const uint32_t c = key >> kLocalBits;
+            psum += c;   // the samples of fast records (the decoders count only the rare ones)
             // padding keys (c = 0) add 0 to a lane-distinct dummy word: cheaper on the shared-memory
             // pipe than a predicated (branching) update, measured
             const uint32_t addr = c ? tab_addr + (key & ((1u << kLocalBits) - 1)) * 4 : dummy_addr;
@@ -555,6 +597,8 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
 #endif
           }
         }
+        st.valid += psum;
+        psum = 0;
         PT_MARK(10);
         named_bar(kBarProc, kProcThreads);   // inbox slot j%kInbox fully read
         PT_MARK(11);
