@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
     // ======================= decoders: wait only on data (ring_full) and on a clean staging
     //                         buffer (buf_ready); decode + scatter; signal decoded
     const uint32_t dtid = tid;
-    const uint32_t n_instr = a.n_instr, R = a.R, mg = a.mg, nG = 0u - G, Rm256 = R - 256u;
+    const uint32_t n_instr = a.n_instr, R = a.R, mg = a.mg, nG = 0u - G;
     const uint32_t trash_addr = smem_addr(trash + lane);
     auto load_chunk = [&](const uint4 *rs, uint32_t len, uint4 (&v)[kDecodeRecs / 2]) {
       const bool full = len == (uint32_t)CHUNK;
@@ -394,23 +394,13 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
       //      bin (pc / G) * 2R + class * R + reason | count << 13, stored at position cnt[b]++ of
       //      bucket b's zero-padded slot (invalid and padding records count in the dummy bucket G
       //      and land in a trash word; counts > 7 and slot overflow go through L2 atomics)
-      uint32_t vsum = 0, bads = 0, badr = 0, rare = 0;
-      static_assert(kDecodeRecs <= 32, "one rare bit per record");
+      uint32_t csum = 0, bads = 0, badr = 0;
       // records are processed in batches of kDecodeBatch pairs: all slot allocations (atomics) of a
-      // batch are issued before its key stores, so their latencies overlap.  Record word w =
-      // flags << 24 | reason << 16 | count, t = w >> 16.  Validity (Q12): t < R (ACT) or
-      // 0x101 <= t < 0x100 + R (LAT with a reason); then class * R + reason = t + flags * (R - 256).
-      // Fast records (valid, count <= 7) get key = local bin | count << 13 = the low 16 bits of
-      // (w << 13) + q * 2R + t + flags * (R - 256) (the st.u16 drops the reason / flag bits that
-      // w << 13 carries above bit 15).  Invalid records and counts > 7 go to the dummy bucket G,
-      // whose counter never hands out a slot, so one compare (pos < cap) selects the rare path
-      // for them and for slot overflow; it runs once per chunk and re-derives each case.  Samples
-      // of fast records are summed by the processors (from the keys), not here.
-      uint32_t cnt_r, sg_r, trash_r, nG_r;   // opaque copies: kept in registers, not rematerialised per record
-      asm volatile("mov.b32 %0, %1;" : "=r"(cnt_r) : "r"(cnt_addr));
-      asm volatile("mov.b32 %0, %1;" : "=r"(sg_r) : "r"(sg_addr));
-      asm volatile("mov.b32 %0, %1;" : "=r"(trash_r) : "r"(trash_addr));
-      asm volatile("mov.b32 %0, %1;" : "=r"(nG_r) : "r"(nG));
+      // batch are issued before its key stores, so their latencies overlap.  Validity (Q12): t =
+      // flags:reason is valid iff t < R (ACT) or 0x101 <= t < 0x100 + R (LAT with a reason); then
+      // class * R + reason = t - (t >> 8) * (256 - R).  Invalid records and counts > 7 go to the
+      // dummy bucket G, whose counter never hands out a slot, so one compare (pos < cap) selects
+      // the rare branch for them and for slot overflow; the branch re-derives which case it is.
 #pragma unroll
       for (int u0 = 0; u0 < kDecodeRecs / 2; u0 += kDecodeBatch) {
         constexpr int kB = 2 * kDecodeBatch;
@@ -422,53 +412,46 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
           if (u >= kDecodeRecs / 2) break;
           const uint4 v = vv[u];
           const uint32_t pc = h ? v.z : v.x, w = h ? v.w : v.y;
-          const uint32_t t = w >> 16;
-          const bool fast = pc < n_instr && (w & 0xfff8u) == 0u && (t < R || t - 0x101u < R - 1u);
-          const uint32_t q = __umulhi(pc, mg);
-          uint32_t b;
-          asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(b) : "r"(q), "r"(nG_r), "r"(pc));   // pc mod G
+          const uint32_t t = w >> 16, c = w & 0xffffu;
+          const uint32_t tl = t - (t >> 8) * (256u - R);
+          const bool fast = pc < n_instr && (t < R || t - 0x101u < R - 1u) && c <= kMaxKeyCount;
+          const uint32_t q = __umulhi(pc, mg), b = q * nG + pc;
           const uint32_t be = fast ? b : G;
-          key[i] = (w << kLocalBits) + q * twoR + t + (w >> 24) * Rm256;
-          slot[i] = sg_r + be * (kPartCap * 2);
+          key[i] = c * (1u << kLocalBits) + q * twoR + tl;
+          slot[i] = sg_addr + be * (kPartCap * 2);
 #ifndef GPA_ABLATE_DEC_ATOM
-          asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(pos[i]) : "r"(cnt_r + be * 4) : "memory");
+          asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(pos[i]) : "r"(cnt_addr + be * 4) : "memory");
 #else
-          pos[i] = (dtid + i) % 40u + (cnt_r == 0xFFFFFFFFu ? be : 0u);
+          pos[i] = (dtid + i) % 40u + (cnt_addr == 0xFFFFFFFFu ? be : 0u);
 #endif
+          csum += c;        // padding records have count 0
         }
 #pragma unroll
         for (int i = 0; i < kB; ++i) {
           const int u = u0 + i / 2, h = i & 1;
           if (u >= kDecodeRecs / 2) break;
           const bool keep = pos[i] < (uint32_t)kPartCap;
-          const uint32_t dst = keep ? slot[i] + pos[i] * 2 : trash_r;
+          const uint32_t dst = keep ? slot[i] + pos[i] * 2 : trash_addr;
 #ifndef GPA_ABLATE_DEC_STS
           asm volatile("st.shared.u16 [%0], %1;" ::"r"(dst), "h"((unsigned short)key[i]) : "memory");
 #else
           if (dst == 0xFFFFFFFFu) asm volatile("st.shared.u16 [%0], %1;" ::"r"(dst), "h"((unsigned short)key[i]) : "memory");
 #endif
-          rare |= keep ? 0u : 1u << (2 * u + h);
-        }
-      }
-      if (rare) {   // rare: an invalid record, a count > 7 or slot overflow (skew); one branch per chunk
-#pragma unroll
-        for (int i = 0; i < kDecodeRecs; ++i) {
-          if (!((rare >> i) & 1u)) continue;
-          const int u = i / 2, h = i & 1;
-          const uint4 v = vv[u];
-          const uint32_t pc = h ? v.z : v.x, w = h ? v.w : v.y;
-          const uint32_t t = w >> 16, c = w & 0xffffu;
-          if (pc < n_instr && (t < R || t - 0x101u < R - 1u)) {
-            const uint32_t tl = t - (t >> 8) * (256u - R);
-            atomicAdd((unsigned long long *)&a.C[(uint64_t)pc * twoR + tl], (unsigned long long)c);
-            vsum += c;
-          } else {
-            bads += c;
-            badr += (full || 2 * (u * kDecodeThreads + dtid) < len) ? 1u : 0u;   // padding is not a record
+          if (!keep) {       // rare: an invalid record, a count > 7 or slot overflow (skew)
+            const uint4 v = vv[u];
+            const uint32_t pc = h ? v.z : v.x, w = h ? v.w : v.y;
+            const uint32_t t = w >> 16, c = w & 0xffffu;
+            if (pc < n_instr && (t < R || t - 0x101u < R - 1u)) {
+              const uint32_t tl = t - (t >> 8) * (256u - R);
+              atomicAdd((unsigned long long *)&a.C[(uint64_t)pc * twoR + tl], (unsigned long long)c);
+            } else {
+              bads += c;
+              badr += (full || 2 * (u * kDecodeThreads + dtid) < len) ? 1u : 0u;   // padding is not a record
+            }
           }
         }
       }
-      st.valid += vsum;
+      st.valid += csum - bads;
       st.bad_samples += bads;
       st.bad_records += badr;
       // generic-proxy staging writes must be ordered before the control warp's bulk store
@@ -572,7 +555,6 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
     } else {
       const uint32_t ctid = tid - kProcBase;
       const uint32_t tab_addr = smem_addr(tab), dummy_addr = smem_addr(tab + a.bpb + (ctid & 31));
-      uint32_t psum = 0;   // < 2^32: flushed into st.valid every chunk
       PT_DECL
       for (uint32_t j = 0; j < n_chunks; ++j) {
         PT_START;
@@ -586,7 +568,6 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
           for (int e = 0; e < 8; ++e) {
             const uint32_t key = (w4[e >> 1] >> ((e & 1) * 16)) & 0xffffu;
             const uint32_t c = key >> kLocalBits;
-            psum += c;   // the samples of fast records (the decoders count only the rare ones)
             // padding keys (c = 0) add 0 to a lane-distinct dummy word: cheaper on the shared-memory
             // pipe than a predicated (branching) update, measured
             const uint32_t addr = c ? tab_addr + (key & ((1u << kLocalBits) - 1)) * 4 : dummy_addr;
@@ -597,8 +578,6 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
 #endif
           }
         }
-        st.valid += psum;
-        psum = 0;
         PT_MARK(10);
         named_bar(kBarProc, kProcThreads);   // inbox slot j%kInbox fully read
         PT_MARK(11);
