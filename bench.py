@@ -317,6 +317,14 @@ def run_batch(args):
                          "ingest_share_of_step": ingest_ms / ms_per_step, "blame_rollup_estimate_ms": analyze_ms},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
         }
+        if world > 1:
+            # the DP-1 exchange: one SUM all-reduce of [counts | stats]; bus bandwidth 2(p-1)/p * bytes / t
+            # against NVLink 5's 900 GB/s per direction; the time includes the
+            # collective's wait for the slowest rank's ingest, so it bounds the exchange from above
+            rb = red.numel() * 8
+            bus = 2 * (world - 1) / world * rb / (reduce_ms / 1e3) / 1e9 if reduce_ms > 0 else None
+            line["allreduce"] = {"bytes": rb, "ms": reduce_ms, "busbw_gbs": bus, "peak_gbs": 900.0,
+                                 "frac": bus / 900.0 if bus else None, "backend": dist.get_backend()}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -369,10 +377,9 @@ def main():
     recs = spec.device(rank * n_per, n_per)          # this rank's shard, device-resident
     torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
-    counts = P.view("counts")
-    stats = P.view("stats")
+    red = P.reduce_view()    # [counts | stats]: the one buffer the DP-1 step all-reduces
 
-    def step(ev_a=None, ev_b=None, ev_c=None):
+    def step(ev_a=None, ev_b=None, ev_c=None, ev_r=None):
         P.reset()
         if ev_a is not None:
             ev_a.record(stream)
@@ -380,8 +387,9 @@ def main():
         if ev_b is not None:
             ev_b.record(stream)
         if world > 1:
-            dist.all_reduce(counts, op=dist.ReduceOp.SUM)
-            dist.all_reduce(stats, op=dist.ReduceOp.SUM)
+            dist.all_reduce(red, op=dist.ReduceOp.SUM)
+        if ev_r is not None:
+            ev_r.record(stream)
         P.analyze()          # blame + aggregate + estimate (one CUDA graph of the library's kernels)
         if ev_c is not None:
             ev_c.record(stream)
@@ -399,7 +407,7 @@ def main():
     sampler = ClockSampler(local)
     sampler.start()
     time.sleep(0.3)
-    ing = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(3)) for _ in range(args.steps)]
+    ing = [tuple(torch.cuda.Event(enable_timing=True) for _ in range(4)) for _ in range(args.steps)]
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = P.launches
     torch.cuda.synchronize()
@@ -413,12 +421,13 @@ def main():
         dist.barrier()
     clocks = sampler.stop()
     ms = t0.elapsed_time(t1)
-    ingest_ms = sum(a.elapsed_time(b) for a, b, _ in ing) / args.steps
-    analyze_ms = sum(b.elapsed_time(c) for _, b, c in ing) / args.steps
+    ingest_ms = sum(a.elapsed_time(b) for a, b, _, _ in ing) / args.steps
+    analyze_ms = sum(r.elapsed_time(c) for _, _, c, r in ing) / args.steps
+    reduce_ms = sum(b.elapsed_time(r) for _, b, _, r in ing) / args.steps
     if world > 1:
-        t = torch.tensor([ms, ingest_ms], dtype=torch.float64, device=dev)
+        t = torch.tensor([ms, ingest_ms, reduce_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, ingest_ms = float(t[0]), float(t[1])
+        ms, ingest_ms, reduce_ms = float(t[0]), float(t[1]), float(t[2])
     ms_per_step = ms / args.steps
 
     # correctness guard on the timed output: every record of every rank was counted
@@ -444,8 +453,7 @@ def main():
             P.reset()
             P.ingest_host(host)
             if world > 1:
-                dist.all_reduce(counts, op=dist.ReduceOp.SUM)
-                dist.all_reduce(stats, op=dist.ReduceOp.SUM)
+                dist.all_reduce(red, op=dist.ReduceOp.SUM)
             P.analyze()
             P.read_estimates_array()
         eb.record(stream)
@@ -490,6 +498,14 @@ def main():
                          "blame_rollup_estimate_ms": analyze_ms},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
         }
+        if world > 1:
+            # the DP-1 exchange: one SUM all-reduce of [counts | stats]; bus bandwidth 2(p-1)/p * bytes / t
+            # against NVLink 5's 900 GB/s per direction; the time includes the
+            # collective's wait for the slowest rank's ingest, so it bounds the exchange from above
+            rb = red.numel() * 8
+            bus = 2 * (world - 1) / world * rb / (reduce_ms / 1e3) / 1e9 if reduce_ms > 0 else None
+            line["allreduce"] = {"bytes": rb, "ms": reduce_ms, "busbw_gbs": bus, "peak_gbs": 900.0,
+                                 "frac": bus / 900.0 if bus else None, "backend": dist.get_backend()}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -313,8 +313,10 @@ Offsets layout(const gpa_program_desc *d, const HostPlan &h) {
   Layout a;
   Offsets o;
   // outputs first (large, hot)
-  o.C = a.take(n * 2 * R * 8);
-  o.stats = a.take(4 * 8);
+  // the count table and the stats are one contiguous block, so a multi-GPU step sums both with
+  // a single collective (Program.reduce_view)
+  o.C = a.take(n * 2 * R * 8 + 4 * 8);
+  o.stats = o.C + n * 2 * R * 8;
   o.AL = a.take(n * 2 * 8);
   o.cand = a.take(E);
   o.selfm = a.take(n);

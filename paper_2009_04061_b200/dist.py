@@ -33,7 +33,7 @@ def sharded_step(program, records, group=None, stream=None, estimate=True):
     program.reset(stream)
     program.ingest(records, stream=stream)
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        allreduce_counts(program.view("counts"), program.view("stats"), group)
+        dist.all_reduce(program.reduce_view(), op=dist.ReduceOp.SUM, group=group)   # counts + stats, one call
     if estimate:
         program.analyze(stream)      # blame + aggregate + estimate as one CUDA graph
     else:

@@ -397,6 +397,20 @@ class Program:
         _check(lib().gpa_get_stats(self.handle, out, self._s(stream)), "gpa_get_stats")
         return [int(x) for x in out]
 
+    def reduce_view(self):
+        """int64 view (no copy) of the count table followed by the 4 stats words: the one buffer a
+        data-parallel step all-reduces (they are contiguous in the workspace by construction)."""
+        torch = self.torch
+        offs = []
+        for name in ("counts", "stats"):
+            off, nb = ctypes.c_uint64(0), ctypes.c_uint64(0)
+            _check(lib().gpa_view(self.handle, VIEW[name], ctypes.byref(off), ctypes.byref(nb)), "gpa_view")
+            offs.append((off.value, nb.value))
+        (c0, cn), (s0, sn) = offs
+        if s0 != c0 + cn:
+            raise RuntimeError("count table and stats are not contiguous in the workspace")
+        return self.ws[c0: s0 + sn].view(torch.int64)
+
     def view(self, name):
         """torch view (no copy) of a device result inside the workspace."""
         torch = self.torch

@@ -122,3 +122,46 @@ def test_dp2_reduce_scatter_path_single_rank_nccl():
         compare(g, o, rel=REL)
     finally:
         dist.destroy_process_group()
+
+
+def test_dp1_reduce_view_single_collective_nccl():
+    """DP-1 exchange: the count table and the stats are one contiguous buffer
+    (Program.reduce_view), so one SUM all-reduce combines ranks.  The view aliases both results,
+    and a world-size-1 NCCL sharded_step equals the oracle on the shard; summing two shards'
+    views equals ingesting both shards (integer monoid)."""
+    import os
+    import socket
+    import torch
+    import torch.distributed as dist
+    import gpagen
+    from paper_2009_04061_b200 import Program
+    from paper_2009_04061_b200.dist import sharded_step
+    from gpagen.patterns import table2
+    from tests._common import collect
+    prog = gpagen.random_program(900, 4, 10, 3, seed=77)
+    recs = StreamSpec(prog, seed=78, count_max=9, invalid_ppm=5_000).host(0, 300_001)
+    half = len(recs) // 2
+    A, B, AB = Program(prog), Program(prog), Program(prog)
+    for P, part in ((A, recs[:half]), (B, recs[half:]), (AB, recs)):
+        P.reset()
+        P.ingest(torch.from_numpy(np.ascontiguousarray(part).view(np.int64)).cuda())
+    torch.cuda.synchronize()
+    ra = A.reduce_view()
+    assert ra.numel() == prog.n_instr * 2 * prog.n_reasons + 4
+    assert torch.equal(ra[:-4], A.view("counts").flatten()) and torch.equal(ra[-4:], A.view("stats"))
+    ra += B.reduce_view()          # what the all-reduce computes for two ranks
+    assert torch.equal(ra, AB.reduce_view())
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        P = Program(prog)
+        P.set_patterns(table2(prog.n_reasons))
+        sharded_step(P, torch.from_numpy(recs.view(np.int64)).cuda())
+        torch.cuda.synchronize()
+        compare(collect(P), run_oracle(prog, recs), rel=REL)
+    finally:
+        dist.destroy_process_group()
