@@ -14,7 +14,10 @@ constexpr int kReasonsMax = 16;
 constexpr int kColsMax = kReasonsMax + 6;   // NCOL = R + 6
 constexpr int kSlotsMax = 2 * kColsMax + 2; // V values + (A, L)
 constexpr int kPatternsMax = 32;
-constexpr int kChunk = 128;                 // rollup chunk length (instructions)
+#ifndef GPA_ROLL_CHUNK
+#define GPA_ROLL_CHUNK 64
+#endif
+constexpr int kChunk = GPA_ROLL_CHUNK;      // rollup chunk length (instructions), a multiple of 32
 constexpr int kMaxIngestCtas = 256;         // per-CTA partial tables reserved (smem variant)
 constexpr size_t kSmemTableMax = 224 * 1024;// largest CTA-private table (bytes; sm_100a opt-in is 227 KB)
 // partitioned ingest (variant P): bucket exchange through L2

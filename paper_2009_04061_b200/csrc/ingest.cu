@@ -147,13 +147,21 @@ k_ingest(const uint2 *__restrict__ rec, uint64_t n_rec, uint32_t head, uint32_t 
   }
 }
 
-// Sum the per-CTA tables bin by bin (coalesced across threads) into the u64 table.
+// Sum the per-CTA tables bin by bin (coalesced across threads) into the u64 table: blockIdx.y
+// takes a group of kReduceGroup CTA tables (all loads of a thread independent and in flight
+// together), and the group sums meet in C through u64 atomics (integer adds: exact in any order).
+constexpr uint32_t kReduceGroup = 16;
 __global__ void k_ingest_reduce(const uint32_t *__restrict__ partials, uint32_t n_ctas,
                                 uint32_t bins, uint64_t *__restrict__ C) {
+  const uint32_t c0 = blockIdx.y * kReduceGroup;
   for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < bins; b += gridDim.x * blockDim.x) {
+    uint32_t v[kReduceGroup];
+#pragma unroll
+    for (uint32_t c = 0; c < kReduceGroup; ++c) v[c] = c0 + c < n_ctas ? partials[(uint64_t)(c0 + c) * bins + b] : 0u;
     uint64_t s = 0;
-    for (uint32_t c = 0; c < n_ctas; ++c) s += partials[(uint64_t)c * bins + b];
-    if (s) C[b] += s;
+#pragma unroll
+    for (uint32_t c = 0; c < kReduceGroup; ++c) s += v[c];
+    if (s) atomicAdd((unsigned long long *)&C[b], (unsigned long long)s);
   }
 }
 
@@ -795,8 +803,9 @@ cudaError_t launch_ingest(const DevProgram &p, int variant, const void *records,
     k_ingest<true><<<grid, kIngestThreads, smem, s>>>(rec, n, head, p.n, p.R, bins, p.C, p.partials, p.stats);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
+    const uint32_t groups = (grid + kReduceGroup - 1) / kReduceGroup;
     const uint32_t rgrid = std::max<uint32_t>(1, std::min<uint32_t>((bins + 255) / 256, 4 * n_sms));
-    k_ingest_reduce<<<rgrid, 256, 0, s>>>(p.partials, grid, bins, p.C);
+    k_ingest_reduce<<<dim3(rgrid, groups), 256, 0, s>>>(p.partials, grid, bins, p.C);
     return cudaGetLastError();
   }
   if (variant == VAR_L2) {

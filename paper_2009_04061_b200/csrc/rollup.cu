@@ -96,7 +96,7 @@ __device__ __forceinline__ void warp_sum_rows(uint32_t lane, uint32_t nv, uint32
 }
 
 #ifndef GPA_ROLL_MEMBERS
-#define GPA_ROLL_MEMBERS 8
+#define GPA_ROLL_MEMBERS 16
 #endif
 constexpr int kRollMembers = GPA_ROLL_MEMBERS;   // members (row loads) in flight per lane
 
