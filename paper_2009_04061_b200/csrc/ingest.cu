@@ -23,6 +23,7 @@
 // Variant L (k_ingest_l2): tables larger than shared memory; one RED.E.ADD.64 per record into
 //   the L2-resident u64 table.
 #include <algorithm>
+#include <cstdlib>
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -255,8 +256,8 @@ constexpr int kTrash = 32;                         // lane-distinct sink for dro
 constexpr uint32_t kLocalBits = 13;                // key = local bin (13 bits) | count (3 bits)
 constexpr uint32_t kMaxKeyCount = 7;
 constexpr uint32_t kDummyCount = 1u << 30;        // dummy-bucket counter start (never < kPartCap)
-// a chunk adds at most G * cap * 7 samples to any one table entry: flushing the u32 table every
-// kFlushEvery chunks keeps every entry below 2^32
+// a chunk adds at most G * cap * 7 samples to any one table entry: a launch of at most kFlushEvery
+// chunks (the host splits longer streams) keeps every entry below 2^32 until the final flush
 constexpr uint32_t kBarProc = 2;   // named barrier of the processor warps (0 is __syncthreads)
 constexpr uint32_t kFlushEvery = (uint32_t)(0xffffffffull / ((uint64_t)kPartMaxCtas * kPartCap * kMaxKeyCount));
 static_assert(kPartChunk % (2 * kDecodeThreads) == 0, "whole record pairs per decode thread");
@@ -593,14 +594,6 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
           mbar_arrive(&inbox_free[j % kInbox]);
           red_release_add(&a.sync[kPartBufs + j % kPartBufs], 1u);   // this CTA drained chunk j
         }
-        if ((j + 1) % kFlushEvery == 0) {   // u32 table entries cannot wrap: flush every kFlushEvery chunks
-          for (uint32_t i = ctid; i < a.bpb; i += kProcThreads) {
-            const uint32_t bin = ((i / twoR) * G + me) * twoR + i % twoR;
-            if (tab[i]) atomicAdd((unsigned long long *)&a.C[bin], (unsigned long long)tab[i]);
-            tab[i] = 0;
-          }
-          named_bar(kBarProc, kProcThreads);
-        }
       }
       PT_FLUSH;
     }
@@ -845,8 +838,28 @@ cudaError_t launch_ingest(const DevProgram &p, int variant, const void *records,
     CUtensorMap xmap;
     e = make_exchange_map(&xmap, p.part_x, G);
     if (e != cudaSuccess) return e;
-    void *args[] = {&a, &xmap};
-    return cudaLaunchCooperativeKernel(kern, dim3(G), dim3(kPartThreads), args, smem, s);
+    // a launch runs at most kFlushEvery chunks, so no u32 table entry can wrap before the
+    // kernel's final flush into the u64 table (> 6.5e10 records: several launches)
+    // (GPA_PART_LAUNCH_CHUNKS lowers the limit: a test hook that exercises the split on small streams)
+    uint64_t launch_chunks = kFlushEvery;
+    if (const char *env = getenv("GPA_PART_LAUNCH_CHUNKS")) {
+      const unsigned long long v = strtoull(env, nullptr, 10);
+      if (v > 0 && v < launch_chunks) launch_chunks = v;
+    }
+    const uint64_t body = a.n_even, max_launch = launch_chunks * G * kPartChunk;
+    const uint2 *base = a.rec;
+    for (uint64_t off = 0; off < body; off += max_launch) {
+      a.rec = base + off;
+      a.n_even = std::min<uint64_t>(max_launch, body - off);
+      if (off > 0) {
+        e = cudaMemsetAsync(p.part_sync, 0, 2 * kPartBufs * sizeof(unsigned int), s);
+        if (e != cudaSuccess) return e;
+      }
+      void *args[] = {&a, &xmap};
+      e = cudaLaunchCooperativeKernel(kern, dim3(G), dim3(kPartThreads), args, smem, s);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
   }
   return cudaErrorNotSupported;
 }

@@ -231,3 +231,30 @@ def test_read_estimates_array_matches_struct_list():
             for f in ("speedup", "M", "eq3", "eq4", "T", "A", "best_scope", "unbounded", "matched", "model"):
                 a, b = getattr(e, f), arr[k, q][f]
                 assert a == b or (np.isnan(a) and np.isnan(b))
+
+
+def test_part_stream_split_into_launches(monkeypatch):
+    """Streams longer than one launch's wrap-free bound (kFlushEvery chunks, ~6.5e10 records at
+    G = 148) are split by the host into several launches, each ending with its u32 -> u64 flush.
+    The bound is lowered through the test hook so a small stream spans several launches."""
+    monkeypatch.setenv("GPA_PART_LAUNCH_CHUNKS", "2")
+    prog = gp.random_program(6000, 6, 20, 4, seed=51)
+    recs = StreamSpec(prog, seed=52, count_max=9, invalid_ppm=2_000).host(0, 4_000_001)
+    g = run_gpu(prog, recs, offset_records=1)
+    assert g["program"].variant == "part"
+    compare(g, run_oracle(prog, recs), rel=REL)
+
+
+def test_smem_table_u32_wrap_carried():
+    """Variant S keeps u32 per-CTA tables: a bin that passes 2^32 inside one CTA (68k records of
+    count 65535 per CTA on one (pc, class, reason)) is carried into the u64 table exactly."""
+    prog = gp.random_program(300, 2, 6, 3, seed=61)
+    hot = np.uint64(5) | (np.uint64(65535) << np.uint64(32)) | (np.uint64(1) << np.uint64(48)) \
+        | (np.uint64(1) << np.uint64(56))                        # pc 5, count 65535, MEM, LAT
+    recs = np.full(10_000_000, hot, dtype=np.uint64)
+    recs[::97] = StreamSpec(prog, seed=62, count_max=4).host(0, len(recs[::97]))
+    g = run_gpu(prog, recs)
+    assert g["program"].variant == "smem"
+    o = run_oracle(prog, recs)
+    assert int(o["C"].max()) > 2 ** 32 * 100
+    compare(g, o, rel=REL)
