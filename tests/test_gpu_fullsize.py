@@ -58,3 +58,55 @@ def test_config4_full_batch_as_benchmarked():
     P.analyze()
     torch.cuda.synchronize()
     compare(collect(P), run_oracle(prog, host), rel=REL)
+
+
+def test_config5_ten_billion_samples_as_eight_shards():
+    """Config 5 at full size on one B200: the 10^10-record stream cut into the 8 rank shards
+    bench.py uses (1.25e9 records each, counter-based, so every shard is the same records at any
+    rank count).  Each shard is histogrammed by the partitioned ingest into its own program; the
+    sum of the shards' [counts | stats] views (what the DP-1 all-reduce computes) equals the
+    L2-atomic variant's table over all 10^10 records, bit for bit, and holds every sample.  The
+    replicated analysis of the summed table matches the oracle run on the same counts."""
+    import torch
+    import oracle
+    from paper_2009_04061_b200 import Program
+    from tests._common import oracle_pattern
+    free, _ = torch.cuda.mem_get_info()
+    if free < 40 * 2 ** 30:
+        pytest.skip("needs ~12 GB of device memory")
+    prog = gp.config_program(3)
+    spec = config_stream(prog, 3)
+    world, n_per = 8, 1_250_000_000
+    buf = torch.empty(n_per * 8, dtype=torch.uint8, device="cuda")
+    L = Program(prog)
+    L.variant = "l2"
+    L.reset()
+    total = None
+    for r in range(world):
+        spec.device(r * n_per, n_per, out_tensor=buf)
+        P = Program(prog)
+        assert P.variant == "part"
+        P.reset()
+        P.ingest(buf)
+        L.ingest(buf)
+        v = P.reduce_view().clone()
+        total = v if total is None else total + v
+        del P
+    torch.cuda.synchronize()
+    del buf
+    assert torch.equal(total, L.reduce_view())
+    assert int(total[-4]) == world * n_per and int(total[-3]) == 0     # count-1 records, all valid
+    pats = table2(prog.n_reasons)
+    A = Program(prog)
+    A.set_patterns(pats)
+    A.reset()
+    A.reduce_view().copy_(total)
+    A.analyze()
+    torch.cuda.synchronize()
+    g = collect(A)
+    C = total[:-4].cpu().numpy().view(np.uint64).reshape(prog.n_instr, 2, prog.n_reasons)
+    op = oracle.OracleProgram(prog)
+    b = op.blame(C)
+    o = {"C": C, "stats": total[-4:-1].cpu().numpy().view(np.uint64), **b, **op.rollup(C, b["V"]),
+         "est": op.estimate(C, b, [oracle_pattern(p) for p in pats])}
+    compare(g, o, rel=REL)
