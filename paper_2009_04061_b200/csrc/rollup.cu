@@ -77,6 +77,18 @@ __device__ __forceinline__ void warp_sum_rows(uint32_t lane, uint32_t nv, uint32
     if (s < nv) {
       double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
       uint32_t pos = b;
+      for (; pos + 16 <= e; pos += 16) {   // 16 row loads in flight; member u still adds into a(u % 4)
+        double x[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) x[u] = vals[(uint64_t)item(pos + u) * nv + s];
+#pragma unroll
+        for (int u = 0; u < 16; u += 4) {
+          a0 = __dadd_rn(a0, x[u]);
+          a1 = __dadd_rn(a1, x[u + 1]);
+          a2 = __dadd_rn(a2, x[u + 2]);
+          a3 = __dadd_rn(a3, x[u + 3]);
+        }
+      }
       for (; pos + 4 <= e; pos += 4) {
         const double x0 = vals[(uint64_t)item(pos) * nv + s], x1 = vals[(uint64_t)item(pos + 1) * nv + s];
         const double x2 = vals[(uint64_t)item(pos + 2) * nv + s], x3 = vals[(uint64_t)item(pos + 3) * nv + s];
