@@ -1,5 +1,5 @@
 """Tuning probe: median time of the analysis graph (gpa_analyze: blame + rollup + estimate) for
-configs 2 and 3 with an alternative build of the library (`python tools/analyze_time.py lib|product`)."""
+configs 2 and 3 with an alternative build of the library (`python tools/analyze_time.py lib|product [2,3,4]`)."""
 import os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -11,10 +11,16 @@ from paper_2009_04061_b200 import gpa as G
 lib_path = sys.argv[1]
 if lib_path != "product":
     G.LIB_PATH = os.path.join(ROOT, lib_path)
+from gpagen import batch
+cfgs = [int(c) for c in sys.argv[2].split(",")] if len(sys.argv) > 2 else [2, 3]
 out = []
-for cfg, n in ((2, 10_000_000), (3, 100_000_000)):
-    prog = gpagen.config_program(cfg)
-    recs = gpagen.config_stream(prog, cfg).device(0, n)
+for cfg in cfgs:
+    if cfg == 4:    # the batch program; plain ingest gives the same counts as the segment ingest
+        prog = batch.config4_program()
+        recs = batch.config4_stream(prog).device(0, 100_000_000)
+    else:
+        prog = gpagen.config_program(cfg)
+        recs = gpagen.config_stream(prog, cfg).device(0, {2: 10_000_000, 3: 100_000_000}[cfg])
     P = G.Program(prog)
     P.set_patterns(table2(prog.n_reasons))
     P.reset(); P.ingest(recs)
