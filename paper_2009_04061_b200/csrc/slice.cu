@@ -11,6 +11,7 @@
 // open-addressing index), so the work is an irregular per-thread graph walk with no
 // communication.  Two launches: edge counts per use, then (after a host prefix sum) the edges.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "gpa_internal.cuh"
@@ -353,9 +354,16 @@ cudaError_t launch_slice(const gpa_sass_desc *h, uint32_t *h_row_ptr, uint64_t c
             (const uint8_t *)up(h->guard, n), (const uint8_t *)up(h->wbar, n), (const uint8_t *)up(h->rbar, n),
             (const uint8_t *)up(h->wait, n), (const uint16_t *)up(h->dst, (size_t)n * 8),
             (const uint16_t *)up(h->src, (size_t)n * 8)};
-  // threads: enough for the GPU, bounded by a ~2 GB scratch
+  // threads: one per use up to what the GPU holds, bounded by the scratch budget (a quarter of the
+  // free device memory, at most GPA_SLICE_SCRATCH_MB, default 4 GB: measured best of 1-16 GB, the
+  // mapping of a larger pool allocation costs more than the extra concurrency saves)
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) free_b = 2ull << 30;
+  uint64_t budget = std::min<uint64_t>(free_b / 4, 4ull << 30);
+  if (const char *env = getenv("GPA_SLICE_SCRATCH_MB")) budget = std::min<uint64_t>(budget, strtoull(env, nullptr, 10) << 20);
+  budget = std::max<uint64_t>(budget, 64ull << 20);
   uint64_t threads = std::min<uint64_t>((uint64_t)std::max(n_sms, 1) * 8 * kSlThreads, ((uint64_t)n + kSlThreads - 1) / kSlThreads * kSlThreads);
-  threads = std::min<uint64_t>(threads, std::max<uint64_t>(kSlThreads, ((2ull << 30) / per_thread) / kSlThreads * kSlThreads));
+  threads = std::min<uint64_t>(threads, std::max<uint64_t>(kSlThreads, (budget / per_thread) / kSlThreads * kSlThreads));
   threads = std::max<uint64_t>(threads, kSlThreads);
   void *d_scr = alloc(threads * per_thread), *d_cnt = alloc((size_t)std::max<uint32_t>(n, 1) * 4), *d_err = alloc(4);
   if (e == cudaSuccess) e = cudaMemsetAsync(d_err, 0, 4, st);

@@ -148,9 +148,9 @@ def slice_sass(sass, stream=None):
                                                  "src", "wbar", "rbar", "wait")])
     row_ptr = np.zeros(n + 1, np.uint32)
     ne = ctypes.c_uint64(0)
-    cap = 0
+    cap = 8 * n + 1024   # room for the usual ~2 edges per instruction: one call (a second only on overflow)
     out = None
-    for _ in range(2):   # the first call may only report the edge count
+    for _ in range(2):   # a call with too small arrays reports the edge count, then the retry fills them
         out = {"edge_def": np.zeros(max(cap, 1), np.uint32), "edge_kind": np.zeros(max(cap, 1), np.uint8),
                "edge_min_len": np.zeros(max(cap, 1), np.uint32), "edge_max_len": np.zeros(max(cap, 1), np.uint32),
                "edge_dom_k": np.zeros(max(cap, 1), np.int32)}
