@@ -18,6 +18,7 @@ namespace {
 
 __global__ void k_summaries(const uint64_t *__restrict__ C, uint32_t n, uint32_t R,
                             uint64_t *__restrict__ AL) {
+  pdl_wait();
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const uint64_t *row = C + (uint64_t)i * 2 * R;
     uint64_t a = 0, l = 0;
@@ -37,6 +38,7 @@ __device__ __forceinline__ uint32_t rule1_mask(uint32_t c) {
 }
 
 __global__ void k_blame_rows(DevProgram p) {
+  pdl_wait();
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < p.n; j += gridDim.x * blockDim.x) {
     const uint64_t *row = p.C + (uint64_t)j * 2 * p.R;
     const uint64_t dep = row[R_MEM] + row[p.R + R_MEM] + row[R_EXEC] + row[p.R + R_EXEC] +
@@ -86,6 +88,7 @@ __global__ void k_blame_rows(DevProgram p) {
 }
 
 __global__ void k_def_reduce(DevProgram p) {
+  pdl_wait();
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += gridDim.x * blockDim.x) {
     double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
     for (uint32_t k = p.def_ptr[i]; k < p.def_ptr[i + 1]; ++k) {
@@ -121,16 +124,17 @@ inline uint32_t grid_for(uint64_t items, uint32_t threads, int n_sms) {
 // summaries + candidates / shares / self flags (rows a2-a4): everything the estimate step reads
 cudaError_t launch_blame_rows(const DevProgram &p, int n_sms, cudaStream_t s, uint64_t *launches) {
   k_summaries<<<grid_for(p.n, 256, n_sms), 256, 0, s>>>(p.C, p.n, p.R, p.AL);
-  k_blame_rows<<<grid_for(p.n, 128, n_sms), 128, 0, s>>>(p);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = launch_pdl(p.n, k_blame_rows, grid_for(p.n, 128, n_sms), 128, 0, s, p);
   *launches += 2;
-  return cudaGetLastError();
+  return e;
 }
 
 // def-side reduction (rows a5-a6): B, read by the rollup only
 cudaError_t launch_def_reduce(const DevProgram &p, int n_sms, cudaStream_t s, uint64_t *launches) {
-  k_def_reduce<<<grid_for(p.n, 128, n_sms), 128, 0, s>>>(p);
+  const cudaError_t e = launch_pdl(p.n, k_def_reduce, grid_for(p.n, 128, n_sms), 128, 0, s, p);
   *launches += 1;
-  return cudaGetLastError();
+  return e;
 }
 
 cudaError_t launch_blame(const DevProgram &p, int n_sms, cudaStream_t s, uint64_t *launches) {

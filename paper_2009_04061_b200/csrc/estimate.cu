@@ -28,6 +28,7 @@ namespace {
 constexpr int kEstGroup = GPA_EST_GROUP;
 
 __global__ void k_est_rows(DevProgram p, EstimatePlan ep) {
+  pdl_wait();
   __shared__ gpa_pattern sp[kPatternsMax];
   __shared__ int8_t sslot[kPatternsMax];
   for (uint32_t q = threadIdx.x; q < ep.n_pat; q += blockDim.x) {
@@ -89,6 +90,7 @@ __global__ void k_est_rows(DevProgram p, EstimatePlan ep) {
 // per-edge matched samples of the loop-scoped patterns (mval[slot][e]), edge-parallel and
 // coalesced; the same arithmetic as k_est_rows, so the item values and the row sums agree
 __global__ void k_est_edges(DevProgram p, EstimatePlan ep) {
+  pdl_wait();
   __shared__ gpa_pattern sp[kPatternsMax];
   __shared__ int8_t sslot[kPatternsMax];
   __shared__ uint32_t slot_q[kPatternsMax], n_slot_q;
@@ -139,6 +141,7 @@ struct SegLaunch {
 };
 
 __global__ void k_segsum(SegLaunch L) {
+  pdl_wait();
   const uint32_t lane = threadIdx.x & 31;
   const SegFamily &F = L.fam[blockIdx.y];
   const uint64_t items = (uint64_t)F.n_seg * L.n_pat;
@@ -179,6 +182,7 @@ __device__ __forceinline__ double eq2(double T, double M) {
 // takes the max with ties to the lowest scope id (loops before functions), as a sequential scan
 // in scope order would.
 __global__ void k_est_final(DevProgram p, EstimatePlan ep) {
+  pdl_wait();
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t total = p.n_kernels * ep.n_pat;
   const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
@@ -277,7 +281,8 @@ cudaError_t launch_estimate_sums(const DevProgram &p, const EstimatePlan &ep, in
   for (uint32_t q = 0; q < ep.n_pat; ++q) any_slot |= ep.loop_slot[q] >= 0;
   if (any_slot && p.E) {
     const uint32_t ge = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(((uint64_t)p.E + 255) / 256, (uint64_t)n_sms * 16));
-    k_est_edges<<<ge, 256, 0, s>>>(p, ep);
+    const cudaError_t e = launch_pdl(p.n, k_est_edges, ge, 256, 0, s, p, ep);
+    if (e != cudaSuccess) return e;
     *launches += 1;
   }
   SegLaunch a{};
@@ -292,7 +297,8 @@ cudaError_t launch_estimate_sums(const DevProgram &p, const EstimatePlan &ep, in
   }
   const uint64_t w1 = std::max<uint64_t>((uint64_t)p.n_loops, p.n_funcs) * ep.n_pat;
   dim3 g1((uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((w1 + 3) / 4, (uint64_t)n_sms * 32)), 2);
-  k_segsum<<<g1, 128, 0, s>>>(a);
+  cudaError_t e = launch_pdl(p.n, k_segsum, g1, 128, 0, s, a);
+  if (e != cudaSuccess) return e;
   // stage 2: loops inclusive (preorder subtree ranges over exclusive sums) and kernels
   SegLaunch b{};
   b.n_pat = ep.n_pat;
@@ -305,9 +311,9 @@ cudaError_t launch_estimate_sums(const DevProgram &p, const EstimatePlan &ep, in
   }
   const uint64_t w2 = std::max<uint64_t>((uint64_t)p.n_loops, p.n_kernels) * ep.n_pat;
   dim3 g2((uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((w2 + 3) / 4, (uint64_t)n_sms * 32)), 2);
-  k_segsum<<<g2, 128, 0, s>>>(b);
+  e = launch_pdl(p.n, k_segsum, g2, 128, 0, s, b);
   *launches += 3;
-  return cudaGetLastError();
+  return e;
 }
 
 // Eqs. 2-5 / 10 per (kernel, pattern): needs the sums above and the rollup's A sums

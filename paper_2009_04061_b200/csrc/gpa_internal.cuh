@@ -3,6 +3,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <utility>
 
 #include <vector>
 
@@ -20,6 +21,31 @@ constexpr int kPatternsMax = 32;
 constexpr int kChunk = GPA_ROLL_CHUNK;      // rollup chunk length (instructions), a multiple of 32
 constexpr int kMaxIngestCtas = 256;         // per-CTA partial tables reserved (smem variant)
 constexpr size_t kSmemTableMax = 224 * 1024;// largest CTA-private table (bytes; sm_100a opt-in is 227 KB)
+// Programmatic dependent launch (sm_90+): the analysis kernels start with griddepcontrol.wait, so
+// a kernel launched with the programmatic-serialization attribute may be scheduled while its
+// predecessor drains and waits for its completion (and memory flush) before touching any data.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+#ifndef GPA_PDL
+#define GPA_PDL 1
+#endif
+// Only for programs below kPdlMaxInstr instructions: there the analysis kernels are short and
+// latency-bound (config 3: 92 -> 82 us); on config 4's 4.5 M instructions the overlap cost 1 %.
+constexpr uint32_t kPdlMaxInstr = 1u << 20;
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(uint32_t n_instr, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = GPA_PDL && n_instr < kPdlMaxInstr;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 // partitioned ingest (variant P): bucket exchange through L2
 // GPA_* macros below (and in ingest.cu / rollup.cu / estimate.cu / runtime.cu) are tuning knobs:
 // tools/variant_build.py builds alternative libraries with other values for A/B timing on the GPU

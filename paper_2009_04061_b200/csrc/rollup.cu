@@ -27,6 +27,7 @@ namespace {
 // Same values as vvalue().
 constexpr uint32_t kVrowsThreads = 128;
 __global__ void __launch_bounds__(kVrowsThreads) k_vrows(DevProgram p, double *__restrict__ vbuf) {
+  pdl_wait();
   extern __shared__ double2 vstage[];          // [kVrowsThreads / 32][32 rows][ncol]
   const uint32_t ncol = p.ncol, R = p.R, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double2 *ws = vstage + (size_t)warp * 32 * ncol;
@@ -116,6 +117,7 @@ constexpr int kRollMembers = GPA_ROLL_MEMBERS;   // members (row loads) in fligh
 // the row loads of consecutive members are independent and stay in flight together
 __global__ void __launch_bounds__(128) k_rollup_chunks(RollupPlan rp, uint32_t nv, const double *__restrict__ vbuf,
                                                        const uint64_t *__restrict__ AL) {
+  pdl_wait();
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t ch = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; ch < rp.n_chunks; ch += warps) {
@@ -162,6 +164,7 @@ __global__ void __launch_bounds__(128) k_rollup_segments(uint32_t nv, const doub
                                                          const uint32_t *__restrict__ seg_end, uint32_t n_seg,
                                                          const uint32_t *__restrict__ out_row,
                                                          double *__restrict__ out_v, uint64_t *__restrict__ out_al) {
+  pdl_wait();
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t sg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; sg < n_seg; sg += warps) {
@@ -181,6 +184,7 @@ __global__ void __launch_bounds__(128) k_rollup_segments(uint32_t nv, const doub
 // the same left-to-right order as the oracle's per-instruction accumulation
 __global__ void __launch_bounds__(128) k_rollup_packs(RollupPlan rp, uint32_t nv, const double *__restrict__ vbuf,
                                                       const uint64_t *__restrict__ AL) {
+  pdl_wait();
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t pk = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; pk < rp.n_packs; pk += warps) {
@@ -249,8 +253,7 @@ cudaError_t launch_vrows(const DevProgram &p, double *vbuf, int n_sms, cudaStrea
   const size_t smem = (size_t)kVrowsThreads * p.ncol * sizeof(double2);   // 32 rows per warp
   cudaError_t e = cudaFuncSetAttribute(k_vrows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_vrows<<<g, kVrowsThreads, smem, s>>>(p, vbuf);
-  return cudaGetLastError();
+  return launch_pdl(p.n, k_vrows, g, kVrowsThreads, smem, s, p, vbuf);
 }
 
 // fork (optional, graph capture): the packs of short segments write rows disjoint from the
@@ -268,10 +271,15 @@ cudaError_t launch_rollup_fork(const DevProgram &p, const RollupPlan &rp, int n_
   cudaStream_t ps = split ? side : s;
   if (rp.n_packs) k_rollup_packs<<<warp_grid(rp.n_packs, n_sms), 128, 0, ps>>>(rp, nv, rp.vbuf, p.AL);
   if (split && (e = cudaEventRecord(join, side)) != cudaSuccess) return e;
-  if (rp.n_chunks) k_rollup_chunks<<<warp_grid(rp.n_chunks, n_sms), 128, 0, s>>>(rp, nv, rp.vbuf, p.AL);
-  if (rp.n_seg1)
-    k_rollup_segments<<<warp_grid(rp.n_seg1, n_sms), 128, 0, s>>>(
-        nv, rp.part_v, rp.part_al, nullptr, rp.seg1_begin, rp.seg1_end, rp.n_seg1, rp.seg1_id, rp.rows_v, rp.rows_al);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  if (rp.n_chunks && (e = launch_pdl(p.n, k_rollup_chunks, warp_grid(rp.n_chunks, n_sms), 128, 0, s, rp, nv,
+                                     (const double *)rp.vbuf, (const uint64_t *)p.AL)) != cudaSuccess)
+    return e;
+  if (rp.n_seg1 && (e = launch_pdl(p.n, k_rollup_segments, warp_grid(rp.n_seg1, n_sms), 128, 0, s, nv,
+                                   (const double *)rp.part_v, (const uint64_t *)rp.part_al, (const uint32_t *)nullptr,
+                                   (const uint32_t *)rp.seg1_begin, (const uint32_t *)rp.seg1_end, rp.n_seg1,
+                                   (const uint32_t *)rp.seg1_id, rp.rows_v, rp.rows_al)) != cudaSuccess)
+    return e;
   if (split && (e = cudaStreamWaitEvent(s, join, 0)) != cudaSuccess) return e;   // stage 2 reads the pack rows
   k_rollup_segments<<<warp_grid(rp.n_seg2, n_sms), 128, 0, s>>>(
       nv, rp.rows_v, rp.rows_al, rp.seg2_perm, rp.seg2_begin, rp.seg2_end, rp.n_seg2, nullptr,
