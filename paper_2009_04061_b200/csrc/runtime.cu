@@ -784,7 +784,13 @@ gpa_status gpa_analyze(gpa_program *p, void *stream) {
     // two branches after the blame rows: def reduction -> rollup, and the estimate sums (which read
     // only cand / share / selfm and C); they join before Eqs. 2-5 / 10, which need the rollup's A sums
     CUDA_TRY(cudaStreamBeginCapture(p->capture_stream, cudaStreamCaptureModeThreadLocal));
-    cudaStream_t cs = p->capture_stream, ss = p->side_stream;
+#ifndef GPA_EST_FORK
+#define GPA_EST_FORK 1
+#endif
+#ifndef GPA_PACK_FORK
+#define GPA_PACK_FORK 1
+#endif
+    cudaStream_t cs = p->capture_stream, ss = GPA_EST_FORK ? p->side_stream : p->capture_stream;
     cudaError_t e = launch_blame_rows(p->d, p->n_sms, cs, &n);
     if (e == cudaSuccess && npat) {
       e = cudaEventRecord(p->ev_fork, cs);
@@ -793,7 +799,9 @@ gpa_status gpa_analyze(gpa_program *p, void *stream) {
       if (e == cudaSuccess) e = cudaEventRecord(p->ev_join, ss);
     }
     if (e == cudaSuccess) e = launch_def_reduce(p->d, p->n_sms, cs, &n);
-    if (e == cudaSuccess) e = launch_rollup_fork(p->d, p->rp, p->n_sms, cs, p->pack_stream, p->ev_pfork, p->ev_pjoin, &n);
+    if (e == cudaSuccess)
+      e = launch_rollup_fork(p->d, p->rp, p->n_sms, cs, GPA_PACK_FORK ? p->pack_stream : nullptr, p->ev_pfork,
+                             p->ev_pjoin, &n);
     if (e == cudaSuccess && npat) {
       e = cudaStreamWaitEvent(cs, p->ev_join, 0);
       if (e == cudaSuccess) e = launch_estimate_final(p->d, p->ep, p->n_sms, cs, &n);
