@@ -317,14 +317,6 @@ def run_batch(args):
                          "ingest_share_of_step": ingest_ms / ms_per_step, "blame_rollup_estimate_ms": analyze_ms},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
         }
-        if world > 1:
-            # the DP-1 exchange: one SUM all-reduce of [counts | stats]; bus bandwidth 2(p-1)/p * bytes / t
-            # against NVLink 5's 900 GB/s per direction; the time includes the
-            # collective's wait for the slowest rank's ingest, so it bounds the exchange from above
-            rb = red.numel() * 8
-            bus = 2 * (world - 1) / world * rb / (reduce_ms / 1e3) / 1e9 if reduce_ms > 0 else None
-            line["allreduce"] = {"bytes": rb, "ms": reduce_ms, "busbw_gbs": bus, "peak_gbs": 900.0,
-                                 "frac": bus / 900.0 if bus else None, "backend": dist.get_backend()}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -430,6 +422,23 @@ def main():
         ms, ingest_ms, reduce_ms = float(t[0]), float(t[1]), float(t[2])
     ms_per_step = ms / args.steps
 
+    ar_ms = 0.0
+    if world > 1:   # the collective alone, on a buffer the size of [counts | stats] (outside the timed region)
+        scratch = torch.zeros_like(red)   # same size as [counts | stats]; sums stay 0
+        dist.barrier()
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        dist.all_reduce(scratch, op=dist.ReduceOp.SUM)
+        a0.record(stream)
+        for _ in range(10):
+            dist.all_reduce(scratch, op=dist.ReduceOp.SUM)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        t = torch.tensor([a0.elapsed_time(a1) / 10], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ar_ms = float(t[0])
+        del scratch
+
     # correctness guard on the timed output: every record of every rank was counted
     st = P.stats()
     total = n_per * world
@@ -500,12 +509,14 @@ def main():
         }
         if world > 1:
             # the DP-1 exchange: one SUM all-reduce of [counts | stats]; bus bandwidth 2(p-1)/p * bytes / t
-            # against NVLink 5's 900 GB/s per direction; the time includes the
-            # collective's wait for the slowest rank's ingest, so it bounds the exchange from above
+            # against NVLink 5's 900 GB/s per direction.  "ms" is the in-step time
+            # (it includes the wait for the slowest rank's ingest); "standalone_ms" times the same
+            # collective alone on a same-size buffer, all ranks aligned, after the timed region
             rb = red.numel() * 8
-            bus = 2 * (world - 1) / world * rb / (reduce_ms / 1e3) / 1e9 if reduce_ms > 0 else None
-            line["allreduce"] = {"bytes": rb, "ms": reduce_ms, "busbw_gbs": bus, "peak_gbs": 900.0,
-                                 "frac": bus / 900.0 if bus else None, "backend": dist.get_backend()}
+            bus = 2 * (world - 1) / world * rb / (ar_ms / 1e3) / 1e9 if ar_ms > 0 else None
+            line["allreduce"] = {"bytes": rb, "ms": reduce_ms, "standalone_ms": ar_ms, "busbw_gbs": bus,
+                                 "peak_gbs": 900.0, "frac": bus / 900.0 if bus else None,
+                                 "backend": dist.get_backend()}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
