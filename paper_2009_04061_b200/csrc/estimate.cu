@@ -236,11 +236,25 @@ __global__ void k_est_final(DevProgram p, EstimatePlan ep) {
         double best = -1.0;
         int32_t bs = -1;
         if (q.model == 2 || q.model == 4) {
-          for (uint32_t x = ep.kloop_ptr[k] + lane; x < ep.kloop_ptr[k + 1]; x += 32) {
-            const uint32_t l = ep.kloops[x];
-            const double Al = (double)ep.loop_incl_al[2 * (uint64_t)l];
-            const double sv = eq2(Td, fmin(Al, ep.lM_incl[(uint64_t)qi * p.n_loops + l]));
-            if (bs < 0 || sv > best) { best = sv; bs = (int32_t)l; }
+          // four loop scopes per lane in flight (ids first, then their A and M^L), evaluated in the
+          // same per-lane order as one at a time
+          const uint32_t x0 = ep.kloop_ptr[k], x1 = ep.kloop_ptr[k + 1];
+          for (uint32_t xb = x0 + lane; xb < x1; xb += 4 * 32) {
+            uint32_t l[4];
+            double Al[4], Ml[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) l[u] = xb + 32u * u < x1 ? ep.kloops[xb + 32u * u] : 0xffffffffu;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              Al[u] = l[u] != 0xffffffffu ? (double)ep.loop_incl_al[2 * (uint64_t)l[u]] : 0.0;
+              Ml[u] = l[u] != 0xffffffffu ? ep.lM_incl[(uint64_t)qi * p.n_loops + l[u]] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              if (l[u] == 0xffffffffu) break;
+              const double sv = eq2(Td, fmin(Al[u], Ml[u]));
+              if (bs < 0 || sv > best) { best = sv; bs = (int32_t)l[u]; }
+            }
           }
         }
         if (q.model == 3 || q.model == 4) {
