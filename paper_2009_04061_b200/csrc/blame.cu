@@ -54,8 +54,42 @@ __global__ void k_blame_rows(DevProgram p) {
       p.selfm[j] = 0;
       continue;
     }
+    // the first kBlameCache edges of the row: every load issued before any use (ids, then the
+    // defs' fields), kept in registers for both passes; longer rows continue with plain loads.
+    // The arithmetic and its order are those of the edge-at-a-time loop.
+    constexpr uint32_t kBlameCache = 4;
+    uint32_t cm[kBlameCache];
+    double cw[kBlameCache];
+    {
+      uint32_t cd[kBlameCache], cmin[kBlameCache], cmax[kBlameCache];
+      int32_t cdom[kBlameCache];
+#pragma unroll
+      for (uint32_t u = 0; u < kBlameCache; ++u) {
+        const bool in = e0 + u < e1;
+        cd[u] = in ? p.edge_def[e0 + u] : 0u;
+        cdom[u] = in ? p.edge_dom[e0 + u] : 0;
+        cmin[u] = in ? p.edge_min[e0 + u] : 0u;
+        cmax[u] = in ? p.edge_max[e0 + u] : 1u;
+      }
+#pragma unroll
+      for (uint32_t u = 0; u < kBlameCache; ++u) {
+        const bool in = e0 + u < e1;
+        const uint32_t lat = in ? p.latency[cd[u]] : 0u, cls = in ? p.opclass[cd[u]] : 0u;
+        const uint64_t a = in ? p.AL[2 * (uint64_t)cd[u]] : 0ull;
+        const bool keep = in && cdom[u] < 0 && cmin[u] <= lat;   // rules 2, 3
+        cm[u] = keep ? rule1_mask(cls) : 0u;
+        cw[u] = __ddiv_rn((double)(a ? a : 1ull), (double)cmax[u]);
+      }
+    }
     double W0 = 0.0, W1 = 0.0, W2 = 0.0;
-    for (uint32_t e = e0; e < e1; ++e) {
+#pragma unroll
+    for (uint32_t u = 0; u < kBlameCache; ++u) {
+      if (!cm[u]) continue;
+      if (cm[u] & 1u) W0 = __dadd_rn(W0, cw[u]);
+      W1 = __dadd_rn(W1, cw[u]);
+      if (cm[u] & 4u) W2 = __dadd_rn(W2, cw[u]);
+    }
+    for (uint32_t e = e0 + kBlameCache; e < e1; ++e) {
       const uint32_t d = p.edge_def[e];
       const bool keep = p.edge_dom[e] < 0 && p.edge_min[e] <= p.latency[d];   // rules 2, 3
       if (!keep) continue;
@@ -66,14 +100,9 @@ __global__ void k_blame_rows(DevProgram p) {
       W1 = __dadd_rn(W1, w);
       if (m & 4u) W2 = __dadd_rn(W2, w);
     }
-    for (uint32_t e = e0; e < e1; ++e) {
-      const uint32_t d = p.edge_def[e];
-      const bool keep = p.edge_dom[e] < 0 && p.edge_min[e] <= p.latency[d];
-      const uint32_t m = keep ? rule1_mask(p.opclass[d]) : 0u;
+    auto put = [&](uint32_t e, uint32_t m, double w) {
       double s0 = 0.0, s1 = 0.0, s2 = 0.0;
       if (m) {
-        const uint64_t a = p.AL[2 * (uint64_t)d];
-        const double w = __ddiv_rn((double)(a ? a : 1ull), (double)p.edge_max[e]);
         if (m & 1u) s0 = __ddiv_rn(w, W0);
         s1 = __ddiv_rn(w, W1);
         if (m & 4u) s2 = __ddiv_rn(w, W2);
@@ -82,6 +111,16 @@ __global__ void k_blame_rows(DevProgram p) {
       p.share[3 * (uint64_t)e] = s0;
       p.share[3 * (uint64_t)e + 1] = s1;
       p.share[3 * (uint64_t)e + 2] = s2;
+    };
+#pragma unroll
+    for (uint32_t u = 0; u < kBlameCache; ++u)
+      if (e0 + u < e1) put(e0 + u, cm[u], cw[u]);
+    for (uint32_t e = e0 + kBlameCache; e < e1; ++e) {
+      const uint32_t d = p.edge_def[e];
+      const bool keep = p.edge_dom[e] < 0 && p.edge_min[e] <= p.latency[d];
+      const uint32_t m = keep ? rule1_mask(p.opclass[d]) : 0u;
+      const uint64_t a = m ? p.AL[2 * (uint64_t)d] : 0ull;
+      put(e, m, m ? __ddiv_rn((double)(a ? a : 1ull), (double)p.edge_max[e]) : 0.0);
     }
     p.selfm[j] = (uint8_t)((W0 > 0.0 ? 0u : 1u) | (W1 > 0.0 ? 0u : 2u) | (W2 > 0.0 ? 0u : 4u));
   }
