@@ -5,11 +5,13 @@ estimate), and the ingest kernel's achieved fraction of the measured HBM rooflin
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload large|rodinia] [--impl reference]
   torchrun --nproc-per-node N bench.py --gpus N ...     (one rank per GPU, NCCL all-reduce)
 
-Workload (DESIGN.md §6): BASELINE.json config 3 -- the 50k-instruction PeleC/ExaTENSOR-shaped
+Workload (DESIGN.md §8): BASELINE.json config 3 -- the 50k-instruction PeleC/ExaTENSOR-shaped
 program with 10^9 synthetic PC-sample records per GPU (8 GB, device-resident, far larger than
-L2, so no flush is needed between steps).  At N > 1 rank r ingests records [r*1e9, (r+1)*1e9) of
-the same counter-based stream (config 5's sharding), the count table is all-reduced over NCCL,
-and blame / rollup / estimate run replicated: weak scaling.
+L2, so no flush is needed between steps) at EVERY N.  At N > 1 rank r ingests records
+[r*1e9, (r+1)*1e9) of the same counter-based stream (config 5's sharding), the count table is
+all-reduced over NCCL, and blame / rollup / estimate run replicated: weak scaling, the same
+per-GPU load at N = 1, 2, 4, 8.  `--gpus N` without torchrun re-launches itself under
+`torch.distributed.run --nproc-per-node N`; under torchrun `--gpus` must equal WORLD_SIZE.
 
 One step = reset -> ingest -> [all_reduce] -> blame -> aggregate -> estimate, all enqueued on one
 stream; timed with CUDA events, W warm-up steps, K timed steps, barrier + synchronize on both
@@ -32,7 +34,6 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "PC samples/sec attributed (ingest+blame+rollup) at 1/2/4/8 B200; % HBM peak"
-CONFIG5_PER_GPU = 1_250_000_000    # config 5 (10^10 samples on 8 GPUs), used per GPU at every N > 1
 WORKLOADS = {
     # name: (config id, records per GPU)
     "large": (3, 1_000_000_000),
@@ -107,11 +108,67 @@ def _traffic_from_profile(workload, records):
         return None
 
 
-def _cpu_count():
+def _host_info():
+    """The box's host CPU beside the oracle's timing (north_star: "core count stated")."""
+    model = None
     try:
-        return len(os.sched_getaffinity(0))
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
     except Exception:
-        return os.cpu_count()
+        usable = os.cpu_count()
+    return {"cpu_model": model, "nproc": os.cpu_count(), "usable_cores": usable}
+
+
+def _check_world(args):
+    """--gpus N must match the launch: without torchrun, N > 1 re-executes this script under
+    torch.distributed.run (one rank per GPU); under torchrun, WORLD_SIZE must equal N."""
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is None:
+        if args.gpus > 1:
+            import socket
+            sk = socket.socket()
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+            sk.close()
+            cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+                   "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+            if os.environ.get("GPA_BENCH_DRYRUN") == "1":     # test hook: show the re-launch, do not run it
+                print(json.dumps({"relaunch": cmd}), flush=True)
+                sys.exit(0)
+            os.execv(sys.executable, cmd)
+        return 1
+    if int(ws) != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}: launch one rank per GPU\n")
+        sys.exit(2)
+    return int(ws)
+
+
+def large_config(args, world, prog, cfg, n_per):
+    """The `config` object of the large / rodinia arms (printed identically by --impl reference)."""
+    return {"workload": f"{args.workload}: BASELINE config {cfg} program ({prog.n_instr} instrs, {prog.n_edges} edges, "
+                        f"{prog.n_loops} loops), {n_per} records per GPU"
+                        + (f" (config 5's 10^10-record stream sharded as {n_per} per GPU)" if world > 1 else ""),
+            "records_per_gpu": n_per, "records_total": n_per * world,
+            "l2": "inputs larger than L2 (8 B/record)" if n_per * 8 > 126 << 20 else "inputs smaller than L2",
+            "parallelism": f"dp{world} (sample-stream shards + NCCL all-reduce of counts)"}
+
+
+def step_alg_bytes(prog, n_records, table_word=8):
+    """SURVEY §8(d) algorithmic bytes of one whole step (ingest + blame + rollup): records once,
+    instruction SoA + CSR read once, count table written and read once, per-instruction blame and
+    the rollup outputs written once."""
+    n, E, R = prog.n_instr, prog.n_edges, prog.n_reasons
+    ncol = 10 + R - 4
+    segs = prog.n_lines + 2 * prog.n_loops + (len(prog.func_begin) - 1) + (len(prog.kernel_func_begin) - 1)
+    return (8 * n_records + 4 * (n + 1) + 16 * n + 20 * E + 2 * n * 2 * R * table_word + 64 * n
+            + segs * (ncol * 2 * 8 + 16))
 
 
 def oracle_throughput(prog, records: np.ndarray, patterns):
@@ -128,31 +185,67 @@ def oracle_throughput(prog, records: np.ndarray, patterns):
 
 
 def run_reference(args):
-    """--impl reference: the CPU oracle on the host cores (rank 0 only), bounded samples."""
+    """--impl reference: the CPU oracle on the host cores (rank 0 only) on our arm's workload and
+    config; each step is a bounded sample (the first `sample` records of the same stream), sized so
+    the whole --warmup W --steps K run stays within a few minutes."""
+    world = _check_world_ref(args)
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     import gpagen
     from gpagen.patterns import table2
-    cfg, _ = WORKLOADS[args.workload]
-    prog = gpagen.config_program(cfg)
-    sample = args.ref_sample
-    recs = gpagen.config_stream(prog, cfg).host(0, sample)
+    if args.workload == "batch":
+        from gpagen import batch
+        prog = batch.config4_program()
+        spec = batch.config4_stream(prog)
+        n_per = args.records or WORKLOADS["batch"][1]
+        config = batch_config(args, world, prog, n_per)
+        cfg = 4
+    else:
+        cfg, n_per = WORKLOADS[args.workload]
+        n_per = args.records or n_per
+        prog = gpagen.config_program(cfg)
+        spec = gpagen.config_stream(prog, cfg)
+        config = large_config(args, world, prog, cfg, n_per)
     pats = table2(prog.n_reasons)
+    if args.ref_sample:
+        sample = min(args.ref_sample, n_per)
+    else:   # size the sample from a pilot run: the whole W + K run within ~150 s of oracle time
+        pilot = min(n_per, 5_000_000)
+        rate = pilot / oracle_throughput(prog, spec.host(0, pilot), pats)
+        sample = int(min(n_per, max(pilot, rate * 150.0 / max(1, args.steps + args.warmup))))
+        sample -= sample % 1_000_000 if sample > 1_000_000 else 0
+    recs = spec.host(0, sample)
     for _ in range(args.warmup):
         oracle_throughput(prog, recs, pats)
     times = [oracle_throughput(prog, recs, pats) for _ in range(args.steps)]
     t = sum(times) / len(times)
     v = sample / t
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": args.gpus,
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u64+f64", "data": "synthetic",
-            "config": {"workload": f"{args.workload} (BASELINE config {cfg})", "records_per_step": sample},
+            "scaling": "strong" if args.workload == "batch" else "weak", "vs_baseline": None, "dtype": "u64+f64",
+            "data": "synthetic", "config": config,
             "cpu_baseline": {"value": v, "unit": "samples/s", "cores": 1, "kind": "oracle",
-                             "sample": f"first {sample} records of the config-{cfg} stream per step"},
+                             "sample": f"first {sample} of the {n_per} records of this workload's stream per step "
+                                       "(histogram+blame+rollup+estimate, single-threaded)",
+                             "host": _host_info()},
             "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
+
+def _check_world_ref(args):
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is not None and int(ws) != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}\n")
+        sys.exit(2)
+    return args.gpus if ws is None else int(ws)
+
+
+def batch_config(args, world, prog, n_total):
+    return {"workload": f"batch: BASELINE config 4, {prog.n_kernels} kernels, {prog.n_instr} instrs, "
+                        f"{prog.n_edges} edges, {n_total} records grouped by kernel launch",
+            "records_total": n_total, "l2": "inputs larger than L2 (0.8 GB records, 0.65 GB table)",
+            "parallelism": f"dp2-{world} (kernel partition, no count collective)"}
 
 
 def _local_device() -> int:
@@ -184,7 +277,7 @@ def run_batch(args):
     from paper_2009_04061_b200 import Program
     from paper_2009_04061_b200.dist import gather_estimates, partition_kernels, slice_program
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    world = _check_world(args)
     rank = int(os.environ.get("RANK", "0"))
     local = _local_device()
     torch.cuda.set_device(local)
@@ -261,8 +354,8 @@ def run_batch(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, ingest_ms, analyze_ms = (float(x) for x in t)
     ms_per_step = ms / args.steps
-    st = P.stats()
-    assert st[0] + st[1] == n_mine, (st, n_mine)
+    st = P.stats()   # valid + invalid samples = every sample of this rank's records (count 1 each)
+    assert st[0] + st[2] == n_mine, (st, n_mine)
     est = P.read_estimates_array()
     allest = gather_estimates(np.ascontiguousarray(est["speedup"]))
     assert allest.shape[0] == prog.n_kernels
@@ -301,20 +394,22 @@ def run_batch(args):
         t_or = oracle_throughput(prog, h, pats)
         cpu = {"value": sample / t_or, "unit": "samples/s", "cores": 1, "kind": "oracle",
                "sample": f"first {sample} records of the config-4 stream (whole 4.5M-instruction batch); "
-                         "histogram+blame+rollup+estimate", "seconds": t_or}
+                         "histogram+blame+rollup+estimate", "seconds": t_or, "host": _host_info()}
     if rank == 0:
+        step_bytes = step_alg_bytes(sub, n_mine)
         line = {
             "metric": METRIC, "value": n_total / (ms_per_step / 1e3), "unit": "samples/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u64+f64", "data": "synthetic",
-            "config": {"workload": f"batch: BASELINE config 4, {prog.n_kernels} kernels, {prog.n_instr} instrs, "
-                                   f"{prog.n_edges} edges, {n_total} records grouped by kernel launch",
-                       "records_total": n_total, "l2": "inputs larger than L2 (0.8 GB records, 0.65 GB table)",
-                       "parallelism": f"dp2-{world} (kernel partition, no count collective)"},
+            "config": batch_config(args, world, prog, n_total),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": None, "kernel": "ingest_segments", "peak_kind": peak_kind,
                          "alg_bytes_per_launch": alg_bytes, "ingest_ms": ingest_ms,
-                         "ingest_share_of_step": ingest_ms / ms_per_step, "blame_rollup_estimate_ms": analyze_ms},
+                         "ingest_share_of_step": ingest_ms / ms_per_step, "blame_rollup_estimate_ms": analyze_ms,
+                         "step": {"alg_bytes": step_bytes, "ms": ms_per_step,
+                                  "achieved": step_bytes / (ms_per_step / 1e3) / 1e9,
+                                  "frac": step_bytes / (ms_per_step / 1e3) / 1e9 / peak,
+                                  "note": "rank 0's slice: SURVEY §8(d) bytes of ingest+blame+rollup over the whole step"}},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
         }
         print(json.dumps(line), flush=True)
@@ -333,7 +428,8 @@ def main():
     ap.add_argument("--variant", default=None, help="force ingest variant (smem|part|l2)")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--ref-sample", type=int, default=50_000_000)
+    ap.add_argument("--ref-sample", type=int, default=0,
+                    help="records per reference step (default: sized from a pilot run, <= records per GPU)")
     ap.add_argument("--profile", action="store_true", help="one short step for ncu (no JSON rules)")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -347,16 +443,14 @@ def main():
     from gpagen.patterns import table2
     from paper_2009_04061_b200 import Program
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    world = _check_world(args)
     rank = int(os.environ.get("RANK", "0"))
     local = _local_device()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         _init_dist(dist, dev)
-    cfg, n_per = WORKLOADS[args.workload]
-    if args.workload == "large" and world > 1:
-        n_per = CONFIG5_PER_GPU       # BASELINE config 5: 10^10 samples over 8 GPUs
+    cfg, n_per = WORKLOADS[args.workload]    # the same records per GPU at every N (weak scaling)
     if args.records:
         n_per = args.records
     prog = gpagen.config_program(cfg)
@@ -440,9 +534,9 @@ def main():
         del scratch
 
     # correctness guard on the timed output: every record of every rank was counted
-    st = P.stats()
+    st = P.stats()   # valid + invalid samples = every sample of every rank (timed streams: count 1)
     total = n_per * world
-    assert st[0] + st[1] == total, (st, total)
+    assert st[0] + st[2] == total, (st, total)
 
     # end to end through the C ABI from pinned host memory (H2D inside the timed region)
     e2e = None
@@ -488,23 +582,25 @@ def main():
         t_or = oracle_throughput(prog, h, pats)
         cpu = {"value": sample / t_or, "unit": "samples/s", "cores": 1, "kind": "oracle",
                "sample": f"{sample} records (the same device stream, copied to host); histogram+blame+rollup+estimate",
-               "seconds": t_or}
+               "seconds": t_or, "host": _host_info()}
     if rank == 0:
+        step_bytes = step_alg_bytes(prog, n_per)
         line = {
             "metric": METRIC, "value": total / (ms_per_step / 1e3), "unit": "samples/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "u64+f64", "data": "synthetic",
-            "config": {"workload": f"{args.workload}: BASELINE config {cfg if world == 1 else '5 (config-3 program)'}, "
-                                   f"{prog.n_instr} instrs, "
-                                   f"{prog.n_edges} edges, {prog.n_loops} loops, {n_per} records/GPU",
-                       "records_per_gpu": n_per, "records_total": total, "l2": "inputs larger than L2 (8 B/record)",
-                       "parallelism": f"dp{world} (sample-stream shards + NCCL all-reduce of counts)",
-                       "ingest_variant": P.variant},
+            "config": large_config(args, world, prog, cfg, n_per),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": _traffic_from_profile(args.workload, n_per),
-                         "kernel": "ingest", "peak_kind": peak_kind, "alg_bytes_per_launch": alg_bytes,
+                         "kernel": f"ingest ({P.variant} variant)", "peak_kind": peak_kind,
+                         "alg_bytes_per_launch": alg_bytes,
                          "ingest_ms": ingest_ms, "ingest_share_of_step": ingest_ms / ms_per_step,
-                         "blame_rollup_estimate_ms": analyze_ms},
+                         "blame_rollup_estimate_ms": analyze_ms,
+                         "step": {"alg_bytes": step_bytes, "ms": ms_per_step,
+                                  "achieved": step_bytes / (ms_per_step / 1e3) / 1e9,
+                                  "frac": step_bytes / (ms_per_step / 1e3) / 1e9 / peak,
+                                  "note": "SURVEY §8(d) bytes of ingest+blame+rollup (per GPU) over the whole "
+                                          "timed step (incl. estimate and, at N > 1, the all-reduce)"}},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
         }
         if world > 1:

@@ -743,6 +743,12 @@ gpa_status gpa_set_patterns(gpa_program *p, const gpa_pattern *pats, uint32_t n_
   CUDA_TRY(cudaMemcpyAsync(p->pats_dev, pats, n_pat * sizeof(gpa_pattern), cudaMemcpyHostToDevice, s));
   CUDA_TRY(cudaStreamSynchronize(s));
   p->ep.n_pat = n_pat;
+  // the analyze graph bakes the pattern plan (n_pat, loop_slot, whether k_est_edges runs) into its
+  // kernel parameters: any new pattern set invalidates it
+  if (p->analyze_exec) {
+    cudaGraphExecDestroy(p->analyze_exec);
+    p->analyze_exec = nullptr;
+  }
   for (uint32_t q = 0, slot = 0; q < (uint32_t)kPatternsMax; ++q)
     p->ep.loop_slot[q] = (q < n_pat && (pats[q].model == 2 || pats[q].model == 4)) ? (int8_t)slot++ : (int8_t)-1;
   p->view_bytes[GPA_VIEW_ESTIMATES] = (size_t)p->d.n_kernels * n_pat * sizeof(gpa_estimate_out);

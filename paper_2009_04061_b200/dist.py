@@ -28,17 +28,24 @@ def allreduce_counts(counts, stats=None, group=None):
 
 def sharded_step(program, records, group=None, stream=None, estimate=True):
     """One data-parallel step on this rank: reset -> ingest(local shard) -> all-reduce -> blame ->
-    aggregate -> estimate.  `records` is this rank's device-resident shard."""
+    aggregate -> estimate.  `records` is this rank's device-resident shard.
+
+    The whole step runs with `stream` as torch's current stream: NCCL's all_reduce waits for, and is
+    waited on by, the current stream only, so this is what orders the collective after the ingest
+    and before the analysis when a caller passes a stream of its own."""
+    import torch
     import torch.distributed as dist
-    program.reset(stream)
-    program.ingest(records, stream=stream)
-    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.all_reduce(program.reduce_view(), op=dist.ReduceOp.SUM, group=group)   # counts + stats, one call
-    if estimate:
-        program.analyze(stream)      # blame + aggregate + estimate as one CUDA graph
-    else:
-        program.blame(stream)
-        program.aggregate(stream)
+    s = stream if stream is not None else torch.cuda.current_stream(program.device)
+    with torch.cuda.stream(s):
+        program.reset(s)
+        program.ingest(records, stream=s)
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+            dist.all_reduce(program.reduce_view(), op=dist.ReduceOp.SUM, group=group)   # counts + stats, one call
+        if estimate:
+            program.analyze(s)      # blame + aggregate + estimate as one CUDA graph
+        else:
+            program.blame(s)
+            program.aggregate(s)
 
 
 # ----------------------------------------------------------------------------- DP-2

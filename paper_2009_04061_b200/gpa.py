@@ -200,6 +200,12 @@ def simulate_sass(sass, n_sm, cap_per_sm, func=0, schedulers=4, warps_per_schedu
     return rec, tr, counts
 
 
+def _need_contiguous(t, what: str):
+    """The C ABI takes a base pointer and a record count: a strided view would be read as if dense."""
+    if not t.is_contiguous():
+        raise GpaError(f"{what}() needs a contiguous tensor (got strides {tuple(t.stride())})")
+
+
 def _check(rc: int, what: str):
     if rc != 0:
         raise GpaError(f"{what} failed ({rc}): {lib().gpa_last_error().decode()}")
@@ -296,6 +302,7 @@ class Program:
         t = samples
         if not t.is_cuda:
             raise GpaError("ingest() takes a device tensor; use ingest_host() for host memory")
+        _need_contiguous(t, "ingest")
         nrec = int(t.numel() * t.element_size() // 8) if n is None else int(n)
         _check(lib().gpa_ingest_samples(self.handle, t.data_ptr(), nrec, self._s(stream)), "gpa_ingest_samples")
 
@@ -306,6 +313,7 @@ class Program:
         for t in (samples, seg_begin, seg_kernel):
             if not t.is_cuda:
                 raise GpaError("ingest_segments() takes device tensors")
+            _need_contiguous(t, "ingest_segments")
         if seg_begin.element_size() != 8 or seg_kernel.element_size() != 4:
             raise GpaError("seg_begin must hold 8-byte and seg_kernel 4-byte integers")
         n_seg = int(seg_kernel.numel())
@@ -319,6 +327,7 @@ class Program:
     def ingest_host(self, samples, n=None, stream=None):
         """samples: host numpy array / CPU tensor of 8-byte records (pinned memory overlaps)."""
         if hasattr(samples, "data_ptr"):
+            _need_contiguous(samples, "ingest_host")
             ptr, nbytes = samples.data_ptr(), samples.numel() * samples.element_size()
         else:
             a = np.ascontiguousarray(samples)
@@ -417,7 +426,6 @@ class Program:
         off, nb = ctypes.c_uint64(0), ctypes.c_uint64(0)
         _check(lib().gpa_view(self.handle, VIEW[name], ctypes.byref(off), ctypes.byref(nb)), "gpa_view")
         raw = self.ws[off.value: off.value + nb.value]
-        nv = 2 * self.ncol
         shapes = {
             "counts": (torch.int64, (self.n_instr, 2, self.R)), "stats": (torch.int64, (4,)),
             "instr_al": (torch.int64, (self.n_instr, 2)), "cand": (torch.uint8, (self.n_edges,)),
@@ -435,7 +443,6 @@ class Program:
         if name == "estimates":
             return raw
         dt, shape = shapes[name]
-        del nv
         return raw.view(dt).view(shape)
 
     def instr_vector(self, stream=None):

@@ -111,7 +111,9 @@ def compare(g, o, rel=1e-9, exact_blame=False, prog=None):
         assert_close_rel(g[k + "_v"], o[k + "_v"], rel, k)
         assert np.array_equal(g[k + "_v"][..., 7:, :], o[k + "_v"][..., 7:, :]), k + " integer columns"
         assert np.array_equal(g[k + "_al"], o[k + "_al"]), k + "_al"
+    assert len(g["est"]) == len(o["est"]), ("kernels", len(g["est"]), len(o["est"]))
     for k_g, k_o in zip(g["est"], o["est"]):
+        assert len(k_g) == len(k_o), ("patterns", len(k_g), len(k_o))
         for a, b in zip(k_g, k_o):
             assert a.T == b.T and a.A == b.A and a.model == b.model
             assert a.matched == b.matched and a.unbounded == b.unbounded
