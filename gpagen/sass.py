@@ -216,3 +216,137 @@ def program_from_sass(S: Sass, csr: dict, n_reasons: int = 9):
     prog.pc_weight = np.ones(n)
     prog.pc_profile = np.zeros(n, np.uint8)
     return prog
+
+
+def random_cfg_sass(seed: int, max_instr: int = 24, n_regs: int = 5, n_funcs: int = 1) -> Sass:
+    """Small functions (<= max_instr instructions each) with structured but irregular control flow,
+    for the brute-force slicing checks: nested loops, multi-block loop bodies, loops with several
+    back edges (`continue`: a body block branching back to the header), multi-exit loops (`break`:
+    a body block branching to the loop's exit), if/else diamonds and one-armed ifs.  Few registers,
+    so def-use chains cross loops and arms; predicated defs (3 predicates) and barriers as in
+    random_sass.  Blocks are laid out in address order, a loop's header first.  A draw whose
+    function exceeds max_instr, or that has no back edge when loops are wanted (about 3 in 4
+    draws), is redrawn from the next sub-seed."""
+    for attempt in range(1000):
+        S = _cfg_draw(np.random.default_rng([seed, attempt]), max_instr, n_regs, n_funcs)
+        fl = np.diff(S.func_begin.astype(np.int64))
+        has_back = any(S.block_begin[t] <= S.block_begin[b + 1] - 1 for b in range(len(S.block_begin) - 1)
+                       for t in S.succ[S.succ_ptr[b]:S.succ_ptr[b + 1]])
+        if fl.max() <= max_instr and (has_back or np.random.default_rng([seed, attempt, 1]).random() < 0.25):
+            return S
+    raise RuntimeError("random_cfg_sass: no draw fits")
+
+
+def _cfg_draw(rng, max_instr, n_regs, n_funcs):
+    instrs, blocks, succs, funcs = [], [], [], [0]
+
+    def new_block():
+        blocks.append([len(instrs), None])
+        succs.append([])
+        return len(blocks) - 1
+
+    def emit():
+        g = ALWAYS
+        if rng.random() < 0.2:
+            g = int(rng.integers(0, 3)) | (NEG if rng.random() < 0.5 else 0)
+        u = rng.random()
+        ins = dict(guard=g)
+        if u < 0.12:                                        # ISETP
+            ins.update(dst=[P(int(rng.integers(0, 3)))], src=[int(rng.integers(0, n_regs))])
+        elif u < 0.3:                                       # variable-latency load with barriers
+            b = int(rng.integers(0, 3))
+            ins.update(dst=[int(rng.integers(0, n_regs))], src=[int(rng.integers(0, n_regs))], wbar=1 << b,
+                       cls=int(rng.choice([0, 2, 3])), lat=1024)
+            if rng.random() < 0.4:
+                ins["rbar"] = 1 << int((b + 1) % 3)
+        elif u < 0.4:                                       # a pure reader (store-like)
+            ins.update(src=[int(x) for x in rng.integers(0, n_regs, int(rng.integers(1, 3)))])
+        else:                                               # arithmetic
+            ins.update(dst=[int(rng.integers(0, n_regs))],
+                       src=[int(x) for x in rng.integers(0, n_regs, int(rng.integers(0, 3)))])
+        if rng.random() < 0.25:
+            ins["wait"] = int(rng.integers(1, 8))
+        instrs.append(ins)
+
+    def close(b, targets):
+        blocks[b][1] = len(instrs)
+        succs[b].extend(targets)
+
+    def room(f0):
+        return max_instr - (len(instrs) - f0)
+
+    def region(cur, depth, f0, loop):
+        """Emit a region starting in open block `cur`; returns the open block it ends in.  `loop`:
+        (header block, list collecting break sources) of the innermost enclosing loop, or None."""
+        for _ in range(int(rng.integers(1, 4))):
+            left = room(f0)
+            if left <= 2:
+                break
+            r = rng.random()
+            if r < 0.4 and left >= 6 and depth < 3:        # loop: header, body region, latch
+                emit(); close(cur, [len(blocks)])
+                h = new_block(); emit()
+                breaks = []
+                body = region(h, depth + 1, f0, (h, breaks))
+                emit()                                      # latch: back edge + exit
+                latch = body
+                ex_id = len(blocks)
+                close(latch, [h, ex_id])
+                for b in breaks:
+                    succs[b].append(ex_id)
+                cur = new_block(); emit()
+            elif r < 0.6 and left >= 5:                    # if/else diamond (or one-armed if)
+                emit()
+                one_arm = rng.random() < 0.3
+                t = len(blocks)
+                close(cur, [t])
+                tb = new_block(); emit()
+                tend = region(tb, depth + 1, f0, loop) if rng.random() < 0.4 else tb
+                if one_arm:
+                    j = len(blocks)
+                    close(tend, [j])
+                    succs[cur].append(j)
+                else:
+                    e = len(blocks)
+                    succs[cur].append(e)
+                    eb_pending = tend
+                    close(tend, [])
+                    eb = new_block(); emit()
+                    j = len(blocks)
+                    close(eb, [j])
+                    succs[eb_pending].append(j)
+                cur = new_block(); emit()
+            elif r < 0.8 and loop is not None and left >= 3:   # continue / break out of the body
+                emit()
+                nxt = len(blocks)
+                if rng.random() < 0.5:
+                    close(cur, [nxt, loop[0]])             # continue: a second back edge to the header
+                else:
+                    close(cur, [nxt])
+                    loop[1].append(cur)                    # break: edge to the loop exit (patched)
+                cur = new_block(); emit()
+            else:
+                for _ in range(int(rng.integers(1, 4))):
+                    if room(f0) > 1:
+                        emit()
+        return cur
+
+    for _ in range(n_funcs):
+        f0 = len(instrs)
+        b = new_block()
+        emit()
+        if rng.random() < 0.2:                              # the entry block heads a loop
+            breaks = []
+            body = region(b, 1, f0, (b, breaks))
+            emit()
+            ex_id = len(blocks)
+            close(body, [b, ex_id])
+            for bb in breaks:
+                succs[bb].append(ex_id)
+            b = new_block(); emit()
+        end = region(b, 0, f0, None)
+        if len(instrs) == blocks[end][0]:
+            emit()
+        close(end, [])
+        funcs.append(len(instrs))
+    return _build(instrs, [tuple(x) for x in blocks], succs, funcs)

@@ -635,32 +635,45 @@ int or_occupancy(const or_arch *a, const or_launch *L, const uint32_t *grid_bloc
 }
 
 /* ---------------------------------------------------------------- backward slicing (NEXT #1)
- * P:289-321.  For every use j and every register j reads (source operands, its guard predicate,
- * the virtual barrier registers B0-B5 of its wait mask), search backward along the
- * control flow graph of j's function.  A search state is (instruction x about to be examined, P =
- * union of the predicates of the defs of the register already passed on this path).  Examining x:
- * if x defines the register (destination operand, or write / read barrier for a B register,
- * P:301-302) it is a dependency source at path length L = steps from x to j; P grows by x's
- * predicate and the path stops once P contains j's predicate.  Otherwise the search
- * continues to x-1, or to the last instruction of every predecessor block.  Q35-Q39. */
+ * P:289-321; readings DESIGN.md §3.2 Q35-Q39 (definitions over backward paths, the same
+ * ones tests/slice_enum.py evaluates by listing paths).
+ *
+ * For a use j and a register r that j reads (a source operand, its guard predicate, or a virtual
+ * barrier register B0-B5 of its wait mask), a backward path is x_1, x_2, ... with
+ * x_1 in prev(j) and x_{t+1} in prev(x_t), inside j's function; prev(x) = x-1 inside a block, else
+ * the last instruction of every predecessor block.  P = the union of the predicates of the defs of
+ * r passed so far; the path stops after a def x_t of r once P contains j's predicate.
+ * Every def of r met at step t is a dependency source at length t.  A step from the first
+ * instruction x of a block to the last instruction y of a predecessor block crosses a back edge
+ * when y >= x.  For a def i:
+ *   min_len = the fewest steps over the paths reaching i,
+ *   K*      = the fewest back-edge crossings over those paths,
+ *   max_len = the most steps over the paths with exactly K* crossings ("the longest one"; the
+ *             unrolled-once convention of SPEC S:185: a back edge only when the pair needs it),
+ *   dom_k   = the smallest unpredicated k (k != i, j) reading every register linking i and j that
+ *             lies on every such path (rule 2), else -1.
+ * A search state is (x, P); states with the crossing count added, (x, P, k), form "layers" k in
+ * which every step goes to a lower address, so each layer is a DAG processed by descending x. */
 
-#define SL_ALL 0x4000u   /* '_' */
+#define SL_ALL 0x4000u   /* the '_' predicate */
 #define SL_NONE 0xFFFFu
+#define SL_NIL 0xFFFFFFFFu
 
-static uint32_t sl_pbit(uint8_t g) {         /* predicate of an instruction as a P-set bit */
+static uint32_t sl_pbit(uint8_t g) {          /* predicate of an instruction as a P-set bit */
   uint32_t r = g & 7u;
   if (r == 7u) return SL_ALL;
   return (g & 8u) ? (1u << (7u + r)) : (1u << r);
 }
-static uint32_t sl_norm(uint32_t P) {         /* {p_i} u {!p_i} = {_} */
+static uint32_t sl_union(uint32_t P, uint32_t b) {   /* P + {b}, with {p_i, !p_i} = {_} */
   uint32_t i;
+  P |= b;
   for (i = 0; i < 7; ++i)
     if ((P >> i & 1u) && (P >> (7 + i) & 1u)) P |= SL_ALL;
   return P;
 }
-static int sl_contains(uint32_t P, uint32_t pbit) { return (P & SL_ALL) || (P & pbit); }
+static int sl_contains(uint32_t P, uint32_t b) { return (P & SL_ALL) || (P & b); }
 
-/* registers read by instruction x: out[] = reg ids (0..254, 256..262, 512+b), kinds[] */
+/* registers read by x: out[] = 0..254 (R), 256..262 (P), 512+b (B_b); kinds[] = REG / PRED / BAR */
 static int sl_reads(const or_sass *s, uint32_t x, uint32_t *out, uint8_t *kinds) {
   int n = 0, t;
   for (t = 0; t < 4; ++t) {
@@ -673,7 +686,7 @@ static int sl_reads(const or_sass *s, uint32_t x, uint32_t *out, uint8_t *kinds)
     if (s->wait[x] >> t & 1u) { out[n] = 512u + t; kinds[n] = 4u; ++n; }
   return n;
 }
-static int sl_defines(const or_sass *s, uint32_t x, uint32_t r) {
+static int sl_defines(const or_sass *s, uint32_t x, uint32_t r) {   /* P:301-302 for barriers */
   int t;
   if (r >= 512u) return ((s->wbar[x] | s->rbar[x]) >> (r - 512u)) & 1u;
   for (t = 0; t < 4; ++t)
@@ -689,268 +702,258 @@ static int sl_reads_reg(const or_sass *s, uint32_t x, uint32_t r) {
   return 0;
 }
 
-typedef struct {
-  uint32_t *x, *P, *dist, *lng, *rpo_pos, *hslot;
-  uint8_t *term;
-  uint32_t n, cap;
-  uint32_t *hkey_x, *hkey_p, *hval, hcap;   /* open-addressing index (x, P) -> state */
-} sl_graph;
+typedef struct {                 /* the CFG at instruction level */
+  const or_sass *s;
+  uint32_t *blk_of, *pred_ptr, *pred;
+  uint32_t *kids, *roots;        /* prev() output buffers (max predecessor count + 1) */
+} sl_cfg;
 
-static uint32_t sl_hash(const sl_graph *g, uint32_t x, uint32_t P) {
-  return (x * 2654435761u ^ (P + 1u) * 40503u) & (g->hcap - 1u);
-}
-static uint32_t sl_find(const sl_graph *g, uint32_t x, uint32_t P) {
-  uint32_t h = sl_hash(g, x, P);
-  while (g->hval[h] != 0xFFFFFFFFu) {
-    if (g->hkey_x[h] == x && g->hkey_p[h] == P) return g->hval[h];
-    h = (h + 1u) & (g->hcap - 1u);
-  }
-  return 0xFFFFFFFFu;
-}
-static uint32_t sl_insert(sl_graph *g, uint32_t x, uint32_t P) {
-  uint32_t h = sl_hash(g, x, P);
-  while (g->hval[h] != 0xFFFFFFFFu) {
-    if (g->hkey_x[h] == x && g->hkey_p[h] == P) return g->hval[h];
-    h = (h + 1u) & (g->hcap - 1u);
-  }
-  g->hkey_x[h] = x; g->hkey_p[h] = P; g->hval[h] = g->n;
-  g->x[g->n] = x; g->P[g->n] = P; g->hslot[g->n] = h;
-  return g->n++;
-}
-static void sl_clear(sl_graph *g) {
-  uint32_t i;
-  for (i = 0; i < g->n; ++i) g->hval[g->hslot[i]] = 0xFFFFFFFFu;
-  g->n = 0;
-}
-
-/* predecessors of instruction x in backward order: x-1 in its block, else the last instruction
- * of each predecessor block (ascending block id) */
-static int sl_prev(const or_sass *s, const uint32_t *blk_of, const uint32_t *pred_ptr, const uint32_t *pred,
-                   uint32_t x, uint32_t *out) {
-  uint32_t b = blk_of[x], e;
+/* prev(x): x-1 inside its block, else the last instruction of each predecessor block */
+static int sl_prev(const sl_cfg *c, uint32_t x, uint32_t *out) {
+  uint32_t b = c->blk_of[x], e;
   int n = 0;
-  if (x > s->block_begin[b]) { out[0] = x - 1; return 1; }
-  for (e = pred_ptr[b]; e < pred_ptr[b + 1] && n < 64; ++e) out[n++] = s->block_begin[pred[e] + 1] - 1;
+  if (x > c->s->block_begin[b]) { out[0] = x - 1; return 1; }
+  for (e = c->pred_ptr[b]; e < c->pred_ptr[b + 1]; ++e) out[n++] = c->s->block_begin[c->pred[e] + 1] - 1;
   return n;
 }
 
-/* the mask a state passes on to its predecessors (P grown by a def's predicate), and whether the
- * state ends its path */
-static uint32_t sl_out_mask(const or_sass *s, uint32_t x, uint32_t P, uint32_t r, uint32_t pj, int *term) {
-  int is_def = sl_defines(s, x, r);
-  if (is_def) P = sl_norm(P | sl_pbit(s->guard[x]));
-  *term = is_def && sl_contains(P, pj);
+/* a growable list of search states (x, P, k) with a per-instruction chain for lookups; states are
+ * appended in discovery order, so a breadth-first search walks the list itself as its queue */
+typedef struct {
+  uint32_t n, cap;
+  uint32_t *x, *P, *k, *next, *val;   /* val: distance (BFS) or longest length (layers) */
+  uint8_t *flag;
+  uint32_t *head;                     /* [n_instr] latest state of instruction x, SL_NIL if none */
+} sl_states;
+
+static void sl_states_init(sl_states *S, uint32_t n_instr) {
+  uint32_t i;
+  S->n = 0; S->cap = 64;
+  S->x = (uint32_t *)malloc(4u * S->cap); S->P = (uint32_t *)malloc(4u * S->cap);
+  S->k = (uint32_t *)malloc(4u * S->cap); S->next = (uint32_t *)malloc(4u * S->cap);
+  S->val = (uint32_t *)malloc(4u * S->cap); S->flag = (uint8_t *)malloc(S->cap);
+  S->head = (uint32_t *)malloc(4u * (n_instr ? n_instr : 1));
+  for (i = 0; i < n_instr; ++i) S->head[i] = SL_NIL;
+}
+static void sl_states_clear(sl_states *S) {
+  uint32_t i;
+  for (i = 0; i < S->n; ++i) S->head[S->x[i]] = SL_NIL;
+  S->n = 0;
+}
+static void sl_states_free(sl_states *S) {
+  free(S->x); free(S->P); free(S->k); free(S->next); free(S->val); free(S->flag); free(S->head);
+}
+static uint32_t sl_find(const sl_states *S, uint32_t x, uint32_t P, uint32_t k) {
+  uint32_t i;
+  for (i = S->head[x]; i != SL_NIL; i = S->next[i])
+    if (S->P[i] == P && S->k[i] == k) return i;
+  return SL_NIL;
+}
+static uint32_t sl_add(sl_states *S, uint32_t x, uint32_t P, uint32_t k, uint32_t val) {
+  uint32_t i = S->n++;
+  if (i == S->cap) {
+    S->cap *= 2;
+    S->x = (uint32_t *)realloc(S->x, 4u * S->cap); S->P = (uint32_t *)realloc(S->P, 4u * S->cap);
+    S->k = (uint32_t *)realloc(S->k, 4u * S->cap); S->next = (uint32_t *)realloc(S->next, 4u * S->cap);
+    S->val = (uint32_t *)realloc(S->val, 4u * S->cap); S->flag = (uint8_t *)realloc(S->flag, S->cap);
+  }
+  S->x[i] = x; S->P[i] = P; S->k[i] = k; S->val[i] = val; S->flag[i] = 0;
+  S->next[i] = S->head[x]; S->head[x] = i;
+  return i;
+}
+
+/* what a path carries past state (x, P): the new P, and whether the path stops at x */
+static uint32_t sl_pass(const or_sass *s, uint32_t x, uint32_t P, uint32_t r, uint32_t pj, int *stop) {
+  *stop = 0;
+  if (!sl_defines(s, x, r)) return P;
+  P = sl_union(P, sl_pbit(s->guard[x]));
+  *stop = sl_contains(P, pj);
   return P;
+}
+
+/* per (use j, def i) accumulator over the registers linking them */
+typedef struct {
+  uint32_t def, mn, kstar, mx;
+  uint8_t kind;
+  uint8_t *dom_ok;   /* [function length]: k = f0 + index still qualifies for rule 2 */
+  uint8_t *sep;      /* scratch: k separates the def from j for the current register */
+} sl_acc;
+
+/* breadth-first search from the roots over (x, P) (k = 0), never entering instruction `blocked`
+ * (SL_NIL: none); val = path length */
+static void sl_bfs(const sl_cfg *c, const uint32_t *roots, int nroot, uint32_t r, uint32_t pj, uint32_t blocked,
+                   sl_states *S) {
+  uint32_t u;
+  int q, nk, stop;
+  sl_states_clear(S);
+  for (q = 0; q < nroot; ++q)
+    if (roots[q] != blocked && sl_find(S, roots[q], 0u, 0u) == SL_NIL) sl_add(S, roots[q], 0u, 0u, 1u);
+  for (u = 0; u < S->n; ++u) {
+    const uint32_t Pout = sl_pass(c->s, S->x[u], S->P[u], r, pj, &stop);
+    if (stop) continue;
+    nk = sl_prev(c, S->x[u], c->kids);
+    for (q = 0; q < nk; ++q)
+      if (c->kids[q] != blocked && sl_find(S, c->kids[q], Pout, 0u) == SL_NIL)
+        sl_add(S, c->kids[q], Pout, 0u, S->val[u] + 1u);
+  }
+}
+
+/* One register r of use j (function [f0, f1)): merges into acc[] the defs of r the search reaches
+ * -- their kinds, minimum lengths (breadth-first over (x, P)), K* and the longest length at K*
+ * (layers), and the rule-2 candidates (the breadth-first search with each candidate removed). */
+static void sl_register(const sl_cfg *c, uint32_t f0, uint32_t f1, uint32_t j, uint32_t r, uint8_t kind,
+                        sl_states *bfs, sl_states *lay, sl_acc *acc, uint32_t *n_acc) {
+  const or_sass *s = c->s;
+  const uint32_t pj = sl_pbit(s->guard[j]), nf = f1 - f0;
+  uint32_t i, a, L, x, k;
+  const int nroot = sl_prev(c, j, c->roots);
+  int q, nk, stop;
+
+  /* ---- minimum lengths; the defs reached, their kinds */
+  sl_bfs(c, c->roots, nroot, r, pj, SL_NIL, bfs);
+  for (i = 0; i < bfs->n; ++i) {
+    const uint32_t d = bfs->x[i];
+    uint8_t kk = kind;
+    if (!sl_defines(s, d, r)) continue;
+    for (a = 0; a < *n_acc && acc[a].def != d; ++a) {}
+    if (a == *n_acc) {                           /* first register linking d to j */
+      acc[a].def = d; acc[a].mn = SL_NIL; acc[a].kstar = SL_NIL; acc[a].mx = 0; acc[a].kind = 0;
+      memset(acc[a].dom_ok, 1, nf);
+      ++*n_acc;
+    }
+    if (bfs->val[i] < acc[a].mn) acc[a].mn = bfs->val[i];
+    if (r >= 512u && ((s->rbar[d] >> (r - 512u)) & 1u)) {   /* WAR: j overwrites what d reads */
+      int tt, uu;
+      for (tt = 0; tt < 4; ++tt)
+        for (uu = 0; uu < 4; ++uu) {
+          const uint16_t w = s->dst[4u * j + tt];
+          if (w != SL_NONE && w != 255u && w == s->src[4u * d + uu]) kk |= 8u;
+        }
+    }
+    acc[a].kind |= kk;
+  }
+
+  /* ---- layers k = 0, 1, ...: the longest length of every (x, P, k); stop after a layer that
+   *      adds no (x, P) pair absent from the layers below (no later layer can add one then).
+   *      bfs->flag marks the (x, P) pairs met in some layer so far. */
+  sl_states_clear(lay);
+  for (i = 0; i < bfs->n; ++i) bfs->flag[i] = 0;
+  for (q = 0; q < nroot; ++q) {
+    const uint32_t k0 = c->roots[q] >= j ? 1u : 0u;
+    if (sl_find(lay, c->roots[q], 0u, k0) == SL_NIL) sl_add(lay, c->roots[q], 0u, k0, 1u);
+  }
+  for (L = 0;; ++L) {
+    int any = 0, fresh = 0;
+    for (x = f1; x-- > f0;) {                    /* descending address: in-layer steps go down */
+      uint32_t st;
+      for (st = lay->head[x]; st != SL_NIL; st = lay->next[st]) {
+        uint32_t Pout, pair;
+        if (lay->k[st] != L) continue;
+        any = 1;
+        pair = sl_find(bfs, x, lay->P[st], 0u);
+        if (!bfs->flag[pair]) { bfs->flag[pair] = 1; fresh = 1; }
+        Pout = sl_pass(s, x, lay->P[st], r, pj, &stop);
+        if (stop) continue;
+        nk = sl_prev(c, x, c->kids);
+        for (q = 0; q < nk; ++q) {
+          const uint32_t k2 = L + (c->kids[q] >= x ? 1u : 0u);
+          const uint32_t t = sl_find(lay, c->kids[q], Pout, k2);
+          if (t == SL_NIL) sl_add(lay, c->kids[q], Pout, k2, lay->val[st] + 1u);
+          else if (lay->val[st] + 1u > lay->val[t]) lay->val[t] = lay->val[st] + 1u;
+        }
+      }
+    }
+    /* layer 0 is empty only when every root is behind a back edge: go on to layer 1 then */
+    if (any ? !fresh : L > 0) break;
+  }
+  for (i = 0; i < lay->n; ++i) {                 /* K* and the longest length at K* */
+    const uint32_t d = lay->x[i];
+    if (!sl_defines(s, d, r)) continue;
+    for (a = 0; a < *n_acc && acc[a].def != d; ++a) {}
+    if (lay->k[i] < acc[a].kstar) { acc[a].kstar = lay->k[i]; acc[a].mx = lay->val[i]; }
+    else if (lay->k[i] == acc[a].kstar && lay->val[i] > acc[a].mx) acc[a].mx = lay->val[i];
+  }
+
+  /* ---- rule 2 for this register: k separates def d from j iff k reads r, has no guard, k is
+   *      neither d nor j, and the search with k removed reaches no state of d */
+  for (a = 0; a < *n_acc; ++a) memset(acc[a].sep, 0, nf);
+  for (k = f0; k < f1; ++k) {
+    if (k == j || (s->guard[k] & 7u) != 7u || !sl_reads_reg(s, k, r)) continue;
+    sl_bfs(c, c->roots, nroot, r, pj, k, lay);   /* lay reused */
+    for (a = 0; a < *n_acc; ++a)
+      if (acc[a].def != k && lay->head[acc[a].def] == SL_NIL) acc[a].sep[k - f0] = 1;
+  }
+  for (a = 0; a < *n_acc; ++a)                   /* the defs r links to j: dom_ok &= sep */
+    if (sl_defines(s, acc[a].def, r) && bfs->head[acc[a].def] != SL_NIL)
+      for (k = 0; k < nf; ++k) acc[a].dom_ok[k] &= acc[a].sep[k];
 }
 
 int64_t or_slice(const or_sass *s, uint64_t cap, uint32_t *row_ptr, uint32_t *edge_def, uint8_t *edge_kind,
                  uint32_t *edge_min, uint32_t *edge_max, int32_t *edge_dom) {
   const uint32_t n = s->n_instr, NB = s->n_blocks;
-  uint32_t *blk_of = (uint32_t *)malloc(sizeof(uint32_t) * (n ? n : 1));
-  uint32_t *pred_ptr = (uint32_t *)calloc(NB + 1, sizeof(uint32_t));
-  uint32_t *pred = (uint32_t *)malloc(sizeof(uint32_t) * (s->succ_ptr[NB] ? s->succ_ptr[NB] : 1));
+  sl_cfg c;
   uint32_t *fill = (uint32_t *)calloc(NB + 1, sizeof(uint32_t));
-  uint32_t b, e, j, f, maxf = 1;
+  uint32_t b, e, j, f, maxf = 1, maxp = 1, a, a2;
   uint64_t E = 0;
   int64_t ret = -1;
-  sl_graph g;
-  uint32_t *queue, *stack, *sidx, *rpo, *mark, *cands;
-  uint32_t *acc_def, *acc_min, *acc_max, *acc_last;
-  int32_t *acc_dom;
-  uint8_t *acc_kind;
+  sl_states bfs, lay;
+  sl_acc *acc;
+  c.s = s;
+  c.blk_of = (uint32_t *)malloc(sizeof(uint32_t) * (n ? n : 1));
+  c.pred_ptr = (uint32_t *)calloc(NB + 1, sizeof(uint32_t));
+  c.pred = (uint32_t *)malloc(sizeof(uint32_t) * (s->succ_ptr[NB] ? s->succ_ptr[NB] : 1));
   for (b = 0; b < NB; ++b)
-    for (j = s->block_begin[b]; j < s->block_begin[b + 1]; ++j) blk_of[j] = b;
+    for (j = s->block_begin[b]; j < s->block_begin[b + 1]; ++j) c.blk_of[j] = b;
   for (b = 0; b < NB; ++b)
-    for (e = s->succ_ptr[b]; e < s->succ_ptr[b + 1]; ++e) pred_ptr[s->succ[e] + 1]++;
-  for (b = 0; b < NB; ++b) pred_ptr[b + 1] += pred_ptr[b];
+    for (e = s->succ_ptr[b]; e < s->succ_ptr[b + 1]; ++e) c.pred_ptr[s->succ[e] + 1]++;
+  for (b = 0; b < NB; ++b) {
+    if (c.pred_ptr[b + 1] > maxp) maxp = c.pred_ptr[b + 1];
+    c.pred_ptr[b + 1] += c.pred_ptr[b];
+  }
   for (b = 0; b < NB; ++b)                       /* ascending source block id per target */
     for (e = s->succ_ptr[b]; e < s->succ_ptr[b + 1]; ++e) {
       uint32_t t = s->succ[e];
-      pred[pred_ptr[t] + fill[t]++] = b;
+      c.pred[c.pred_ptr[t] + fill[t]++] = b;
     }
+  c.kids = (uint32_t *)malloc(4u * (maxp + 1u));
+  c.roots = (uint32_t *)malloc(4u * (maxp + 1u));
   for (f = 0; f < s->n_funcs; ++f)
     if (s->func_begin[f + 1] - s->func_begin[f] > maxf) maxf = s->func_begin[f + 1] - s->func_begin[f];
-  g.cap = 16u * maxf + 1024u;                    /* states per search (<= 16 P-sets per instruction) */
-  g.hcap = 1u;
-  while (g.hcap < 2u * g.cap) g.hcap <<= 1;
-  g.x = (uint32_t *)malloc(4u * g.cap); g.P = (uint32_t *)malloc(4u * g.cap);
-  g.dist = (uint32_t *)malloc(4u * g.cap); g.lng = (uint32_t *)malloc(4u * g.cap);
-  g.rpo_pos = (uint32_t *)malloc(4u * g.cap); g.hslot = (uint32_t *)malloc(4u * g.cap);
-  g.term = (uint8_t *)malloc(g.cap);
-  g.hkey_x = (uint32_t *)malloc(4u * g.hcap); g.hkey_p = (uint32_t *)malloc(4u * g.hcap);
-  g.hval = (uint32_t *)malloc(4u * g.hcap);
-  queue = (uint32_t *)malloc(4u * g.cap); stack = (uint32_t *)malloc(4u * g.cap);
-  sidx = (uint32_t *)malloc(4u * g.cap); rpo = (uint32_t *)malloc(4u * g.cap);
-  mark = (uint32_t *)malloc(4u * g.cap); cands = (uint32_t *)malloc(4u * g.cap);
-  acc_def = (uint32_t *)malloc(4u * g.cap); acc_min = (uint32_t *)malloc(4u * g.cap);
-  acc_max = (uint32_t *)malloc(4u * g.cap); acc_dom = (int32_t *)malloc(4u * g.cap);
-  acc_last = (uint32_t *)malloc(4u * g.cap);
-  acc_kind = (uint8_t *)malloc(g.cap);
-  for (e = 0; e < g.hcap; ++e) g.hval[e] = 0xFFFFFFFFu;
-  g.n = 0;
+  sl_states_init(&bfs, n);
+  sl_states_init(&lay, n);
+  acc = (sl_acc *)malloc(sizeof(sl_acc) * maxf);
+  for (a = 0; a < maxf; ++a) { acc[a].dom_ok = (uint8_t *)malloc(maxf); acc[a].sep = (uint8_t *)malloc(maxf); }
   row_ptr[0] = 0;
-  for (j = 0; j < n; ++j) {
-    uint32_t reads[16], n_acc = 0, a, a2;
+  for (f = 0, j = 0; j < n; ++j) {
+    uint32_t reads[16], n_acc = 0;
     uint8_t kinds[16];
     const int nr = sl_reads(s, j, reads, kinds);
-    const uint32_t pj = sl_pbit(s->guard[j]);
     int ri;
-    for (ri = 0; ri < nr; ++ri) {
-      const uint32_t r = reads[ri];
-      uint32_t head = 0, tail = 0, i, roots[64], kids[64], n_cand = 0, sp = 0, cnt = 0;
-      int nroot, nk, q, term;
-      /* ---- BFS over states from the virtual root at j (shortest path lengths), Q36 */
-      sl_clear(&g);
-      nroot = sl_prev(s, blk_of, pred_ptr, pred, j, roots);
-      for (q = 0; q < nroot; ++q)
-        if (sl_find(&g, roots[q], 0u) == 0xFFFFFFFFu) {
-          uint32_t id = sl_insert(&g, roots[q], 0u);
-          g.dist[id] = 1u;
-          queue[tail++] = id;
-        }
-      while (head < tail) {
-        uint32_t u = queue[head++];
-        const uint32_t Pout = sl_out_mask(s, g.x[u], g.P[u], r, pj, &term);
-        g.term[u] = (uint8_t)term;
-        if (term) continue;
-        nk = sl_prev(s, blk_of, pred_ptr, pred, g.x[u], kids);
-        for (q = 0; q < nk; ++q)
-          if (sl_find(&g, kids[q], Pout) == 0xFFFFFFFFu) {
-            uint32_t v;
-            if (g.n + 1u >= g.cap) goto fail;           /* state budget */
-            v = sl_insert(&g, kids[q], Pout);
-            g.dist[v] = g.dist[u] + 1u;
-            queue[tail++] = v;
-          }
-      }
-      /* ---- DFS in the same successor order; longest paths over the edges that go forward in
-       *      the reverse postorder (the DFS back edges -- loops -- are cut), Q37 */
-      for (i = 0; i < g.n; ++i) { mark[i] = 0; g.lng[i] = 0; }
-      for (q = 0; q < nroot; ++q) {
-        const uint32_t c = sl_find(&g, roots[q], 0u);
-        if (mark[c]) continue;
-        mark[c] = 1; stack[0] = c; sidx[0] = 0; sp = 1;
-        while (sp) {
-          const uint32_t u = stack[sp - 1];
-          nk = 0;
-          if (!g.term[u]) {
-            const uint32_t Pout = sl_out_mask(s, g.x[u], g.P[u], r, pj, &term);
-            nk = sl_prev(s, blk_of, pred_ptr, pred, g.x[u], kids);
-            if ((int)sidx[sp - 1] < nk) {
-              const uint32_t v = sl_find(&g, kids[sidx[sp - 1]++], Pout);
-              if (!mark[v]) { mark[v] = 1; stack[sp] = v; sidx[sp] = 0; ++sp; }
-              continue;
-            }
-          }
-          rpo[cnt++] = u;                                /* postorder */
-          --sp;
-        }
-      }
-      for (i = 0; i < cnt; ++i) g.rpo_pos[rpo[i]] = cnt - 1 - i;
-      for (q = 0; q < nroot; ++q) g.lng[sl_find(&g, roots[q], 0u)] = 1u;
-      for (i = cnt; i-- > 0;) {                          /* reverse postorder */
-        const uint32_t u = rpo[i];
-        uint32_t Pout;
-        if (g.term[u]) continue;
-        Pout = sl_out_mask(s, g.x[u], g.P[u], r, pj, &term);
-        nk = sl_prev(s, blk_of, pred_ptr, pred, g.x[u], kids);
-        for (q = 0; q < nk; ++q) {
-          const uint32_t v = sl_find(&g, kids[q], Pout);
-          if (g.rpo_pos[v] > g.rpo_pos[u] && g.lng[u] + 1u > g.lng[v]) g.lng[v] = g.lng[u] + 1u;
-        }
-      }
-      /* ---- rule-2 candidates: unpredicated readers of r met by the search (ascending), Q38 */
-      for (i = 0; i < g.n; ++i) {
-        const uint32_t k = g.x[i];
-        if (k == j || (s->guard[k] & 7u) != 7u || !sl_reads_reg(s, k, r)) continue;
-        for (a = 0; a < n_cand && cands[a] != k; ++a) {}
-        if (a == n_cand) cands[n_cand++] = k;
-      }
-      for (a = 1; a < n_cand; ++a)
-        for (a2 = a; a2 > 0 && cands[a2 - 1] > cands[a2]; --a2) {
-          const uint32_t t0 = cands[a2]; cands[a2] = cands[a2 - 1]; cands[a2 - 1] = t0;
-        }
-      /* ---- the defs this read found */
-      for (i = 0; i < g.n; ++i) {
-        const uint32_t x = g.x[i];
-        uint8_t kind;
-        int32_t dom = -1;
-        uint32_t c;
-        if (!sl_defines(s, x, r)) continue;
-        for (a = 0; a < n_acc && acc_def[a] != x; ++a) {}
-        kind = kinds[ri];
-        if (r >= 512u && ((s->rbar[x] >> (r - 512u)) & 1u)) {   /* WAR: j overwrites what x reads */
-          int tt, uu;
-          for (tt = 0; tt < 4; ++tt)
-            for (uu = 0; uu < 4; ++uu) {
-              const uint16_t d = s->dst[4u * j + tt];
-              if (d != SL_NONE && d != 255u && d == s->src[4u * x + uu]) kind |= 8u;
-            }
-        }
-        if (a == n_acc) {                          /* first state of def x in this row */
-          acc_def[a] = x; acc_kind[a] = 0; acc_min[a] = 0xFFFFFFFFu; acc_max[a] = 0; acc_dom[a] = -2;
-          acc_last[a] = 0;
-          ++n_acc;
-        }
-        acc_kind[a] |= kind;
-        if (g.dist[i] < acc_min[a]) acc_min[a] = g.dist[i];
-        if (g.lng[i] > acc_max[a]) acc_max[a] = g.lng[i];
-        if (acc_last[a] == (uint32_t)ri + 1u) continue;   /* rule 2 already settled for (x, this read) */
-        acc_last[a] = (uint32_t)ri + 1u;
-        /* rule 2: the smallest candidate k != x on every path from j to every state of x */
-        for (c = 0; c < n_cand && dom < 0; ++c) {
-          uint32_t h2 = 0, t2 = 0, st;
-          int reach = 0;
-          const uint32_t k = cands[c];
-          if (k == x) continue;
-          for (st = 0; st < g.n; ++st) mark[st] = 0;
-          for (q = 0; q < nroot; ++q) {
-            const uint32_t cc = sl_find(&g, roots[q], 0u);
-            if (g.x[cc] != k && !mark[cc]) { mark[cc] = 1; queue[t2++] = cc; }
-          }
-          while (h2 < t2 && !reach) {
-            const uint32_t u = queue[h2++];
-            uint32_t Pout;
-            if (g.x[u] == x) { reach = 1; break; }
-            if (g.term[u]) continue;
-            Pout = sl_out_mask(s, g.x[u], g.P[u], r, pj, &term);
-            nk = sl_prev(s, blk_of, pred_ptr, pred, g.x[u], kids);
-            for (q = 0; q < nk; ++q) {
-              const uint32_t v = sl_find(&g, kids[q], Pout);
-              if (g.x[v] != k && !mark[v]) { mark[v] = 1; queue[t2++] = v; }
-            }
-          }
-          if (!reach) dom = (int32_t)k;
-        }
-        /* merged over the reads reaching x: kept only if all agree (Q38) */
-        if (acc_dom[a] == -2) acc_dom[a] = dom;
-        else if (acc_dom[a] != dom) acc_dom[a] = -1;
-      }
-    }
-    for (a = 1; a < n_acc; ++a)                          /* defs ascending */
-      for (a2 = a; a2 > 0 && acc_def[a2 - 1] > acc_def[a2]; --a2) {
-        uint32_t t0 = acc_def[a2]; acc_def[a2] = acc_def[a2 - 1]; acc_def[a2 - 1] = t0;
-        t0 = acc_min[a2]; acc_min[a2] = acc_min[a2 - 1]; acc_min[a2 - 1] = t0;
-        t0 = acc_max[a2]; acc_max[a2] = acc_max[a2 - 1]; acc_max[a2 - 1] = t0;
-        { const uint8_t t1 = acc_kind[a2]; acc_kind[a2] = acc_kind[a2 - 1]; acc_kind[a2 - 1] = t1; }
-        { const int32_t t3 = acc_dom[a2]; acc_dom[a2] = acc_dom[a2 - 1]; acc_dom[a2 - 1] = t3; }
+    while (s->func_begin[f + 1] <= j) ++f;
+    for (ri = 0; ri < nr; ++ri)
+      sl_register(&c, s->func_begin[f], s->func_begin[f + 1], j, reads[ri], kinds[ri], &bfs, &lay, acc, &n_acc);
+    for (a = 1; a < n_acc; ++a)                  /* defs ascending */
+      for (a2 = a; a2 > 0 && acc[a2 - 1].def > acc[a2].def; --a2) {
+        const sl_acc t0 = acc[a2]; acc[a2] = acc[a2 - 1]; acc[a2 - 1] = t0;
       }
     for (a = 0; a < n_acc; ++a) {
+      int32_t dom = -1;
+      uint32_t k;
       if (E >= cap) goto fail;
-      edge_def[E] = acc_def[a]; edge_kind[E] = acc_kind[a];
-      edge_min[E] = acc_min[a]; edge_max[E] = acc_max[a];
-      edge_dom[E] = acc_dom[a] < 0 ? -1 : acc_dom[a];
+      for (k = 0; k < s->func_begin[f + 1] - s->func_begin[f] && dom < 0; ++k)
+        if (acc[a].dom_ok[k]) dom = (int32_t)(s->func_begin[f] + k);
+      edge_def[E] = acc[a].def; edge_kind[E] = acc[a].kind;
+      edge_min[E] = acc[a].mn; edge_max[E] = acc[a].mx; edge_dom[E] = dom;
       ++E;
     }
     row_ptr[j + 1] = (uint32_t)E;
   }
   ret = (int64_t)E;
 fail:
-  free(blk_of); free(pred_ptr); free(pred); free(fill);
-  free(g.x); free(g.P); free(g.dist); free(g.lng); free(g.rpo_pos); free(g.hslot); free(g.term);
-  free(g.hkey_x); free(g.hkey_p); free(g.hval);
-  free(queue); free(stack); free(sidx); free(rpo); free(mark); free(cands);
-  free(acc_def); free(acc_min); free(acc_max); free(acc_dom); free(acc_kind); free(acc_last);
+  free(fill); free(c.blk_of); free(c.pred_ptr); free(c.pred); free(c.kids); free(c.roots);
+  sl_states_free(&bfs); sl_states_free(&lay);
+  for (a = 0; a < maxf; ++a) { free(acc[a].dom_ok); free(acc[a].sep); }
+  free(acc);
   return ret;
 }
 

@@ -1,10 +1,14 @@
 """Pins of the oracle's backward slicing (readings DESIGN.md
-§3.2 Q35-Q39): the def-use graph of gpagen.sass.slice_fixture() derived by hand, and properties
-of random programs that any correct slicer has."""
+§3.2 Q35-Q39): the def-use graph of gpagen.sass.slice_fixture() derived by hand, SPEC's path-length
+examples, the brute-force path enumerator of tests/slice_enum.py (the definitions
+evaluated path by path; no code shared with oracle/) on 1,500 random <= 24-instruction CFGs with
+nested, multi-exit and multi-back-edge loops, and properties of larger random programs."""
 import numpy as np
+import pytest
 
 import oracle
 from gpagen import sass
+from tests.slice_enum import slice_all
 
 REG, PRED, BAR, WAR = 1, 2, 4, 8
 
@@ -19,9 +23,10 @@ EXPECTED = {
     7: [(3, REG | BAR, 4, 4, -1), (5, REG | BAR, 2, 2, -1)],   # @P0 LDG then @!P0 LDC cover '_'
     8: [(4, REG, 4, 4, -1), (7, REG, 1, 1, -1)],
     9: [(4, REG, 3, 3, -1)],
-    # R4 from both arms (1 step; 5 steps through one loop iteration), R6 loop-carried from the
-    # FFMA, whose value the MOV at 13 reads on every path: rule 2
-    10: [(8, REG, 1, 5, -1), (9, REG, 1, 5, -1), (12, REG, 2, 2, 13)],
+    # R4 from both arms, 1 step without the back edge (K* = 0, so the path through one more loop
+    # iteration does not count: S:185); R6 loop-carried from the FFMA (K* = 1: 10 <- 13 <- 12),
+    # whose value the MOV at 13 reads on every path: rule 2
+    10: [(8, REG, 1, 1, -1), (9, REG, 1, 1, -1), (12, REG, 2, 2, 13)],
     11: [(10, REG, 1, 1, -1)],
     12: [(10, REG, 2, 2, 11), (11, REG | BAR, 1, 1, -1)],    # the LDS at 11 reads R5: rule 2
     13: [(11, BAR | WAR, 2, 2, -1), (12, REG, 1, 1, -1)],    # read barrier B3 + MOV overwrites R5: WAR
@@ -71,3 +76,55 @@ def test_random_programs_slicing_properties():
                     assert int(csr["edge_min_len"][e]) == j - i
                 if k >= 0:
                     assert k != i and k != j and func_of[k] == func_of[j] and S.guard[k] == sass.ALWAYS
+
+
+def test_enumerator_reproduces_hand_derivation():
+    """The brute-force enumerator itself is pinned to the hand-derived fixture."""
+    assert slice_all(sass.slice_fixture()) == EXPECTED
+
+
+def _spec_cases():
+    """SPEC S:175-177 path_distance examples as SASS: (program, use j, def i, min, max)."""
+    R1, R2 = 1, 2
+    # adjacent instructions in one block: min = max = 1
+    adj = sass._build([dict(dst=[R1]), dict(src=[R1])], [(0, 2)], [[]])
+    # diamond with arms of 2 and 5 instructions: min 3, max 6 (arm + the join instruction)
+    I = [dict(dst=[R1])] + [dict(dst=[9])] * 2 + [dict(dst=[9])] * 5 + [dict(src=[R1])]
+    dia = sass._build(I, [(0, 1), (1, 3), (3, 8), (8, 9)], [[1, 2], [3], [3], []])
+    # j before i in a loop body (loop block [2, 6) with a back edge): R1 is defined at 4 after the
+    # use at 3, so the path needs the back edge once: 3 <- 2 <- 5 <- 4, min = max = 3; R2 defined
+    # before the loop: reachable without the back edge (K* = 0), 3 <- 2 <- 1, min = max = 2
+    I = [dict(dst=[9]), dict(dst=[R2]), dict(dst=[9]), dict(src=[R1, R2]), dict(dst=[R1]), dict(dst=[9]), dict()]
+    lp = sass._build(I, [(0, 2), (2, 6), (6, 7)], [[1], [1, 2], []])
+    return [(adj, 1, 0, 1, 1), (dia, 8, 0, 3, 6), (lp, 3, 4, 3, 3), (lp, 3, 1, 2, 2)]
+
+
+@pytest.mark.parametrize("case", range(4))
+def test_spec_path_length_examples(case):
+    S, j, i, mn, mx = _spec_cases()[case]
+    for rows in (_rows(oracle.slice_program(S)), slice_all(S)):
+        e = {d: (a, b) for d, _, a, b, _ in rows[j]}
+        assert e[i] == (mn, mx)
+
+
+def test_oracle_matches_path_enumeration_on_random_cfgs():
+    """the oracle's CSR equals the brute-force definitions (min_len, K* /
+    max_len, dom_k over every path, kinds) on 1,500 random tiny CFGs: nested loops, multi-block
+    bodies, `continue` (several back edges), `break` (multi-exit), loops headed by the entry
+    block, 1-3 functions."""
+    n_back = 0
+    for seed in range(1500):
+        S = sass.random_cfg_sass(seed, n_funcs=1 + seed % 3)
+        assert np.diff(S.func_begin.astype(np.int64)).max() <= 24
+        n_back += sum(int(S.block_begin[t]) <= int(S.block_begin[b + 1]) - 1 for b in range(len(S.block_begin) - 1)
+                      for t in S.succ[S.succ_ptr[b]:S.succ_ptr[b + 1]])
+        assert _rows(oracle.slice_program(S)) == slice_all(S), seed
+    assert n_back > 2000
+
+
+def test_enumerator_reduction_equals_direct_enumeration():
+    """The enumerator's shortcut (simple paths for minima / K* / rule 2) agrees with listing every
+    path of at most B back-edge crossings."""
+    for seed in range(8):
+        S = sass.random_cfg_sass(seed)
+        assert slice_all(S) == slice_all(S, reduced=False)
