@@ -1,15 +1,22 @@
 // slice.cu -- the step before the path: backward slicing of SASS fields into
 // the def-use CSR that gpa_program_create takes (readings DESIGN.md §3.2 Q35-Q39).
 //
-// One thread per use instruction j (grid-stride), independent of all others: for every register j
-// reads (source operands, its guard predicate, the virtual barrier registers of its wait mask) it
-// explores the backward state graph of j's function -- states (instruction x about to be examined,
-// P = predicates of the defs of the register passed so far) -- breadth first (shortest path
-// lengths), orders it depth first (longest path lengths over the edges that go forward in the
-// reverse postorder), and tests rule 2 by re-running the breadth-first search with each
-// unpredicated reader blocked.  Each thread owns a slice of a scratch buffer (state arrays and an
-// open-addressing index), so the work is an irregular per-thread graph walk with no
-// communication.  Two launches: edge counts per use, then (after a host prefix sum) the edges.
+// One thread per use instruction j (grid-stride), independent of all others.  For every register r j
+// reads (source operands, its guard predicate, the virtual barrier registers of its wait mask) the
+// thread explores the backward state graph of j's function -- states (instruction x about to be
+// examined, P = predicates of the defs of r passed so far), P:310-320 -- and evaluates the
+// definitions of DESIGN.md §3.2 Q36-Q38 (tests/slice_enum.py lists them path by path):
+//   * min_len: breadth-first distances over the (x, P) pairs;
+//   * K* and max_len: the pairs counting-sorted by descending address once, then "layers" L = 0, 1,
+//     ... of back-edge crossings, two length arrays over the pair ids (layer L, layer L+1): inside
+//     a layer every step goes to a lower address, so one descending sweep per layer settles its
+//     longest lengths; the sweep stops after a layer that meets no new pair;
+//   * rule 2: per def, candidates k ascending (unpredicated readers of every linking register met
+//     by the search), each tested by a breadth-first search with k removed, on the pair table of
+//     each linking register in turn (rebuilt only when the register changes).
+// Each thread owns a slice of a scratch buffer (pair arrays, an open-addressing index, the layer
+// arrays), so the work is an irregular per-thread graph walk with no communication.  Two launches:
+// edge counts per use, then (after a host prefix sum) the edges.
 #include <algorithm>
 #include <cstdlib>
 #include <vector>
@@ -27,16 +34,16 @@ constexpr uint32_t kSlThreads = 64;
 
 struct SliceIn {
   uint32_t n, n_blocks;
-  const uint32_t *block_begin, *blk_of, *pred_ptr, *pred;
+  const uint32_t *block_begin, *blk_of, *pred_ptr, *pred, *func_begin, *func_of;
   const uint8_t *guard, *wbar, *rbar, *wait;
   const uint16_t *dst, *src;
 };
 
 struct SliceScratch {   // per-thread views into the scratch buffer
-  uint32_t *x, *P, *dist, *lng, *rpo_pos, *hslot, *queue, *stack, *sidx, *rpo, *mark, *cands;
+  uint32_t *x, *P, *dist, *hslot, *order, *cur, *nxt, *stamp, *queue, *cnt, *cand;
   uint32_t *hx, *hp, *hv;
-  uint8_t *term;
-  uint32_t cap, hcap, n;
+  uint8_t *seen;
+  uint32_t cap, hcap, n, gen, nfmax;
 };
 
 __device__ __forceinline__ uint32_t pbit(uint8_t g) {
@@ -115,148 +122,175 @@ __device__ uint32_t hinsert(SliceScratch &g, uint32_t x, uint32_t P) {
 }
 
 struct RowAcc {
-  uint32_t def, mn, mx, last;
-  int32_t dom;
+  uint32_t def, mn, kstar, mx;
+  uint16_t regs;   // read indices of j linking the def
   uint8_t kind;
 };
 
-// the edges of use j, defs ascending, into out[] (when non-null); returns the count, or -1 when
-// the per-search state budget or the row capacity is exceeded
-__device__ int slice_row(const SliceIn &s, SliceScratch &g, RowAcc *acc, uint32_t acc_cap, uint32_t j,
-                         uint32_t *o_def, uint8_t *o_kind, uint32_t *o_min, uint32_t *o_max, int32_t *o_dom) {
+// breadth-first search from j over (x, P) for register r: the pair table (x, P, dist) and its index;
+// false when the per-search budget is exceeded
+__device__ bool build_pairs(const SliceIn &s, SliceScratch &g, uint32_t j, uint32_t r, uint32_t pj,
+                            const uint32_t *roots, int nroot) {
+  uint32_t kids[kSlMaxKids];
+  bool stop;
+  for (uint32_t i = 0; i < g.n; ++i) g.hv[g.hslot[i]] = kSlEmpty;
+  g.n = 0;
+  for (int q = 0; q < nroot; ++q)
+    if (hfind(g, roots[q], 0u) == kSlEmpty) {
+      const uint32_t id = hinsert(g, roots[q], 0u);
+      g.dist[id] = 1u;
+    }
+  for (uint32_t u = 0; u < g.n; ++u) {    // pairs are appended in discovery order: the list is the queue
+    const uint32_t Pout = out_mask(s, g.x[u], g.P[u], r, pj, stop);
+    if (stop) continue;
+    const int nk = prev_of(s, g.x[u], kids);
+    for (int q = 0; q < nk; ++q)
+      if (hfind(g, kids[q], Pout) == kSlEmpty) {
+        if (g.n + 1u >= g.cap) return false;
+        const uint32_t v = hinsert(g, kids[q], Pout);
+        g.dist[v] = g.dist[u] + 1u;
+      }
+  }
+  return true;
+}
+
+// with instruction k removed, does the search of the current pair table reach a state of def i?
+__device__ bool reaches_without(const SliceIn &s, SliceScratch &g, uint32_t r, uint32_t pj, const uint32_t *roots,
+                                int nroot, uint32_t k, uint32_t i) {
+  uint32_t kids[kSlMaxKids];
+  bool stop;
+  const uint32_t gen = ++g.gen;
+  uint32_t head = 0, tail = 0;
+  for (int q = 0; q < nroot; ++q) {
+    if (roots[q] == k) continue;
+    const uint32_t c = hfind(g, roots[q], 0u);
+    if (g.stamp[c] != gen) { g.stamp[c] = gen; g.queue[tail++] = c; }
+  }
+  while (head < tail) {
+    const uint32_t u = g.queue[head++];
+    if (g.x[u] == i) return true;
+    const uint32_t Pout = out_mask(s, g.x[u], g.P[u], r, pj, stop);
+    if (stop) continue;
+    const int nk = prev_of(s, g.x[u], kids);
+    for (int q = 0; q < nk; ++q) {
+      if (kids[q] == k) continue;
+      const uint32_t v = hfind(g, kids[q], Pout);
+      if (g.stamp[v] != gen) { g.stamp[v] = gen; g.queue[tail++] = v; }
+    }
+  }
+  return false;
+}
+
+// the edges of use j (function [f0, f1)), defs ascending, into out[] (when non-null); returns the
+// count, or -1 when the per-search state budget or the row capacity is exceeded
+__device__ int slice_row(const SliceIn &s, SliceScratch &g, RowAcc *acc, uint32_t acc_cap, uint32_t j, uint32_t f0,
+                         uint32_t f1, uint32_t *o_def, uint8_t *o_kind, uint32_t *o_min, uint32_t *o_max,
+                         int32_t *o_dom) {
   uint32_t reads[16];
   uint8_t kinds[16];
   const int nr = reads_of(s, j, reads, kinds);
-  const uint32_t pj = pbit(s.guard[j]);
+  const uint32_t pj = pbit(s.guard[j]), nf = f1 - f0;
   uint32_t n_acc = 0;
   uint32_t roots[kSlMaxKids], kids[kSlMaxKids];
+  const int nroot = prev_of(s, j, roots);
+  bool stop;
   for (int ri = 0; ri < nr; ++ri) {
     const uint32_t r = reads[ri];
-    bool term;
-    // ---- breadth first from the root at j
-    for (uint32_t i = 0; i < g.n; ++i) g.hv[g.hslot[i]] = kSlEmpty;
-    g.n = 0;
-    uint32_t head = 0, tail = 0;
-    const int nroot = prev_of(s, j, roots);
-    for (int q = 0; q < nroot; ++q)
-      if (hfind(g, roots[q], 0u) == kSlEmpty) {
-        const uint32_t id = hinsert(g, roots[q], 0u);
-        g.dist[id] = 1u;
-        g.queue[tail++] = id;
-      }
-    while (head < tail) {
-      const uint32_t u = g.queue[head++];
-      const uint32_t Pout = out_mask(s, g.x[u], g.P[u], r, pj, term);
-      g.term[u] = term;
-      if (term) continue;
-      const int nk = prev_of(s, g.x[u], kids);
-      for (int q = 0; q < nk; ++q)
-        if (hfind(g, kids[q], Pout) == kSlEmpty) {
-          if (g.n + 1u >= g.cap) return -1;
-          const uint32_t v = hinsert(g, kids[q], Pout);
-          g.dist[v] = g.dist[u] + 1u;
-          g.queue[tail++] = v;
-        }
-    }
-    // ---- depth first (same successor order): reverse postorder; longest paths forward in it
-    for (uint32_t i = 0; i < g.n; ++i) { g.mark[i] = 0; g.lng[i] = 0; }
-    uint32_t cnt = 0;
-    for (int q = 0; q < nroot; ++q) {
-      const uint32_t c = hfind(g, roots[q], 0u);
-      if (g.mark[c]) continue;
-      g.mark[c] = 1; g.stack[0] = c; g.sidx[0] = 0;
-      uint32_t sp = 1;
-      while (sp) {
-        const uint32_t u = g.stack[sp - 1];
-        if (!g.term[u]) {
-          const uint32_t Pout = out_mask(s, g.x[u], g.P[u], r, pj, term);
-          const int nk = prev_of(s, g.x[u], kids);
-          if ((int)g.sidx[sp - 1] < nk) {
-            const uint32_t v = hfind(g, kids[g.sidx[sp - 1]++], Pout);
-            if (!g.mark[v]) { g.mark[v] = 1; g.stack[sp] = v; g.sidx[sp] = 0; ++sp; }
-            continue;
-          }
-        }
-        g.rpo[cnt++] = u;
-        --sp;
-      }
-    }
-    for (uint32_t i = 0; i < cnt; ++i) g.rpo_pos[g.rpo[i]] = cnt - 1 - i;
-    for (int q = 0; q < nroot; ++q) g.lng[hfind(g, roots[q], 0u)] = 1u;
-    for (uint32_t i = cnt; i-- > 0;) {
-      const uint32_t u = g.rpo[i];
-      if (g.term[u]) continue;
-      const uint32_t Pout = out_mask(s, g.x[u], g.P[u], r, pj, term);
-      const int nk = prev_of(s, g.x[u], kids);
-      for (int q = 0; q < nk; ++q) {
-        const uint32_t v = hfind(g, kids[q], Pout);
-        if (g.rpo_pos[v] > g.rpo_pos[u] && g.lng[u] + 1u > g.lng[v]) g.lng[v] = g.lng[u] + 1u;
-      }
-    }
-    // ---- rule-2 candidates: unpredicated readers of r met by the search, ascending
-    uint32_t n_cand = 0;
+    if (!build_pairs(s, g, j, r, pj, roots, nroot)) return -1;
+    // ---- the defs reached: kinds, minimum lengths
     for (uint32_t i = 0; i < g.n; ++i) {
-      const uint32_t k = g.x[i];
-      if (k == j || (s.guard[k] & 7u) != 7u || !reads_reg(s, k, r)) continue;
+      const uint32_t d = g.x[i];
+      if (!defines(s, d, r)) continue;
       uint32_t a = 0;
-      while (a < n_cand && g.cands[a] != k) ++a;
-      if (a == n_cand) g.cands[n_cand++] = k;
-    }
-    for (uint32_t a = 1; a < n_cand; ++a)
-      for (uint32_t b = a; b > 0 && g.cands[b - 1] > g.cands[b]; --b) {
-        const uint32_t t = g.cands[b]; g.cands[b] = g.cands[b - 1]; g.cands[b - 1] = t;
-      }
-    // ---- the defs this read found
-    for (uint32_t i = 0; i < g.n; ++i) {
-      const uint32_t x = g.x[i];
-      if (!defines(s, x, r)) continue;
-      uint32_t a = 0;
-      while (a < n_acc && acc[a].def != x) ++a;
-      uint8_t kind = kinds[ri];
-      if (r >= 512u && ((s.rbar[x] >> (r - 512u)) & 1u)) {   // WAR
-        for (int tt = 0; tt < 4; ++tt)
-          for (int uu = 0; uu < 4; ++uu) {
-            const uint16_t d = s.dst[4u * j + tt];
-            if (d != kSlNone && d != 255u && d == s.src[4u * x + uu]) kind |= 8u;
-          }
-      }
+      while (a < n_acc && acc[a].def != d) ++a;
       if (a == n_acc) {
         if (n_acc >= acc_cap) return -1;
-        acc[a] = RowAcc{x, 0xFFFFFFFFu, 0u, 0u, -2, 0};
+        acc[a] = RowAcc{d, 0xFFFFFFFFu, 0xFFFFFFFFu, 0u, 0, 0};
         ++n_acc;
       }
-      acc[a].kind |= kind;
-      acc[a].mn = min(acc[a].mn, g.dist[i]);
-      acc[a].mx = max(acc[a].mx, g.lng[i]);
-      if (acc[a].last == (uint32_t)ri + 1u) continue;
-      acc[a].last = (uint32_t)ri + 1u;
-      int32_t dom = -1;
-      for (uint32_t c = 0; c < n_cand && dom < 0; ++c) {
-        const uint32_t k = g.cands[c];
-        if (k == x) continue;
-        for (uint32_t st = 0; st < g.n; ++st) g.mark[st] = 0;
-        uint32_t h2 = 0, t2 = 0;
-        bool reach = false;
-        for (int q = 0; q < nroot; ++q) {
-          const uint32_t cc = hfind(g, roots[q], 0u);
-          if (g.x[cc] != k && !g.mark[cc]) { g.mark[cc] = 1; g.queue[t2++] = cc; }
-        }
-        while (h2 < t2 && !reach) {
-          const uint32_t u = g.queue[h2++];
-          if (g.x[u] == x) { reach = true; break; }
-          if (g.term[u]) continue;
-          const uint32_t Pout = out_mask(s, g.x[u], g.P[u], r, pj, term);
-          const int nk = prev_of(s, g.x[u], kids);
-          for (int q = 0; q < nk; ++q) {
-            const uint32_t v = hfind(g, kids[q], Pout);
-            if (g.x[v] != k && !g.mark[v]) { g.mark[v] = 1; g.queue[t2++] = v; }
+      uint8_t kind = kinds[ri];
+      if (r >= 512u && ((s.rbar[d] >> (r - 512u)) & 1u)) {   // WAR
+        for (int tt = 0; tt < 4; ++tt)
+          for (int uu = 0; uu < 4; ++uu) {
+            const uint16_t w = s.dst[4u * j + tt];
+            if (w != kSlNone && w != 255u && w == s.src[4u * d + uu]) kind |= 8u;
           }
-        }
-        if (!reach) dom = (int32_t)k;
       }
-      if (acc[a].dom == -2) acc[a].dom = dom;
-      else if (acc[a].dom != dom) acc[a].dom = -1;
+      acc[a].kind |= kind;
+      acc[a].regs |= (uint16_t)(1u << ri);
+      acc[a].mn = min(acc[a].mn, g.dist[i]);
     }
+    // ---- pairs by descending address (counting sort over the function)
+    for (uint32_t t = 0; t <= nf; ++t) g.cnt[t] = 0;
+    for (uint32_t i = 0; i < g.n; ++i) ++g.cnt[f1 - 1u - g.x[i] + 1u];
+    for (uint32_t t = 0; t < nf; ++t) g.cnt[t + 1] += g.cnt[t];
+    for (uint32_t i = 0; i < g.n; ++i) g.order[g.cnt[f1 - 1u - g.x[i]]++] = i;
+    // ---- layers of back-edge crossings: cur = layer L lengths, nxt = layer L+1 (0 = no state)
+    for (uint32_t i = 0; i < g.n; ++i) { g.cur[i] = 0; g.nxt[i] = 0; g.seen[i] = 0; }
+    for (int q = 0; q < nroot; ++q) {
+      const uint32_t c = hfind(g, roots[q], 0u);
+      if (roots[q] >= j) g.nxt[c] = 1u; else g.cur[c] = 1u;
+    }
+    for (uint32_t L = 0;; ++L) {
+      bool any = false, fresh = false;
+      for (uint32_t t = 0; t < g.n; ++t) {
+        const uint32_t u = g.order[t], v = g.cur[u];
+        if (!v) continue;
+        any = true;
+        if (!g.seen[u]) { g.seen[u] = 1; fresh = true; }
+        const uint32_t x = g.x[u];
+        if (defines(s, x, r)) {
+          uint32_t a = 0;
+          while (acc[a].def != x) ++a;
+          if (L < acc[a].kstar) { acc[a].kstar = L; acc[a].mx = v; }
+          else if (L == acc[a].kstar && v > acc[a].mx) acc[a].mx = v;
+        }
+        const uint32_t Pout = out_mask(s, x, g.P[u], r, pj, stop);
+        if (stop) continue;
+        const int nk = prev_of(s, x, kids);
+        for (int q = 0; q < nk; ++q) {
+          const uint32_t w = hfind(g, kids[q], Pout);
+          uint32_t *lay = kids[q] >= x ? g.nxt : g.cur;   // a back edge starts layer L+1
+          if (v + 1u > lay[w]) lay[w] = v + 1u;
+        }
+      }
+      if (any ? !fresh : L > 0) break;   // layer 0 is empty only when every root is behind a back edge
+      uint32_t *t = g.cur; g.cur = g.nxt; g.nxt = t;
+      for (uint32_t i = 0; i < g.n; ++i) g.nxt[i] = 0;
+    }
+  }
+  // ---- rule 2, per def: the smallest unpredicated k (not the def, not j) reading every
+  //      linking register that every path of each of them passes
+  for (uint32_t a = 0; a < n_acc; ++a) {
+    const uint32_t i = acc[a].def, regs = acc[a].regs;
+    const int r0 = __ffs(regs) - 1;
+    if (!build_pairs(s, g, j, reads[r0], pj, roots, nroot)) return -1;
+    int cur_reg = r0;
+    for (uint32_t t = 0; t < nf; ++t) g.cnt[t] = 0;
+    for (uint32_t u = 0; u < g.n; ++u) g.cnt[g.x[u] - f0] = 1;   // instructions the search meets
+    uint32_t n_cand = 0;
+    for (uint32_t k = f0; k < f1; ++k) {
+      if (!g.cnt[k - f0] || k == j || k == i || (s.guard[k] & 7u) != 7u) continue;
+      bool all = true;
+      for (int ri = 0; ri < nr && all; ++ri)
+        if ((regs >> ri) & 1u) all = reads_reg(s, k, reads[ri]);
+      if (all) g.cand[n_cand++] = k;
+    }
+    int32_t dom = -1;
+    for (uint32_t c = 0; c < n_cand && dom < 0; ++c) {
+      const uint32_t k = g.cand[c];
+      bool sep = true;
+      for (int ri = 0; ri < nr && sep; ++ri) {
+        if (!((regs >> ri) & 1u)) continue;
+        if (cur_reg != ri) {
+          if (!build_pairs(s, g, j, reads[ri], pj, roots, nroot)) return -1;
+          cur_reg = ri;
+        }
+        sep = !reaches_without(s, g, reads[ri], pj, roots, nroot, k, i);
+      }
+      if (sep) dom = (int32_t)k;
+    }
+    acc[a].kstar = (uint32_t)dom;   // reused: the rule-2 result
   }
   for (uint32_t a = 1; a < n_acc; ++a)
     for (uint32_t b = a; b > 0 && acc[b - 1].def > acc[b].def; --b) {
@@ -265,38 +299,42 @@ __device__ int slice_row(const SliceIn &s, SliceScratch &g, RowAcc *acc, uint32_
   if (o_def)
     for (uint32_t a = 0; a < n_acc; ++a) {
       o_def[a] = acc[a].def; o_kind[a] = acc[a].kind; o_min[a] = acc[a].mn; o_max[a] = acc[a].mx;
-      o_dom[a] = acc[a].dom < 0 ? -1 : acc[a].dom;
+      o_dom[a] = (int32_t)acc[a].kstar;
     }
   return (int)n_acc;
 }
 
 // pass 1 (row_ptr == nullptr): counts[j]; pass 2: edges at row_ptr[j]
 __global__ void __launch_bounds__(kSlThreads) k_slice(SliceIn s, uint8_t *scratch, size_t per_thread, uint32_t cap,
-                                                      uint32_t hcap, uint32_t *counts, const uint32_t *row_ptr,
-                                                      uint32_t *e_def, uint8_t *e_kind, uint32_t *e_min,
-                                                      uint32_t *e_max, int32_t *e_dom, int *error) {
+                                                      uint32_t hcap, uint32_t nfmax, uint32_t *counts,
+                                                      const uint32_t *row_ptr, uint32_t *e_def, uint8_t *e_kind,
+                                                      uint32_t *e_min, uint32_t *e_max, int32_t *e_dom, int *error) {
   const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
   uint8_t *base = scratch + (size_t)tid * per_thread;
   SliceScratch g;
   uint32_t *w = reinterpret_cast<uint32_t *>(base);
   g.cap = cap;
   g.hcap = hcap;
-  g.x = w; w += cap; g.P = w; w += cap; g.dist = w; w += cap; g.lng = w; w += cap; g.rpo_pos = w; w += cap;
-  g.hslot = w; w += cap; g.queue = w; w += cap; g.stack = w; w += cap; g.sidx = w; w += cap; g.rpo = w; w += cap;
-  g.mark = w; w += cap; g.cands = w; w += cap;
+  g.nfmax = nfmax;
+  g.x = w; w += cap; g.P = w; w += cap; g.dist = w; w += cap; g.hslot = w; w += cap; g.order = w; w += cap;
+  g.cur = w; w += cap; g.nxt = w; w += cap; g.stamp = w; w += cap; g.queue = w; w += cap;
+  g.cnt = w; w += nfmax + 1; g.cand = w; w += nfmax;
   g.hx = w; w += hcap; g.hp = w; w += hcap; g.hv = w; w += hcap;
   RowAcc *acc = reinterpret_cast<RowAcc *>(w);
-  g.term = reinterpret_cast<uint8_t *>(acc + cap);
+  g.seen = reinterpret_cast<uint8_t *>(acc + cap);
   for (uint32_t h = 0; h < hcap; ++h) g.hv[h] = kSlEmpty;
+  for (uint32_t i = 0; i < cap; ++i) g.stamp[i] = 0;
   g.n = 0;
+  g.gen = 0;
   for (uint32_t j = tid; j < s.n; j += gridDim.x * blockDim.x) {
+    const uint32_t f = s.func_of[j], f0 = s.func_begin[f], f1 = s.func_begin[f + 1];
     int c;
     if (!row_ptr) {
-      c = slice_row(s, g, acc, cap, j, nullptr, nullptr, nullptr, nullptr, nullptr);
+      c = slice_row(s, g, acc, cap, j, f0, f1, nullptr, nullptr, nullptr, nullptr, nullptr);
       if (c >= 0) counts[j] = (uint32_t)c;
     } else {
       const uint32_t o = row_ptr[j];
-      c = slice_row(s, g, acc, cap, j, e_def + o, e_kind + o, e_min + o, e_max + o, e_dom + o);
+      c = slice_row(s, g, acc, cap, j, f0, f1, e_def + o, e_kind + o, e_min + o, e_max + o, e_dom + o);
       if (c >= 0 && (uint32_t)c != row_ptr[j + 1] - o) c = -1;
     }
     if (c < 0) atomicExch(error, 1);
@@ -305,8 +343,8 @@ __global__ void __launch_bounds__(kSlThreads) k_slice(SliceIn s, uint8_t *scratc
 
 }  // namespace
 
-size_t slice_scratch_per_thread(uint32_t cap, uint32_t hcap) {
-  return (size_t)cap * (12 * 4 + sizeof(RowAcc) + 1) + (size_t)hcap * 12 + 64;
+size_t slice_scratch_per_thread(uint32_t cap, uint32_t hcap, uint32_t nfmax) {
+  return (size_t)cap * (9 * 4 + sizeof(RowAcc) + 1) + (size_t)hcap * 12 + ((size_t)nfmax * 2 + 1) * 4 + 64;
 }
 
 cudaError_t launch_slice(const gpa_sass_desc *h, uint32_t *h_row_ptr, uint64_t cap_edges, uint32_t *h_def,
@@ -331,10 +369,13 @@ cudaError_t launch_slice(const gpa_sass_desc *h, uint32_t *h_row_ptr, uint64_t c
   }
   uint32_t maxf = 1;
   for (uint32_t f = 0; f < h->n_funcs; ++f) maxf = std::max(maxf, h->func_begin[f + 1] - h->func_begin[f]);
-  const uint32_t cap = 4u * maxf + 256u;   // states per search (Q39)
+  const uint32_t cap = 4u * maxf + 256u;   // (x, P) pairs per search (Q39)
   uint32_t hcap = 1;
   while (hcap < 2u * cap) hcap <<= 1;
-  const size_t per_thread = (slice_scratch_per_thread(cap, hcap) + 255) & ~(size_t)255;
+  const size_t per_thread = (slice_scratch_per_thread(cap, hcap, maxf) + 255) & ~(size_t)255;
+  std::vector<uint32_t> func_of(std::max<uint32_t>(n, 1));
+  for (uint32_t f = 0; f < h->n_funcs; ++f)
+    for (uint32_t j = h->func_begin[f]; j < h->func_begin[f + 1]; ++j) func_of[j] = f;
   // device copies (every allocation is released on every path)
   std::vector<void *> owned;
   cudaError_t e = cudaSuccess;
@@ -351,6 +392,7 @@ cudaError_t launch_slice(const gpa_sass_desc *h, uint32_t *h_row_ptr, uint64_t c
   };
   SliceIn s{n, NB, (const uint32_t *)up(h->block_begin, (NB + 1) * 4), (const uint32_t *)up(blk_of.data(), (size_t)n * 4),
             (const uint32_t *)up(pred_ptr.data(), (NB + 1) * 4), (const uint32_t *)up(pred.data(), (size_t)pred_ptr[NB] * 4),
+            (const uint32_t *)up(h->func_begin, (size_t)(h->n_funcs + 1) * 4), (const uint32_t *)up(func_of.data(), (size_t)n * 4),
             (const uint8_t *)up(h->guard, n), (const uint8_t *)up(h->wbar, n), (const uint8_t *)up(h->rbar, n),
             (const uint8_t *)up(h->wait, n), (const uint16_t *)up(h->dst, (size_t)n * 8),
             (const uint16_t *)up(h->src, (size_t)n * 8)};
@@ -371,7 +413,7 @@ cudaError_t launch_slice(const gpa_sass_desc *h, uint32_t *h_row_ptr, uint64_t c
   std::vector<uint32_t> cnt(std::max<uint32_t>(n, 1));
   int err = 0;
   if (e == cudaSuccess) {
-    k_slice<<<grid, kSlThreads, 0, st>>>(s, (uint8_t *)d_scr, per_thread, cap, hcap, (uint32_t *)d_cnt, nullptr, nullptr,
+    k_slice<<<grid, kSlThreads, 0, st>>>(s, (uint8_t *)d_scr, per_thread, cap, hcap, maxf, (uint32_t *)d_cnt, nullptr, nullptr,
                                          nullptr, nullptr, nullptr, nullptr, (int *)d_err);
     e = cudaGetLastError();
   }
@@ -393,7 +435,7 @@ cudaError_t launch_slice(const gpa_sass_desc *h, uint32_t *h_row_ptr, uint64_t c
     void *d_rp = up(h_row_ptr, ((size_t)n + 1) * 4);
     void *d_def = alloc(E * 4), *d_kind = alloc(E), *d_min = alloc(E * 4), *d_max = alloc(E * 4), *d_dom = alloc(E * 4);
     if (e == cudaSuccess) {
-      k_slice<<<grid, kSlThreads, 0, st>>>(s, (uint8_t *)d_scr, per_thread, cap, hcap, (uint32_t *)d_cnt,
+      k_slice<<<grid, kSlThreads, 0, st>>>(s, (uint8_t *)d_scr, per_thread, cap, hcap, maxf, (uint32_t *)d_cnt,
                                            (const uint32_t *)d_rp, (uint32_t *)d_def, (uint8_t *)d_kind, (uint32_t *)d_min,
                                            (uint32_t *)d_max, (int32_t *)d_dom, (int *)d_err);
       e = cudaGetLastError();
