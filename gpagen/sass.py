@@ -224,17 +224,37 @@ def random_cfg_sass(seed: int, max_instr: int = 24, n_regs: int = 5, n_funcs: in
     back edges (`continue`: a body block branching back to the header), multi-exit loops (`break`:
     a body block branching to the loop's exit), if/else diamonds and one-armed ifs.  Few registers,
     so def-use chains cross loops and arms; predicated defs (3 predicates) and barriers as in
-    random_sass.  Blocks are laid out in address order, a loop's header first.  A draw whose
-    function exceeds max_instr, or that has no back edge when loops are wanted (about 3 in 4
-    draws), is redrawn from the next sub-seed."""
+    random_sass.  Blocks are laid out in address order, a loop's header first.  Functions are
+    drawn one by one; a draw longer than max_instr, or without a back edge when loops are wanted
+    (about 3 in 4 draws), is redrawn from the next sub-seed."""
+    if n_funcs > 1:
+        return concat_sass([random_cfg_sass(int(np.random.default_rng([seed, f]).integers(1 << 62)), max_instr, n_regs)
+                            for f in range(n_funcs)])
     for attempt in range(1000):
-        S = _cfg_draw(np.random.default_rng([seed, attempt]), max_instr, n_regs, n_funcs)
-        fl = np.diff(S.func_begin.astype(np.int64))
+        S = _cfg_draw(np.random.default_rng([seed, attempt]), max_instr, n_regs, 1)
         has_back = any(S.block_begin[t] <= S.block_begin[b + 1] - 1 for b in range(len(S.block_begin) - 1)
                        for t in S.succ[S.succ_ptr[b]:S.succ_ptr[b + 1]])
-        if fl.max() <= max_instr and (has_back or np.random.default_rng([seed, attempt, 1]).random() < 0.25):
+        if S.n_instr <= max_instr and (has_back or np.random.default_rng([seed, attempt, 1]).random() < 0.25):
             return S
     raise RuntimeError("random_cfg_sass: no draw fits")
+
+
+def concat_sass(parts) -> Sass:
+    """Functions of several Sass descriptions laid out one after another (ids renumbered)."""
+    fb, bb, sp, su = [0], [0], [0], []
+    arr = {k: [] for k in ("guard", "dst", "src", "wbar", "rbar", "wait", "opclass", "latency")}
+    i0 = b0 = 0
+    for S in parts:
+        fb += [int(x) + i0 for x in S.func_begin[1:]]
+        bb += [int(x) + i0 for x in S.block_begin[1:]]
+        su += [int(x) + b0 for x in S.succ]
+        sp += [int(x) + sp[-1] for x in S.succ_ptr[1:]]
+        for k in arr:
+            arr[k].append(getattr(S, k))
+        i0 += S.n_instr
+        b0 += len(S.block_begin) - 1
+    return Sass(np.array(fb, np.uint32), np.array(bb, np.uint32), np.array(sp, np.uint32), np.array(su, np.uint32),
+                *[np.concatenate(arr[k]) for k in ("guard", "dst", "src", "wbar", "rbar", "wait", "opclass", "latency")])
 
 
 def _cfg_draw(rng, max_instr, n_regs, n_funcs):
