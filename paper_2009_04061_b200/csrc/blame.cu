@@ -126,6 +126,126 @@ __global__ void k_blame_rows(DevProgram p) {
   }
 }
 
+// Warp-cooperative form of k_blame_rows (north_star: "CSR edge-parallel ... warp-level ... pruning
+// and normalisation"): a warp takes a tile of 32 use rows.  (1) lane = row: the live test from the
+// row's dependency-reason counts; (2) lanes over the tile's edges (coalesced edge fields, the defs'
+// latency / class / A_i gathered by 32 lanes at once): rules 1-3 and the weight of every edge, staged
+// in shared memory; (3) lane = row: W per dependency reason summed over the row's edges in CSR order
+// from shared memory (the sequential order of the definition, so shares stay bit-identical to a
+// sequential evaluation), self flags; (4) lanes over edges again: shares w / W written coalesced.
+// Tiles with more than kTileEdges edges fall back to the row-per-lane loop of k_blame_rows.
+constexpr uint32_t kTileEdges = 256;
+constexpr uint32_t kBlameWarps = 4;
+__global__ void __launch_bounds__(32 * kBlameWarps) k_blame_tiles(DevProgram p) {
+  pdl_wait();
+  __shared__ double sw[kBlameWarps][kTileEdges];
+  __shared__ uint8_t sm[kBlameWarps][kTileEdges];
+  __shared__ double sW[kBlameWarps][3][32];
+  __shared__ uint8_t slive[kBlameWarps][32];
+  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint32_t n_tiles = (p.n + 31) / 32, warps = gridDim.x * kBlameWarps;
+  double *w_ = sw[wib];
+  uint8_t *m_ = sm[wib];
+  for (uint32_t tile = blockIdx.x * kBlameWarps + wib; tile < n_tiles; tile += warps) {
+    const uint32_t j0 = tile * 32, j = j0 + lane;
+    const bool in = j < p.n;
+    const uint32_t E0 = p.row_ptr[j0], E1 = p.row_ptr[min(j0 + 32, p.n)];
+    bool live = false;
+    if (in) {
+      const uint64_t *row = p.C + (uint64_t)j * 2 * p.R;
+      live = (row[R_MEM] + row[p.R + R_MEM] + row[R_EXEC] + row[p.R + R_EXEC] + row[R_SYNC] + row[p.R + R_SYNC]) != 0;
+    }
+    if (E1 - E0 > kTileEdges) {   // rare: a long row -- lane-per-row, CSR order
+      if (in) {
+        const uint32_t e0 = p.row_ptr[j], e1 = p.row_ptr[j + 1];
+        double W0 = 0.0, W1 = 0.0, W2 = 0.0;
+        if (live)
+          for (uint32_t e = e0; e < e1; ++e) {
+            const uint32_t d = p.edge_def[e];
+            if (!(p.edge_dom[e] < 0 && p.edge_min[e] <= p.latency[d])) continue;
+            const uint32_t m = rule1_mask(p.opclass[d]);
+            const uint64_t a = p.AL[2 * (uint64_t)d];
+            const double w = __ddiv_rn((double)(a ? a : 1ull), (double)p.edge_max[e]);
+            if (m & 1u) W0 = __dadd_rn(W0, w);
+            W1 = __dadd_rn(W1, w);
+            if (m & 4u) W2 = __dadd_rn(W2, w);
+          }
+        for (uint32_t e = e0; e < e1; ++e) {
+          uint32_t m = 0;
+          double w = 0.0;
+          if (live) {
+            const uint32_t d = p.edge_def[e];
+            if (p.edge_dom[e] < 0 && p.edge_min[e] <= p.latency[d]) {
+              m = rule1_mask(p.opclass[d]);
+              const uint64_t a = p.AL[2 * (uint64_t)d];
+              w = __ddiv_rn((double)(a ? a : 1ull), (double)p.edge_max[e]);
+            }
+          }
+          p.cand[e] = (uint8_t)m;
+          p.share[3 * (uint64_t)e] = (m & 1u) ? __ddiv_rn(w, W0) : 0.0;
+          p.share[3 * (uint64_t)e + 1] = m ? __ddiv_rn(w, W1) : 0.0;
+          p.share[3 * (uint64_t)e + 2] = (m & 4u) ? __ddiv_rn(w, W2) : 0.0;
+        }
+        p.selfm[j] = live ? (uint8_t)((W0 > 0.0 ? 0u : 1u) | (W1 > 0.0 ? 0u : 2u) | (W2 > 0.0 ? 0u : 4u)) : 0;
+      }
+      continue;
+    }
+    slive[wib][lane] = live;
+    __syncwarp();
+    // (2) per edge: rules 1-3 and the weight, lanes over the tile's edges
+    for (uint32_t e = E0 + lane; e < E1; e += 32) {
+      const uint32_t u = p.edge_use[e];
+      uint32_t m = 0;
+      double w = 0.0;
+      if (slive[wib][u - j0]) {
+        const uint32_t d = p.edge_def[e], mn = p.edge_min[e], mx = p.edge_max[e];
+        const int32_t dom = p.edge_dom[e];
+        const uint32_t lat = p.latency[d], cls = p.opclass[d];
+        const uint64_t a = p.AL[2 * (uint64_t)d];
+        if (dom < 0 && mn <= lat) {   // rules 2, 3
+          m = rule1_mask(cls);
+          w = __ddiv_rn((double)(a ? a : 1ull), (double)mx);
+        }
+      }
+      w_[e - E0] = w;
+      m_[e - E0] = (uint8_t)m;
+    }
+    __syncwarp();
+    // (3) lane = row: W per reason in CSR order, self flags
+    if (in) {
+      double W0 = 0.0, W1 = 0.0, W2 = 0.0;
+      if (live) {
+        const uint32_t e0 = p.row_ptr[j] - E0, e1 = p.row_ptr[j + 1] - E0;
+        for (uint32_t k = e0; k < e1; ++k) {
+          const uint32_t m = m_[k];
+          if (!m) continue;
+          const double w = w_[k];
+          if (m & 1u) W0 = __dadd_rn(W0, w);
+          W1 = __dadd_rn(W1, w);
+          if (m & 4u) W2 = __dadd_rn(W2, w);
+        }
+        p.selfm[j] = (uint8_t)((W0 > 0.0 ? 0u : 1u) | (W1 > 0.0 ? 0u : 2u) | (W2 > 0.0 ? 0u : 4u));
+      } else {
+        p.selfm[j] = 0;
+      }
+      sW[wib][0][lane] = W0;
+      sW[wib][1][lane] = W1;
+      sW[wib][2][lane] = W2;
+    }
+    __syncwarp();
+    // (4) lanes over edges: candidate masks and shares
+    for (uint32_t e = E0 + lane; e < E1; e += 32) {
+      const uint32_t m = m_[e - E0], r = p.edge_use[e] - j0;
+      const double w = w_[e - E0];
+      p.cand[e] = (uint8_t)m;
+      p.share[3 * (uint64_t)e] = (m & 1u) ? __ddiv_rn(w, sW[wib][0][r]) : 0.0;
+      p.share[3 * (uint64_t)e + 1] = m ? __ddiv_rn(w, sW[wib][1][r]) : 0.0;
+      p.share[3 * (uint64_t)e + 2] = (m & 4u) ? __ddiv_rn(w, sW[wib][2][r]) : 0.0;
+    }
+    __syncwarp();
+  }
+}
+
 __global__ void k_def_reduce(DevProgram p) {
   pdl_wait();
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += gridDim.x * blockDim.x) {
@@ -164,7 +284,19 @@ inline uint32_t grid_for(uint64_t items, uint32_t threads, int n_sms) {
 cudaError_t launch_blame_rows(const DevProgram &p, int n_sms, cudaStream_t s, uint64_t *launches) {
   k_summaries<<<grid_for(p.n, 256, n_sms), 256, 0, s>>>(p.C, p.n, p.R, p.AL);
   cudaError_t e = cudaGetLastError();
-  if (e == cudaSuccess) e = launch_pdl(p.n, k_blame_rows, grid_for(p.n, 128, n_sms), 128, 0, s, p);
+#ifndef GPA_BLAME_TILES
+#define GPA_BLAME_TILES 1
+#endif
+  if (e == cudaSuccess) {
+    if (GPA_BLAME_TILES) {
+      const uint32_t tiles = (p.n + 31) / 32;
+      const uint32_t g = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((tiles + kBlameWarps - 1) / kBlameWarps,
+                                                                            (uint64_t)n_sms * 16));
+      e = launch_pdl(p.n, k_blame_tiles, g, 32 * kBlameWarps, 0, s, p);
+    } else {
+      e = launch_pdl(p.n, k_blame_rows, grid_for(p.n, 128, n_sms), 128, 0, s, p);
+    }
+  }
   *launches += 2;
   return e;
 }

@@ -37,12 +37,12 @@ __global__ void k_est_rows(DevProgram p, EstimatePlan ep) {
   }
   __syncthreads();
   const uint64_t stride_items = (uint64_t)p.E + p.n;
-  const uint32_t n_groups = (ep.n_pat + kEstGroup - 1) / kEstGroup;
-  const uint32_t total = p.n * n_groups;          // < 2^32 (checked by the launcher)
-  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
-    // row-major: the pattern groups of a row run on neighbouring threads, so its C row and edges
-    // are fetched from DRAM once and served from L1 to the other groups
-    const uint32_t j = t / n_groups, grp = t - j * n_groups;
+  // a CTA = one warp per pattern group over the same 32 rows: the pattern fields are uniform in a
+  // warp (no divergence on them), and a row's C entries and edges are fetched from DRAM once and
+  // served from L1 to the other groups' warps
+  const uint32_t grp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (uint32_t j = blockIdx.x * 32 + lane; j - lane < p.n; j += gridDim.x * 32) {
+    if (j >= p.n) continue;
     const uint32_t q0 = grp * kEstGroup;
     const uint32_t nq = min((uint32_t)kEstGroup, ep.n_pat - q0);
     const uint64_t *row = p.C + (uint64_t)j * 2 * p.R;
@@ -286,11 +286,9 @@ __global__ void k_est_final(DevProgram p, EstimatePlan ep) {
 // (cand, share, selfm) and C, so it can run beside the def reduction and the rollup
 cudaError_t launch_estimate_sums(const DevProgram &p, const EstimatePlan &ep, int n_sms, cudaStream_t s,
                                  uint64_t *launches) {
-  const uint32_t threads = 128;
-  const uint64_t work = (uint64_t)p.n * ((ep.n_pat + kEstGroup - 1) / kEstGroup);
-  if (work >= (1ull << 32)) return cudaErrorInvalidValue;   // k_est_rows indexes (row, group) in 32 bits
-  const uint32_t g = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((work + threads - 1) / threads, (uint64_t)n_sms * 32));
-  k_est_rows<<<g, threads, 0, s>>>(p, ep);
+  const uint32_t n_groups = (ep.n_pat + kEstGroup - 1) / kEstGroup;   // <= 8: a warp per group
+  const uint32_t g = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(((uint64_t)p.n + 31) / 32, (uint64_t)n_sms * 64));
+  k_est_rows<<<g, 32 * n_groups, 0, s>>>(p, ep);
   bool any_slot = false;
   for (uint32_t q = 0; q < ep.n_pat; ++q) any_slot |= ep.loop_slot[q] >= 0;
   if (any_slot && p.E) {

@@ -105,28 +105,27 @@ struct DevProgram {
   double *share, *B;
 };
 
-// Rollup plan (create-time): chunks over an instruction order, then segments.
+// Rollup plan (create-time).  Tiles of 32 consecutive instructions; in each tile the
+// maximal runs of equal line, equal innermost loop (loop members only) and equal function.  A run
+// whose segment (line / loop-exclusive / function) has no other run is written straight into the
+// segment's row; the other runs write partial rows, summed per segment in program order (stage 1).
 struct RollupPlan {
-  const uint32_t *order;        // [n_order] instruction ids: line-major | loop-major | identity
-  const uint32_t *chunk_begin;  // [n_chunks] positions in order
-  const uint32_t *chunk_end;
-  uint32_t n_chunks;
-  double *part_v;               // [n_chunks][2*ncol]
-  uint64_t *part_al;            // [n_chunks][2]
-  // stage 1: rows [0, n_rows1) = lines, loops excl, funcs.  Segments of <= kChunk positions are
-  // packed (pack p = segments [pack_seg[p], pack_seg[p+1]), positions segpos[s]..segpos[s+1]) and
-  // summed directly into their rows; longer ones (n_seg1, row seg1_id[i]) over chunk ranges
-  const uint32_t *seg1_begin, *seg1_end, *seg1_id;
+  const uint32_t *tile_run_ptr; // [n_tiles+1] runs of tile t
+  const uint32_t *run_be;       // [n_runs] begin | end << 8 (offsets in the tile, end exclusive)
+  const uint32_t *run_dst;      // [n_runs] row id, or kPartialBit | partial row id
+  uint32_t n_tiles;
+  double *part_v;               // [n_partials][2*ncol]
+  uint64_t *part_al;            // [n_partials][2]
+  // stage 1: segments with 0 or >= 2 runs, summed over their partial rows (seg1_perm positions)
+  const uint32_t *seg1_perm, *seg1_begin, *seg1_end, *seg1_id;
   uint32_t n_seg1, n_rows1;
-  const uint32_t *pack_seg, *segpos;
-  uint32_t n_packs;
-  // stage 2: segments (loops incl, kernels) over rows via perm -> rows [n_seg1, n_seg1 + n_seg2)
+  // stage 2: segments (loops incl, kernels) over rows via perm -> rows [n_rows1, n_rows1 + n_seg2)
   const uint32_t *seg2_perm, *seg2_begin, *seg2_end;
   uint32_t n_seg2;
   double *rows_v;               // [n_rows][2*ncol]
   uint64_t *rows_al;            // [n_rows][2]
-  double *vbuf;                 // [n][2*ncol] per-instruction vectors V
 };
+constexpr uint32_t kPartialBit = 0x80000000u;
 
 // per-kernel occupancy (gpa_set_launches) for parallel_rule 3 / 4
 struct KernOcc {
@@ -179,8 +178,6 @@ cudaError_t launch_rollup(const DevProgram &p, const RollupPlan &rp, int n_sms, 
 cudaError_t launch_estimate(const DevProgram &p, const EstimatePlan &ep, int n_sms,
                             cudaStream_t s, uint64_t *launches);
 cudaError_t launch_vrows(const DevProgram &p, double *vbuf, int n_sms, cudaStream_t s);
-cudaError_t launch_rollup_fork(const DevProgram &p, const RollupPlan &rp, int n_sms, cudaStream_t s,
-                               cudaStream_t side, cudaEvent_t fork, cudaEvent_t join, uint64_t *launches);
 cudaError_t launch_slice(const gpa_sass_desc *h, uint32_t *h_row_ptr, uint64_t cap_edges, uint32_t *h_def,
                          uint8_t *h_kind, uint32_t *h_min, uint32_t *h_max, int32_t *h_dom, uint64_t *n_edges,
                          int n_sms, cudaStream_t st, int *status);
@@ -311,8 +308,6 @@ struct gpa_program {
   cudaStream_t capture_stream = nullptr;
   cudaStream_t side_stream = nullptr;          // analyze graph: the estimate branch
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  cudaStream_t pack_stream = nullptr;          // analyze graph: the rollup's short-segment packs
-  cudaEvent_t ev_pfork = nullptr, ev_pjoin = nullptr;
   cudaGraphExec_t analyze_exec = nullptr;
   uint32_t analyze_npat = 0xffffffffu;
   uint64_t analyze_launches = 0;

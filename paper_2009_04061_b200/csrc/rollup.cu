@@ -2,18 +2,18 @@
 // (line, loop exclusive/inclusive, function, kernel, Q16).
 //
 // Hand-written segmented reductions (no CUB), deterministic: every sum has a fixed order.
-//   k_vrows            V[i] = {NCOL x (all, lat)} for every instruction, one
-//                      thread per instruction with independent vector loads and 16-byte (all, lat)
-//                      stores; this is also the instruction level of the rollup (gpa_instr_vector).
-//   k_rollup_chunks    one warp per <=128-instruction chunk of a create-time order (line-major |
-//                      loop-major | function ranges); member ids are loaded once and broadcast by
-//                      shuffles, lane s owns value slot s (and s+32) of the row, so each member
-//                      row is one coalesced load and four interleaved accumulators keep loads in
-//                      flight.  Slots NV, NV+1 carry (A_i, L_i).
-//   k_rollup_segments  one warp per segment, same scheme over rows: chunk partials (stage 1:
-//                      lines, loops-exclusive, functions) or earlier rows through a permutation
-//                      (stage 2: loops-inclusive = preorder subtree ranges of the loop-exclusive
-//                      rows; kernels = their function rows).
+//   k_rollup_tiles     one warp per tile of 32 consecutive instructions: lane = instruction builds
+//                      V[i] = {NCOL x (all, lat)} from B, C, the class and the
+//                      self flags into shared memory, then lane = value slot sums the tile's runs of
+//                      equal line, equal innermost loop and equal function (create-time run lists)
+//                      in member order -- a run that is its segment's only run is the segment's row,
+//                      the others write partial rows.  B and C are read once, coalesced, in program
+//                      order; V is never materialised in HBM.
+//   k_rollup_segments  one warp per segment: stage 1 sums the partial rows of segments with several
+//                      runs (functions, loops, lines that recur) in program order; stage 2 the
+//                      loops-inclusive (preorder subtree ranges of the loop-exclusive rows) and the
+//                      kernels (their function rows).
+//   k_vrows            V for gpa_instr_vector (the instruction level, on request; not in the graph).
 #include <algorithm>
 
 #include "gpa_internal.cuh"
@@ -108,55 +108,6 @@ __device__ __forceinline__ void warp_sum_rows(uint32_t lane, uint32_t nv, uint32
   }
 }
 
-#ifndef GPA_ROLL_MEMBERS
-#define GPA_ROLL_MEMBERS 16
-#endif
-constexpr int kRollMembers = GPA_ROLL_MEMBERS;   // members (row loads) in flight per lane
-
-// chunk of <= 128 members: member ids are loaded once (4 per lane) and broadcast by shuffles, so
-// the row loads of consecutive members are independent and stay in flight together
-__global__ void __launch_bounds__(128) k_rollup_chunks(RollupPlan rp, uint32_t nv, const double *__restrict__ vbuf,
-                                                       const uint64_t *__restrict__ AL) {
-  pdl_wait();
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t ch = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; ch < rp.n_chunks; ch += warps) {
-    const uint32_t b = rp.chunk_begin[ch], len = rp.chunk_end[ch] - b;
-    uint32_t ids[kChunk / 32];
-#pragma unroll
-    for (int t = 0; t < kChunk / 32; ++t) ids[t] = (lane + 32 * t < len) ? rp.order[b + lane + 32 * t] : 0u;
-    for (uint32_t s0 = 0; s0 < nv + 2; s0 += 32) {   // uniform trip count: shuffles need all lanes
-      const uint32_t s = s0 + lane;
-      double acc[4] = {0.0, 0.0, 0.0, 0.0};   // member u adds into acc[u % 4]: the order of the
-      uint64_t al = 0;                          // four-accumulator scheme (a0..a3) is unchanged
-      const bool is_v = s < nv, is_al = s >= nv && s < nv + 2;
-#pragma unroll
-      for (int t = 0; t < kChunk / 32; ++t) {
-        const uint32_t m_end = len > 32u * t ? min(32u, len - 32u * t) : 0u;
-        for (uint32_t m = 0; m < m_end; m += kRollMembers) {
-          uint32_t id[kRollMembers];
-#pragma unroll
-          for (int u = 0; u < kRollMembers; ++u) id[u] = __shfl_sync(0xffffffffu, ids[t], (m + u) & 31);
-          if (is_v) {
-            double x[kRollMembers];
-#pragma unroll
-            for (int u = 0; u < kRollMembers; ++u) x[u] = m + u < m_end ? vbuf[(uint64_t)id[u] * nv + s] : 0.0;
-#pragma unroll
-            for (int u = 0; u < kRollMembers; ++u) acc[u & 3] = __dadd_rn(acc[u & 3], x[u]);
-          } else if (is_al) {
-            const uint32_t c = s - nv;
-#pragma unroll
-            for (int u = 0; u < kRollMembers; ++u)
-              if (m + u < m_end) al += AL[2 * (uint64_t)id[u] + c];
-          }
-        }
-      }
-      if (is_v) rp.part_v[(uint64_t)ch * nv + s] = __dadd_rn(__dadd_rn(acc[0], acc[1]), __dadd_rn(acc[2], acc[3]));
-      else if (is_al) rp.part_al[2 * (uint64_t)ch + (s - nv)] = al;
-    }
-  }
-}
-
 __global__ void __launch_bounds__(128) k_rollup_segments(uint32_t nv, const double *__restrict__ in_v,
                                                          const uint64_t *__restrict__ in_al,
                                                          const uint32_t *__restrict__ perm,
@@ -178,64 +129,71 @@ __global__ void __launch_bounds__(128) k_rollup_segments(uint32_t nv, const doub
   }
 }
 
-// packs of short segments (<= kChunk positions in all): one warp per pack, lane = value slot;
-// member rows are fetched kRollMembers at a time across segment boundaries and added in member
-// order into the current segment's sum, which is written to its row when the segment ends --
-// the same left-to-right order as the oracle's per-instruction accumulation
-__global__ void __launch_bounds__(128) k_rollup_packs(RollupPlan rp, uint32_t nv, const double *__restrict__ vbuf,
-                                                      const uint64_t *__restrict__ AL) {
+// one warp per tile of 32 instructions (4 warps per block): V rows built by lane = instruction into
+// shared memory (the k_vrows arithmetic), then lane = value slot sums each run of the tile in member
+// order and stores the run's row (or partial row) -- one coalesced row store per run
+constexpr uint32_t kTileWarps = 4;
+__global__ void __launch_bounds__(32 * kTileWarps) k_rollup_tiles(DevProgram p, RollupPlan rp) {
   pdl_wait();
-  const uint32_t lane = threadIdx.x & 31;
-  const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t pk = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; pk < rp.n_packs; pk += warps) {
-    const uint32_t sa = rp.pack_seg[pk], sb = rp.pack_seg[pk + 1];
-    const uint32_t P0 = rp.segpos[sa], P1 = rp.segpos[sb], len = P1 - P0;
-    if (len > (uint32_t)kChunk) continue;          // a long segment: chunked + k_rollup_segments
-    uint32_t ids[kChunk / 32];
+  extern __shared__ double2 tstage[];          // [kTileWarps][32 rows][ncol] + [kTileWarps][32][2] u64
+  const uint32_t ncol = p.ncol, nv = 2 * ncol, R = p.R, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double2 *ws = tstage + (size_t)warp * 32 * ncol;
+  uint64_t *wal = reinterpret_cast<uint64_t *>(tstage + (size_t)kTileWarps * 32 * ncol) + (size_t)warp * 64;
+  const uint32_t warps = gridDim.x * kTileWarps;
+  for (uint32_t t = blockIdx.x * kTileWarps + warp; t < rp.n_tiles; t += warps) {
+    const uint32_t i = 32 * t + lane;
+    if (i < p.n) {
+      const double2 *b2 = reinterpret_cast<const double2 *>(p.B + 8 * (uint64_t)i);
+      const double2 bm = b2[BG_MEM], be = b2[BG_EXEC], bw = b2[BG_WAR], bs = b2[BG_SYNC];
+      const uint32_t cls = p.opclass[i], sf = p.selfm[i];
+      const uint64_t *row = p.C + (uint64_t)i * 2 * R;
+      uint64_t act[kReasonsMax], lat[kReasonsMax];
 #pragma unroll
-    for (int t = 0; t < kChunk / 32; ++t) ids[t] = (lane + 32 * t < len) ? rp.order[P0 + lane + 32 * t] : 0u;
-    for (uint32_t s0 = 0; s0 < nv + 2; s0 += 32) {   // uniform trip count: shuffles need all lanes
+      for (uint32_t r = 1; r < kReasonsMax; ++r) {
+        act[r] = r < R ? row[r] : 0ull;
+        lat[r] = r < R ? row[R + r] : 0ull;
+      }
+      const uint64_t a = p.AL[2 * (uint64_t)i], l = p.AL[2 * (uint64_t)i + 1];
+      double2 *out = ws + (size_t)lane * ncol;
+      const double2 z = make_double2(0.0, 0.0);
+      out[COL_MEM_GLOBAL] = (cls != OC_LOCAL && cls != OC_CONSTANT) ? bm : z;
+      out[COL_MEM_LOCAL] = cls == OC_LOCAL ? bm : z;
+      out[COL_MEM_CONSTANT] = cls == OC_CONSTANT ? bm : z;
+      out[COL_EXEC_SHARED] = cls == OC_SHARED ? be : z;
+      out[COL_EXEC_ARITH] = cls != OC_SHARED ? be : z;
+      out[COL_EXEC_WAR] = bw;
+      out[COL_SYNC] = bs;
+#pragma unroll
+      for (uint32_t r = 1; r < kReasonsMax; ++r) {
+        if (r >= R) break;
+        const bool on = r > R_SYNC || ((sf >> (r - 1)) & 1u);
+        out[6 + r] = on ? make_double2((double)(act[r] + lat[r]), (double)lat[r]) : z;
+      }
+      wal[2 * lane] = a;
+      wal[2 * lane + 1] = l;
+    }
+    __syncwarp();
+    const double *wv = reinterpret_cast<const double *>(ws);
+    const uint32_t r0 = rp.tile_run_ptr[t], r1 = rp.tile_run_ptr[t + 1];
+    for (uint32_t s0 = 0; s0 < nv + 2; s0 += 32) {
       const uint32_t s = s0 + lane;
-      const bool is_v = s < nv, is_al = s >= nv && s < nv + 2;
-      uint32_t seg = sa, seg_end = rp.segpos[sa + 1];
-      double acc = 0.0;
-      uint64_t al = 0;
-      auto flush_to = [&](uint32_t pos) {          // close every segment that ends at or before pos
-        while (seg < sb && seg_end <= pos) {
-          if (is_v) rp.rows_v[(uint64_t)seg * nv + s] = acc;
-          else if (is_al) rp.rows_al[2 * (uint64_t)seg + (s - nv)] = al;
-          acc = 0.0;
-          al = 0;
-          ++seg;
-          if (seg < sb) seg_end = rp.segpos[seg + 1];
-        }
-      };
-#pragma unroll
-      for (int t = 0; t < kChunk / 32; ++t) {
-        const uint32_t m_end = len > 32u * t ? min(32u, len - 32u * t) : 0u;
-        for (uint32_t m = 0; m < m_end; m += kRollMembers) {
-          uint32_t id[kRollMembers];
-#pragma unroll
-          for (int u = 0; u < kRollMembers; ++u) id[u] = __shfl_sync(0xffffffffu, ids[t], (m + u) & 31);
-          double x[kRollMembers];
-          uint64_t y[kRollMembers];
-#pragma unroll
-          for (int u = 0; u < kRollMembers; ++u) {
-            const bool in = m + u < m_end;
-            x[u] = (in && is_v) ? vbuf[(uint64_t)id[u] * nv + s] : 0.0;
-            y[u] = (in && is_al) ? AL[2 * (uint64_t)id[u] + (s - nv)] : 0ull;
-          }
-#pragma unroll
-          for (int u = 0; u < kRollMembers; ++u) {
-            if (m + u >= m_end) break;
-            flush_to(P0 + 32 * t + m + u);
-            acc = __dadd_rn(acc, x[u]);
-            al += y[u];
-          }
+      for (uint32_t r = r0; r < r1; ++r) {
+        const uint32_t be2 = rp.run_be[r], dst = rp.run_dst[r];
+        const uint32_t b = be2 & 0xffu, e = be2 >> 8;
+        const bool part = (dst & kPartialBit) != 0;
+        const uint64_t row_id = dst & ~kPartialBit;
+        if (s < nv) {
+          double acc = 0.0;
+          for (uint32_t m = b; m < e; ++m) acc = __dadd_rn(acc, wv[(size_t)m * nv + s]);
+          (part ? rp.part_v : rp.rows_v)[row_id * nv + s] = acc;
+        } else if (s < nv + 2) {
+          uint64_t acc = 0;
+          for (uint32_t m = b; m < e; ++m) acc += wal[2 * m + (s - nv)];
+          (part ? rp.part_al : rp.rows_al)[2 * row_id + (s - nv)] = acc;
         }
       }
-      flush_to(P1);
     }
+    __syncwarp();
   }
 }
 
@@ -256,41 +214,31 @@ cudaError_t launch_vrows(const DevProgram &p, double *vbuf, int n_sms, cudaStrea
   return launch_pdl(p.n, k_vrows, g, kVrowsThreads, smem, s, p, vbuf);
 }
 
-// fork (optional, graph capture): the packs of short segments write rows disjoint from the
-// chunked long segments', so they run on stream `side` between events fork / join
-cudaError_t launch_rollup_fork(const DevProgram &p, const RollupPlan &rp, int n_sms, cudaStream_t s,
-                               cudaStream_t side, cudaEvent_t fork, cudaEvent_t join, uint64_t *launches) {
-  const uint32_t nv = 2 * p.ncol;
-  cudaError_t e = launch_vrows(p, rp.vbuf, n_sms, s);
-  if (e != cudaSuccess) return e;
-  const bool split = side && rp.n_packs;
-  if (split) {
-    if ((e = cudaEventRecord(fork, s)) != cudaSuccess) return e;
-    if ((e = cudaStreamWaitEvent(side, fork, 0)) != cudaSuccess) return e;
-  }
-  cudaStream_t ps = split ? side : s;
-  if (rp.n_packs) k_rollup_packs<<<warp_grid(rp.n_packs, n_sms), 128, 0, ps>>>(rp, nv, rp.vbuf, p.AL);
-  if (split && (e = cudaEventRecord(join, side)) != cudaSuccess) return e;
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  if (rp.n_chunks && (e = launch_pdl(p.n, k_rollup_chunks, warp_grid(rp.n_chunks, n_sms), 128, 0, s, rp, nv,
-                                     (const double *)rp.vbuf, (const uint64_t *)p.AL)) != cudaSuccess)
-    return e;
-  if (rp.n_seg1 && (e = launch_pdl(p.n, k_rollup_segments, warp_grid(rp.n_seg1, n_sms), 128, 0, s, nv,
-                                   (const double *)rp.part_v, (const uint64_t *)rp.part_al, (const uint32_t *)nullptr,
-                                   (const uint32_t *)rp.seg1_begin, (const uint32_t *)rp.seg1_end, rp.n_seg1,
-                                   (const uint32_t *)rp.seg1_id, rp.rows_v, rp.rows_al)) != cudaSuccess)
-    return e;
-  if (split && (e = cudaStreamWaitEvent(s, join, 0)) != cudaSuccess) return e;   // stage 2 reads the pack rows
-  k_rollup_segments<<<warp_grid(rp.n_seg2, n_sms), 128, 0, s>>>(
-      nv, rp.rows_v, rp.rows_al, rp.seg2_perm, rp.seg2_begin, rp.seg2_end, rp.n_seg2, nullptr,
-      rp.rows_v + (uint64_t)rp.n_rows1 * nv, rp.rows_al + 2 * (uint64_t)rp.n_rows1);
-  *launches += 2 + (rp.n_chunks ? 1 : 0) + (rp.n_packs ? 1 : 0) + (rp.n_seg1 ? 1 : 0);
-  return cudaGetLastError();
-}
-
 cudaError_t launch_rollup(const DevProgram &p, const RollupPlan &rp, int n_sms, cudaStream_t s,
                           uint64_t *launches) {
-  return launch_rollup_fork(p, rp, n_sms, s, nullptr, nullptr, nullptr, launches);
+  const uint32_t nv = 2 * p.ncol;
+  const size_t smem = (size_t)kTileWarps * 32 * p.ncol * sizeof(double2) + (size_t)kTileWarps * 64 * sizeof(uint64_t);
+  cudaError_t e = cudaFuncSetAttribute(k_rollup_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const uint32_t g = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((rp.n_tiles + kTileWarps - 1) / kTileWarps,
+                                                                         (uint64_t)n_sms * 16));
+  if (rp.n_tiles && (e = launch_pdl(p.n, k_rollup_tiles, g, 32 * kTileWarps, smem, s, p, rp)) != cudaSuccess) return e;
+  // stage 1: segments with several runs (and empty ones) from their partial rows
+  if (rp.n_seg1 && (e = launch_pdl(p.n, k_rollup_segments, warp_grid(rp.n_seg1, n_sms), 128, 0, s, nv,
+                                   (const double *)rp.part_v, (const uint64_t *)rp.part_al,
+                                   (const uint32_t *)rp.seg1_perm, (const uint32_t *)rp.seg1_begin,
+                                   (const uint32_t *)rp.seg1_end, rp.n_seg1, (const uint32_t *)rp.seg1_id, rp.rows_v,
+                                   rp.rows_al)) != cudaSuccess)
+    return e;
+  // stage 2: loops inclusive and kernels over the stage-1 rows
+  if (rp.n_seg2 && (e = launch_pdl(p.n, k_rollup_segments, warp_grid(rp.n_seg2, n_sms), 128, 0, s, nv,
+                                   (const double *)rp.rows_v, (const uint64_t *)rp.rows_al,
+                                   (const uint32_t *)rp.seg2_perm, (const uint32_t *)rp.seg2_begin,
+                                   (const uint32_t *)rp.seg2_end, rp.n_seg2, (const uint32_t *)nullptr,
+                                   rp.rows_v + (uint64_t)rp.n_rows1 * nv, rp.rows_al + 2 * (uint64_t)rp.n_rows1)) != cudaSuccess)
+    return e;
+  *launches += (rp.n_tiles ? 1 : 0) + (rp.n_seg1 ? 1 : 0) + (rp.n_seg2 ? 1 : 0);
+  return cudaGetLastError();
 }
 
 }  // namespace gpa

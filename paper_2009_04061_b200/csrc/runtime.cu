@@ -128,9 +128,9 @@ struct HostPlan {
   // create-time arrays (host)
   std::vector<uint32_t> edge_use, def_ptr, def_perm;
   std::vector<int32_t> edge_lca, loop_func;
-  std::vector<uint32_t> order, chunk_begin, chunk_end, seg1_begin, seg1_end, seg1_id, seg2_perm, seg2_begin,
-      seg2_end;
-  std::vector<uint32_t> pack_seg, segpos;   // small segments packed per warp: pack -> first segment; positions
+  std::vector<uint32_t> tile_run_ptr, run_be, run_dst, seg1_perm, seg1_begin, seg1_end, seg1_id, seg2_perm,
+      seg2_begin, seg2_end;
+  uint32_t n_partials = 0;
   std::vector<uint32_t> loop_items, loop_item_ptr, pre_perm, pre_begin, pre_end, kloop_ptr, kloops;
   uint32_t n_rows = 0;
 };
@@ -174,57 +174,58 @@ gpa_status build_plan(const gpa_program_desc *d, HostPlan &h) {
   h.edge_lca.resize(E);
   for (uint32_t e = 0; e < E; ++e) h.edge_lca[e] = lca(d->loop_id[d->edge_def[e]], d->loop_id[h.edge_use[e]]);
 
-  // ---- rollup order: line-major | loop-major (in-loop instructions) | identity
-  std::vector<uint32_t> line_ptr(d->n_lines + 1, 0), loop_ptr(L + 1, 0);
-  for (uint32_t i = 0; i < n; ++i) {
-    line_ptr[d->line_id[i] + 1]++;
-    if (d->loop_id[i] >= 0) loop_ptr[d->loop_id[i] + 1]++;
-  }
-  for (uint32_t l = 0; l < d->n_lines; ++l) line_ptr[l + 1] += line_ptr[l];
-  for (uint32_t l = 0; l < L; ++l) loop_ptr[l + 1] += loop_ptr[l];
-  const uint32_t n_in_loops = loop_ptr[L];
-  h.order.resize((size_t)n + n_in_loops + n);
-  {
-    std::vector<uint32_t> cl(line_ptr.begin(), line_ptr.end() - 1), cp(loop_ptr.begin(), loop_ptr.end() - 1);
-    for (uint32_t i = 0; i < n; ++i) {
-      h.order[cl[d->line_id[i]]++] = i;
-      if (d->loop_id[i] >= 0) h.order[n + cp[d->loop_id[i]]++] = i;
-      h.order[n + n_in_loops + i] = i;
-    }
-  }
-  // stage-1 segments in row order (lines, loops exclusive, functions) as position ranges of the
-  // order; segments of <= kChunk positions are packed, consecutive, into warps of <= kChunk
-  // positions (k_rollup_packs writes their rows directly); longer ones are cut into chunks whose
-  // partial sums k_rollup_segments adds (rows seg1_id)
-  std::vector<uint32_t> spos;
-  for (uint32_t l = 0; l <= d->n_lines; ++l) spos.push_back(line_ptr[l]);
-  for (uint32_t l = 1; l <= L; ++l) spos.push_back(n + loop_ptr[l]);
-  for (uint32_t f = 1; f <= d->n_funcs; ++f) spos.push_back(n + n_in_loops + d->func_begin[f]);
+  // ---- rollup runs: tiles of 32 instructions; per tile the maximal runs of equal line, equal
+  //      innermost loop (loop members) and equal function, in program order (segment ids: lines,
+  //      then loops, then functions -- the stage-1 row order)
   const uint32_t n_seg1 = d->n_lines + L + d->n_funcs;
-  h.segpos = spos;   // segment s = positions [segpos[s], segpos[s+1])
   {
-    uint32_t pack_pos = 0, pack_open = 0;
-    for (uint32_t sg = 0; sg < n_seg1; ++sg) {
-      const uint32_t pos0 = spos[sg], pos1 = spos[sg + 1], len = pos1 - pos0;
-      if (len <= (uint32_t)kChunk) {
-        if (!pack_open || pos1 - pack_pos > (uint32_t)kChunk || h.pack_seg.back() + 64 <= sg) {
-          h.pack_seg.push_back(sg);
-          pack_pos = pos0;
-          pack_open = 1;
+    const uint32_t n_tiles = (n + 31) / 32;
+    std::vector<uint32_t> func_of(n);
+    for (uint32_t f = 0; f < d->n_funcs; ++f)
+      for (uint32_t i = d->func_begin[f]; i < d->func_begin[f + 1]; ++i) func_of[i] = f;
+    auto seg_of = [&](int kind, uint32_t i) -> int64_t {
+      if (kind == 0) return d->line_id[i];
+      if (kind == 1) return d->loop_id[i] >= 0 ? (int64_t)d->n_lines + d->loop_id[i] : -1;
+      return (int64_t)d->n_lines + L + func_of[i];
+    };
+    std::vector<uint32_t> run_seg;
+    std::vector<uint32_t> runs_of(n_seg1, 0);
+    h.tile_run_ptr.assign(n_tiles + 1, 0);
+    for (uint32_t t = 0; t < n_tiles; ++t) {
+      const uint32_t i0 = 32 * t, i1 = std::min(n, i0 + 32);
+      for (int kind = 0; kind < 3; ++kind)
+        for (uint32_t i = i0; i < i1;) {
+          const int64_t sg = seg_of(kind, i);
+          uint32_t k = i + 1;
+          while (k < i1 && seg_of(kind, k) == sg) ++k;
+          if (sg >= 0) {
+            h.run_be.push_back((i - i0) | ((k - i0) << 8));
+            run_seg.push_back((uint32_t)sg);
+            runs_of[sg]++;
+          }
+          i = k;
         }
-        continue;
-      }
-      pack_open = 0;
-      h.pack_seg.push_back(sg);          // a long segment closes the pack (its own "pack" is empty)
-      h.seg1_id.push_back(sg);
-      h.seg1_begin.push_back((uint32_t)h.chunk_begin.size());
-      for (uint32_t p = pos0; p < pos1; p += kChunk) {
-        h.chunk_begin.push_back(p);
-        h.chunk_end.push_back(std::min(pos1, p + (uint32_t)kChunk));
-      }
-      h.seg1_end.push_back((uint32_t)h.chunk_begin.size());
+      h.tile_run_ptr[t + 1] = (uint32_t)h.run_be.size();
     }
-    h.pack_seg.push_back(n_seg1);
+    // destinations: a segment's only run writes its row; runs of multi-run segments write partials
+    std::vector<std::vector<uint32_t>> parts(n_seg1);
+    h.run_dst.resize(run_seg.size());
+    for (size_t r = 0; r < run_seg.size(); ++r) {
+      const uint32_t sg = run_seg[r];
+      if (runs_of[sg] == 1) {
+        h.run_dst[r] = sg;
+      } else {
+        parts[sg].push_back(h.n_partials);
+        h.run_dst[r] = kPartialBit | h.n_partials++;
+      }
+    }
+    for (uint32_t sg = 0; sg < n_seg1; ++sg) {
+      if (runs_of[sg] == 1) continue;       // 0 runs (an all-nested loop): stage 1 writes zeros
+      h.seg1_id.push_back(sg);
+      h.seg1_begin.push_back((uint32_t)h.seg1_perm.size());
+      h.seg1_perm.insert(h.seg1_perm.end(), parts[sg].begin(), parts[sg].end());
+      h.seg1_end.push_back((uint32_t)h.seg1_perm.size());
+    }
   }
   // ---- loop preorder (children visited in increasing id), subtree ranges
   std::vector<std::vector<uint32_t>> kids(L);
@@ -298,8 +299,8 @@ gpa_status build_plan(const gpa_program_desc *d, HostPlan &h) {
 struct Offsets {
   size_t opclass, iflags, latency, line_id, loop_id, func_begin, kfb, kgb, row_ptr, edge_def, edge_min,
       edge_max, edge_use, edge_dom, edge_lca, edge_kind, def_ptr, def_perm;
-  size_t order, chunk_begin, chunk_end, seg1_begin, seg1_end, seg1_id, pack_seg, segpos, seg2_perm, seg2_begin, seg2_end, part_v,
-      part_al, rows_v, rows_al, vbuf;
+  size_t tile_run_ptr, run_be, run_dst, seg1_perm, seg1_begin, seg1_end, seg1_id, seg2_perm, seg2_begin, seg2_end,
+      part_v, part_al, rows_v, rows_al;
   size_t pats, mval, mrow, loop_items, loop_item_ptr, pre_perm, pre_begin, pre_end, kloop_ptr, kloops,
       loop_func, lM_excl, lM_incl, fM, kM, est, hot, n_hot, rank, cov, occ;
   size_t C, stats, AL, cand, selfm, share, B, partials, part_x, part_sync;
@@ -348,22 +349,20 @@ Offsets layout(const gpa_program_desc *d, const HostPlan &h) {
   o.edge_kind = a.take(E);
   o.def_ptr = a.take((n + 1) * 4);
   o.def_perm = a.take(E * 4);
-  o.order = a.take(h.order.size() * 4);
-  o.chunk_begin = a.take(h.chunk_begin.size() * 4);
-  o.chunk_end = a.take(h.chunk_end.size() * 4);
+  o.tile_run_ptr = a.take(h.tile_run_ptr.size() * 4);
+  o.run_be = a.take(h.run_be.size() * 4);
+  o.run_dst = a.take(h.run_dst.size() * 4);
+  o.seg1_perm = a.take(h.seg1_perm.size() * 4);
   o.seg1_begin = a.take(h.seg1_begin.size() * 4);
   o.seg1_end = a.take(h.seg1_end.size() * 4);
   o.seg1_id = a.take(h.seg1_id.size() * 4);
-  o.pack_seg = a.take(h.pack_seg.size() * 4);
-  o.segpos = a.take(h.segpos.size() * 4);
   o.seg2_perm = a.take(h.seg2_perm.size() * 4);
   o.seg2_begin = a.take(h.seg2_begin.size() * 4);
   o.seg2_end = a.take(h.seg2_end.size() * 4);
-  o.part_v = a.take(h.chunk_begin.size() * 2 * ncol * 8);
-  o.part_al = a.take(h.chunk_begin.size() * 2 * 8);
+  o.part_v = a.take((size_t)h.n_partials * 2 * ncol * 8);
+  o.part_al = a.take((size_t)h.n_partials * 2 * 8);
   o.rows_v = a.take((size_t)h.n_rows * 2 * ncol * 8);
   o.rows_al = a.take((size_t)h.n_rows * 2 * 8);
-  o.vbuf = a.take(n * 2 * ncol * 8);
   o.pats = a.take(kPatWs * sizeof(gpa_pattern));
   o.mval = a.take((size_t)kLoopPatWs * (E + n) * 8);
   o.mrow = a.take((size_t)kPatWs * n * 8);
@@ -458,14 +457,13 @@ gpa_status gpa_program_create(const gpa_program_desc *d, void *d_workspace, size
   UP(o.edge_kind, d->edge_kind, E);
   UP(o.def_ptr, h.def_ptr.data(), n + 1);
   UP(o.def_perm, h.def_perm.data(), E);
-  UP(o.order, h.order.data(), h.order.size());
-  UP(o.chunk_begin, h.chunk_begin.data(), h.chunk_begin.size());
-  UP(o.chunk_end, h.chunk_end.data(), h.chunk_end.size());
+  UP(o.tile_run_ptr, h.tile_run_ptr.data(), h.tile_run_ptr.size());
+  UP(o.run_be, h.run_be.data(), h.run_be.size());
+  UP(o.run_dst, h.run_dst.data(), h.run_dst.size());
+  UP(o.seg1_perm, h.seg1_perm.data(), h.seg1_perm.size());
   UP(o.seg1_begin, h.seg1_begin.data(), h.seg1_begin.size());
   UP(o.seg1_end, h.seg1_end.data(), h.seg1_end.size());
   UP(o.seg1_id, h.seg1_id.data(), h.seg1_id.size());
-  UP(o.pack_seg, h.pack_seg.data(), h.pack_seg.size());
-  UP(o.segpos, h.segpos.data(), h.segpos.size());
   UP(o.seg2_perm, h.seg2_perm.data(), h.seg2_perm.size());
   UP(o.seg2_begin, h.seg2_begin.data(), h.seg2_begin.size());
   UP(o.seg2_end, h.seg2_end.data(), h.seg2_end.size());
@@ -507,27 +505,24 @@ gpa_status gpa_program_create(const gpa_program_desc *d, void *d_workspace, size
   DP(part_x, uint32_t *, part_x); DP(part_sync, unsigned int *, part_sync);
 #undef DP
   RollupPlan &rp = p->rp;
-  rp.order = (const uint32_t *)(ws + o.order);
-  rp.chunk_begin = (const uint32_t *)(ws + o.chunk_begin);
-  rp.chunk_end = (const uint32_t *)(ws + o.chunk_end);
-  rp.n_chunks = (uint32_t)h.chunk_begin.size();
+  rp.tile_run_ptr = (const uint32_t *)(ws + o.tile_run_ptr);
+  rp.run_be = (const uint32_t *)(ws + o.run_be);
+  rp.run_dst = (const uint32_t *)(ws + o.run_dst);
+  rp.n_tiles = (uint32_t)h.tile_run_ptr.size() - 1;
+  rp.seg1_perm = (const uint32_t *)(ws + o.seg1_perm);
   rp.part_v = (double *)(ws + o.part_v);
   rp.part_al = (uint64_t *)(ws + o.part_al);
   rp.seg1_begin = (const uint32_t *)(ws + o.seg1_begin);
   rp.seg1_end = (const uint32_t *)(ws + o.seg1_end);
-  rp.n_seg1 = (uint32_t)h.seg1_begin.size();   // long segments (chunked)
+  rp.n_seg1 = (uint32_t)h.seg1_begin.size();   // segments with 0 or >= 2 runs
   rp.seg1_id = (const uint32_t *)(ws + o.seg1_id);
   rp.n_rows1 = d->n_lines + d->n_loops + d->n_funcs;
-  rp.pack_seg = (const uint32_t *)(ws + o.pack_seg);
-  rp.n_packs = (uint32_t)h.pack_seg.size() - 1;
-  rp.segpos = (const uint32_t *)(ws + o.segpos);
   rp.seg2_perm = (const uint32_t *)(ws + o.seg2_perm);
   rp.seg2_begin = (const uint32_t *)(ws + o.seg2_begin);
   rp.seg2_end = (const uint32_t *)(ws + o.seg2_end);
   rp.n_seg2 = (uint32_t)h.seg2_begin.size();
   rp.rows_v = (double *)(ws + o.rows_v);
   rp.rows_al = (uint64_t *)(ws + o.rows_al);
-  rp.vbuf = (double *)(ws + o.vbuf);
   EstimatePlan &ep = p->ep;
   ep.pats = (const gpa_pattern *)(ws + o.pats);
   p->pats_dev = (gpa_pattern *)(ws + o.pats);
@@ -609,9 +604,6 @@ gpa_status gpa_program_destroy(gpa_program *p) {
   if (p->side_stream) cudaStreamDestroy(p->side_stream);
   if (p->ev_fork) cudaEventDestroy(p->ev_fork);
   if (p->ev_join) cudaEventDestroy(p->ev_join);
-  if (p->pack_stream) cudaStreamDestroy(p->pack_stream);
-  if (p->ev_pfork) cudaEventDestroy(p->ev_pfork);
-  if (p->ev_pjoin) cudaEventDestroy(p->ev_pjoin);
   if (p->staging) cudaFree(p->staging);
   if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
   for (int i = 0; i < 2; ++i) {
@@ -782,9 +774,6 @@ gpa_status gpa_analyze(gpa_program *p, void *stream) {
     if (!p->side_stream) CUDA_TRY(cudaStreamCreateWithFlags(&p->side_stream, cudaStreamNonBlocking));
     if (!p->ev_fork) CUDA_TRY(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
     if (!p->ev_join) CUDA_TRY(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
-    if (!p->pack_stream) CUDA_TRY(cudaStreamCreateWithFlags(&p->pack_stream, cudaStreamNonBlocking));
-    if (!p->ev_pfork) CUDA_TRY(cudaEventCreateWithFlags(&p->ev_pfork, cudaEventDisableTiming));
-    if (!p->ev_pjoin) CUDA_TRY(cudaEventCreateWithFlags(&p->ev_pjoin, cudaEventDisableTiming));
     cudaGraph_t g = nullptr;
     uint64_t n = 0;
     // two branches after the blame rows: def reduction -> rollup, and the estimate sums (which read
@@ -792,9 +781,6 @@ gpa_status gpa_analyze(gpa_program *p, void *stream) {
     CUDA_TRY(cudaStreamBeginCapture(p->capture_stream, cudaStreamCaptureModeThreadLocal));
 #ifndef GPA_EST_FORK
 #define GPA_EST_FORK 1
-#endif
-#ifndef GPA_PACK_FORK
-#define GPA_PACK_FORK 1
 #endif
     cudaStream_t cs = p->capture_stream, ss = GPA_EST_FORK ? p->side_stream : p->capture_stream;
     cudaError_t e = launch_blame_rows(p->d, p->n_sms, cs, &n);
@@ -806,8 +792,7 @@ gpa_status gpa_analyze(gpa_program *p, void *stream) {
     }
     if (e == cudaSuccess) e = launch_def_reduce(p->d, p->n_sms, cs, &n);
     if (e == cudaSuccess)
-      e = launch_rollup_fork(p->d, p->rp, p->n_sms, cs, GPA_PACK_FORK ? p->pack_stream : nullptr, p->ev_pfork,
-                             p->ev_pjoin, &n);
+      e = launch_rollup(p->d, p->rp, p->n_sms, cs, &n);
     if (e == cudaSuccess && npat) {
       e = cudaStreamWaitEvent(cs, p->ev_join, 0);
       if (e == cudaSuccess) e = launch_estimate_final(p->d, p->ep, p->n_sms, cs, &n);
