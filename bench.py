@@ -2,7 +2,7 @@
 """Benchmark of GPA's hot path on B200: PC samples/s attributed (ingest + blame + rollup +
 estimate), and the ingest kernel's achieved fraction of the measured HBM roofline.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload large|rodinia] [--impl reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload large|rodinia|batch|pelec] [--impl reference]
   torchrun --nproc-per-node N bench.py --gpus N ...     (one rank per GPU, NCCL all-reduce)
 
 Workload: BASELINE.json config 3 -- the 50k-instruction PeleC/ExaTENSOR-shaped
@@ -39,6 +39,7 @@ WORKLOADS = {
     "large": (3, 1_000_000_000),
     "rodinia": (2, 10_000_000),
     "batch": (4, 100_000_000),      # records in total (the batch is partitioned, DP-2)
+    "pelec": (6, 1_000_000_000),    # not a BASELINE config: 200k-instruction kernel
 }
 
 
@@ -152,7 +153,8 @@ def _check_world(args):
 
 def large_config(args, world, prog, cfg, n_per):
     """The `config` object of the large / rodinia arms (printed identically by --impl reference)."""
-    return {"workload": f"{args.workload}: BASELINE config {cfg} program ({prog.n_instr} instrs, {prog.n_edges} edges, "
+    what = f"BASELINE config {cfg}" if cfg != 6 else "PeleC-scale (P:708-714, beyond BASELINE's configs)"
+    return {"workload": f"{args.workload}: {what} program ({prog.n_instr} instrs, {prog.n_edges} edges, "
                         f"{prog.n_loops} loops), {n_per} records per GPU"
                         + (f" (config 5's 10^10-record stream sharded as {n_per} per GPU)" if world > 1 else ""),
             "records_per_gpu": n_per, "records_total": n_per * world,

@@ -325,7 +325,8 @@ CONFIG_SEED_BASE = 0x2009040610
 
 
 def config_program(cfg: int) -> Program:
-    """Programs of BASELINE.json configs 1-4 (config 5 reuses config 3's program)."""
+    """Programs of BASELINE.json configs 1-4 (config 5 reuses config 3's program); 6 = a 200k-instruction
+    PeleC-scale kernel (bench --workload pelec)."""
     seed = CONFIG_SEED_BASE + cfg
     if cfg == 1:
         return tiny_fixture()
@@ -339,6 +340,11 @@ def config_program(cfg: int) -> Program:
     if cfg == 4:
         from .batch import config4_program
         return config4_program()
+    if cfg == 6:   # not a BASELINE config: a PeleC-scale kernel, 15-bit local ingest bins
+        mix = {ARITH_FIXED: .46, ARITH_LONG: .07, GLOBAL: .10, SHARED: .07, LOCAL: .04,
+               CONSTANT: .03, CONVERT: .03, SYNC: .02, CONTROL: .08, MISC: .09, TEXTURE: .01}
+        return random_program(200000, 128, 600, 6, CONFIG_SEED_BASE + 6, depth_bias=1.5,
+                              weight_sigma=0.75, class_mix=mix, name="pelec")
     raise ValueError(f"no program for config {cfg}")
 
 

@@ -11,7 +11,7 @@
 //   bins = 3.6 MB).  The bin space is split over the G = #SM CTAs of a persistent cooperative
 //   grid by pc mod G, each CTA holding its bins in shared memory.  Per round every CTA streams
 //   kPartChunk records (direct 16-byte loads), counting-sorts them by destination CTA into
-//   zero-padded slots of 2-byte keys {local bin:13 | count:3} in shared memory, and writes its
+//   zero-padded slots of 2-byte keys {local bin:13-15 | count:3-1} in shared memory, and writes its
 //   whole row of slots into an L2-resident exchange buffer with one bulk store; each CTA then
 //   fetches its column of every producer's row with one 2-D TMA tile load and adds the keys into
 //   its table with shared-memory atomics.  Warp-specialised (decoders / control / publisher /
@@ -19,7 +19,8 @@
 //   per-buffer release/acquire counters between CTAs (16 exchange buffers in flight), so HBM
 //   sees each record once and the keys stay in L2.  Counts > 7, slot overflow (extreme skew)
 //   and malformed records go through L2 atomics / the stats, so the result is exact for any
-//   distribution.
+//   distribution.  Tables of up to 2^15 bins per CTA (programs of ~250k instructions at R = 9)
+//   stay on this path (15-bit local bins, counts > 1 via L2).
 // Variant L (k_ingest_l2): tables larger than shared memory; one RED.E.ADD.64 per record into
 //   the L2-resident u64 table.
 #include <algorithm>
@@ -253,8 +254,12 @@ constexpr int kInbox = GPA_PART_INBOX;                          // consumer inbo
 #endif
 constexpr int kStage = GPA_PART_STAGE;                          // staging buffers (decode k+1 never waits for chunk k's store)
 constexpr int kTrash = 32;                         // lane-distinct sink for dropped keys / padding
-constexpr uint32_t kLocalBits = 13;                // key = local bin (13 bits) | count (3 bits)
+// key = local bin (LB bits) | count (16 - LB bits, at most 7): LB = 13 for tables below 8,192 bins
+// per CTA (config 3), 14 / 15 for the larger tables of 100k-250k-instruction programs, whose
+// records of count > 1 / > 3 take the rare (L2 atomic) branch
+constexpr uint32_t kMinLocalBits = 13, kMaxLocalBits = 15;
 constexpr uint32_t kMaxKeyCount = 7;
+template <uint32_t LB> constexpr uint32_t key_max_count() { return (1u << (16 - LB)) - 1 < kMaxKeyCount ? (1u << (16 - LB)) - 1 : kMaxKeyCount; }
 constexpr uint32_t kDummyCount = 1u << 30;        // dummy-bucket counter start (never < kPartCap)
 // a chunk adds at most G * cap * 7 samples to any one table entry: a launch of at most kFlushEvery
 // chunks (the host splits longer streams) keeps every entry below 2^32 until the final flush
@@ -301,7 +306,9 @@ __device__ __forceinline__ void tma_tile_load_2d(void *dst, const CUtensorMap *t
       : "memory");
 }
 
+template <uint32_t LB>
 __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, const __grid_constant__ CUtensorMap xmap) {
+  constexpr uint32_t kLocalBits = LB, kKeyMaxCount = key_max_count<LB>();
   constexpr int CHUNK = kPartChunk;
   constexpr int kDecodeRecs = CHUNK / kDecodeThreads;   // records per decode thread per chunk
 #ifndef GPA_PART_BATCH
@@ -423,7 +430,7 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
           const uint32_t pc = h ? v.z : v.x, w = h ? v.w : v.y;
           const uint32_t t = w >> 16, c = w & 0xffffu;
           const uint32_t tl = t - (t >> 8) * (256u - R);
-          const bool fast = pc < n_instr && (t < R || t - 0x101u < R - 1u) && c <= kMaxKeyCount;
+          const bool fast = pc < n_instr && (t < R || t - 0x101u < R - 1u) && c <= kKeyMaxCount;
           const uint32_t q = __umulhi(pc, mg), b = q * nG + pc;
           const uint32_t be = fast ? b : G;
           key[i] = c * (1u << kLocalBits) + q * twoR + tl;
@@ -587,7 +594,18 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
             const uint32_t c = key >> kLocalBits;
             // padding keys (c = 0) add 0 to a lane-distinct dummy word: cheaper on the shared-memory
             // pipe than a predicated (branching) update, measured
+#ifdef GPA_PROC_PRED
+            asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t@p red.shared.add.u32 [%0], %1;\n\t}" ::"r"(
+                             tab_addr + (key & ((1u << kLocalBits) - 1)) * 4),
+                         "r"(c)
+                         : "memory");
+            continue;
+#endif
+#ifdef GPA_PROC_SAMEADDR
+            const uint32_t addr = tab_addr + (key & ((1u << kLocalBits) - 1)) * 4;   // padding: +0 to bin 0
+#else
             const uint32_t addr = c ? tab_addr + (key & ((1u << kLocalBits) - 1)) * 4 : dummy_addr;
+#endif
 #ifndef GPA_ABLATE_PROC_RED
             asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(c) : "memory");
 #else
@@ -777,7 +795,7 @@ static bool part_shape(const DevProgram &p, int n_sms, uint32_t &G, uint32_t &pp
   G = part_grid(n_sms);
   ppb = (p.n + G - 1) / G;
   bpb = ppb * 2 * p.R;
-  return ppb < 4096 && bpb < (1u << kLocalBits) && G <= 256;   // 2-byte keys: 13-bit local bins; TMA box <= 256
+  return bpb < (1u << kMaxLocalBits) && G <= 256;   // 2-byte keys: <= 15-bit local bins; TMA box <= 256
 }
 
 bool part_feasible(const DevProgram &p, int n_sms, size_t smem_optin) {
@@ -831,7 +849,9 @@ cudaError_t launch_ingest(const DevProgram &p, int variant, const void *records,
     a.stats = p.stats;
     a.X = reinterpret_cast<uint16_t *>(p.part_x);
     a.sync = p.part_sync;
-    const void *kern = (const void *)k_ingest_part;
+    const uint32_t lbits = std::max<uint32_t>(kMinLocalBits, 32u - __builtin_clz(bpb));   // bpb < 2^lbits
+    const void *kern = lbits == 13 ? (const void *)k_ingest_part<13> : lbits == 14 ? (const void *)k_ingest_part<14>
+                                                                                    : (const void *)k_ingest_part<15>;
     const size_t smem = part_smem_bytes(a.bpb, G);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

@@ -325,7 +325,7 @@ Offsets layout(const gpa_program_desc *d, const HostPlan &h) {
   o.B = a.take(n * 8 * 8);
   o.partials = (n * 2 * R * 4 <= kSmemTableMax) ? a.take((size_t)kMaxIngestCtas * n * 2 * R * 4) : a.take(0);
   {
-    const bool part = n * 2 * R * 4 > kSmemTableMax && n <= (size_t)kPartMaxCtas * 4095;  // see part_feasible
+    const bool part = n * 2 * R * 4 > kSmemTableMax && n * 2 * R < ((size_t)kPartMaxCtas << 15);  // see part_feasible (15-bit local bins)
     const size_t pairs = (size_t)kPartBufs * kPartMaxCtas * kPartMaxCtas;
     o.part_x = a.take(part ? pairs * kPartCap * 2 : 0);   // 2-byte keys
     o.part_sync = a.take(part ? 2 * kPartBufs * 4 : 0);   // producer + consumer counters per buffer

@@ -94,6 +94,19 @@ def test_part_large_tables_smaller_chunk(n_instr, R):
     compare(g, run_oracle(prog, recs), rel=REL)
 
 
+@pytest.mark.parametrize("n_instr,R,count_max", [(150_000, 9, 1), (150_000, 9, 5), (100_000, 16, 3),
+                                                 (120_000, 9, 3)])
+def test_part_wide_local_bins(n_instr, R, count_max):
+    """PeleC / Quicksilver-sized kernels: per-CTA tables of 9,126-21,632
+    bins need 14- or 15-bit local keys (1-2 count bits), and stay on the exchange path instead of
+    the L2-atomic fallback; records whose count does not fit the key go through L2 atomics."""
+    prog = gp.random_program(n_instr, 8, 60, 8, seed=61, n_reasons=R)
+    recs = StreamSpec(prog, seed=62, count_max=count_max, invalid_ppm=1_000).host(0, 4_000_001)
+    g = run_gpu(prog, recs, offset_records=1)
+    assert g["program"].variant == "part"
+    compare(g, run_oracle(prog, recs), rel=REL)
+
+
 def test_part_skewed_stream_overflow():
     """A hot PC takes half the samples: its bucket overflows the exchange slots and the excess
     goes through L2 atomics; counts stay exact."""
