@@ -11,7 +11,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(HERE, "libgpa_b200.so")
-SOURCES = ["runtime.cu", "ingest.cu", "blame.cu", "rollup.cu", "estimate.cu", "advice.cu", "slice.cu", "simulate.cu"]
+SOURCES = ["runtime.cu", "ingest.cu", "blame.cu", "rollup.cu", "estimate.cu", "advice.cu", "slice.cu", "simulate.cu", "fused.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
          "-Xptxas", "-v", "-I", os.path.join(ROOT, "include")]

@@ -5,7 +5,7 @@
 //   k_blame_rows  one thread per use row j (a3, a4): rules 1-3 per in-edge, weights
 //                 max(A_i,1)/max_len (Q1-Q4), W summed in CSR order, shares w/W
 //                 (Eq. 1), self flags when no candidate survives (Q5)
-//   k_def_reduce  one thread per def i over the create-time def-major transpose (a5, a6):
+//   k_def_tiles   a warp per 32 defs over the create-time def-major transpose (a5, a6):
 //                 S_j[r]*share and SL_j[r]*share summed into i's category
 // fp64 adds/multiplies use __dadd_rn/__dmul_rn (no FMA contraction), and every sum runs in
 // CSR/edge order, so results match a sequential evaluation of the definitions exactly.
@@ -16,10 +16,10 @@
 namespace gpa {
 namespace {
 
-__global__ void k_summaries(const uint64_t *__restrict__ C, uint32_t n, uint32_t R,
-                            uint64_t *__restrict__ AL) {
+__device__ __forceinline__ void body_summaries(const uint64_t *__restrict__ C, uint32_t n, uint32_t R,
+                            uint64_t *__restrict__ AL, uint32_t bx, uint32_t gx) {
   pdl_wait();
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+  for (uint32_t i = bx * blockDim.x + threadIdx.x; i < n; i += gx * blockDim.x) {
     const uint64_t *row = C + (uint64_t)i * 2 * R;
     uint64_t a = 0, l = 0;
     for (uint32_t r = 0; r < R; ++r) {
@@ -29,6 +29,11 @@ __global__ void k_summaries(const uint64_t *__restrict__ C, uint32_t n, uint32_t
     AL[2 * (uint64_t)i] = a;
     AL[2 * (uint64_t)i + 1] = l;
   }
+}
+
+__global__ void k_summaries(const uint64_t *__restrict__ C, uint32_t n, uint32_t R,
+                            uint64_t *__restrict__ AL) {
+  body_summaries(C, n, R, AL, blockIdx.x, gridDim.x);
 }
 
 // rule 1 (Q6): bit r-1 set when def class c may cause a stall of reason r
@@ -136,17 +141,24 @@ __global__ void k_blame_rows(DevProgram p) {
 // Tiles with more than kTileEdges edges fall back to the row-per-lane loop of k_blame_rows.
 constexpr uint32_t kTileEdges = 256;
 constexpr uint32_t kBlameWarps = 4;
-__global__ void __launch_bounds__(32 * kBlameWarps) k_blame_tiles(DevProgram p) {
+struct BlameSmem {
+  double sw[kBlameWarps][kTileEdges];
+  double sW[kBlameWarps][3][32];
+  uint8_t sm[kBlameWarps][kTileEdges];
+  uint8_t slive[kBlameWarps][32];
+};
+__device__ __forceinline__ void body_blame_tiles(DevProgram p, uint32_t bx, uint32_t gx) {
   pdl_wait();
-  __shared__ double sw[kBlameWarps][kTileEdges];
-  __shared__ uint8_t sm[kBlameWarps][kTileEdges];
-  __shared__ double sW[kBlameWarps][3][32];
-  __shared__ uint8_t slive[kBlameWarps][32];
+  BlameSmem &S = dyn_smem<BlameSmem>();
+  auto &sw = S.sw;
+  auto &sm = S.sm;
+  auto &sW = S.sW;
+  auto &slive = S.slive;
   const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const uint32_t n_tiles = (p.n + 31) / 32, warps = gridDim.x * kBlameWarps;
+  const uint32_t n_tiles = (p.n + 31) / 32, warps = gx * kBlameWarps;
   double *w_ = sw[wib];
   uint8_t *m_ = sm[wib];
-  for (uint32_t tile = blockIdx.x * kBlameWarps + wib; tile < n_tiles; tile += warps) {
+  for (uint32_t tile = bx * kBlameWarps + wib; tile < n_tiles; tile += warps) {
     const uint32_t j0 = tile * 32, j = j0 + lane;
     const bool in = j < p.n;
     const uint32_t E0 = p.row_ptr[j0], E1 = p.row_ptr[min(j0 + 32, p.n)];
@@ -246,32 +258,109 @@ __global__ void __launch_bounds__(32 * kBlameWarps) k_blame_tiles(DevProgram p) 
   }
 }
 
-__global__ void k_def_reduce(DevProgram p) {
-  pdl_wait();
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += gridDim.x * blockDim.x) {
-    double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-    for (uint32_t k = p.def_ptr[i]; k < p.def_ptr[i + 1]; ++k) {
-      const uint32_t e = p.def_perm[k];
-      const uint32_t m = p.cand[e];
-      if (!m) continue;
-      const uint64_t *row = p.C + (uint64_t)p.edge_use[e] * 2 * p.R;
+__global__ void __launch_bounds__(32 * kBlameWarps) k_blame_tiles(DevProgram p) {
+  body_blame_tiles(p, blockIdx.x, gridDim.x);
+}
+
+// one lane per def: S_j[r]*share and SL_j[r]*share over the def's out-edges in def-major order
+__device__ __forceinline__ void def_reduce_one(const DevProgram &p, uint32_t i) {
+  double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+  for (uint32_t k = p.def_ptr[i]; k < p.def_ptr[i + 1]; ++k) {
+    const uint32_t e = p.def_perm[k];
+    const uint32_t m = p.cand[e];
+    if (!m) continue;
+    const uint64_t *row = p.C + (uint64_t)p.edge_use[e] * 2 * p.R;
 #pragma unroll
-      for (uint32_t r = R_MEM; r <= R_SYNC; ++r) {
-        if (!(m & (1u << (r - 1)))) continue;
-        const double sh = p.share[3 * (uint64_t)e + (r - 1)];
-        const uint64_t lat = row[p.R + r], all = row[r] + lat;
-        const uint32_t g = r == R_MEM ? BG_MEM : r == R_SYNC ? BG_SYNC : ((p.edge_kind[e] & K_WAR) ? BG_WAR : BG_EXEC);
-        acc[g][0] = __dadd_rn(acc[g][0], __dmul_rn((double)all, sh));
-        acc[g][1] = __dadd_rn(acc[g][1], __dmul_rn((double)lat, sh));
-      }
-    }
-    double *out = p.B + 8 * (uint64_t)i;
-#pragma unroll
-    for (int g = 0; g < 4; ++g) {
-      out[2 * g] = acc[g][0];
-      out[2 * g + 1] = acc[g][1];
+    for (uint32_t r = R_MEM; r <= R_SYNC; ++r) {
+      if (!(m & (1u << (r - 1)))) continue;
+      const double sh = p.share[3 * (uint64_t)e + (r - 1)];
+      const uint64_t lat = row[p.R + r], all = row[r] + lat;
+      const uint32_t g = r == R_MEM ? BG_MEM : r == R_SYNC ? BG_SYNC : ((p.edge_kind[e] & K_WAR) ? BG_WAR : BG_EXEC);
+      acc[g][0] = __dadd_rn(acc[g][0], __dmul_rn((double)all, sh));
+      acc[g][1] = __dadd_rn(acc[g][1], __dmul_rn((double)lat, sh));
     }
   }
+  double *out = p.B + 8 * (uint64_t)i;
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    out[2 * g] = acc[g][0];
+    out[2 * g + 1] = acc[g][1];
+  }
+}
+
+// Warp-cooperative def reduction: a warp takes 32 consecutive defs.  (1) lanes over the tile's
+// out-edge positions (def-major order, coalesced def_perm): the products S_j[r]*share and
+// SL_j[r]*share of every candidate reason, gathered from the use rows by 32 lanes at once and staged
+// in shared memory with the Fig. 6 group of the EXEC reason; (2) lane = def: the sums over its
+// positions in order, reasons MEM, EXEC, SYNC -- the sequential order of def_reduce_one, so B is
+// bit-identical.  Tiles with more than kDefTileEdges positions take def_reduce_one per lane.
+constexpr uint32_t kDefTileEdges = 128;
+constexpr uint32_t kDefWarps = 4;
+struct DefSmem {
+  double2 sprod[kDefWarps][3][kDefTileEdges];   // (all, lat) * share per dependency reason
+  uint8_t sm[kDefWarps][kDefTileEdges];         // candidate mask | exec group is WAR << 3
+};
+__device__ __forceinline__ void body_def_tiles(DevProgram p, uint32_t bx, uint32_t gx) {
+  pdl_wait();
+  DefSmem &S = dyn_smem<DefSmem>();
+  auto &sprod = S.sprod;
+  auto &sm = S.sm;
+  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint32_t n_tiles = (p.n + 31) / 32, warps = gx * kDefWarps;
+  double2(*prod)[kDefTileEdges] = sprod[wib];
+  uint8_t *m_ = sm[wib];
+  for (uint32_t tile = bx * kDefWarps + wib; tile < n_tiles; tile += warps) {
+    const uint32_t i0 = tile * 32, i = i0 + lane;
+    const uint32_t K0 = p.def_ptr[i0], K1 = p.def_ptr[min(i0 + 32, p.n)];
+    if (K1 - K0 > kDefTileEdges) {   // rare: a long tile
+      if (i < p.n) def_reduce_one(p, i);
+      continue;
+    }
+    // (1) lanes over positions
+    for (uint32_t k = K0 + lane; k < K1; k += 32) {
+      const uint32_t e = p.def_perm[k];
+      const uint32_t m = p.cand[e];
+      uint32_t mm = m;
+      if (m) {
+        const uint64_t *row = p.C + (uint64_t)p.edge_use[e] * 2 * p.R;
+        if (p.edge_kind[e] & K_WAR) mm |= 8u;
+#pragma unroll
+        for (uint32_t r = R_MEM; r <= R_SYNC; ++r) {
+          if (!(m & (1u << (r - 1)))) continue;
+          const double sh = p.share[3 * (uint64_t)e + (r - 1)];
+          const uint64_t lat = row[p.R + r], all = row[r] + lat;
+          prod[r - 1][k - K0] = make_double2(__dmul_rn((double)all, sh), __dmul_rn((double)lat, sh));
+        }
+      }
+      m_[k - K0] = (uint8_t)mm;
+    }
+    __syncwarp();
+    // (2) lane = def: sums in position order
+    if (i < p.n) {
+      double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+      const uint32_t k0 = p.def_ptr[i] - K0, k1 = p.def_ptr[i + 1] - K0;
+      for (uint32_t k = k0; k < k1; ++k) {
+        const uint32_t mm = m_[k];
+        if (!(mm & 7u)) continue;
+#pragma unroll
+        for (uint32_t r = R_MEM; r <= R_SYNC; ++r) {
+          if (!(mm & (1u << (r - 1)))) continue;
+          const uint32_t g = r == R_MEM ? BG_MEM : r == R_SYNC ? BG_SYNC : ((mm & 8u) ? BG_WAR : BG_EXEC);
+          const double2 v = prod[r - 1][k];
+          acc[g][0] = __dadd_rn(acc[g][0], v.x);
+          acc[g][1] = __dadd_rn(acc[g][1], v.y);
+        }
+      }
+      double2 *out = reinterpret_cast<double2 *>(p.B + 8 * (uint64_t)i);
+#pragma unroll
+      for (int g = 0; g < 4; ++g) out[g] = make_double2(acc[g][0], acc[g][1]);
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void __launch_bounds__(32 * kDefWarps) k_def_tiles(DevProgram p) {
+  body_def_tiles(p, blockIdx.x, gridDim.x);
 }
 
 inline uint32_t grid_for(uint64_t items, uint32_t threads, int n_sms) {
@@ -280,6 +369,7 @@ inline uint32_t grid_for(uint64_t items, uint32_t threads, int n_sms) {
 
 }  // namespace
 
+#ifndef GPA_FUSED_TU
 // summaries + candidates / shares / self flags (rows a2-a4): everything the estimate step reads
 cudaError_t launch_blame_rows(const DevProgram &p, int n_sms, cudaStream_t s, uint64_t *launches) {
   k_summaries<<<grid_for(p.n, 256, n_sms), 256, 0, s>>>(p.C, p.n, p.R, p.AL);
@@ -292,7 +382,7 @@ cudaError_t launch_blame_rows(const DevProgram &p, int n_sms, cudaStream_t s, ui
       const uint32_t tiles = (p.n + 31) / 32;
       const uint32_t g = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((tiles + kBlameWarps - 1) / kBlameWarps,
                                                                             (uint64_t)n_sms * 16));
-      e = launch_pdl(p.n, k_blame_tiles, g, 32 * kBlameWarps, 0, s, p);
+      e = launch_pdl(p.n, k_blame_tiles, g, 32 * kBlameWarps, sizeof(BlameSmem), s, p);
     } else {
       e = launch_pdl(p.n, k_blame_rows, grid_for(p.n, 128, n_sms), 128, 0, s, p);
     }
@@ -303,7 +393,10 @@ cudaError_t launch_blame_rows(const DevProgram &p, int n_sms, cudaStream_t s, ui
 
 // def-side reduction (rows a5-a6): B, read by the rollup only
 cudaError_t launch_def_reduce(const DevProgram &p, int n_sms, cudaStream_t s, uint64_t *launches) {
-  const cudaError_t e = launch_pdl(p.n, k_def_reduce, grid_for(p.n, 128, n_sms), 128, 0, s, p);
+  const uint32_t tiles = (p.n + 31) / 32;
+  const uint32_t g = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((tiles + kDefWarps - 1) / kDefWarps,
+                                                                        (uint64_t)n_sms * 16));
+  const cudaError_t e = launch_pdl(p.n, k_def_tiles, g, 32 * kDefWarps, sizeof(DefSmem), s, p);
   *launches += 1;
   return e;
 }
@@ -312,5 +405,7 @@ cudaError_t launch_blame(const DevProgram &p, int n_sms, cudaStream_t s, uint64_
   cudaError_t e = launch_blame_rows(p, n_sms, s, launches);
   return e != cudaSuccess ? e : launch_def_reduce(p, n_sms, s, launches);
 }
+
+#endif  // GPA_FUSED_TU
 
 }  // namespace gpa

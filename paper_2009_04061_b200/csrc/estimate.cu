@@ -2,10 +2,11 @@
 // P:457-460) and the estimators of §5.2: Eq. 2, Eq. 3, Eq. 4
 // (P:496-503), Eq. 5 (Q16), Eqs. 6-10 (Q18), per kernel.
 //
-//   k_est_rows    one thread per (use row j, pattern group): the matched samples of each
-//                 in-edge (blamed at the def, scope loop = lca(def, use)) and of j itself
-//                 (self / pass-through columns, scope loop = loop of j); row totals mrow[q][j]
-//                 and, for loop-scoped patterns, per-item values for the loop reduction.
+//   k_est_tiles   a CTA per tile of 32 use rows, a warp per pattern group: the matched samples
+//                 of each in-edge (blamed at the def, scope loop = lca(def, use)), edge-parallel,
+//                 and of each row j itself (self / pass-through columns, scope loop = loop of j);
+//                 row totals mrow[q][j] and, for loop-scoped patterns, the per-item values
+//                 (edges and instructions) of the loop reduction.
 //   k_segsum      one warp per (segment, pattern): fixed-order strided sums + xor-shuffle tree
 //                 (deterministic).  Stage 1: loop-exclusive (by scope-loop item lists) and
 //                 function sums; stage 2: loop-inclusive (preorder subtree ranges) and kernel sums.
@@ -27,101 +28,128 @@ namespace {
 #endif
 constexpr int kEstGroup = GPA_EST_GROUP;
 
-__global__ void k_est_rows(DevProgram p, EstimatePlan ep) {
+// Warp-cooperative form (the blame tiles' pattern): a CTA takes a tile of 32 consecutive use rows,
+// one warp per pattern group.  (1) lane = row: the row's all / latency samples of the dependency
+// reasons (X) and its loop are staged in shared memory; (2) lanes over the tile's in-edges
+// (coalesced edge fields, one EdgeInfo per edge): the matched samples of every pattern of the group,
+// staged in shared memory, and written out as the per-edge item values of the loop-scoped patterns
+// (the mval edge part); (3) lane = row: the
+// row sum over its edges in CSR order from shared memory, plus the row's own part -- the order of
+// the sequential definition, so mrow is bit-identical to a row-by-row evaluation (an edge without a
+// candidate reason adds +0.0 to a non-negative sum: no change).  Tiles with more than kEstTileEdges
+// edges take the row-per-lane loop.
+constexpr uint32_t kEstTileEdges = 128;
+constexpr uint32_t kEstWarps = 4;   // pattern groups per CTA (kPatternsMax / kEstGroup at most)
+struct EstSmem {
+  double sv[kEstWarps][kEstGroup][kEstTileEdges];
+  double sX[kEstWarps][32][8];   // per row: XA[1..3], XL[1..3]
+  int32_t sloop[kEstWarps][32];
+};
+__device__ __forceinline__ void body_est_tiles(DevProgram p, EstimatePlan ep, uint32_t bx, uint32_t gx) {
   pdl_wait();
   __shared__ gpa_pattern sp[kPatternsMax];
   __shared__ int8_t sslot[kPatternsMax];
+  EstSmem &S = dyn_smem<EstSmem>();
+  auto &sv = S.sv;
+  auto &sX = S.sX;
+  auto &sloop = S.sloop;
   for (uint32_t q = threadIdx.x; q < ep.n_pat; q += blockDim.x) {
     sp[q] = ep.pats[q];
     sslot[q] = ep.loop_slot[q];
   }
   __syncthreads();
   const uint64_t stride_items = (uint64_t)p.E + p.n;
-  // a CTA = one warp per pattern group over the same 32 rows: the pattern fields are uniform in a
-  // warp (no divergence on them), and a row's C entries and edges are fetched from DRAM once and
-  // served from L1 to the other groups' warps
   const uint32_t grp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (uint32_t j = blockIdx.x * 32 + lane; j - lane < p.n; j += gridDim.x * 32) {
-    if (j >= p.n) continue;
-    const uint32_t q0 = grp * kEstGroup;
-    const uint32_t nq = min((uint32_t)kEstGroup, ep.n_pat - q0);
-    const uint64_t *row = p.C + (uint64_t)j * 2 * p.R;
-    double XA[4], XL[4];   // all / latency samples of the dependency reasons at j
+  if (grp * kEstGroup >= ep.n_pat) return;   // spare warps (fewer pattern groups than warps)
+  const uint32_t q0 = grp * kEstGroup;
+  const uint32_t nq = min((uint32_t)kEstGroup, ep.n_pat - q0);
+  const uint32_t n_tiles = (p.n + 31) / 32;
+  double(*v_)[kEstTileEdges] = sv[grp];
+  double(*X_)[8] = sX[grp];
+  int32_t *loop_ = sloop[grp];
+  for (uint32_t t = bx; t < n_tiles; t += gx) {
+    const uint32_t j0 = 32 * t, j = j0 + lane;
+    const bool in = j < p.n;
+    const uint32_t E0 = p.row_ptr[j0], E1 = p.row_ptr[min(j0 + 32, p.n)];
+    // (1) lane = row
+    double XA[4], XL[4];
+    const uint64_t *row = p.C + (uint64_t)(in ? j : j0) * 2 * p.R;
 #pragma unroll
     for (int r = 1; r <= 3; ++r) {
-      const uint64_t lat = row[p.R + r];
+      const uint64_t lat = in ? row[p.R + r] : 0ull;
       XL[r] = (double)lat;
-      XA[r] = (double)(lat + row[r]);
+      XA[r] = (double)(lat + (in ? row[r] : 0ull));
+      X_[lane][r - 1] = XA[r];
+      X_[lane][r + 2] = XL[r];
     }
-    const uint32_t e0 = p.row_ptr[j], e1 = p.row_ptr[j + 1];
-    const int32_t loop_j = p.loop_id[j];
+    const int32_t loop_j = in ? p.loop_id[j] : -1;
+    loop_[lane] = loop_j;
     double sum[kEstGroup];
 #pragma unroll
     for (int k = 0; k < kEstGroup; ++k) sum[k] = 0.0;
-    for (uint32_t e = e0; e < e1; ++e) {   // loads only: per-edge values go to k_est_edges
-      const EdgeInfo x = edge_info(p, e, loop_j);
-      if (!x.m) continue;                  // no candidate reason: adds 0 to every pattern
+    if (E1 - E0 > kEstTileEdges) {   // rare: a long tile -- lane per row, CSR order
+      if (in) {
+        for (uint32_t e = p.row_ptr[j]; e < p.row_ptr[j + 1]; ++e) {
+          const EdgeInfo x = edge_info(p, e, loop_j);
+#pragma unroll
+          for (int k = 0; k < kEstGroup; ++k) {
+            if ((uint32_t)k >= nq) break;
+            const gpa_pattern &q = sp[q0 + k];
+            const double v = q.model == 5 ? 0.0 : edge_match(q, x, q.sample_class ? XL : XA);
+            sum[k] = __dadd_rn(sum[k], v);
+            if (sslot[q0 + k] >= 0) ep.mval[(uint64_t)sslot[q0 + k] * stride_items + e] = v;
+          }
+        }
+      }
+    } else {
+      __syncwarp();
+      // (2) lanes over the tile's edges
+      for (uint32_t e = E0 + lane; e < E1; e += 32) {
+        const uint32_t u = p.edge_use[e] - j0;
+        const EdgeInfo x = edge_info(p, e, loop_[u]);
+        const double xa[4] = {0.0, X_[u][0], X_[u][1], X_[u][2]}, xl[4] = {0.0, X_[u][3], X_[u][4], X_[u][5]};
+#pragma unroll
+        for (int k = 0; k < kEstGroup; ++k) {
+          if ((uint32_t)k >= nq) break;
+          const gpa_pattern &q = sp[q0 + k];
+          const double v = q.model == 5 ? 0.0 : edge_match(q, x, q.sample_class ? xl : xa);
+          v_[k][e - E0] = v;
+          if (sslot[q0 + k] >= 0) ep.mval[(uint64_t)sslot[q0 + k] * stride_items + e] = v;
+        }
+      }
+      __syncwarp();
+      // (3) lane = row: CSR-order sums from shared memory
+      if (in) {
+        const uint32_t e0 = p.row_ptr[j] - E0, e1 = p.row_ptr[j + 1] - E0;
+        for (uint32_t k2 = e0; k2 < e1; ++k2) {
+#pragma unroll
+          for (int k = 0; k < kEstGroup; ++k) sum[k] = __dadd_rn(sum[k], v_[k][k2]);   // unused groups: 0 + 0
+        }
+      }
+    }
+    if (in) {
+      const uint32_t cls_j = p.opclass[j], flags_j = p.iflags[j], self_j = p.selfm[j];
 #pragma unroll
       for (int k = 0; k < kEstGroup; ++k) {
         if ((uint32_t)k >= nq) break;
-        const gpa_pattern &q = sp[q0 + k];
-        if (q.model == 5) continue;
-        sum[k] = __dadd_rn(sum[k], edge_match(q, x, q.sample_class ? XL : XA));
+        const uint32_t qi = q0 + k;
+        const gpa_pattern &q = sp[qi];
+        if (q.model == 5) {
+          ep.mrow[(uint64_t)qi * p.n + j] = 0.0;
+          continue;
+        }
+        const double mi = instr_match(q, p.R, row, q.sample_class ? XL : XA, cls_j, flags_j, self_j, loop_j);
+        const int slot = sslot[qi];
+        if (slot >= 0) ep.mval[(uint64_t)slot * stride_items + p.E + j] = mi;
+        ep.mrow[(uint64_t)qi * p.n + j] = __dadd_rn(sum[k], mi);
       }
     }
-    const uint32_t cls_j = p.opclass[j], flags_j = p.iflags[j], self_j = p.selfm[j];
-#pragma unroll
-    for (int k = 0; k < kEstGroup; ++k) {
-      if ((uint32_t)k >= nq) break;
-      const uint32_t qi = q0 + k;
-      const gpa_pattern &q = sp[qi];
-      if (q.model == 5) {
-        ep.mrow[(uint64_t)qi * p.n + j] = 0.0;
-        continue;
-      }
-      const double mi = instr_match(q, p.R, row, q.sample_class ? XL : XA, cls_j, flags_j, self_j, loop_j);
-      const int slot = sslot[qi];
-      if (slot >= 0) ep.mval[(uint64_t)slot * stride_items + p.E + j] = mi;
-      ep.mrow[(uint64_t)qi * p.n + j] = __dadd_rn(sum[k], mi);
-    }
+    __syncwarp();
   }
 }
 
-// per-edge matched samples of the loop-scoped patterns (mval[slot][e]), edge-parallel and
-// coalesced; the same arithmetic as k_est_rows, so the item values and the row sums agree
-__global__ void k_est_edges(DevProgram p, EstimatePlan ep) {
-  pdl_wait();
-  __shared__ gpa_pattern sp[kPatternsMax];
-  __shared__ int8_t sslot[kPatternsMax];
-  __shared__ uint32_t slot_q[kPatternsMax], n_slot_q;
-  if (threadIdx.x == 0) {
-    uint32_t c = 0;
-    for (uint32_t q = 0; q < ep.n_pat; ++q)
-      if (ep.loop_slot[q] >= 0 && ep.pats[q].model != 5) slot_q[c++] = q;
-    n_slot_q = c;
-  }
-  for (uint32_t q = threadIdx.x; q < ep.n_pat; q += blockDim.x) {
-    sp[q] = ep.pats[q];
-    sslot[q] = ep.loop_slot[q];
-  }
-  __syncthreads();
-  const uint64_t stride_items = (uint64_t)p.E + p.n;
-  for (uint32_t e = blockIdx.x * blockDim.x + threadIdx.x; e < p.E; e += gridDim.x * blockDim.x) {
-    const uint32_t j = p.edge_use[e];
-    const uint64_t *row = p.C + (uint64_t)j * 2 * p.R;
-    double XA[4], XL[4];
-#pragma unroll
-    for (int r = 1; r <= 3; ++r) {
-      const uint64_t lat = row[p.R + r];
-      XL[r] = (double)lat;
-      XA[r] = (double)(lat + row[r]);
-    }
-    const EdgeInfo x = edge_info(p, e, p.loop_id[j]);
-    for (uint32_t k = 0; k < n_slot_q; ++k) {
-      const gpa_pattern &q = sp[slot_q[k]];
-      ep.mval[(uint64_t)sslot[slot_q[k]] * stride_items + e] = edge_match(q, x, q.sample_class ? XL : XA);
-    }
-  }
+__global__ void __launch_bounds__(32 * kEstWarps) k_est_tiles(DevProgram p, EstimatePlan ep) {
+  body_est_tiles(p, ep, blockIdx.x, gridDim.x);
 }
 
 struct SegFamily {
@@ -140,13 +168,13 @@ struct SegLaunch {
   uint32_t n_fam, n_pat;
 };
 
-__global__ void k_segsum(SegLaunch L) {
+__device__ __forceinline__ void body_segsum(SegLaunch L, uint32_t fam, uint32_t bx, uint32_t gx) {
   pdl_wait();
   const uint32_t lane = threadIdx.x & 31;
-  const SegFamily &F = L.fam[blockIdx.y];
+  const SegFamily &F = L.fam[fam];
   const uint64_t items = (uint64_t)F.n_seg * L.n_pat;
-  const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
-  for (uint64_t w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < items; w += warps) {
+  const uint32_t warps = (gx * blockDim.x) >> 5;
+  for (uint64_t w = (bx * blockDim.x + threadIdx.x) >> 5; w < items; w += warps) {
     const uint32_t q = (uint32_t)(w / F.n_seg), s = (uint32_t)(w % F.n_seg);
     const int32_t vr = F.vrow[q];
     double acc = 0.0;
@@ -172,6 +200,10 @@ __global__ void k_segsum(SegLaunch L) {
   }
 }
 
+__global__ void k_segsum(SegLaunch L) {
+  body_segsum(L, blockIdx.y, blockIdx.x, gridDim.x);
+}
+
 __device__ __forceinline__ double eq2(double T, double M) {
   if (T <= 0.0) return 1.0;
   if (M >= T) return INFINITY;
@@ -181,12 +213,12 @@ __device__ __forceinline__ double eq2(double T, double M) {
 // one warp per (kernel, pattern); lanes stride over the kernel's scopes for Eq. 5 and the warp
 // takes the max with ties to the lowest scope id (loops before functions), as a sequential scan
 // in scope order would.
-__global__ void k_est_final(DevProgram p, EstimatePlan ep) {
+__device__ __forceinline__ void body_est_final(DevProgram p, EstimatePlan ep, uint32_t bx, uint32_t gx) {
   pdl_wait();
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t total = p.n_kernels * ep.n_pat;
-  const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < total; t += warps) {
+  const uint32_t warps = (gx * blockDim.x) >> 5;
+  for (uint32_t t = (bx * blockDim.x + threadIdx.x) >> 5; t < total; t += warps) {
     const uint32_t k = t / ep.n_pat, qi = t % ep.n_pat;
     const gpa_pattern q = ep.pats[qi];
     const uint64_t A = ep.kern_al[2 * (uint64_t)k], T = A + ep.kern_al[2 * (uint64_t)k + 1];
@@ -280,39 +312,23 @@ __global__ void k_est_final(DevProgram p, EstimatePlan ep) {
   }
 }
 
-}  // namespace
+__global__ void k_est_final(DevProgram p, EstimatePlan ep) {
+  body_est_final(p, ep, blockIdx.x, gridDim.x);
+}
 
-// matched samples per item, loop / function / kernel sums: reads only the blame rows' outputs
-// (cand, share, selfm) and C, so it can run beside the def reduction and the rollup
-cudaError_t launch_estimate_sums(const DevProgram &p, const EstimatePlan &ep, int n_sms, cudaStream_t s,
-                                 uint64_t *launches) {
-  const uint32_t n_groups = (ep.n_pat + kEstGroup - 1) / kEstGroup;   // <= 8: a warp per group
-  const uint32_t g = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(((uint64_t)p.n + 31) / 32, (uint64_t)n_sms * 64));
-  k_est_rows<<<g, 32 * n_groups, 0, s>>>(p, ep);
-  bool any_slot = false;
-  for (uint32_t q = 0; q < ep.n_pat; ++q) any_slot |= ep.loop_slot[q] >= 0;
-  if (any_slot && p.E) {
-    const uint32_t ge = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(((uint64_t)p.E + 255) / 256, (uint64_t)n_sms * 16));
-    const cudaError_t e = launch_pdl(p.n, k_est_edges, ge, 256, 0, s, p, ep);
-    if (e != cudaSuccess) return e;
-    *launches += 1;
-  }
-  SegLaunch a{};
+// the two k_segsum stages: (1) loops exclusive (by scope-loop items) and functions, (2) loops
+// inclusive (preorder subtree ranges over the exclusive sums) and kernels
+inline void make_seg_launches(const DevProgram &p, const EstimatePlan &ep, SegLaunch &a, SegLaunch &b) {
+  a = SegLaunch{};
   a.n_pat = ep.n_pat;
   a.n_fam = 2;
-  // stage 1: loops (exclusive, by scope-loop items) and functions
   a.fam[0] = SegFamily{ep.mval, (uint64_t)p.E + p.n, ep.loop_items, ep.loop_item_ptr, nullptr, p.n_loops, ep.lM_excl, {}};
   a.fam[1] = SegFamily{ep.mrow, p.n, nullptr, p.func_begin, nullptr, p.n_funcs, ep.fM, {}};
   for (int q = 0; q < kPatternsMax; ++q) {
     a.fam[0].vrow[q] = ep.loop_slot[q];
     a.fam[1].vrow[q] = q < (int)ep.n_pat ? q : -1;
   }
-  const uint64_t w1 = std::max<uint64_t>((uint64_t)p.n_loops, p.n_funcs) * ep.n_pat;
-  dim3 g1((uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((w1 + 3) / 4, (uint64_t)n_sms * 32)), 2);
-  cudaError_t e = launch_pdl(p.n, k_segsum, g1, 128, 0, s, a);
-  if (e != cudaSuccess) return e;
-  // stage 2: loops inclusive (preorder subtree ranges over exclusive sums) and kernels
-  SegLaunch b{};
+  b = SegLaunch{};
   b.n_pat = ep.n_pat;
   b.n_fam = 2;
   b.fam[0] = SegFamily{ep.lM_excl, p.n_loops, ep.pre_perm, ep.pre_begin, ep.pre_end, p.n_loops, ep.lM_incl, {}};
@@ -321,6 +337,24 @@ cudaError_t launch_estimate_sums(const DevProgram &p, const EstimatePlan &ep, in
     b.fam[0].vrow[q] = ep.loop_slot[q] >= 0 ? q : -1;
     b.fam[1].vrow[q] = q < (int)ep.n_pat ? q : -1;
   }
+}
+
+}  // namespace
+
+#ifndef GPA_FUSED_TU
+// matched samples per item, loop / function / kernel sums: reads only the blame rows' outputs
+// (cand, share, selfm) and C, so it can run beside the def reduction and the rollup
+cudaError_t launch_estimate_sums(const DevProgram &p, const EstimatePlan &ep, int n_sms, cudaStream_t s,
+                                 uint64_t *launches) {
+  const uint32_t n_groups = (ep.n_pat + kEstGroup - 1) / kEstGroup;   // <= 8: a warp per group
+  const uint32_t g = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(((uint64_t)p.n + 31) / 32, (uint64_t)n_sms * 64));
+  k_est_tiles<<<g, 32 * n_groups, sizeof(EstSmem), s>>>(p, ep);
+  SegLaunch a, b;
+  make_seg_launches(p, ep, a, b);
+  const uint64_t w1 = std::max<uint64_t>((uint64_t)p.n_loops, p.n_funcs) * ep.n_pat;
+  dim3 g1((uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((w1 + 3) / 4, (uint64_t)n_sms * 32)), 2);
+  cudaError_t e = launch_pdl(p.n, k_segsum, g1, 128, 0, s, a);
+  if (e != cudaSuccess) return e;
   const uint64_t w2 = std::max<uint64_t>((uint64_t)p.n_loops, p.n_kernels) * ep.n_pat;
   dim3 g2((uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((w2 + 3) / 4, (uint64_t)n_sms * 32)), 2);
   e = launch_pdl(p.n, k_segsum, g2, 128, 0, s, b);
@@ -342,5 +376,7 @@ cudaError_t launch_estimate(const DevProgram &p, const EstimatePlan &ep, int n_s
   cudaError_t e = launch_estimate_sums(p, ep, n_sms, s, launches);
   return e != cudaSuccess ? e : launch_estimate_final(p, ep, n_sms, s, launches);
 }
+
+#endif  // GPA_FUSED_TU
 
 }  // namespace gpa

@@ -25,12 +25,25 @@ constexpr size_t kSmemTableMax = 224 * 1024;// largest CTA-private table (bytes;
 // a kernel launched with the programmatic-serialization attribute may be scheduled while its
 // predecessor drains and waits for its completion (and memory flush) before touching any data.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// The tile kernels carve their staging buffers out of dynamic shared memory (a struct per kernel),
+// so the fused analysis kernel, whose phases run one after another, reuses one region for all.
+#ifdef __CUDACC__
+template <typename T>
+__device__ __forceinline__ T &dyn_smem() {
+  extern __shared__ __align__(16) uint8_t gpa_dyn_smem[];
+  return *reinterpret_cast<T *>(gpa_dyn_smem);
+}
+#endif
 #ifndef GPA_PDL
 #define GPA_PDL 1
 #endif
 // Only for programs below kPdlMaxInstr instructions: there the analysis kernels are short and
 // latency-bound (config 3: 92 -> 82 us); on config 4's 4.5 M instructions the overlap cost 1 %.
 constexpr uint32_t kPdlMaxInstr = 1u << 20;
+#ifndef GPA_FUSED_CTAS
+#define GPA_FUSED_CTAS 4096
+#endif
+constexpr uint32_t kFusedMaxCtas = GPA_FUSED_CTAS;   // grid of the fused analysis kernel (at most)
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(uint32_t n_instr, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
                               cudaStream_t s, Args &&...args) {
@@ -190,6 +203,10 @@ cudaError_t launch_ingest_segments(const DevProgram &p, const void *records, uin
                                    const uint32_t *seg_kernel, uint32_t n_seg, uint32_t pc_base, uint32_t max_tab_bins,
                                    int n_sms, cudaStream_t s);
 size_t ingest_smem_bytes(const DevProgram &p);
+// the whole analysis as one cooperative launch (fused.cu; small programs, <= 16 patterns)
+bool fused_feasible(uint32_t n_pat);
+cudaError_t launch_analyze_fused(const DevProgram &p, const RollupPlan &rp, const EstimatePlan &ep, int n_sms,
+                                 uint32_t max_ctas, cudaStream_t s, uint64_t *launches);
 bool part_feasible(const DevProgram &p, int n_sms, size_t smem_optin);
 
 #ifdef __CUDACC__
@@ -311,4 +328,5 @@ struct gpa_program {
   cudaGraphExec_t analyze_exec = nullptr;
   uint32_t analyze_npat = 0xffffffffu;
   uint64_t analyze_launches = 0;
+  int analyze_mode = GPA_ANALYZE_AUTO;   // gpa_set_analyze_mode
 };

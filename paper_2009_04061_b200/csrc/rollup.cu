@@ -28,7 +28,7 @@ namespace {
 constexpr uint32_t kVrowsThreads = 128;
 __global__ void __launch_bounds__(kVrowsThreads) k_vrows(DevProgram p, double *__restrict__ vbuf) {
   pdl_wait();
-  extern __shared__ double2 vstage[];          // [kVrowsThreads / 32][32 rows][ncol]
+  double2 *vstage = &dyn_smem<double2>();      // [kVrowsThreads / 32][32 rows][ncol]
   const uint32_t ncol = p.ncol, R = p.R, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double2 *ws = vstage + (size_t)warp * 32 * ncol;
   const uint32_t stride = gridDim.x * blockDim.x;
@@ -108,17 +108,17 @@ __device__ __forceinline__ void warp_sum_rows(uint32_t lane, uint32_t nv, uint32
   }
 }
 
-__global__ void __launch_bounds__(128) k_rollup_segments(uint32_t nv, const double *__restrict__ in_v,
+__device__ __forceinline__ void body_rollup_segments(uint32_t nv, const double *__restrict__ in_v,
                                                          const uint64_t *__restrict__ in_al,
                                                          const uint32_t *__restrict__ perm,
                                                          const uint32_t *__restrict__ seg_begin,
                                                          const uint32_t *__restrict__ seg_end, uint32_t n_seg,
                                                          const uint32_t *__restrict__ out_row,
-                                                         double *__restrict__ out_v, uint64_t *__restrict__ out_al) {
+                                                         double *__restrict__ out_v, uint64_t *__restrict__ out_al, uint32_t bx, uint32_t gx) {
   pdl_wait();
   const uint32_t lane = threadIdx.x & 31;
-  const uint32_t warps = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t sg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; sg < n_seg; sg += warps) {
+  const uint32_t warps = (gx * blockDim.x) >> 5;
+  for (uint32_t sg = (bx * blockDim.x + threadIdx.x) >> 5; sg < n_seg; sg += warps) {
     const uint64_t row = out_row ? out_row[sg] : sg;
     if (perm)
       warp_sum_rows(lane, nv, seg_begin[sg], seg_end[sg], [perm](uint32_t pos) { return perm[pos]; }, in_v, in_al,
@@ -129,18 +129,28 @@ __global__ void __launch_bounds__(128) k_rollup_segments(uint32_t nv, const doub
   }
 }
 
+__global__ void __launch_bounds__(128) k_rollup_segments(uint32_t nv, const double *__restrict__ in_v,
+                                                         const uint64_t *__restrict__ in_al,
+                                                         const uint32_t *__restrict__ perm,
+                                                         const uint32_t *__restrict__ seg_begin,
+                                                         const uint32_t *__restrict__ seg_end, uint32_t n_seg,
+                                                         const uint32_t *__restrict__ out_row,
+                                                         double *__restrict__ out_v, uint64_t *__restrict__ out_al) {
+  body_rollup_segments(nv, in_v, in_al, perm, seg_begin, seg_end, n_seg, out_row, out_v, out_al, blockIdx.x, gridDim.x);
+}
+
 // one warp per tile of 32 instructions (4 warps per block): V rows built by lane = instruction into
 // shared memory (the k_vrows arithmetic), then lane = value slot sums each run of the tile in member
 // order and stores the run's row (or partial row) -- one coalesced row store per run
 constexpr uint32_t kTileWarps = 4;
-__global__ void __launch_bounds__(32 * kTileWarps) k_rollup_tiles(DevProgram p, RollupPlan rp) {
+__device__ __forceinline__ void body_rollup_tiles(DevProgram p, RollupPlan rp, uint32_t bx, uint32_t gx) {
   pdl_wait();
-  extern __shared__ double2 tstage[];          // [kTileWarps][32 rows][ncol] + [kTileWarps][32][2] u64
+  double2 *tstage = &dyn_smem<double2>();      // [kTileWarps][32 rows][ncol] + [kTileWarps][32][2] u64
   const uint32_t ncol = p.ncol, nv = 2 * ncol, R = p.R, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   double2 *ws = tstage + (size_t)warp * 32 * ncol;
   uint64_t *wal = reinterpret_cast<uint64_t *>(tstage + (size_t)kTileWarps * 32 * ncol) + (size_t)warp * 64;
-  const uint32_t warps = gridDim.x * kTileWarps;
-  for (uint32_t t = blockIdx.x * kTileWarps + warp; t < rp.n_tiles; t += warps) {
+  const uint32_t warps = gx * kTileWarps;
+  for (uint32_t t = bx * kTileWarps + warp; t < rp.n_tiles; t += warps) {
     const uint32_t i = 32 * t + lane;
     if (i < p.n) {
       const double2 *b2 = reinterpret_cast<const double2 *>(p.B + 8 * (uint64_t)i);
@@ -197,6 +207,10 @@ __global__ void __launch_bounds__(32 * kTileWarps) k_rollup_tiles(DevProgram p, 
   }
 }
 
+__global__ void __launch_bounds__(32 * kTileWarps) k_rollup_tiles(DevProgram p, RollupPlan rp) {
+  body_rollup_tiles(p, rp, blockIdx.x, gridDim.x);
+}
+
 inline uint32_t warp_grid(uint64_t warps, int n_sms) {
   const uint64_t blocks = (warps + 3) / 4;   // 128 threads = 4 warps per block
   return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(blocks, (uint64_t)n_sms * 32));
@@ -204,6 +218,7 @@ inline uint32_t warp_grid(uint64_t warps, int n_sms) {
 
 }  // namespace
 
+#ifndef GPA_FUSED_TU
 cudaError_t launch_vrows(const DevProgram &p, double *vbuf, int n_sms, cudaStream_t s) {
   const uint64_t total = (uint64_t)p.n;
   const uint32_t g = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((total + kVrowsThreads - 1) / kVrowsThreads,
@@ -240,5 +255,7 @@ cudaError_t launch_rollup(const DevProgram &p, const RollupPlan &rp, int n_sms, 
   *launches += (rp.n_tiles ? 1 : 0) + (rp.n_seg1 ? 1 : 0) + (rp.n_seg2 ? 1 : 0);
   return cudaGetLastError();
 }
+
+#endif  // GPA_FUSED_TU
 
 }  // namespace gpa

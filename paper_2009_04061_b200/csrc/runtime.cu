@@ -735,7 +735,7 @@ gpa_status gpa_set_patterns(gpa_program *p, const gpa_pattern *pats, uint32_t n_
   CUDA_TRY(cudaMemcpyAsync(p->pats_dev, pats, n_pat * sizeof(gpa_pattern), cudaMemcpyHostToDevice, s));
   CUDA_TRY(cudaStreamSynchronize(s));
   p->ep.n_pat = n_pat;
-  // the analyze graph bakes the pattern plan (n_pat, loop_slot, whether k_est_edges runs) into its
+  // the analyze graph bakes the pattern plan (n_pat, loop_slot) into its
   // kernel parameters: any new pattern set invalidates it
   if (p->analyze_exec) {
     cudaGraphExecDestroy(p->analyze_exec);
@@ -760,11 +760,41 @@ gpa_status gpa_estimate(gpa_program *p, void *stream) {
   return GPA_OK;
 }
 
+static gpa_status analyze_graph(gpa_program *p, uint32_t npat, void *stream);
+
 gpa_status gpa_analyze(gpa_program *p, void *stream) {
   gpa_status st = check_prog(p);
   if (st) return st;
   if (!(p->state & ST_COUNTS)) return fail(GPA_ERR_BAD_STATE, "gpa_analyze before gpa_reset_counts/gpa_ingest_samples");
   const uint32_t npat = (p->state & ST_PATTERNS) ? p->ep.n_pat : 0;
+  const bool fused = p->analyze_mode == GPA_ANALYZE_FUSED ||
+                     (p->analyze_mode == GPA_ANALYZE_AUTO && p->d.n <= GPA_FUSED_MAX_INSTR && fused_feasible(npat));
+  if (fused) {
+    if (!fused_feasible(npat)) return fail(GPA_ERR_INVALID_ARGUMENT, "fused analysis needs <= 16 patterns (%u set)", npat);
+    EstimatePlan ep = p->ep;
+    ep.n_pat = npat;
+    const cudaError_t e = launch_analyze_fused(p->d, p->rp, ep, p->n_sms, kFusedMaxCtas, (cudaStream_t)stream,
+                                               &p->launches);
+    if (e != cudaSuccess) return cuda_fail(e, "fused analysis launch");
+  } else {
+    const gpa_status gs = analyze_graph(p, npat, stream);
+    if (gs) return gs;
+  }
+  p->state |= ST_BLAMED | ST_AGGREGATED;
+  p->state = npat ? (p->state | ST_ESTIMATED) & ~ST_ADVISED : p->state & ~(ST_ESTIMATED | ST_ADVISED);
+  return GPA_OK;
+}
+
+gpa_status gpa_set_analyze_mode(gpa_program *p, int mode) {
+  gpa_status st = check_prog(p);
+  if (st) return st;
+  if (mode < GPA_ANALYZE_AUTO || mode > GPA_ANALYZE_FUSED) return fail(GPA_ERR_INVALID_ARGUMENT, "analyze mode %d unknown", mode);
+  p->analyze_mode = mode;
+  return GPA_OK;
+}
+
+// the multi-kernel analysis, captured once as a CUDA graph and replayed
+static gpa_status analyze_graph(gpa_program *p, uint32_t npat, void *stream) {
   if (!p->analyze_exec || p->analyze_npat != npat) {
     if (p->analyze_exec) {
       cudaGraphExecDestroy(p->analyze_exec);
@@ -808,8 +838,6 @@ gpa_status gpa_analyze(gpa_program *p, void *stream) {
   }
   CUDA_TRY(cudaGraphLaunch(p->analyze_exec, (cudaStream_t)stream));
   p->launches += p->analyze_launches;
-  p->state |= ST_BLAMED | ST_AGGREGATED;
-  p->state = npat ? (p->state | ST_ESTIMATED) & ~ST_ADVISED : p->state & ~(ST_ESTIMATED | ST_ADVISED);
   return GPA_OK;
 }
 

@@ -94,7 +94,8 @@ EXPORTS = ["gpa_validate_program", "gpa_workspace_size", "gpa_program_create", "
            "gpa_aggregate", "gpa_set_patterns", "gpa_estimate", "gpa_read_estimates", "gpa_get_stats",
            "gpa_view", "gpa_instr_vector", "gpa_program_info", "gpa_ingest_variant",
            "gpa_set_ingest_variant", "gpa_launch_count", "gpa_last_error", "gpa_version", "gpa_analyze",
-           "gpa_ingest_segments", "gpa_advise", "gpa_read_advice", "gpa_set_launches", "gpa_slice", "gpa_simulate"]
+           "gpa_ingest_segments", "gpa_advise", "gpa_read_advice", "gpa_set_launches", "gpa_slice", "gpa_simulate",
+           "gpa_set_analyze_mode"]
 
 _lib = None
 
@@ -118,7 +119,7 @@ def lib():
             "gpa_view": [vp, ctypes.c_int, vp, vp], "gpa_instr_vector": [vp, vp, vp],
             "gpa_program_info": [vp, vp], "gpa_ingest_variant": [vp, vp],
             "gpa_set_ingest_variant": [vp, ctypes.c_int], "gpa_launch_count": [vp, vp],
-            "gpa_analyze": [vp, vp],
+            "gpa_analyze": [vp, vp], "gpa_set_analyze_mode": [vp, ctypes.c_int],
             "gpa_ingest_segments": [vp, vp, u64, vp, vp, u32, u32, vp],
             "gpa_advise": [vp, u32, vp], "gpa_read_advice": [vp, vp, vp, vp, vp, vp],
             "gpa_set_launches": [vp, vp, vp, vp],
@@ -351,8 +352,20 @@ class Program:
         _check(lib().gpa_estimate(self.handle, self._s(stream)), "gpa_estimate")
 
     def analyze(self, stream=None):
-        """blame + aggregate + estimate (if patterns are set) replayed as one CUDA graph."""
+        """blame + aggregate + estimate (if patterns are set): one CUDA graph replay, or one fused
+        cooperative kernel for small programs (see `analyze_mode`)."""
         _check(lib().gpa_analyze(self.handle, self._s(stream)), "gpa_analyze")
+
+    ANALYZE_MODES = {"auto": 0, "graph": 1, "fused": 2}
+
+    @property
+    def analyze_mode(self) -> str:
+        return getattr(self, "_analyze_mode", "auto")
+
+    @analyze_mode.setter
+    def analyze_mode(self, mode: str):
+        _check(lib().gpa_set_analyze_mode(self.handle, self.ANALYZE_MODES[mode]), "gpa_set_analyze_mode")
+        self._analyze_mode = mode
 
     def step(self, samples, stream=None):
         """One pass of the whole hot path over one batch of device-resident records."""

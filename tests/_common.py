@@ -28,10 +28,13 @@ def run_oracle(prog, records, patterns=None, chunk=None):
     return {"C": C, "stats": stats, **b, **r, "est": est}
 
 
-def run_gpu(prog, records, patterns=None, variant=None, host=False, offset_records=0, segments=None):
+def run_gpu(prog, records, patterns=None, variant=None, host=False, offset_records=0, segments=None,
+            analyze=None):
     """records: numpy uint64 array.  offset_records: place the stream at an 8-byte (not 16-byte)
     aligned address to exercise the unaligned head.  segments: (seg_begin, seg_kernel, pc_base)
-    to ingest through gpa_ingest_segments (records grouped by kernel launch)."""
+    to ingest through gpa_ingest_segments (records grouped by kernel launch).  analyze: None runs
+    gpa_blame / gpa_aggregate / gpa_estimate one by one; "auto" / "graph" / "fused" runs gpa_analyze
+    in that mode."""
     import torch
     from paper_2009_04061_b200 import Program
     patterns = table2(prog.n_reasons) if patterns is None else patterns
@@ -54,9 +57,13 @@ def run_gpu(prog, records, patterns=None, variant=None, host=False, offset_recor
             P.ingest_segments(view, torch.from_numpy(np.asarray(seg_begin).astype(np.int64)).cuda(),
                               torch.from_numpy(np.asarray(seg_kernel).astype(np.uint32).view(np.int32)).cuda(),
                               pc_base=pc_base)
-    P.blame()
-    P.aggregate()
-    P.estimate()
+    if analyze is None:
+        P.blame()
+        P.aggregate()
+        P.estimate()
+    else:
+        P.analyze_mode = analyze
+        P.analyze()
     torch.cuda.synchronize()
     return collect(P)
 

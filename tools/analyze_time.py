@@ -1,5 +1,6 @@
 """Tuning probe: median time of the analysis graph (gpa_analyze: blame + rollup + estimate) for
-configs 2 and 3 with an alternative build of the library (`python tools/analyze_time.py lib|product [2,3,4]`)."""
+configs 2 and 3 with an alternative build of the library
+(`python tools/analyze_time.py lib|product [2,3,4] [auto|graph|fused]`)."""
 import os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
@@ -13,6 +14,7 @@ if lib_path != "product":
     G.LIB_PATH = os.path.join(ROOT, lib_path)
 from gpagen import batch
 cfgs = [int(c) for c in sys.argv[2].split(",")] if len(sys.argv) > 2 else [2, 3]
+mode = sys.argv[3] if len(sys.argv) > 3 else "auto"
 out = []
 for cfg in cfgs:
     if cfg == 4:    # the batch program; plain ingest gives the same counts as the segment ingest
@@ -23,6 +25,7 @@ for cfg in cfgs:
         recs = gpagen.config_stream(prog, cfg).device(0, {2: 10_000_000, 3: 100_000_000}[cfg])
     P = G.Program(prog)
     P.set_patterns(table2(prog.n_reasons))
+    P.analyze_mode = mode
     P.reset(); P.ingest(recs)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     ts = []
@@ -31,7 +34,7 @@ for cfg in cfgs:
         if it >= 5:
             ts.append(ev[0].elapsed_time(ev[1]))
     est = P.read_estimates_array()
-    np.save(os.path.join(ROOT, "gpurun_out", f"est_{cfg}_{os.path.basename(lib_path)}.npy"),
+    np.save(os.path.join(ROOT, "gpurun_out", f"est_{cfg}_{os.path.basename(lib_path)}_{mode}.npy"),
             np.stack([est["speedup"], est["M"]]))
     out.append(f"cfg{cfg} analyze {np.median(ts) * 1e3:.1f} us")
-print(lib_path + ": " + "  ".join(out))
+print(lib_path + f" [{mode}]: " + "  ".join(out))

@@ -6,7 +6,7 @@ for i in 1 2 3; do
 done
 python - "$@" <<'PY'
 import sys, numpy as np, os
-a=np.load("gpurun_out/counts_product.npy")
+a=np.load("gpurun_out/counts3_product.npy")
 for v in sys.argv[1:]:
-    b=np.load("gpurun_out/counts_"+os.path.basename(v)+".npy"); print(v, "equal", np.array_equal(a,b))
+    b=np.load("gpurun_out/counts3_"+os.path.basename(v)+".npy"); print(v, "equal", np.array_equal(a,b))
 PY
