@@ -309,15 +309,14 @@ gpa_status gpa_analyze(gpa_program *prog, void *stream);
 
 /* How gpa_analyze runs the analysis.  GPA_ANALYZE_GRAPH: the CUDA graph of per-step kernels
  * above.  GPA_ANALYZE_FUSED: one cooperative kernel running the same device code phase by phase
- * with grid-wide barriers between dependent phases (no launch gaps; for small programs, where the
- * graph is bound by launch latency; needs <= 16 patterns, else gpa_analyze returns
- * GPA_ERR_INVALID_ARGUMENT).  GPA_ANALYZE_AUTO (default): fused for programs of at most
- * GPA_FUSED_MAX_INSTR instructions and <= 16 patterns, the graph otherwise.  Both give
- * bit-identical results.  Errors: GPA_ERR_INVALID_ARGUMENT for an unknown mode. */
+ * with grid-wide barriers between dependent phases (no launch gaps; both give bit-identical
+ * results).  GPA_ANALYZE_AUTO (default) is the graph: on B200 the fused kernel measured slower at
+ * every program size tried (config 2: 40 vs 53-90 us), because the graph runs the
+ * independent branches (def reduction | estimate sums) side by side while every CTA of the fused
+ * kernel runs them one after the other.  Errors: GPA_ERR_INVALID_ARGUMENT for an unknown mode. */
 #define GPA_ANALYZE_AUTO 0
 #define GPA_ANALYZE_GRAPH 1
 #define GPA_ANALYZE_FUSED 2
-#define GPA_FUSED_MAX_INSTR 16384u
 gpa_status gpa_set_analyze_mode(gpa_program *prog, int mode);
 
 /* Copy the estimates to host memory h_out[n_kernels * n_patterns] (synchronizes). */

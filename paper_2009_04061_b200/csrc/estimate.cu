@@ -5,8 +5,8 @@
 //   k_est_tiles   a CTA per tile of 32 use rows, a warp per pattern group: the matched samples
 //                 of each in-edge (blamed at the def, scope loop = lca(def, use)), edge-parallel,
 //                 and of each row j itself (self / pass-through columns, scope loop = loop of j);
-//                 row totals mrow[q][j] and, for loop-scoped patterns, the per-item values
-//                 (edges and instructions) of the loop reduction.
+//                 row totals summed per function run of the tile (fpart) and, for loop-scoped
+//                 patterns, the per-item values (edges and instructions) of the loop reduction.
 //   k_segsum      one warp per (segment, pattern): fixed-order strided sums + xor-shuffle tree
 //                 (deterministic).  Stage 1: loop-exclusive (by scope-loop item lists) and
 //                 function sums; stage 2: loop-inclusive (preorder subtree ranges) and kernel sums.
@@ -33,11 +33,13 @@ constexpr int kEstGroup = GPA_EST_GROUP;
 // reasons (X) and its loop are staged in shared memory; (2) lanes over the tile's in-edges
 // (coalesced edge fields, one EdgeInfo per edge): the matched samples of every pattern of the group,
 // staged in shared memory, and written out as the per-edge item values of the loop-scoped patterns
-// (the mval edge part); (3) lane = row: the
-// row sum over its edges in CSR order from shared memory, plus the row's own part -- the order of
-// the sequential definition, so mrow is bit-identical to a row-by-row evaluation (an edge without a
-// candidate reason adds +0.0 to a non-negative sum: no change).  Tiles with more than kEstTileEdges
-// edges take the row-per-lane loop.
+// (the mval edge part); (3) lane = row: the row sum over its edges in CSR order from shared memory,
+// plus the row's own part -- the order of the sequential definition, so a row total is
+// bit-identical to a row-by-row evaluation (an edge without a candidate reason adds +0.0 to a
+// non-negative sum: no change); (4) the row totals of each function run of the tile are summed by a
+// segmented shuffle scan and written as one partial per run (k_segsum adds a function's runs in
+// program order), instead of a per-row array.  Tiles with more than kEstTileEdges edges take the
+// row-per-lane loop for (2)-(3).
 constexpr uint32_t kEstTileEdges = 128;
 constexpr uint32_t kEstWarps = 4;   // pattern groups per CTA (kPatternsMax / kEstGroup at most)
 struct EstSmem {
@@ -127,22 +129,31 @@ __device__ __forceinline__ void body_est_tiles(DevProgram p, EstimatePlan ep, ui
         }
       }
     }
-    if (in) {
-      const uint32_t cls_j = p.opclass[j], flags_j = p.iflags[j], self_j = p.selfm[j];
+    // (4) the row totals (edges + own part) summed per function run of the tile: a segmented
+    //     inclusive scan over the lanes (fixed shuffle order), the run's last lane writes its partial
+    const uint32_t fm = ep.tile_fmask[t];
+    const uint32_t run_head = 31 - __clz(fm & (0xffffffffu >> (31 - lane)));   // first lane of my run
+    const bool run_tail = lane == 31 || ((fm >> (lane + 1)) & 1u);
+    const uint64_t run_id = ep.tile_frun_ptr[t] + __popc(fm & (0xffffffffu >> (31 - lane))) - 1;
+    const uint32_t cls_j = in ? p.opclass[j] : 0u, flags_j = in ? p.iflags[j] : 0u, self_j = in ? p.selfm[j] : 0u;
 #pragma unroll
-      for (int k = 0; k < kEstGroup; ++k) {
-        if ((uint32_t)k >= nq) break;
-        const uint32_t qi = q0 + k;
-        const gpa_pattern &q = sp[qi];
-        if (q.model == 5) {
-          ep.mrow[(uint64_t)qi * p.n + j] = 0.0;
-          continue;
-        }
+    for (int k = 0; k < kEstGroup; ++k) {
+      if ((uint32_t)k >= nq) break;
+      const uint32_t qi = q0 + k;
+      const gpa_pattern &q = sp[qi];
+      double tot = 0.0;
+      if (in && q.model != 5) {
         const double mi = instr_match(q, p.R, row, q.sample_class ? XL : XA, cls_j, flags_j, self_j, loop_j);
         const int slot = sslot[qi];
         if (slot >= 0) ep.mval[(uint64_t)slot * stride_items + p.E + j] = mi;
-        ep.mrow[(uint64_t)qi * p.n + j] = __dadd_rn(sum[k], mi);
+        tot = __dadd_rn(sum[k], mi);
       }
+#pragma unroll
+      for (uint32_t off = 1; off < 32; off <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, tot, off);
+        if (lane >= off && lane - off >= run_head) tot = __dadd_rn(tot, y);
+      }
+      if (run_tail) ep.fpart[(uint64_t)qi * ep.n_fruns + run_id] = tot;
     }
     __syncwarp();
   }
@@ -323,7 +334,7 @@ inline void make_seg_launches(const DevProgram &p, const EstimatePlan &ep, SegLa
   a.n_pat = ep.n_pat;
   a.n_fam = 2;
   a.fam[0] = SegFamily{ep.mval, (uint64_t)p.E + p.n, ep.loop_items, ep.loop_item_ptr, nullptr, p.n_loops, ep.lM_excl, {}};
-  a.fam[1] = SegFamily{ep.mrow, p.n, nullptr, p.func_begin, nullptr, p.n_funcs, ep.fM, {}};
+  a.fam[1] = SegFamily{ep.fpart, ep.n_fruns, nullptr, ep.frun_begin, nullptr, p.n_funcs, ep.fM, {}};
   for (int q = 0; q < kPatternsMax; ++q) {
     a.fam[0].vrow[q] = ep.loop_slot[q];
     a.fam[1].vrow[q] = q < (int)ep.n_pat ? q : -1;

@@ -64,13 +64,17 @@ def test_fused_equals_graph_and_oracle(case):
     assert g_fused["program"].analyze_mode == "fused"
 
 
-def test_auto_mode_is_fused_for_small_programs():
+def test_fused_is_one_launch_and_auto_is_the_graph():
     prog, recs = CASES["rodinia"]()
-    g = run_gpu(prog, recs, analyze="auto")
+    g = run_gpu(prog, recs, analyze="fused")
     P = g["program"]
     before = P.launches
     P.analyze()
     assert P.launches - before == 1          # one cooperative launch
+    P.analyze_mode = "auto"
+    before = P.launches
+    P.analyze()
+    assert P.launches - before > 1           # the graph of per-step kernels
 
 
 def test_fused_many_ctas_config3_program():
@@ -96,14 +100,3 @@ def test_fused_estimate_edge_cases():
     g = run_gpu(prog, recs, pats, analyze="fused")
     compare(g, run_oracle(prog, recs, pats), rel=REL)
     assert_same_bits(g, run_gpu(prog, recs, pats, analyze="graph"))
-
-
-def test_auto_mode_uses_the_graph_for_large_programs():
-    prog = gp.config_program(3)           # 50,000 instructions > GPA_FUSED_MAX_INSTR
-    recs = config_stream(prog, 3).host(0, 500_000)
-    g = run_gpu(prog, recs, analyze="auto")
-    P = g["program"]
-    before = P.launches
-    P.analyze()
-    assert P.launches - before > 1
-    compare(g, run_oracle(prog, recs), rel=REL)
