@@ -156,7 +156,8 @@ def large_config(args, world, prog, cfg, n_per):
     what = f"BASELINE config {cfg}" if cfg != 6 else "PeleC-scale (P:708-714, beyond BASELINE's configs)"
     return {"workload": f"{args.workload}: {what} program ({prog.n_instr} instrs, {prog.n_edges} edges, "
                         f"{prog.n_loops} loops), {n_per} records per GPU"
-                        + (f" (config 5's 10^10-record stream sharded as {n_per} per GPU)" if world > 1 else ""),
+                        + (f" (the first {n_per * world} records of config 5's 10^10-record stream, {n_per} per GPU)"
+                           if world > 1 else ""),
             "records_per_gpu": n_per, "records_total": n_per * world,
             "l2": "inputs larger than L2 (8 B/record)" if n_per * 8 > 126 << 20 else "inputs smaller than L2",
             "parallelism": f"dp{world} (sample-stream shards + NCCL all-reduce of counts)"}

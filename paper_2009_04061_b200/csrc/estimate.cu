@@ -2,11 +2,12 @@
 // P:457-460) and the estimators of §5.2: Eq. 2, Eq. 3, Eq. 4
 // (P:496-503), Eq. 5 (Q16), Eqs. 6-10 (Q18), per kernel.
 //
-//   k_est_tiles   a CTA per tile of 32 use rows, a warp per pattern group: the matched samples
-//                 of each in-edge (blamed at the def, scope loop = lca(def, use)), edge-parallel,
-//                 and of each row j itself (self / pass-through columns, scope loop = loop of j);
-//                 row totals summed per function run of the tile (fpart) and, for loop-scoped
-//                 patterns, the per-item values (edges and instructions) of the loop reduction.
+//   k_est_rows    one thread per (use row j, pattern group): the matched samples of each
+//                 in-edge (blamed at the def, scope loop = lca(def, use)) and of j itself
+//                 (self / pass-through columns, scope loop = loop of j); row totals summed per
+//                 function run of the 32-row tile (fpart) and the loop-scoped patterns' per-
+//                 instruction item values.
+//   k_est_edges   per-edge item values of the loop-scoped patterns (edge-parallel).
 //   k_segsum      one warp per (segment, pattern): fixed-order strided sums + xor-shuffle tree
 //                 (deterministic).  Stage 1: loop-exclusive (by scope-loop item lists) and
 //                 function sums; stage 2: loop-inclusive (preorder subtree ranges) and kernel sums.
@@ -28,33 +29,22 @@ namespace {
 #endif
 constexpr int kEstGroup = GPA_EST_GROUP;
 
-// Warp-cooperative form (the blame tiles' pattern): a CTA takes a tile of 32 consecutive use rows,
-// one warp per pattern group.  (1) lane = row: the row's all / latency samples of the dependency
-// reasons (X) and its loop are staged in shared memory; (2) lanes over the tile's in-edges
-// (coalesced edge fields, one EdgeInfo per edge): the matched samples of every pattern of the group,
-// staged in shared memory, and written out as the per-edge item values of the loop-scoped patterns
-// (the mval edge part); (3) lane = row: the row sum over its edges in CSR order from shared memory,
-// plus the row's own part -- the order of the sequential definition, so a row total is
-// bit-identical to a row-by-row evaluation (an edge without a candidate reason adds +0.0 to a
-// non-negative sum: no change); (4) the row totals of each function run of the tile are summed by a
-// segmented shuffle scan and written as one partial per run (k_segsum adds a function's runs in
-// program order), instead of a per-row array.  Tiles with more than kEstTileEdges edges take the
-// row-per-lane loop for (2)-(3).
-constexpr uint32_t kEstTileEdges = 128;
+// one thread per (use row j, group of kEstGroup patterns): the row's counts and in-edges are read
+// once per group and every pattern of the group is evaluated from registers; consecutive threads
+// take consecutive rows (coalesced).  Per (j, pattern) the sum runs over the row's edges in CSR
+// order, then adds j's own part -- the oracle's order.  A CTA = one warp per pattern group over the
+// same 32 rows (a tile): the pattern fields are uniform in a warp, and a row's C entries and edges
+// are fetched from DRAM once and served from L1 to the other groups' warps.  The row totals of each
+// function run of the tile are summed by a segmented shuffle scan and written as one partial per
+// run (k_segsum adds a function's runs in program order) instead of a per-row array.
+// (A warp-cooperative edge-parallel form, the blame tiles' pattern, measured slower on config 4:
+// 1.17 ms against 0.86 ms for this kernel plus k_est_edges -- its shared-memory staging cut the
+// resident warps of this latency-bound loop.)
 constexpr uint32_t kEstWarps = 4;   // pattern groups per CTA (kPatternsMax / kEstGroup at most)
-struct EstSmem {
-  double sv[kEstWarps][kEstGroup][kEstTileEdges];
-  double sX[kEstWarps][32][8];   // per row: XA[1..3], XL[1..3]
-  int32_t sloop[kEstWarps][32];
-};
-__device__ __forceinline__ void body_est_tiles(DevProgram p, EstimatePlan ep, uint32_t bx, uint32_t gx) {
+__device__ __forceinline__ void body_est_rows(DevProgram p, EstimatePlan ep, uint32_t bx, uint32_t gx) {
   pdl_wait();
   __shared__ gpa_pattern sp[kPatternsMax];
   __shared__ int8_t sslot[kPatternsMax];
-  EstSmem &S = dyn_smem<EstSmem>();
-  auto &sv = S.sv;
-  auto &sX = S.sX;
-  auto &sloop = S.sloop;
   for (uint32_t q = threadIdx.x; q < ep.n_pat; q += blockDim.x) {
     sp[q] = ep.pats[q];
     sslot[q] = ep.loop_slot[q];
@@ -62,79 +52,43 @@ __device__ __forceinline__ void body_est_tiles(DevProgram p, EstimatePlan ep, ui
   __syncthreads();
   const uint64_t stride_items = (uint64_t)p.E + p.n;
   const uint32_t grp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (grp * kEstGroup >= ep.n_pat) return;   // spare warps (fewer pattern groups than warps)
+  if (grp * kEstGroup >= ep.n_pat) return;   // spare warps of a wider CTA (the fused analysis kernel)
   const uint32_t q0 = grp * kEstGroup;
   const uint32_t nq = min((uint32_t)kEstGroup, ep.n_pat - q0);
-  const uint32_t n_tiles = (p.n + 31) / 32;
-  double(*v_)[kEstTileEdges] = sv[grp];
-  double(*X_)[8] = sX[grp];
-  int32_t *loop_ = sloop[grp];
-  for (uint32_t t = bx; t < n_tiles; t += gx) {
-    const uint32_t j0 = 32 * t, j = j0 + lane;
+  for (uint32_t t = bx; 32 * t < p.n; t += gx) {
+    const uint32_t j = 32 * t + lane;
     const bool in = j < p.n;
-    const uint32_t E0 = p.row_ptr[j0], E1 = p.row_ptr[min(j0 + 32, p.n)];
-    // (1) lane = row
-    double XA[4], XL[4];
-    const uint64_t *row = p.C + (uint64_t)(in ? j : j0) * 2 * p.R;
+    const uint64_t *row = p.C + (uint64_t)(in ? j : 0u) * 2 * p.R;
+    double XA[4], XL[4];   // all / latency samples of the dependency reasons at j
 #pragma unroll
     for (int r = 1; r <= 3; ++r) {
       const uint64_t lat = in ? row[p.R + r] : 0ull;
       XL[r] = (double)lat;
       XA[r] = (double)(lat + (in ? row[r] : 0ull));
-      X_[lane][r - 1] = XA[r];
-      X_[lane][r + 2] = XL[r];
     }
+    const uint32_t e0 = in ? p.row_ptr[j] : 0u, e1 = in ? p.row_ptr[j + 1] : 0u;
     const int32_t loop_j = in ? p.loop_id[j] : -1;
-    loop_[lane] = loop_j;
     double sum[kEstGroup];
 #pragma unroll
     for (int k = 0; k < kEstGroup; ++k) sum[k] = 0.0;
-    if (E1 - E0 > kEstTileEdges) {   // rare: a long tile -- lane per row, CSR order
-      if (in) {
-        for (uint32_t e = p.row_ptr[j]; e < p.row_ptr[j + 1]; ++e) {
-          const EdgeInfo x = edge_info(p, e, loop_j);
+    for (uint32_t e = e0; e < e1; ++e) {   // loads only: per-edge values go to k_est_edges
+      const EdgeInfo x = edge_info(p, e, loop_j);
+      if (!x.m) continue;                  // no candidate reason: adds 0 to every pattern
 #pragma unroll
-          for (int k = 0; k < kEstGroup; ++k) {
-            if ((uint32_t)k >= nq) break;
-            const gpa_pattern &q = sp[q0 + k];
-            const double v = q.model == 5 ? 0.0 : edge_match(q, x, q.sample_class ? XL : XA);
-            sum[k] = __dadd_rn(sum[k], v);
-            if (sslot[q0 + k] >= 0) ep.mval[(uint64_t)sslot[q0 + k] * stride_items + e] = v;
-          }
-        }
-      }
-    } else {
-      __syncwarp();
-      // (2) lanes over the tile's edges
-      for (uint32_t e = E0 + lane; e < E1; e += 32) {
-        const uint32_t u = p.edge_use[e] - j0;
-        const EdgeInfo x = edge_info(p, e, loop_[u]);
-        const double xa[4] = {0.0, X_[u][0], X_[u][1], X_[u][2]}, xl[4] = {0.0, X_[u][3], X_[u][4], X_[u][5]};
-#pragma unroll
-        for (int k = 0; k < kEstGroup; ++k) {
-          if ((uint32_t)k >= nq) break;
-          const gpa_pattern &q = sp[q0 + k];
-          const double v = q.model == 5 ? 0.0 : edge_match(q, x, q.sample_class ? xl : xa);
-          v_[k][e - E0] = v;
-          if (sslot[q0 + k] >= 0) ep.mval[(uint64_t)sslot[q0 + k] * stride_items + e] = v;
-        }
-      }
-      __syncwarp();
-      // (3) lane = row: CSR-order sums from shared memory
-      if (in) {
-        const uint32_t e0 = p.row_ptr[j] - E0, e1 = p.row_ptr[j + 1] - E0;
-        for (uint32_t k2 = e0; k2 < e1; ++k2) {
-#pragma unroll
-          for (int k = 0; k < kEstGroup; ++k) sum[k] = __dadd_rn(sum[k], v_[k][k2]);   // unused groups: 0 + 0
-        }
+      for (int k = 0; k < kEstGroup; ++k) {
+        if ((uint32_t)k >= nq) break;
+        const gpa_pattern &q = sp[q0 + k];
+        if (q.model == 5) continue;
+        sum[k] = __dadd_rn(sum[k], edge_match(q, x, q.sample_class ? XL : XA));
       }
     }
-    // (4) the row totals (edges + own part) summed per function run of the tile: a segmented
-    //     inclusive scan over the lanes (fixed shuffle order), the run's last lane writes its partial
+    // row totals summed per function run of the tile: a segmented inclusive scan over the lanes
+    // (fixed shuffle order); the run's last lane writes its partial
     const uint32_t fm = ep.tile_fmask[t];
-    const uint32_t run_head = 31 - __clz(fm & (0xffffffffu >> (31 - lane)));   // first lane of my run
+    const uint32_t upto = 0xffffffffu >> (31 - lane);                      // bits 0..lane
+    const uint32_t run_head = 31 - __clz(fm & upto);                       // first lane of my run
     const bool run_tail = lane == 31 || ((fm >> (lane + 1)) & 1u);
-    const uint64_t run_id = ep.tile_frun_ptr[t] + __popc(fm & (0xffffffffu >> (31 - lane))) - 1;
+    const uint64_t run_id = ep.tile_frun_ptr[t] + __popc(fm & upto) - 1;
     const uint32_t cls_j = in ? p.opclass[j] : 0u, flags_j = in ? p.iflags[j] : 0u, self_j = in ? p.selfm[j] : 0u;
 #pragma unroll
     for (int k = 0; k < kEstGroup; ++k) {
@@ -155,13 +109,54 @@ __device__ __forceinline__ void body_est_tiles(DevProgram p, EstimatePlan ep, ui
       }
       if (run_tail) ep.fpart[(uint64_t)qi * ep.n_fruns + run_id] = tot;
     }
-    __syncwarp();
   }
 }
 
-__global__ void __launch_bounds__(32 * kEstWarps) k_est_tiles(DevProgram p, EstimatePlan ep) {
-  body_est_tiles(p, ep, blockIdx.x, gridDim.x);
+__global__ void k_est_rows(DevProgram p, EstimatePlan ep) {
+  body_est_rows(p, ep, blockIdx.x, gridDim.x);
 }
+
+// per-edge matched samples of the loop-scoped patterns (mval[slot][e]), edge-parallel and
+// coalesced; the same arithmetic as k_est_rows, so the item values and the row sums agree
+__device__ __forceinline__ void body_est_edges(DevProgram p, EstimatePlan ep, uint32_t bx, uint32_t gx) {
+  pdl_wait();
+  __shared__ gpa_pattern sp[kPatternsMax];
+  __shared__ int8_t sslot[kPatternsMax];
+  __shared__ uint32_t slot_q[kPatternsMax], n_slot_q;
+  if (threadIdx.x == 0) {
+    uint32_t c = 0;
+    for (uint32_t q = 0; q < ep.n_pat; ++q)
+      if (ep.loop_slot[q] >= 0 && ep.pats[q].model != 5) slot_q[c++] = q;
+    n_slot_q = c;
+  }
+  for (uint32_t q = threadIdx.x; q < ep.n_pat; q += blockDim.x) {
+    sp[q] = ep.pats[q];
+    sslot[q] = ep.loop_slot[q];
+  }
+  __syncthreads();
+  const uint64_t stride_items = (uint64_t)p.E + p.n;
+  for (uint32_t e = bx * blockDim.x + threadIdx.x; e < p.E; e += gx * blockDim.x) {
+    const uint32_t j = p.edge_use[e];
+    const uint64_t *row = p.C + (uint64_t)j * 2 * p.R;
+    double XA[4], XL[4];
+#pragma unroll
+    for (int r = 1; r <= 3; ++r) {
+      const uint64_t lat = row[p.R + r];
+      XL[r] = (double)lat;
+      XA[r] = (double)(lat + row[r]);
+    }
+    const EdgeInfo x = edge_info(p, e, p.loop_id[j]);
+    for (uint32_t k = 0; k < n_slot_q; ++k) {
+      const gpa_pattern &q = sp[slot_q[k]];
+      ep.mval[(uint64_t)sslot[slot_q[k]] * stride_items + e] = edge_match(q, x, q.sample_class ? XL : XA);
+    }
+  }
+}
+
+__global__ void k_est_edges(DevProgram p, EstimatePlan ep) {
+  body_est_edges(p, ep, blockIdx.x, gridDim.x);
+}
+
 
 struct SegFamily {
   const double *values;     // value row v starts at values + v * row_stride
@@ -359,7 +354,15 @@ cudaError_t launch_estimate_sums(const DevProgram &p, const EstimatePlan &ep, in
                                  uint64_t *launches) {
   const uint32_t n_groups = (ep.n_pat + kEstGroup - 1) / kEstGroup;   // <= 8: a warp per group
   const uint32_t g = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(((uint64_t)p.n + 31) / 32, (uint64_t)n_sms * 64));
-  k_est_tiles<<<g, 32 * n_groups, sizeof(EstSmem), s>>>(p, ep);
+  k_est_rows<<<g, 32 * n_groups, 0, s>>>(p, ep);
+  bool any_slot = false;
+  for (uint32_t q = 0; q < ep.n_pat; ++q) any_slot |= ep.loop_slot[q] >= 0;
+  if (any_slot && p.E) {
+    const uint32_t ge = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(((uint64_t)p.E + 255) / 256, (uint64_t)n_sms * 16));
+    const cudaError_t e = launch_pdl(p.n, k_est_edges, ge, 256, 0, s, p, ep);
+    if (e != cudaSuccess) return e;
+    *launches += 1;
+  }
   SegLaunch a, b;
   make_seg_launches(p, ep, a, b);
   const uint64_t w1 = std::max<uint64_t>((uint64_t)p.n_loops, p.n_funcs) * ep.n_pat;

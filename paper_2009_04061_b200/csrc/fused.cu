@@ -9,7 +9,7 @@
 //
 //   1  summaries (A_i, L_i)
 //   2  blame tiles (rules 1-3, Eq. 1 shares, self flags)
-//   3  def reduction (B)            | estimate tiles (matched samples per item)
+//   3  def reduction (B)            | estimate rows / edges (matched samples per item)
 //   4  rollup tiles                 | segment sums stage 1 (loops exclusive, functions)
 //   5  rollup segments stage 1      | segment sums stage 2 (loops inclusive, kernels)
 //   6  rollup segments stage 2
@@ -47,7 +47,7 @@ __device__ __forceinline__ void fmark(int i) {
 #endif
 
 __global__ void __launch_bounds__(kFusedThreads) k_analyze_fused(DevProgram p, RollupPlan rp, EstimatePlan ep,
-                                                                 SegLaunch s1, SegLaunch s2) {
+                                                                 SegLaunch s1, SegLaunch s2, uint32_t any_slot) {
   cooperative_groups::grid_group grid = cooperative_groups::this_grid();
   const uint32_t bx = blockIdx.x, gx = gridDim.x, nv = 2 * p.ncol;
   const bool est = ep.n_pat != 0;
@@ -61,7 +61,10 @@ __global__ void __launch_bounds__(kFusedThreads) k_analyze_fused(DevProgram p, R
   grid.sync();
   FMARK(4);
   body_def_tiles(p, bx, gx);
-  if (est) body_est_tiles(p, ep, bx, gx);
+  if (est) {
+    body_est_rows(p, ep, bx, gx);
+    if (any_slot) body_est_edges(p, ep, bx, gx);
+  }
   FMARK(5);
   grid.sync();
   FMARK(6);
@@ -99,7 +102,7 @@ bool fused_feasible(uint32_t n_pat) { return (n_pat + kEstGroup - 1) / kEstGroup
 // the next phase's first)
 size_t fused_smem_bytes(const DevProgram &p) {
   const size_t roll = (size_t)kTileWarps * 32 * p.ncol * sizeof(double2) + (size_t)kTileWarps * 64 * sizeof(uint64_t);
-  return std::max({roll, sizeof(BlameSmem), sizeof(DefSmem), sizeof(EstSmem)});
+  return std::max({roll, sizeof(BlameSmem), sizeof(DefSmem)});
 }
 
 cudaError_t launch_analyze_fused(const DevProgram &p, const RollupPlan &rp, const EstimatePlan &ep, int n_sms,
@@ -122,7 +125,9 @@ cudaError_t launch_analyze_fused(const DevProgram &p, const RollupPlan &rp, cons
   DevProgram pa = p;
   RollupPlan ra = rp;
   EstimatePlan ea = ep;
-  void *args[] = {&pa, &ra, &ea, &s1, &s2};
+  uint32_t any_slot = 0;
+  for (uint32_t q = 0; q < ep.n_pat; ++q) any_slot |= ep.loop_slot[q] >= 0 && p.E ? 1u : 0u;
+  void *args[] = {&pa, &ra, &ea, &s1, &s2, &any_slot};
   e = cudaLaunchCooperativeKernel((const void *)k_analyze_fused, dim3(grid), dim3(kFusedThreads), args, smem, s);
   *launches += 1;
   return e;

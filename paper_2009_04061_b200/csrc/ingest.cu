@@ -210,13 +210,27 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
       "r"(parity), "r"(1000000u)   // suspend-time hint (ns): park the warp instead of spinning
       : "memory");
 }
+#ifndef GPA_SPIN_RELAXED
+#define GPA_SPIN_RELAXED 0
+#endif
+// wait until *ctr >= target (a counter other CTAs advance with red.release.gpu).  An ld.acquire.gpu
+// per poll compiles to a load plus an L1 invalidation (CCTL.IVALL, 16 M per 10^9 records in round
+// 1's ncu profile); polling with relaxed loads and one acquire fence after the wait
+// (GPA_SPIN_RELAXED=1) measured slower on config 3 (2.22 -> 2.42 ms).
 __device__ __forceinline__ void spin_until(const unsigned int *ctr, unsigned int target) {
   while (true) {
     unsigned int v;
+#if GPA_SPIN_RELAXED
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+#else
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+#endif
     if (v >= target) break;
     __nanosleep(32);
   }
+#if GPA_SPIN_RELAXED
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#endif
 }
 
 #ifdef GPA_PART_TIMING
