@@ -363,6 +363,12 @@ __global__ void __launch_bounds__(32 * kDefWarps) k_def_tiles(DevProgram p) {
   body_def_tiles(p, blockIdx.x, gridDim.x);
 }
 
+// the thread-per-def form, for large programs (launch_def_reduce)
+__global__ void k_def_rows(DevProgram p) {
+  pdl_wait();
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += gridDim.x * blockDim.x) def_reduce_one(p, i);
+}
+
 inline uint32_t grid_for(uint64_t items, uint32_t threads, int n_sms) {
   return (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((items + threads - 1) / threads, (uint64_t)n_sms * 16));
 }
@@ -393,10 +399,18 @@ cudaError_t launch_blame_rows(const DevProgram &p, int n_sms, cudaStream_t s, ui
 
 // def-side reduction (rows a5-a6): B, read by the rollup only
 cudaError_t launch_def_reduce(const DevProgram &p, int n_sms, cudaStream_t s, uint64_t *launches) {
-  const uint32_t tiles = (p.n + 31) / 32;
-  const uint32_t g = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((tiles + kDefWarps - 1) / kDefWarps,
-                                                                        (uint64_t)n_sms * 16));
-  const cudaError_t e = launch_pdl(p.n, k_def_tiles, g, 32 * kDefWarps, sizeof(DefSmem), s, p);
+  // the warp-cooperative tiles for programs below kPdlMaxInstr instructions (config 3's analysis
+  // 78 -> 74 us); on config 4 their 25 KB of staging per CTA slowed the estimate branch running
+  // beside them (analysis 2.21 -> 2.37 ms), so large programs keep a thread per def
+  if (p.n < kPdlMaxInstr) {
+    const uint32_t tiles = (p.n + 31) / 32;
+    const uint32_t g = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((tiles + kDefWarps - 1) / kDefWarps,
+                                                                          (uint64_t)n_sms * 16));
+    const cudaError_t e = launch_pdl(p.n, k_def_tiles, g, 32 * kDefWarps, sizeof(DefSmem), s, p);
+    *launches += 1;
+    return e;
+  }
+  const cudaError_t e = launch_pdl(p.n, k_def_rows, grid_for(p.n, 128, n_sms), 128, 0, s, p);
   *launches += 1;
   return e;
 }

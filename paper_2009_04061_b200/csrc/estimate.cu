@@ -4,9 +4,8 @@
 //
 //   k_est_rows    one thread per (use row j, pattern group): the matched samples of each
 //                 in-edge (blamed at the def, scope loop = lca(def, use)) and of j itself
-//                 (self / pass-through columns, scope loop = loop of j); row totals summed per
-//                 function run of the 32-row tile (fpart) and the loop-scoped patterns' per-
-//                 instruction item values.
+//                 (self / pass-through columns, scope loop = loop of j); row totals mrow[q][j]
+//                 and the loop-scoped patterns' per-instruction item values.
 //   k_est_edges   per-edge item values of the loop-scoped patterns (edge-parallel).
 //   k_segsum      one warp per (segment, pattern): fixed-order strided sums + xor-shuffle tree
 //                 (deterministic).  Stage 1: loop-exclusive (by scope-loop item lists) and
@@ -29,17 +28,13 @@ namespace {
 #endif
 constexpr int kEstGroup = GPA_EST_GROUP;
 
-// one thread per (use row j, group of kEstGroup patterns): the row's counts and in-edges are read
-// once per group and every pattern of the group is evaluated from registers; consecutive threads
-// take consecutive rows (coalesced).  Per (j, pattern) the sum runs over the row's edges in CSR
-// order, then adds j's own part -- the oracle's order.  A CTA = one warp per pattern group over the
-// same 32 rows (a tile): the pattern fields are uniform in a warp, and a row's C entries and edges
-// are fetched from DRAM once and served from L1 to the other groups' warps.  The row totals of each
-// function run of the tile are summed by a segmented shuffle scan and written as one partial per
-// run (k_segsum adds a function's runs in program order) instead of a per-row array.
-// (A warp-cooperative edge-parallel form, the blame tiles' pattern, measured slower on config 4:
-// 1.17 ms against 0.86 ms for this kernel plus k_est_edges -- its shared-memory staging cut the
-// resident warps of this latency-bound loop.)
+// A CTA = one warp per pattern group over the same 32 rows (a tile): the pattern fields are uniform
+// in a warp, and a row's C entries and edges are fetched from DRAM once and served from L1 to the
+// other groups' warps.  Measured and dropped: a warp-cooperative edge-parallel form
+// (the blame tiles' pattern; config 4: 1.17 ms against 0.86 ms for this kernel plus k_est_edges --
+// its shared-memory staging cut the resident warps of this latency-bound loop) and summing the row
+// totals per function run of the tile with a shuffle scan instead of storing them per row (config
+// 4's analysis 2.37 -> 2.49 ms, config 3's 74 -> 76 us).
 constexpr uint32_t kEstWarps = 4;   // pattern groups per CTA (kPatternsMax / kEstGroup at most)
 __device__ __forceinline__ void body_est_rows(DevProgram p, EstimatePlan ep, uint32_t bx, uint32_t gx) {
   pdl_wait();
@@ -82,13 +77,6 @@ __device__ __forceinline__ void body_est_rows(DevProgram p, EstimatePlan ep, uin
         sum[k] = __dadd_rn(sum[k], edge_match(q, x, q.sample_class ? XL : XA));
       }
     }
-    // row totals summed per function run of the tile: a segmented inclusive scan over the lanes
-    // (fixed shuffle order); the run's last lane writes its partial
-    const uint32_t fm = ep.tile_fmask[t];
-    const uint32_t upto = 0xffffffffu >> (31 - lane);                      // bits 0..lane
-    const uint32_t run_head = 31 - __clz(fm & upto);                       // first lane of my run
-    const bool run_tail = lane == 31 || ((fm >> (lane + 1)) & 1u);
-    const uint64_t run_id = ep.tile_frun_ptr[t] + __popc(fm & upto) - 1;
     const uint32_t cls_j = in ? p.opclass[j] : 0u, flags_j = in ? p.iflags[j] : 0u, self_j = in ? p.selfm[j] : 0u;
 #pragma unroll
     for (int k = 0; k < kEstGroup; ++k) {
@@ -102,12 +90,7 @@ __device__ __forceinline__ void body_est_rows(DevProgram p, EstimatePlan ep, uin
         if (slot >= 0) ep.mval[(uint64_t)slot * stride_items + p.E + j] = mi;
         tot = __dadd_rn(sum[k], mi);
       }
-#pragma unroll
-      for (uint32_t off = 1; off < 32; off <<= 1) {
-        const double y = __shfl_up_sync(0xffffffffu, tot, off);
-        if (lane >= off && lane - off >= run_head) tot = __dadd_rn(tot, y);
-      }
-      if (run_tail) ep.fpart[(uint64_t)qi * ep.n_fruns + run_id] = tot;
+      if (in) ep.mrow[(uint64_t)qi * p.n + j] = tot;
     }
   }
 }
@@ -329,7 +312,7 @@ inline void make_seg_launches(const DevProgram &p, const EstimatePlan &ep, SegLa
   a.n_pat = ep.n_pat;
   a.n_fam = 2;
   a.fam[0] = SegFamily{ep.mval, (uint64_t)p.E + p.n, ep.loop_items, ep.loop_item_ptr, nullptr, p.n_loops, ep.lM_excl, {}};
-  a.fam[1] = SegFamily{ep.fpart, ep.n_fruns, nullptr, ep.frun_begin, nullptr, p.n_funcs, ep.fM, {}};
+  a.fam[1] = SegFamily{ep.mrow, p.n, nullptr, p.func_begin, nullptr, p.n_funcs, ep.fM, {}};
   for (int q = 0; q < kPatternsMax; ++q) {
     a.fam[0].vrow[q] = ep.loop_slot[q];
     a.fam[1].vrow[q] = q < (int)ep.n_pat ? q : -1;

@@ -152,11 +152,7 @@ struct EstimatePlan {
   uint32_t n_pat;
   int8_t loop_slot[kPatternsMax];   // pattern -> slot in mval (models 2, 4) or -1
   double *mval;                 // [n_pat][E + n]: edge part then instruction part
-  double *fpart;                // [n_pat][n_fruns]: per function run of a 32-row tile (k_est_tiles)
-  uint32_t n_fruns;
-  const uint32_t *tile_fmask;   // [n_tiles] bit l: row 32t + l starts a function run
-  const uint32_t *tile_frun_ptr;// [n_tiles + 1] first run id of each tile
-  const uint32_t *frun_begin;   // [n_funcs + 1] first run id of each function
+  double *mrow;                 // [n_pat][n]: per use row (edges of the row + instruction part)
   const uint32_t *loop_items;   // [n_items] item ids (edge e, or E + instruction) by scope loop
   const uint32_t *loop_item_ptr;// [n_loops+1]
   const uint32_t *pre_perm;     // [n_loops] loops in preorder

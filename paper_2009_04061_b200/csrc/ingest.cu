@@ -26,7 +26,6 @@
 #include <algorithm>
 #include <cstdlib>
 
-#include <cooperative_groups.h>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -40,10 +39,6 @@ constexpr int kIngestThreads = 1024;
 #define GPA_INGEST_UNROLL 4
 #endif
 constexpr int kUnroll = GPA_INGEST_UNROLL;   // 16-byte loads in flight per thread (variants S and L)
-#ifndef GPA_INGEST_CLUSTER
-#define GPA_INGEST_CLUSTER 2
-#endif
-constexpr uint32_t kIngestCluster = GPA_INGEST_CLUSTER;   // smem variant: CTAs whose tables meet in DSMEM
 
 __device__ __forceinline__ uint4 ld_stream(const uint4 *p) {
   uint4 v;
@@ -151,23 +146,9 @@ k_ingest(const uint2 *__restrict__ rec, uint64_t n_rec, uint32_t head, uint32_t 
   }
   flush_stats(st, stats);
   if (kSmem) {
-    // The CTAs of a thread-block cluster (kIngestCluster, launched with the cluster attribute) sum
-    // their tables through distributed shared memory: CTA rank r adds bins [r*per, (r+1)*per) of
-    // every peer's table and writes the cluster's partial, so k_ingest_reduce reads one table per
-    // cluster instead of one per CTA.  A sum past 2^32 sends its high part to C directly (u32
-    // partials, exact).  Without the attribute the cluster is this CTA alone.
-    cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
-    const uint32_t csize = cl.num_blocks(), crank = cl.block_rank();
-    cl.sync();   // every table of the cluster is complete (and flush_stats' barrier is behind us)
-    const uint32_t per = (bins + csize - 1) / csize, b0 = crank * per, b1 = min(bins, b0 + per);
-    uint32_t *dst = partials + (uint64_t)(blockIdx.x / csize) * bins;
-    for (uint32_t b = b0 + threadIdx.x; b < b1; b += blockDim.x) {
-      uint64_t s = 0;
-      for (uint32_t r = 0; r < csize; ++r) s += cl.map_shared_rank(tab, r)[b];
-      if (s >> 32) atomicAdd((unsigned long long *)&C[b], (unsigned long long)(s & ~0xffffffffull));
-      dst[b] = (uint32_t)s;
-    }
-    cl.sync();   // no CTA leaves while a peer may still read its table
+    // __syncthreads() inside flush_stats ordered every table update before this read-out
+    uint32_t *dst = partials + (uint64_t)blockIdx.x * bins;
+    for (uint32_t b = threadIdx.x; b < bins; b += blockDim.x) dst[b] = tab[b];
   }
 }
 
@@ -855,26 +836,12 @@ cudaError_t launch_ingest(const DevProgram &p, int variant, const void *records,
     grid = std::min<uint32_t>(grid, kMaxIngestCtas);
     cudaError_t e = cudaFuncSetAttribute(k_ingest<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    // clusters of kIngestCluster CTAs when the grid divides into them (148 SMs = 37 x 4)
-    const uint32_t csize = (grid % kIngestCluster == 0) ? kIngestCluster : 1u;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kIngestThreads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = csize;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    e = cudaLaunchKernelEx(&cfg, k_ingest<true>, rec, n, head, p.n, p.R, bins, p.C, p.partials, p.stats);
+    k_ingest<true><<<grid, kIngestThreads, smem, s>>>(rec, n, head, p.n, p.R, bins, p.C, p.partials, p.stats);
+    e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    const uint32_t tables = grid / csize;
-    const uint32_t groups = (tables + kReduceGroup - 1) / kReduceGroup;
+    const uint32_t groups = (grid + kReduceGroup - 1) / kReduceGroup;
     const uint32_t rgrid = std::max<uint32_t>(1, std::min<uint32_t>((bins + 255) / 256, 4 * n_sms));
-    k_ingest_reduce<<<dim3(rgrid, groups), 256, 0, s>>>(p.partials, tables, bins, p.C);
+    k_ingest_reduce<<<dim3(rgrid, groups), 256, 0, s>>>(p.partials, grid, bins, p.C);
     return cudaGetLastError();
   }
   if (variant == VAR_L2) {

@@ -133,9 +133,6 @@ struct HostPlan {
   uint32_t n_partials = 0;
   std::vector<uint32_t> loop_items, loop_item_ptr, pre_perm, pre_begin, pre_end, kloop_ptr, kloops;
   uint32_t n_rows = 0;
-  // estimate tiles: per 32-row tile the rows that start a function run (bit l = row 32t + l), the
-  // tile's first run id, and per function its first run id (runs numbered in program order)
-  std::vector<uint32_t> tile_fmask, tile_frun_ptr, frun_begin;
 };
 
 gpa_status build_plan(const gpa_program_desc *d, HostPlan &h) {
@@ -230,31 +227,6 @@ gpa_status build_plan(const gpa_program_desc *d, HostPlan &h) {
       h.seg1_end.push_back((uint32_t)h.seg1_perm.size());
     }
   }
-  // ---- function runs of the 32-row tiles (estimate tiles: per-run partial sums instead of a
-  //      per-row array)
-  {
-    const uint32_t n_tiles = (n + 31) / 32;
-    std::vector<uint32_t> func_of(n);
-    for (uint32_t f = 0; f < d->n_funcs; ++f)
-      for (uint32_t i = d->func_begin[f]; i < d->func_begin[f + 1]; ++i) func_of[i] = f;
-    h.tile_fmask.assign(n_tiles, 0);
-    h.tile_frun_ptr.assign(n_tiles + 1, 0);
-    h.frun_begin.assign(d->n_funcs + 1, 0);
-    uint32_t runs = 0;
-    for (uint32_t t = 0; t < n_tiles; ++t) {
-      h.tile_frun_ptr[t] = runs;
-      for (uint32_t l = 0; l < 32 && 32 * t + l < n; ++l) {
-        const uint32_t i = 32 * t + l;
-        if (l == 0 || func_of[i] != func_of[i - 1]) {
-          h.tile_fmask[t] |= 1u << l;
-          if (i == d->func_begin[func_of[i]]) h.frun_begin[func_of[i]] = runs;   // a function's first run
-          ++runs;
-        }
-      }
-    }
-    h.tile_frun_ptr[n_tiles] = runs;
-    h.frun_begin[d->n_funcs] = runs;
-  }
   // ---- loop preorder (children visited in increasing id), subtree ranges
   std::vector<std::vector<uint32_t>> kids(L);
   std::vector<uint32_t> roots;
@@ -329,7 +301,7 @@ struct Offsets {
       edge_max, edge_use, edge_dom, edge_lca, edge_kind, def_ptr, def_perm;
   size_t tile_run_ptr, run_be, run_dst, seg1_perm, seg1_begin, seg1_end, seg1_id, seg2_perm, seg2_begin, seg2_end,
       part_v, part_al, rows_v, rows_al;
-  size_t pats, mval, fpart, tile_fmask, tile_frun_ptr, frun_begin, loop_items, loop_item_ptr, pre_perm, pre_begin, pre_end, kloop_ptr, kloops,
+  size_t pats, mval, mrow, loop_items, loop_item_ptr, pre_perm, pre_begin, pre_end, kloop_ptr, kloops,
       loop_func, lM_excl, lM_incl, fM, kM, est, hot, n_hot, rank, cov, occ;
   size_t C, stats, AL, cand, selfm, share, B, partials, part_x, part_sync;
   bool part_reserved = false;
@@ -393,10 +365,7 @@ Offsets layout(const gpa_program_desc *d, const HostPlan &h) {
   o.rows_al = a.take((size_t)h.n_rows * 2 * 8);
   o.pats = a.take(kPatWs * sizeof(gpa_pattern));
   o.mval = a.take((size_t)kLoopPatWs * (E + n) * 8);
-  o.fpart = a.take((size_t)kPatWs * h.tile_frun_ptr.back() * 8);
-  o.tile_fmask = a.take(h.tile_fmask.size() * 4);
-  o.tile_frun_ptr = a.take(h.tile_frun_ptr.size() * 4);
-  o.frun_begin = a.take(h.frun_begin.size() * 4);
+  o.mrow = a.take((size_t)kPatWs * n * 8);
   o.loop_items = a.take(h.loop_items.size() * 4);
   o.loop_item_ptr = a.take((L + 1) * 4);
   o.pre_perm = a.take(L * 4);
@@ -489,9 +458,6 @@ gpa_status gpa_program_create(const gpa_program_desc *d, void *d_workspace, size
   UP(o.def_ptr, h.def_ptr.data(), n + 1);
   UP(o.def_perm, h.def_perm.data(), E);
   UP(o.tile_run_ptr, h.tile_run_ptr.data(), h.tile_run_ptr.size());
-  UP(o.tile_fmask, h.tile_fmask.data(), h.tile_fmask.size());
-  UP(o.tile_frun_ptr, h.tile_frun_ptr.data(), h.tile_frun_ptr.size());
-  UP(o.frun_begin, h.frun_begin.data(), h.frun_begin.size());
   UP(o.run_be, h.run_be.data(), h.run_be.size());
   UP(o.run_dst, h.run_dst.data(), h.run_dst.size());
   UP(o.seg1_perm, h.seg1_perm.data(), h.seg1_perm.size());
@@ -561,11 +527,7 @@ gpa_status gpa_program_create(const gpa_program_desc *d, void *d_workspace, size
   ep.pats = (const gpa_pattern *)(ws + o.pats);
   p->pats_dev = (gpa_pattern *)(ws + o.pats);
   ep.mval = (double *)(ws + o.mval);
-  ep.fpart = (double *)(ws + o.fpart);
-  ep.n_fruns = h.tile_frun_ptr.back();
-  ep.tile_fmask = (const uint32_t *)(ws + o.tile_fmask);
-  ep.tile_frun_ptr = (const uint32_t *)(ws + o.tile_frun_ptr);
-  ep.frun_begin = (const uint32_t *)(ws + o.frun_begin);
+  ep.mrow = (double *)(ws + o.mrow);
   ep.loop_items = (const uint32_t *)(ws + o.loop_items);
   ep.loop_item_ptr = (const uint32_t *)(ws + o.loop_item_ptr);
   ep.pre_perm = (const uint32_t *)(ws + o.pre_perm);
