@@ -182,7 +182,7 @@ typedef enum {
   GPA_VIEW_STATS = 1,      /* u64 [4]: valid samples, invalid records, invalid samples, reserved;
                               starts right after GPA_VIEW_COUNTS' last byte, so one SUM
                               all-reduce of [counts | stats] combines ranks */
-  GPA_VIEW_INSTR_AL = 2,   /* u64 [n_instr][2]: A_i, L_i */
+  GPA_VIEW_INSTR_AL = 2,   /* u64 [n_instr][2]: A_i, L_i (after gpa_aggregate / gpa_analyze) */
   GPA_VIEW_CAND = 3,       /* u8 [E]: candidate mask bit r-1, r in {MEM,EXEC,SYNC} */
   GPA_VIEW_SELF = 4,       /* u8 [n_instr]: self-attribution flags bit r-1 (Q5) */
   GPA_VIEW_SHARE = 5,      /* f64 [E][3]: Eq. 1 share per dependency reason, 0 if not candidate */

@@ -1,12 +1,15 @@
-// blame.cu -- rows a2-a6: summaries, candidate pruning (rules 1-3), Eq. 1 shares for all and
-// latency samples, self-attribution, Fig. 6 classification and the def-side reduction.
+// blame.cu -- rows a2-a6: candidate pruning (rules 1-3), Eq. 1 shares for all and latency
+// samples, self-attribution, Fig. 6 classification and the def-side reduction.
 //
-//   k_summaries   A_i, L_i from the count table (a2)
-//   k_blame_rows  one thread per use row j (a3, a4): rules 1-3 per in-edge, weights
-//                 max(A_i,1)/max_len (Q1-Q4), W summed in CSR order, shares w/W
-//                 (Eq. 1), self flags when no candidate survives (Q5)
+//   k_blame_tiles a warp per 32 use rows (a3, a4): rules 1-3 per in-edge, weights
+//                 max(A_d,1)/max_len (Q1-Q4) with A_d summed from the def's count row,
+//                 W summed in CSR order, shares w/W (Eq. 1), self flags when no
+//                 candidate survives (Q5)
 //   k_def_tiles   a warp per 32 defs over the create-time def-major transpose (a5, a6):
 //                 S_j[r]*share and SL_j[r]*share summed into i's category
+//                 (k_def_rows: a thread per def, for programs of 2^20 instructions and more)
+// A_i and L_i themselves (a2): k_summaries for programs of 2^20 instructions and more (p.al_pre),
+// else summed by the rollup tiles, which read every count row anyway.
 // fp64 adds/multiplies use __dadd_rn/__dmul_rn (no FMA contraction), and every sum runs in
 // CSR/edge order, so results match a sequential evaluation of the definitions exactly.
 #include <algorithm>
@@ -16,8 +19,29 @@
 namespace gpa {
 namespace {
 
+// A_d = sum over reasons of the def's active samples ("issued samples", Q3), from
+// its count row: the row is 2R u64 = R 16-byte units, the active half its first R u64.  Computed
+// where the weight needs it (the gather of one def row per candidate edge) instead of in a separate
+// pass over the whole table; an integer sum, exact in any order.
+__device__ __forceinline__ uint64_t def_issue(const DevProgram &p, uint32_t d) {
+  const uint4 *r4 = reinterpret_cast<const uint4 *>(p.C + (uint64_t)d * 2 * p.R);
+  uint4 v[kReasonsMax / 2];
+#pragma unroll
+  for (uint32_t k = 0; k < kReasonsMax / 2; ++k)
+    if (2 * k < p.R) v[k] = r4[k];
+  uint64_t a = 0;
+#pragma unroll
+  for (uint32_t k = 0; k < kReasonsMax / 2; ++k) {
+    if (2 * k < p.R) a += (uint64_t)v[k].y << 32 | v[k].x;
+    if (2 * k + 1 < p.R) a += (uint64_t)v[k].w << 32 | v[k].z;
+  }
+  return a;
+}
+
+// A_i, L_i for every instruction (a2), one thread per row: a pass over the whole table that pays
+// off only for large programs (p.al_pre, below)
 __device__ __forceinline__ void body_summaries(const uint64_t *__restrict__ C, uint32_t n, uint32_t R,
-                            uint64_t *__restrict__ AL, uint32_t bx, uint32_t gx) {
+                                               uint64_t *__restrict__ AL, uint32_t bx, uint32_t gx) {
   pdl_wait();
   for (uint32_t i = bx * blockDim.x + threadIdx.x; i < n; i += gx * blockDim.x) {
     const uint64_t *row = C + (uint64_t)i * 2 * R;
@@ -31,9 +55,18 @@ __device__ __forceinline__ void body_summaries(const uint64_t *__restrict__ C, u
   }
 }
 
-__global__ void k_summaries(const uint64_t *__restrict__ C, uint32_t n, uint32_t R,
-                            uint64_t *__restrict__ AL) {
+__global__ void k_summaries(const uint64_t *__restrict__ C, uint32_t n, uint32_t R, uint64_t *__restrict__ AL) {
   body_summaries(C, n, R, AL, blockIdx.x, gridDim.x);
+}
+
+// A_d for the weight of an edge: from AL when k_summaries ran (large programs: the gather of one
+// 8-byte word per edge), else summed from the def's count row (small programs: one dependent
+// kernel fewer; on config 4 the 72-byte row gathers cost more than the pass, 2.21 -> 2.44 ms)
+// (a template parameter, so that each instantiation issues only its own loads)
+template <bool kPre>
+__device__ __forceinline__ uint64_t def_A(const DevProgram &p, uint32_t d) {
+  if (kPre) return p.AL[2 * (uint64_t)d];
+  return def_issue(p, d);
 }
 
 // rule 1 (Q6): bit r-1 set when def class c may cause a stall of reason r
@@ -42,96 +75,7 @@ __device__ __forceinline__ uint32_t rule1_mask(uint32_t c) {
   return (mem ? 1u : 0u) | 2u | (c == OC_SYNC ? 4u : 0u);
 }
 
-__global__ void k_blame_rows(DevProgram p) {
-  pdl_wait();
-  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < p.n; j += gridDim.x * blockDim.x) {
-    const uint64_t *row = p.C + (uint64_t)j * 2 * p.R;
-    const uint64_t dep = row[R_MEM] + row[p.R + R_MEM] + row[R_EXEC] + row[p.R + R_EXEC] +
-                         row[R_SYNC] + row[p.R + R_SYNC];
-    const uint32_t e0 = p.row_ptr[j], e1 = p.row_ptr[j + 1];
-    if (dep == 0) {  // not a node of the dependency graph
-      for (uint32_t e = e0; e < e1; ++e) {
-        p.cand[e] = 0;
-        p.share[3 * (uint64_t)e] = 0.0;
-        p.share[3 * (uint64_t)e + 1] = 0.0;
-        p.share[3 * (uint64_t)e + 2] = 0.0;
-      }
-      p.selfm[j] = 0;
-      continue;
-    }
-    // the first kBlameCache edges of the row: every load issued before any use (ids, then the
-    // defs' fields), kept in registers for both passes; longer rows continue with plain loads.
-    // The arithmetic and its order are those of the edge-at-a-time loop.
-    constexpr uint32_t kBlameCache = 4;
-    uint32_t cm[kBlameCache];
-    double cw[kBlameCache];
-    {
-      uint32_t cd[kBlameCache], cmin[kBlameCache], cmax[kBlameCache];
-      int32_t cdom[kBlameCache];
-#pragma unroll
-      for (uint32_t u = 0; u < kBlameCache; ++u) {
-        const bool in = e0 + u < e1;
-        cd[u] = in ? p.edge_def[e0 + u] : 0u;
-        cdom[u] = in ? p.edge_dom[e0 + u] : 0;
-        cmin[u] = in ? p.edge_min[e0 + u] : 0u;
-        cmax[u] = in ? p.edge_max[e0 + u] : 1u;
-      }
-#pragma unroll
-      for (uint32_t u = 0; u < kBlameCache; ++u) {
-        const bool in = e0 + u < e1;
-        const uint32_t lat = in ? p.latency[cd[u]] : 0u, cls = in ? p.opclass[cd[u]] : 0u;
-        const uint64_t a = in ? p.AL[2 * (uint64_t)cd[u]] : 0ull;
-        const bool keep = in && cdom[u] < 0 && cmin[u] <= lat;   // rules 2, 3
-        cm[u] = keep ? rule1_mask(cls) : 0u;
-        cw[u] = __ddiv_rn((double)(a ? a : 1ull), (double)cmax[u]);
-      }
-    }
-    double W0 = 0.0, W1 = 0.0, W2 = 0.0;
-#pragma unroll
-    for (uint32_t u = 0; u < kBlameCache; ++u) {
-      if (!cm[u]) continue;
-      if (cm[u] & 1u) W0 = __dadd_rn(W0, cw[u]);
-      W1 = __dadd_rn(W1, cw[u]);
-      if (cm[u] & 4u) W2 = __dadd_rn(W2, cw[u]);
-    }
-    for (uint32_t e = e0 + kBlameCache; e < e1; ++e) {
-      const uint32_t d = p.edge_def[e];
-      const bool keep = p.edge_dom[e] < 0 && p.edge_min[e] <= p.latency[d];   // rules 2, 3
-      if (!keep) continue;
-      const uint32_t m = rule1_mask(p.opclass[d]);
-      const uint64_t a = p.AL[2 * (uint64_t)d];
-      const double w = __ddiv_rn((double)(a ? a : 1ull), (double)p.edge_max[e]);
-      if (m & 1u) W0 = __dadd_rn(W0, w);
-      W1 = __dadd_rn(W1, w);
-      if (m & 4u) W2 = __dadd_rn(W2, w);
-    }
-    auto put = [&](uint32_t e, uint32_t m, double w) {
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-      if (m) {
-        if (m & 1u) s0 = __ddiv_rn(w, W0);
-        s1 = __ddiv_rn(w, W1);
-        if (m & 4u) s2 = __ddiv_rn(w, W2);
-      }
-      p.cand[e] = (uint8_t)m;
-      p.share[3 * (uint64_t)e] = s0;
-      p.share[3 * (uint64_t)e + 1] = s1;
-      p.share[3 * (uint64_t)e + 2] = s2;
-    };
-#pragma unroll
-    for (uint32_t u = 0; u < kBlameCache; ++u)
-      if (e0 + u < e1) put(e0 + u, cm[u], cw[u]);
-    for (uint32_t e = e0 + kBlameCache; e < e1; ++e) {
-      const uint32_t d = p.edge_def[e];
-      const bool keep = p.edge_dom[e] < 0 && p.edge_min[e] <= p.latency[d];
-      const uint32_t m = keep ? rule1_mask(p.opclass[d]) : 0u;
-      const uint64_t a = m ? p.AL[2 * (uint64_t)d] : 0ull;
-      put(e, m, m ? __ddiv_rn((double)(a ? a : 1ull), (double)p.edge_max[e]) : 0.0);
-    }
-    p.selfm[j] = (uint8_t)((W0 > 0.0 ? 0u : 1u) | (W1 > 0.0 ? 0u : 2u) | (W2 > 0.0 ? 0u : 4u));
-  }
-}
-
-// Warp-cooperative form of k_blame_rows (north_star: "CSR edge-parallel ... warp-level ... pruning
+// Blame rows, warp-cooperative (north_star: "CSR edge-parallel ... warp-level ... pruning
 // and normalisation"): a warp takes a tile of 32 use rows.  (1) lane = row: the live test from the
 // row's dependency-reason counts; (2) lanes over the tile's edges (coalesced edge fields, the defs'
 // latency / class / A_i gathered by 32 lanes at once): rules 1-3 and the weight of every edge, staged
@@ -147,6 +91,7 @@ struct BlameSmem {
   uint8_t sm[kBlameWarps][kTileEdges];
   uint8_t slive[kBlameWarps][32];
 };
+template <bool kPre>
 __device__ __forceinline__ void body_blame_tiles(DevProgram p, uint32_t bx, uint32_t gx) {
   pdl_wait();
   BlameSmem &S = dyn_smem<BlameSmem>();
@@ -176,7 +121,7 @@ __device__ __forceinline__ void body_blame_tiles(DevProgram p, uint32_t bx, uint
             const uint32_t d = p.edge_def[e];
             if (!(p.edge_dom[e] < 0 && p.edge_min[e] <= p.latency[d])) continue;
             const uint32_t m = rule1_mask(p.opclass[d]);
-            const uint64_t a = p.AL[2 * (uint64_t)d];
+            const uint64_t a = def_A<kPre>(p, d);
             const double w = __ddiv_rn((double)(a ? a : 1ull), (double)p.edge_max[e]);
             if (m & 1u) W0 = __dadd_rn(W0, w);
             W1 = __dadd_rn(W1, w);
@@ -189,7 +134,7 @@ __device__ __forceinline__ void body_blame_tiles(DevProgram p, uint32_t bx, uint
             const uint32_t d = p.edge_def[e];
             if (p.edge_dom[e] < 0 && p.edge_min[e] <= p.latency[d]) {
               m = rule1_mask(p.opclass[d]);
-              const uint64_t a = p.AL[2 * (uint64_t)d];
+              const uint64_t a = def_A<kPre>(p, d);
               w = __ddiv_rn((double)(a ? a : 1ull), (double)p.edge_max[e]);
             }
           }
@@ -213,7 +158,7 @@ __device__ __forceinline__ void body_blame_tiles(DevProgram p, uint32_t bx, uint
         const uint32_t d = p.edge_def[e], mn = p.edge_min[e], mx = p.edge_max[e];
         const int32_t dom = p.edge_dom[e];
         const uint32_t lat = p.latency[d], cls = p.opclass[d];
-        const uint64_t a = p.AL[2 * (uint64_t)d];
+        const uint64_t a = def_A<kPre>(p, d);
         if (dom < 0 && mn <= lat) {   // rules 2, 3
           m = rule1_mask(cls);
           w = __ddiv_rn((double)(a ? a : 1ull), (double)mx);
@@ -258,8 +203,9 @@ __device__ __forceinline__ void body_blame_tiles(DevProgram p, uint32_t bx, uint
   }
 }
 
+template <bool kPre>
 __global__ void __launch_bounds__(32 * kBlameWarps) k_blame_tiles(DevProgram p) {
-  body_blame_tiles(p, blockIdx.x, gridDim.x);
+  body_blame_tiles<kPre>(p, blockIdx.x, gridDim.x);
 }
 
 // one lane per def: S_j[r]*share and SL_j[r]*share over the def's out-edges in def-major order
@@ -376,24 +322,20 @@ inline uint32_t grid_for(uint64_t items, uint32_t threads, int n_sms) {
 }  // namespace
 
 #ifndef GPA_FUSED_TU
-// summaries + candidates / shares / self flags (rows a2-a4): everything the estimate step reads
+// candidates / shares / self flags (rows a3-a4): everything the estimate step reads
 cudaError_t launch_blame_rows(const DevProgram &p, int n_sms, cudaStream_t s, uint64_t *launches) {
-  k_summaries<<<grid_for(p.n, 256, n_sms), 256, 0, s>>>(p.C, p.n, p.R, p.AL);
-  cudaError_t e = cudaGetLastError();
-#ifndef GPA_BLAME_TILES
-#define GPA_BLAME_TILES 1
-#endif
-  if (e == cudaSuccess) {
-    if (GPA_BLAME_TILES) {
-      const uint32_t tiles = (p.n + 31) / 32;
-      const uint32_t g = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((tiles + kBlameWarps - 1) / kBlameWarps,
-                                                                            (uint64_t)n_sms * 16));
-      e = launch_pdl(p.n, k_blame_tiles, g, 32 * kBlameWarps, sizeof(BlameSmem), s, p);
-    } else {
-      e = launch_pdl(p.n, k_blame_rows, grid_for(p.n, 128, n_sms), 128, 0, s, p);
-    }
+  if (p.al_pre) {
+    k_summaries<<<grid_for(p.n, 256, n_sms), 256, 0, s>>>(p.C, p.n, p.R, p.AL);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    *launches += 1;
   }
-  *launches += 2;
+  const uint32_t tiles = (p.n + 31) / 32;
+  const uint32_t g = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((tiles + kBlameWarps - 1) / kBlameWarps,
+                                                                        (uint64_t)n_sms * 16));
+  const cudaError_t e = p.al_pre ? launch_pdl(p.n, k_blame_tiles<true>, g, 32 * kBlameWarps, sizeof(BlameSmem), s, p)
+                                  : launch_pdl(p.n, k_blame_tiles<false>, g, 32 * kBlameWarps, sizeof(BlameSmem), s, p);
+  *launches += 1;
   return e;
 }
 

@@ -7,13 +7,12 @@
 // host launchers left out) on one persistent grid of 128-thread CTAs, in the graph's dependency
 // order, with a grid-wide barrier between dependent phases:
 //
-//   1  summaries (A_i, L_i)
-//   2  blame tiles (rules 1-3, Eq. 1 shares, self flags)
-//   3  def reduction (B)            | estimate rows / edges (matched samples per item)
-//   4  rollup tiles                 | segment sums stage 1 (loops exclusive, functions)
-//   5  rollup segments stage 1      | segment sums stage 2 (loops inclusive, kernels)
-//   6  rollup segments stage 2
-//   7  estimates (Eqs. 2-5, 10)
+//   1  blame tiles (rules 1-3, Eq. 1 shares, self flags)
+//   2  def reduction (B)            | estimate rows / edges (matched samples per item)
+//   3  rollup tiles (+ A_i, L_i)    | segment sums stage 1 (loops exclusive, functions)
+//   4  rollup segments stage 1      | segment sums stage 2 (loops inclusive, kernels)
+//   5  rollup segments stage 2
+//   6  estimates (Eqs. 2-5, 10)
 //
 // Every body is the one the multi-kernel graph runs, with the same arithmetic and summation order,
 // so both paths produce bit-identical results (tests/test_gpu_fused.py).
@@ -52,43 +51,50 @@ __global__ void __launch_bounds__(kFusedThreads) k_analyze_fused(DevProgram p, R
   const uint32_t bx = blockIdx.x, gx = gridDim.x, nv = 2 * p.ncol;
   const bool est = ep.n_pat != 0;
   FMARK(0);
-  body_summaries(p.C, p.n, p.R, p.AL, bx, gx);
+  if (p.al_pre) {
+    body_summaries(p.C, p.n, p.R, p.AL, bx, gx);
+    grid.sync();
+    body_blame_tiles<true>(p, bx, gx);
+  } else {
+    body_blame_tiles<false>(p, bx, gx);
+  }
   FMARK(1);
   grid.sync();
   FMARK(2);
-  body_blame_tiles(p, bx, gx);
+  body_def_tiles(p, bx, gx);
+  if (est) {
+#if GPA_EST_EDGEPAR
+    body_est_segs(p, ep, bx, gx);
+    (void)any_slot;
+#else
+    body_est_rows(p, ep, bx, gx);
+    if (any_slot) body_est_edges(p, ep, bx, gx);
+#endif
+  }
   FMARK(3);
   grid.sync();
   FMARK(4);
-  body_def_tiles(p, bx, gx);
-  if (est) {
-    body_est_rows(p, ep, bx, gx);
-    if (any_slot) body_est_edges(p, ep, bx, gx);
-  }
-  FMARK(5);
-  grid.sync();
-  FMARK(6);
   if (rp.n_tiles) body_rollup_tiles(p, rp, bx, gx);
   if (est)
     for (uint32_t f = 0; f < s1.n_fam; ++f) body_segsum(s1, f, bx, gx);
-  FMARK(7);
+  FMARK(5);
   grid.sync();
-  FMARK(8);
+  FMARK(6);
   if (rp.n_seg1)
     body_rollup_segments(nv, rp.part_v, rp.part_al, rp.seg1_perm, rp.seg1_begin, rp.seg1_end, rp.n_seg1, rp.seg1_id,
                          rp.rows_v, rp.rows_al, bx, gx);
   if (est)
     for (uint32_t f = 0; f < s2.n_fam; ++f) body_segsum(s2, f, bx, gx);
-  FMARK(9);
+  FMARK(7);
   grid.sync();
-  FMARK(10);
+  FMARK(8);
   if (rp.n_seg2)
     body_rollup_segments(nv, rp.rows_v, rp.rows_al, rp.seg2_perm, rp.seg2_begin, rp.seg2_end, rp.n_seg2, nullptr,
                          rp.rows_v + (uint64_t)rp.n_rows1 * nv, rp.rows_al + 2 * (uint64_t)rp.n_rows1, bx, gx);
   if (est) {
-    FMARK(11);
+    FMARK(9);
     grid.sync();
-    FMARK(12);
+    FMARK(10);
     body_est_final(p, ep, bx, gx);
   }
   FMARK(15);

@@ -116,6 +116,7 @@ struct DevProgram {
   unsigned int *part_sync;          // [2*kPartBufs]: per exchange buffer, CTAs that produced / consumed it
   uint8_t *cand, *selfm;
   double *share, *B;
+  uint32_t al_pre;                  // 1: k_summaries fills AL before the blame (n >= kPdlMaxInstr)
 };
 
 // Rollup plan (create-time).  Tiles of 32 consecutive instructions; in each tile the

@@ -143,6 +143,10 @@ __global__ void __launch_bounds__(128) k_rollup_segments(uint32_t nv, const doub
 // shared memory (the k_vrows arithmetic), then lane = value slot sums each run of the tile in member
 // order and stores the run's row (or partial row) -- one coalesced row store per run
 constexpr uint32_t kTileWarps = 4;
+#ifndef GPA_ROLL_BATCH
+#define GPA_ROLL_BATCH 8
+#endif
+constexpr uint32_t kRollBatch = GPA_ROLL_BATCH;   // count-row reasons loaded per batch (k_rollup_tiles)
 __device__ __forceinline__ void body_rollup_tiles(DevProgram p, RollupPlan rp, uint32_t bx, uint32_t gx) {
   pdl_wait();
   double2 *tstage = &dyn_smem<double2>();      // [kTileWarps][32 rows][ncol] + [kTileWarps][32][2] u64
@@ -157,13 +161,6 @@ __device__ __forceinline__ void body_rollup_tiles(DevProgram p, RollupPlan rp, u
       const double2 bm = b2[BG_MEM], be = b2[BG_EXEC], bw = b2[BG_WAR], bs = b2[BG_SYNC];
       const uint32_t cls = p.opclass[i], sf = p.selfm[i];
       const uint64_t *row = p.C + (uint64_t)i * 2 * R;
-      uint64_t act[kReasonsMax], lat[kReasonsMax];
-#pragma unroll
-      for (uint32_t r = 1; r < kReasonsMax; ++r) {
-        act[r] = r < R ? row[r] : 0ull;
-        lat[r] = r < R ? row[R + r] : 0ull;
-      }
-      const uint64_t a = p.AL[2 * (uint64_t)i], l = p.AL[2 * (uint64_t)i + 1];
       double2 *out = ws + (size_t)lane * ncol;
       const double2 z = make_double2(0.0, 0.0);
       out[COL_MEM_GLOBAL] = (cls != OC_LOCAL && cls != OC_CONSTANT) ? bm : z;
@@ -173,12 +170,31 @@ __device__ __forceinline__ void body_rollup_tiles(DevProgram p, RollupPlan rp, u
       out[COL_EXEC_ARITH] = cls != OC_SHARED ? be : z;
       out[COL_EXEC_WAR] = bw;
       out[COL_SYNC] = bs;
+      // the count row in batches of kRollBatch reasons (all loads of a batch in flight together),
+      // which bounds the live count registers; A_i, L_i are summed on the way and stored
+      // as the instruction level of the A / L rollup (GPA_VIEW_INSTR_AL) unless k_summaries ran
+      uint64_t a = 0, l = 0;
 #pragma unroll
-      for (uint32_t r = 1; r < kReasonsMax; ++r) {
-        if (r >= R) break;
-        const bool on = r > R_SYNC || ((sf >> (r - 1)) & 1u);
-        out[6 + r] = on ? make_double2((double)(act[r] + lat[r]), (double)lat[r]) : z;
+      for (uint32_t r0 = 0; r0 < kReasonsMax; r0 += kRollBatch) {
+        if (r0 >= R) break;
+        uint64_t act[kRollBatch], lat[kRollBatch];
+#pragma unroll
+        for (uint32_t u = 0; u < kRollBatch; ++u) {
+          act[u] = r0 + u < R ? row[r0 + u] : 0ull;
+          lat[u] = r0 + u < R ? row[R + r0 + u] : 0ull;
+        }
+#pragma unroll
+        for (uint32_t u = 0; u < kRollBatch; ++u) {
+          const uint32_t r = r0 + u;
+          a += act[u];
+          l += lat[u];
+          if (r >= 1 && r < R) {
+            const bool on = r > R_SYNC || ((sf >> (r - 1)) & 1u);
+            out[6 + r] = on ? make_double2((double)(act[u] + lat[u]), (double)lat[u]) : z;
+          }
+        }
       }
+      if (!p.al_pre) reinterpret_cast<ulonglong2 *>(p.AL)[i] = make_ulonglong2(a, l);
       wal[2 * lane] = a;
       wal[2 * lane + 1] = l;
     }

@@ -488,6 +488,7 @@ gpa_status gpa_program_create(const gpa_program_desc *d, void *d_workspace, size
   p->ws_bytes = bytes;
   DevProgram &dp = p->d;
   dp.n = n; dp.E = E; dp.R = d->n_reasons; dp.ncol = d->n_reasons + 6;
+  dp.al_pre = n >= kPdlMaxInstr ? 1u : 0u;   // A_i, L_i by their own pass only for large programs
   dp.n_lines = d->n_lines; dp.n_loops = d->n_loops; dp.n_funcs = d->n_funcs; dp.n_kernels = d->n_kernels;
 #define DP(field, type, off) dp.field = (type)(ws + o.off)
   DP(opclass, const uint8_t *, opclass); DP(iflags, const uint8_t *, iflags);

@@ -25,9 +25,8 @@ for it in range(20):
     G.lib().gpa_debug_fused_timing(buf)
     t = np.array(buf[:], dtype=np.int64)
     if it >= 5:
-        rows.append(np.diff(t[[0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 15]]) / 1e3)
+        rows.append(np.diff(t[[0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 15]]) / 1e3)
 m = np.median(np.array(rows), axis=0)
-names = ["summ", "sync", "blame", "sync", "def+est", "sync", "tiles+seg1", "sync", "rseg1+seg2", "sync",
-         "rseg2", "sync", "final"]
+names = ["blame", "sync", "def+est", "sync", "tiles+seg1", "sync", "rseg1+seg2", "sync", "rseg2", "sync", "final"]
 print(f"cfg{cfg} grid={os.environ.get('GPA_FUSED_GRID', 'auto')}: " + "  ".join(f"{n} {v:.1f}" for n, v in zip(names, m)),
       f"total {m.sum():.1f} us")
