@@ -71,7 +71,10 @@ __device__ __forceinline__ void body_est_rows(DevProgram p, EstimatePlan ep, uin
     double sum[kEstGroup];
 #pragma unroll
     for (int k = 0; k < kEstGroup; ++k) sum[k] = 0.0;
-    for (uint32_t e = e0; e < e1; ++e) {   // loads only: per-edge values go to k_est_edges
+    // a row without dependency-reason samples gets 0 from every edge (X = 0 and, the row not being a
+    // node of the graph, no candidates): skip the walk (no +0.0 adds, so the sums are unchanged)
+    const bool dep = (XA[1] != 0.0) | (XA[2] != 0.0) | (XA[3] != 0.0);
+    for (uint32_t e = e0; dep && e < e1; ++e) {   // loads only: per-edge values go to k_est_edges
       const EdgeInfo x = edge_info(p, e, loop_j);
       if (!x.m) continue;                  // no candidate reason: adds 0 to every pattern
 #pragma unroll

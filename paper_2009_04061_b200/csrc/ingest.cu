@@ -866,7 +866,11 @@ cudaError_t launch_ingest(const DevProgram &p, int variant, const void *records,
     a.stats = p.stats;
     a.X = reinterpret_cast<uint16_t *>(p.part_x);
     a.sync = p.part_sync;
-    const uint32_t lbits = std::max<uint32_t>(kMinLocalBits, 32u - __builtin_clz(bpb));   // bpb < 2^lbits
+#ifndef GPA_PART_FORCE_LB
+#define GPA_PART_FORCE_LB 0   // tuning probe: force the local-bin width
+#endif
+    const uint32_t lbits = GPA_PART_FORCE_LB ? GPA_PART_FORCE_LB
+                                             : std::max<uint32_t>(kMinLocalBits, 32u - __builtin_clz(bpb));   // bpb < 2^lbits
     const void *kern = lbits == 13 ? (const void *)k_ingest_part<13> : lbits == 14 ? (const void *)k_ingest_part<14>
                                                                                     : (const void *)k_ingest_part<15>;
     const size_t smem = part_smem_bytes(a.bpb, G);
