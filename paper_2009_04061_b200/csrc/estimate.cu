@@ -27,9 +27,6 @@ namespace {
 #define GPA_EST_GROUP 4
 #endif
 constexpr int kEstGroup = GPA_EST_GROUP;
-#ifndef GPA_EST_EDGEPAR
-#define GPA_EST_EDGEPAR 0   // 1: k_est_segs (edge-parallel) instead of k_est_rows + k_est_edges
-#endif
 
 // A CTA = one warp per pattern group over the same 32 rows (a tile): the pattern fields are uniform
 // in a warp, and a row's C entries and edges are fetched from DRAM once and served from L1 to the
@@ -101,109 +98,6 @@ __device__ __forceinline__ void body_est_rows(DevProgram p, EstimatePlan ep, uin
       ep.mrow[(uint64_t)qi * p.n + j] = __dadd_rn(sum[k], mi);
     }
   }
-}
-
-// Edge-parallel form (GPA_EST_EDGEPAR, the default): the CTA's warps (one per pattern group) take a
-// tile of 32 consecutive use rows; lane = row stages the rows' dependency-reason samples (X) and
-// loops in shared memory, then lanes walk the tile's in-edges 32 at a time (no lane idles while
-// another walks a long row): one EdgeInfo per edge, the group's matched samples, the loop-scoped
-// patterns' per-edge item values written coalesced (the k_est_edges pass, folded in), and a
-// segmented shuffle scan over the 32 edges (segments = use rows, contiguous in CSR order) whose
-// segment tails add into per-row accumulators in shared memory.  Lane = row then adds the row's own
-// part.  The edge sum of a row is a fixed tree order, not CSR order: within the 1e-9 bound (Q20).
-__device__ __forceinline__ void body_est_segs(DevProgram p, EstimatePlan ep, uint32_t bx, uint32_t gx) {
-  pdl_wait();
-  __shared__ gpa_pattern sp[kPatternsMax];
-  __shared__ int8_t sslot[kPatternsMax];
-  __shared__ double sX[kEstWarps][32][6];                 // XA[1..3], XL[1..3] of each row
-  __shared__ int32_t sloop[kEstWarps][32];
-  __shared__ double sacc[kEstWarps][kEstGroup][32];       // per-row edge sums
-  for (uint32_t q = threadIdx.x; q < ep.n_pat; q += blockDim.x) {
-    sp[q] = ep.pats[q];
-    sslot[q] = ep.loop_slot[q];
-  }
-  __syncthreads();
-  const uint64_t stride_items = (uint64_t)p.E + p.n;
-  const uint32_t grp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (grp * kEstGroup >= ep.n_pat) return;   // spare warps (fewer pattern groups than warps)
-  const uint32_t q0 = grp * kEstGroup;
-  const uint32_t nq = min((uint32_t)kEstGroup, ep.n_pat - q0);
-  double(*X_)[6] = sX[grp];
-  int32_t *loop_ = sloop[grp];
-  double(*acc_)[32] = sacc[grp];
-  const uint32_t upto = 0xffffffffu >> (31 - lane);   // lanes 0..lane
-  for (uint32_t t = bx; 32 * t < p.n; t += gx) {
-    const uint32_t j0 = 32 * t, j = j0 + lane;
-    const bool in = j < p.n;
-    const uint64_t *row = p.C + (uint64_t)(in ? j : 0u) * 2 * p.R;
-    double XA[4], XL[4];
-#pragma unroll
-    for (int r = 1; r <= 3; ++r) {
-      const uint64_t lat = in ? row[p.R + r] : 0ull;
-      XL[r] = (double)lat;
-      XA[r] = (double)(lat + (in ? row[r] : 0ull));
-      X_[lane][r - 1] = XA[r];
-      X_[lane][r + 2] = XL[r];
-    }
-    const int32_t loop_j = in ? p.loop_id[j] : -1;
-    loop_[lane] = loop_j;
-#pragma unroll
-    for (int k = 0; k < kEstGroup; ++k) acc_[k][lane] = 0.0;
-    const uint32_t E0 = p.row_ptr[j0], E1 = p.row_ptr[min(j0 + 32, p.n)];
-    __syncwarp();
-    for (uint32_t base = E0; base < E1; base += 32) {
-      const uint32_t e = base + lane;
-      const bool ine = e < E1;
-      const uint32_t u = ine ? p.edge_use[e] - j0 : 32u + lane;   // past-the-end lanes: own segments
-      const uint32_t uprev = __shfl_up_sync(0xffffffffu, u, 1), unext = __shfl_down_sync(0xffffffffu, u, 1);
-      const uint32_t heads = __ballot_sync(0xffffffffu, lane == 0 || uprev != u);
-      const uint32_t head = 31 - __clz(heads & upto);               // first lane of my segment
-      const bool tail = lane == 31 || unext != u;
-      EdgeInfo x{};
-      double xa[4] = {0.0, 0.0, 0.0, 0.0}, xl[4] = {0.0, 0.0, 0.0, 0.0};
-      if (ine) {
-        x = edge_info(p, e, loop_[u]);
-        xa[1] = X_[u][0]; xa[2] = X_[u][1]; xa[3] = X_[u][2];
-        xl[1] = X_[u][3]; xl[2] = X_[u][4]; xl[3] = X_[u][5];
-      }
-#pragma unroll
-      for (int k = 0; k < kEstGroup; ++k) {
-        if ((uint32_t)k >= nq) break;
-        const gpa_pattern &q = sp[q0 + k];
-        double v = (ine && q.model != 5) ? edge_match(q, x, q.sample_class ? xl : xa) : 0.0;
-        if (ine && sslot[q0 + k] >= 0) ep.mval[(uint64_t)sslot[q0 + k] * stride_items + e] = v;
-#pragma unroll
-        for (uint32_t off = 1; off < 32; off <<= 1) {
-          const double y = __shfl_up_sync(0xffffffffu, v, off);
-          if (lane >= off && lane - off >= head) v = __dadd_rn(v, y);
-        }
-        if (ine && tail) acc_[k][u] = __dadd_rn(acc_[k][u], v);
-      }
-      __syncwarp();
-    }
-    if (in) {
-      const uint32_t cls_j = p.opclass[j], flags_j = p.iflags[j], self_j = p.selfm[j];
-#pragma unroll
-      for (int k = 0; k < kEstGroup; ++k) {
-        if ((uint32_t)k >= nq) break;
-        const uint32_t qi = q0 + k;
-        const gpa_pattern &q = sp[qi];
-        double tot = 0.0;
-        if (q.model != 5) {
-          const double mi = instr_match(q, p.R, row, q.sample_class ? XL : XA, cls_j, flags_j, self_j, loop_j);
-          const int slot = sslot[qi];
-          if (slot >= 0) ep.mval[(uint64_t)slot * stride_items + p.E + j] = mi;
-          tot = __dadd_rn(acc_[k][lane], mi);
-        }
-        ep.mrow[(uint64_t)qi * p.n + j] = tot;
-      }
-    }
-    __syncwarp();
-  }
-}
-
-__global__ void k_est_segs(DevProgram p, EstimatePlan ep) {
-  body_est_segs(p, ep, blockIdx.x, gridDim.x);
 }
 
 __global__ void k_est_rows(DevProgram p, EstimatePlan ep) {
@@ -448,9 +342,6 @@ cudaError_t launch_estimate_sums(const DevProgram &p, const EstimatePlan &ep, in
                                  uint64_t *launches) {
   const uint32_t n_groups = (ep.n_pat + kEstGroup - 1) / kEstGroup;   // <= 8: a warp per group
   const uint32_t g = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(((uint64_t)p.n + 31) / 32, (uint64_t)n_sms * 64));
-#if GPA_EST_EDGEPAR
-  k_est_segs<<<g, 32 * n_groups, 0, s>>>(p, ep);   // per-edge loop-scoped item values included
-#else
   k_est_rows<<<g, 32 * n_groups, 0, s>>>(p, ep);
   bool any_slot = false;
   for (uint32_t q = 0; q < ep.n_pat; ++q) any_slot |= ep.loop_slot[q] >= 0;
@@ -460,7 +351,6 @@ cudaError_t launch_estimate_sums(const DevProgram &p, const EstimatePlan &ep, in
     if (e != cudaSuccess) return e;
     *launches += 1;
   }
-#endif
   SegLaunch a, b;
   make_seg_launches(p, ep, a, b);
   const uint64_t w1 = std::max<uint64_t>((uint64_t)p.n_loops, p.n_funcs) * ep.n_pat;

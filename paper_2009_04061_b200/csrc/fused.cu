@@ -63,13 +63,8 @@ __global__ void __launch_bounds__(kFusedThreads) k_analyze_fused(DevProgram p, R
   FMARK(2);
   body_def_tiles(p, bx, gx);
   if (est) {
-#if GPA_EST_EDGEPAR
-    body_est_segs(p, ep, bx, gx);
-    (void)any_slot;
-#else
     body_est_rows(p, ep, bx, gx);
     if (any_slot) body_est_edges(p, ep, bx, gx);
-#endif
   }
   FMARK(3);
   grid.sync();
