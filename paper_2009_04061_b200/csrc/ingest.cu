@@ -416,9 +416,9 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
       const uint32_t len = slice_len(k, s0);
       const uint32_t sb = k % kStage;
       const uint32_t sg_addr = smem_addr(stag + sb * ibuf_keys), cnt_addr = smem_addr(cnt + sb * (kPartMaxCtas + 8));
+      const uint4 *rs = reinterpret_cast<const uint4 *>(a.rec + s0);
       const bool full = len == (uint32_t)CHUNK;
       PT_START;
-      const uint4 *rs = reinterpret_cast<const uint4 *>(a.rec + s0);
       uint4 vv[kDecodeRecs / 2];   // 16-byte streaming loads, in flight while waiting for the buffer
       load_chunk(rs, len, vv);
       mbar_wait(&buf_ready[sb], (k / kStage) & 1);
