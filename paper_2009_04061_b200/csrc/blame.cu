@@ -119,8 +119,9 @@ __device__ __forceinline__ void body_blame_tiles(DevProgram p, uint32_t bx, uint
         if (live)
           for (uint32_t e = e0; e < e1; ++e) {
             const uint32_t d = p.edge_def[e];
-            if (!(p.edge_dom[e] < 0 && p.edge_min[e] <= p.latency[d])) continue;
-            const uint32_t m = rule1_mask(p.opclass[d]);
+            const DefInfo di = p.dinfo[d];
+            if (!(p.edge_dom[e] < 0 && p.edge_min[e] <= di.latency)) continue;
+            const uint32_t m = rule1_mask(di.cls_flags & 0xffu);
             const uint64_t a = def_A<kPre>(p, d);
             const double w = __ddiv_rn((double)(a ? a : 1ull), (double)p.edge_max[e]);
             if (m & 1u) W0 = __dadd_rn(W0, w);
@@ -132,8 +133,9 @@ __device__ __forceinline__ void body_blame_tiles(DevProgram p, uint32_t bx, uint
           double w = 0.0;
           if (live) {
             const uint32_t d = p.edge_def[e];
-            if (p.edge_dom[e] < 0 && p.edge_min[e] <= p.latency[d]) {
-              m = rule1_mask(p.opclass[d]);
+            const DefInfo di = p.dinfo[d];
+            if (p.edge_dom[e] < 0 && p.edge_min[e] <= di.latency) {
+              m = rule1_mask(di.cls_flags & 0xffu);
               const uint64_t a = def_A<kPre>(p, d);
               w = __ddiv_rn((double)(a ? a : 1ull), (double)p.edge_max[e]);
             }
@@ -157,7 +159,8 @@ __device__ __forceinline__ void body_blame_tiles(DevProgram p, uint32_t bx, uint
       if (slive[wib][u - j0]) {
         const uint32_t d = p.edge_def[e], mn = p.edge_min[e], mx = p.edge_max[e];
         const int32_t dom = p.edge_dom[e];
-        const uint32_t lat = p.latency[d], cls = p.opclass[d];
+        const DefInfo di = p.dinfo[d];
+        const uint32_t lat = di.latency, cls = di.cls_flags & 0xffu;
         const uint64_t a = def_A<kPre>(p, d);
         if (dom < 0 && mn <= lat) {   // rules 2, 3
           m = rule1_mask(cls);

@@ -100,6 +100,16 @@ enum : int { ST_COUNTS = 1, ST_BLAMED = 2, ST_AGGREGATED = 4, ST_PATTERNS = 8, S
 enum : int { VAR_SMEM = 0, VAR_PART = 1, VAR_L2 = 2 };
 
 // Device-side view of a program: plain pointers into the workspace.
+// The fields a def-use edge gathers from its def (blame: latency, class; estimate matching: class,
+// flags, loop), packed per instruction at create time so a gather is one 16-byte load (one
+// sector) instead of one per array
+struct __align__(16) DefInfo {
+  uint32_t latency;
+  int32_t loop;
+  uint32_t cls_flags;   // opclass | iflags << 8
+  uint32_t pad;
+};
+
 struct DevProgram {
   uint32_t n, E, R, ncol, n_lines, n_loops, n_funcs, n_kernels;
   const uint8_t *opclass, *iflags;
@@ -117,6 +127,7 @@ struct DevProgram {
   uint8_t *cand, *selfm;
   double *share, *B;
   uint32_t al_pre;                  // 1: k_summaries fills AL before the blame (n >= kPdlMaxInstr)
+  const DefInfo *dinfo;             // [n] packed latency / loop / class / flags
 };
 
 // Rollup plan (create-time).  Tiles of 32 consecutive instructions; in each tile the
@@ -257,10 +268,11 @@ __device__ __forceinline__ EdgeInfo edge_info(const DevProgram &p, uint32_t e, i
   uint32_t kind = 0;
   if (x.m) {
     const uint32_t d = p.edge_def[e];
-    x.cls = p.opclass[d];
-    x.flags = p.iflags[d];
+    const DefInfo di = p.dinfo[d];
+    x.cls = di.cls_flags & 0xffu;
+    x.flags = di.cls_flags >> 8;
     kind = p.edge_kind[e];
-    x.same = p.loop_id[d] >= 0 && p.loop_id[d] == loop_j;
+    x.same = di.loop >= 0 && di.loop == loop_j;
     const double *sh = p.share + 3 * (uint64_t)e;
     x.sh0 = sh[0]; x.sh1 = sh[1]; x.sh2 = sh[2];
   }

@@ -297,7 +297,7 @@ gpa_status build_plan(const gpa_program_desc *d, HostPlan &h) {
 }
 
 struct Offsets {
-  size_t opclass, iflags, latency, line_id, loop_id, func_begin, kfb, kgb, row_ptr, edge_def, edge_min,
+  size_t dinfo, opclass, iflags, latency, line_id, loop_id, func_begin, kfb, kgb, row_ptr, edge_def, edge_min,
       edge_max, edge_use, edge_dom, edge_lca, edge_kind, def_ptr, def_perm;
   size_t tile_run_ptr, run_be, run_dst, seg1_perm, seg1_begin, seg1_end, seg1_id, seg2_perm, seg2_begin, seg2_end,
       part_v, part_al, rows_v, rows_al;
@@ -331,6 +331,7 @@ Offsets layout(const gpa_program_desc *d, const HostPlan &h) {
     o.part_sync = a.take(part ? 2 * kPartBufs * 4 : 0);   // producer + consumer counters per buffer
     o.part_reserved = part;
   }
+  o.dinfo = a.take(n * sizeof(DefInfo));
   o.opclass = a.take(n);
   o.iflags = a.take(n);
   o.latency = a.take(n * 4);
@@ -437,6 +438,12 @@ gpa_status gpa_program_create(const gpa_program_desc *d, void *d_workspace, size
   cudaStream_t s = (cudaStream_t)stream;
   uint8_t *ws = (uint8_t *)d_workspace;
   const uint32_t n = d->n_instr, E = d->row_ptr[n];
+  {
+    std::vector<DefInfo> di(n);
+    for (uint32_t i = 0; i < n; ++i)
+      di[i] = DefInfo{d->latency[i], d->loop_id[i], (uint32_t)d->opclass[i] | (uint32_t)d->iflags[i] << 8, 0u};
+    UP(o.dinfo, di.data(), n);
+  }
   UP(o.opclass, d->opclass, n);
   UP(o.iflags, d->iflags, n);
   UP(o.latency, d->latency, n);
@@ -491,6 +498,7 @@ gpa_status gpa_program_create(const gpa_program_desc *d, void *d_workspace, size
   dp.al_pre = n >= kPdlMaxInstr ? 1u : 0u;   // A_i, L_i by their own pass only for large programs
   dp.n_lines = d->n_lines; dp.n_loops = d->n_loops; dp.n_funcs = d->n_funcs; dp.n_kernels = d->n_kernels;
 #define DP(field, type, off) dp.field = (type)(ws + o.off)
+  DP(dinfo, const DefInfo *, dinfo);
   DP(opclass, const uint8_t *, opclass); DP(iflags, const uint8_t *, iflags);
   DP(latency, const uint32_t *, latency); DP(line_id, const uint32_t *, line_id);
   DP(loop_id, const int32_t *, loop_id); DP(func_begin, const uint32_t *, func_begin);
