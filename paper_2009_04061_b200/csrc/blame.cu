@@ -82,7 +82,7 @@ __device__ __forceinline__ uint32_t rule1_mask(uint32_t c) {
 // in shared memory; (3) lane = row: W per dependency reason summed over the row's edges in CSR order
 // from shared memory (the sequential order of the definition, so shares stay bit-identical to a
 // sequential evaluation), self flags; (4) lanes over edges again: shares w / W written coalesced.
-// Tiles with more than kTileEdges edges fall back to the row-per-lane loop of k_blame_rows.
+// Tiles with more than kTileEdges edges fall back to a row-per-lane loop.
 constexpr uint32_t kTileEdges = 256;
 constexpr uint32_t kBlameWarps = 4;
 struct BlameSmem {

@@ -35,7 +35,6 @@ constexpr int kEstGroup = GPA_EST_GROUP;
 // its shared-memory staging cut the resident warps of this latency-bound loop) and summing the row
 // totals per function run of the tile with a shuffle scan instead of storing them per row (config
 // 4's analysis 2.37 -> 2.49 ms, config 3's 74 -> 76 us).
-constexpr uint32_t kEstWarps = 4;   // pattern groups per CTA (kPatternsMax / kEstGroup at most)
 __device__ __forceinline__ void body_est_rows(DevProgram p, EstimatePlan ep, uint32_t bx, uint32_t gx) {
   pdl_wait();
   __shared__ gpa_pattern sp[kPatternsMax];

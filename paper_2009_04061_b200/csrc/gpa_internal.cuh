@@ -173,7 +173,6 @@ struct EstimatePlan {
   const int32_t *loop_func;     // [n_loops]
   double *lM_excl, *lM_incl;    // [n_pat][n_loops]
   double *fM, *kM;              // [n_pat][n_funcs], [n_pat][n_kernels]
-  const double *loop_incl_v;    // unused (kept for layout symmetry)
   const uint64_t *loop_incl_al, *func_al, *kern_al;
   gpa_estimate_out *out;        // [n_kernels][n_pat]
 };
