@@ -74,37 +74,44 @@ template <typename ItemFn>
 __device__ __forceinline__ void warp_sum_rows(uint32_t lane, uint32_t nv, uint32_t b, uint32_t e, ItemFn item,
                                               const double *__restrict__ vals, const uint64_t *__restrict__ al,
                                               double *__restrict__ out_v, uint64_t *__restrict__ out_al) {
+  // lane = value slot: slots < nv are the f64 values (fixed order: member u adds into a(u % 4)), the
+  // two slots after them the u64 A / L sums; every slot walks the members with the same batched
+  // 64-bit loads (16 in flight), so the A / L lanes no longer serialise behind the value lanes
   for (uint32_t s = lane; s < nv + 2; s += 32) {
-    if (s < nv) {
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      uint32_t pos = b;
-      for (; pos + 16 <= e; pos += 16) {   // 16 row loads in flight; member u still adds into a(u % 4)
-        double x[16];
+    const bool isv = s < nv;
+    const uint64_t *src = isv ? reinterpret_cast<const uint64_t *>(vals) : al;
+    const uint32_t stride = isv ? nv : 2u, off = isv ? s : s - nv;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    uint64_t acc = 0;
+    auto add = [&](double &a, uint64_t x) {
+      if (isv) a = __dadd_rn(a, __longlong_as_double((long long)x));
+      else acc += x;
+    };
+    uint32_t pos = b;
+    for (; pos + 16 <= e; pos += 16) {   // 16 row loads in flight
+      uint64_t x[16];
 #pragma unroll
-        for (int u = 0; u < 16; ++u) x[u] = vals[(uint64_t)item(pos + u) * nv + s];
+      for (int u = 0; u < 16; ++u) x[u] = src[(uint64_t)item(pos + u) * stride + off];
 #pragma unroll
-        for (int u = 0; u < 16; u += 4) {
-          a0 = __dadd_rn(a0, x[u]);
-          a1 = __dadd_rn(a1, x[u + 1]);
-          a2 = __dadd_rn(a2, x[u + 2]);
-          a3 = __dadd_rn(a3, x[u + 3]);
-        }
+      for (int u = 0; u < 16; u += 4) {
+        add(a0, x[u]);
+        add(a1, x[u + 1]);
+        add(a2, x[u + 2]);
+        add(a3, x[u + 3]);
       }
-      for (; pos + 4 <= e; pos += 4) {
-        const double x0 = vals[(uint64_t)item(pos) * nv + s], x1 = vals[(uint64_t)item(pos + 1) * nv + s];
-        const double x2 = vals[(uint64_t)item(pos + 2) * nv + s], x3 = vals[(uint64_t)item(pos + 3) * nv + s];
-        a0 = __dadd_rn(a0, x0);
-        a1 = __dadd_rn(a1, x1);
-        a2 = __dadd_rn(a2, x2);
-        a3 = __dadd_rn(a3, x3);
-      }
-      for (; pos < e; ++pos) a0 = __dadd_rn(a0, vals[(uint64_t)item(pos) * nv + s]);
-      out_v[s] = __dadd_rn(__dadd_rn(a0, a1), __dadd_rn(a2, a3));
-    } else {
-      uint64_t acc = 0;
-      for (uint32_t pos = b; pos < e; ++pos) acc += al[2 * (uint64_t)item(pos) + (s - nv)];
-      out_al[s - nv] = acc;
     }
+    for (; pos + 4 <= e; pos += 4) {
+      uint64_t x[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) x[u] = src[(uint64_t)item(pos + u) * stride + off];
+      add(a0, x[0]);
+      add(a1, x[1]);
+      add(a2, x[2]);
+      add(a3, x[3]);
+    }
+    for (; pos < e; ++pos) add(a0, src[(uint64_t)item(pos) * stride + off]);
+    if (isv) out_v[s] = __dadd_rn(__dadd_rn(a0, a1), __dadd_rn(a2, a3));
+    else out_al[s - nv] = acc;
   }
 }
 

@@ -15,6 +15,7 @@ if lib_path != "product":
 from gpagen import batch
 cfgs = [int(c) for c in sys.argv[2].split(",")] if len(sys.argv) > 2 else [2, 3]
 mode = sys.argv[3] if len(sys.argv) > 3 else "auto"
+nopat = len(sys.argv) > 4 and sys.argv[4] == "nopat"   # blame + rollup only (no estimate branch)
 out = []
 for cfg in cfgs:
     if cfg == 4:    # the batch program; plain ingest gives the same counts as the segment ingest
@@ -24,7 +25,8 @@ for cfg in cfgs:
         prog = gpagen.config_program(cfg)
         recs = gpagen.config_stream(prog, cfg).device(0, {2: 10_000_000, 3: 100_000_000}[cfg])
     P = G.Program(prog)
-    P.set_patterns(table2(prog.n_reasons))
+    if not nopat:
+        P.set_patterns(table2(prog.n_reasons))
     P.analyze_mode = mode
     P.reset(); P.ingest(recs)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
@@ -33,6 +35,9 @@ for cfg in cfgs:
         ev[0].record(); P.analyze(); ev[1].record(); torch.cuda.synchronize()
         if it >= 5:
             ts.append(ev[0].elapsed_time(ev[1]))
+    if nopat:
+        out.append(f"cfg{cfg} analyze(no patterns) {np.median(ts) * 1e3:.1f} us")
+        continue
     est = P.read_estimates_array()
     np.save(os.path.join(ROOT, "gpurun_out", f"est_{cfg}_{os.path.basename(lib_path)}_{mode}.npy"),
             np.stack([est["speedup"], est["M"]]))
