@@ -163,6 +163,16 @@ __device__ __forceinline__ void body_rollup_tiles(DevProgram p, RollupPlan rp, u
   const uint32_t warps = gx * kTileWarps;
   for (uint32_t t = bx * kTileWarps + warp; t < rp.n_tiles; t += warps) {
     const uint32_t i = 32 * t + lane;
+    // the tile's run descriptors (at most 3 x 32: lines, loops, functions), one per lane, loaded
+    // up front with the rows
+    const uint32_t r0 = rp.tile_run_ptr[t], r1 = rp.tile_run_ptr[t + 1];
+    uint32_t rbe[3], rdst[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const uint32_t r = r0 + 32 * k + lane;
+      rbe[k] = r < r1 ? rp.run_be[r] : 0u;
+      rdst[k] = r < r1 ? rp.run_dst[r] : 0u;
+    }
     if (i < p.n) {
       const double2 *b2 = reinterpret_cast<const double2 *>(p.B + 8 * (uint64_t)i);
       const double2 bm = b2[BG_MEM], be = b2[BG_EXEC], bw = b2[BG_WAR], bs = b2[BG_SYNC];
@@ -207,11 +217,14 @@ __device__ __forceinline__ void body_rollup_tiles(DevProgram p, RollupPlan rp, u
     }
     __syncwarp();
     const double *wv = reinterpret_cast<const double *>(ws);
-    const uint32_t r0 = rp.tile_run_ptr[t], r1 = rp.tile_run_ptr[t + 1];
     for (uint32_t s0 = 0; s0 < nv + 2; s0 += 32) {
       const uint32_t s = s0 + lane;
       for (uint32_t r = r0; r < r1; ++r) {
-        const uint32_t be2 = rp.run_be[r], dst = rp.run_dst[r];
+        // the run's descriptor from the lane that loaded it (a dependent global load per run was
+        // the serial tail of this loop)
+        const uint32_t k = r - r0, src = k & 31u;
+        const uint32_t be2 = __shfl_sync(0xffffffffu, k < 32 ? rbe[0] : k < 64 ? rbe[1] : rbe[2], src);
+        const uint32_t dst = __shfl_sync(0xffffffffu, k < 32 ? rdst[0] : k < 64 ? rdst[1] : rdst[2], src);
         const uint32_t b = be2 & 0xffu, e = be2 >> 8;
         const bool part = (dst & kPartialBit) != 0;
         const uint64_t row_id = dst & ~kPartialBit;
