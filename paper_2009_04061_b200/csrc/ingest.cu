@@ -687,6 +687,10 @@ constexpr uint32_t kSegTile = GPA_SEG_TILE;
 #define GPA_SEG_THREADS 512
 #endif
 constexpr uint32_t kSegThreads = GPA_SEG_THREADS;
+#ifndef GPA_SEG_UNROLL
+#define GPA_SEG_UNROLL 4
+#endif
+constexpr int kSegUnroll = GPA_SEG_UNROLL;   // 16-byte record loads in flight per thread
 
 __global__ void __launch_bounds__(kSegThreads)
 k_ingest_seg(const uint2 *__restrict__ rec, uint64_t n_rec, const uint64_t *__restrict__ seg_begin,
@@ -741,12 +745,12 @@ k_ingest_seg(const uint2 *__restrict__ rec, uint64_t n_rec, const uint64_t *__re
       const uint64_t body = (e - b - hb) >> 1;
       const uint4 *r16 = reinterpret_cast<const uint4 *>(rec + b + hb);
       uint64_t i = threadIdx.x;
-      for (; i + 3 * blockDim.x < body; i += 4 * blockDim.x) {   // four 16-byte loads in flight
-        uint4 v[4];
+      for (; i + (kSegUnroll - 1) * blockDim.x < body; i += kSegUnroll * blockDim.x) {   // loads in flight
+        uint4 v[kSegUnroll];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = ld_stream(r16 + i + u * blockDim.x);
+        for (int u = 0; u < kSegUnroll; ++u) v[u] = ld_stream(r16 + i + u * blockDim.x);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < kSegUnroll; ++u) {
           add(v[u].x, v[u].y);
           add(v[u].z, v[u].w);
         }
