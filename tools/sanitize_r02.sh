@@ -8,4 +8,6 @@ run synccheck synccheck tests/test_gpu_estimate_cases.py tests/test_gpu_batch.py
 run memcheck memcheck tests/test_gpu_parity.py -k "tiny or ragged or random_programs or wide_local or skewed"
 run memcheck memcheck tests/test_gpu_estimate_cases.py tests/test_gpu_advice.py tests/test_gpu_slicing.py tests/test_gpu_simulator.py
 run racecheck racecheck tests/test_gpu_parity.py -k "tiny or random_programs"
+run memcheck memcheck tests/test_gpu_fused.py tests/test_gpu_fuzz.py -k "not config3"
+run racecheck racecheck tests/test_gpu_fused.py -k "tiny or rodinia"
 cat $out
