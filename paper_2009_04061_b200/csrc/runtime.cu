@@ -1,7 +1,7 @@
 // runtime.cu -- host side of the C ABI (include/gpa.h): validation, create-time transposes and
 // permutations, workspace layout, call-order state, launch sequencing, host-ingest staging.
 // Every hot-path step runs in the sm_100a kernels of ingest.cu / blame.cu / rollup.cu /
-// estimate.cu; nothing here computes blame.
+// estimate.cu (fused.cu: the same bodies as one cooperative kernel); nothing here computes blame.
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
