@@ -485,11 +485,13 @@ gpa_status gpa_program_create(const gpa_program_desc *d, void *d_workspace, size
   CUDA_TRY(cudaMemsetAsync(ws + o.C, 0, o.partials - o.C, s));   // outputs zeroed
   CUDA_TRY(cudaStreamSynchronize(s));
 
+  int device = 0, n_sms = 0, optin = 0;   // queried before the handle exists: a failure leaks nothing
+  CUDA_TRY(cudaGetDevice(&device));
+  CUDA_TRY(cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, device));
+  CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
   gpa_program *p = new gpa_program();
-  CUDA_TRY(cudaGetDevice(&p->device));
-  CUDA_TRY(cudaDeviceGetAttribute(&p->n_sms, cudaDevAttrMultiProcessorCount, p->device));
-  int optin = 0;
-  CUDA_TRY(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, p->device));
+  p->device = device;
+  p->n_sms = n_sms;
   p->smem_optin = (size_t)optin;
   p->ws = ws;
   p->ws_bytes = bytes;
