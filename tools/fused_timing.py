@@ -8,7 +8,7 @@ import gpagen
 from gpagen.patterns import table2
 from paper_2009_04061_b200 import gpa as G
 
-G.LIB_PATH = os.path.join(ROOT, "build", "libft.so")
+G.LIB_PATH = os.environ.get("GPA_FT_LIB") or os.path.join(ROOT, "build", "libft.so")
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 if len(sys.argv) > 2:
     os.environ["GPA_FUSED_GRID"] = sys.argv[2]
