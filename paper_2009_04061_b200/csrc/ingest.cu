@@ -144,6 +144,7 @@ k_ingest(const uint2 *__restrict__ rec, uint64_t n_rec, uint32_t head, uint32_t 
     add(v.x, v.y);
     add(v.z, v.w);
   }
+  if (kSmem) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // k_ingest_reduce may launch
   flush_stats(st, stats);
   if (kSmem) {
     // __syncthreads() inside flush_stats ordered every table update before this read-out
@@ -158,6 +159,7 @@ k_ingest(const uint2 *__restrict__ rec, uint64_t n_rec, uint32_t head, uint32_t 
 constexpr uint32_t kReduceGroup = 16;
 __global__ void k_ingest_reduce(const uint32_t *__restrict__ partials, uint32_t n_ctas,
                                 uint32_t bins, uint64_t *__restrict__ C) {
+  pdl_wait();   // launched as a programmatic dependent of k_ingest: scheduled during its tail
   const uint32_t c0 = blockIdx.y * kReduceGroup;
   for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < bins; b += gridDim.x * blockDim.x) {
     uint32_t v[kReduceGroup];
@@ -845,8 +847,8 @@ cudaError_t launch_ingest(const DevProgram &p, int variant, const void *records,
     if (e != cudaSuccess) return e;
     const uint32_t groups = (grid + kReduceGroup - 1) / kReduceGroup;
     const uint32_t rgrid = std::max<uint32_t>(1, std::min<uint32_t>((bins + 255) / 256, 4 * n_sms));
-    k_ingest_reduce<<<dim3(rgrid, groups), 256, 0, s>>>(p.partials, grid, bins, p.C);
-    return cudaGetLastError();
+    return launch_pdl(p.n, k_ingest_reduce, dim3(rgrid, groups), dim3(256), 0, s, (const uint32_t *)p.partials, grid,
+                      bins, p.C);
   }
   if (variant == VAR_L2) {
     if (n_sms > 0) grid = std::min<uint32_t>(grid * 4, 4 * n_sms);
