@@ -211,100 +211,27 @@ __global__ void __launch_bounds__(32 * kBlameWarps) k_blame_tiles(DevProgram p) 
   body_blame_tiles<kPre>(p, blockIdx.x, gridDim.x);
 }
 
-// one lane per def: S_j[r]*share and SL_j[r]*share over the def's out-edges in def-major order
+// one lane per def (def_acc_one, gpa_internal.cuh), B stored
 __device__ __forceinline__ void def_reduce_one(const DevProgram &p, uint32_t i) {
-  double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-  for (uint32_t k = p.def_ptr[i]; k < p.def_ptr[i + 1]; ++k) {
-    const uint32_t e = p.def_perm[k];
-    const uint32_t m = p.cand[e];
-    if (!m) continue;
-    const uint64_t *row = p.C + (uint64_t)p.edge_use[e] * 2 * p.R;
-#pragma unroll
-    for (uint32_t r = R_MEM; r <= R_SYNC; ++r) {
-      if (!(m & (1u << (r - 1)))) continue;
-      const double sh = p.share[3 * (uint64_t)e + (r - 1)];
-      const uint64_t lat = row[p.R + r], all = row[r] + lat;
-      const uint32_t g = r == R_MEM ? BG_MEM : r == R_SYNC ? BG_SYNC : ((p.edge_kind[e] & K_WAR) ? BG_WAR : BG_EXEC);
-      acc[g][0] = __dadd_rn(acc[g][0], __dmul_rn((double)all, sh));
-      acc[g][1] = __dadd_rn(acc[g][1], __dmul_rn((double)lat, sh));
-    }
-  }
-  double *out = p.B + 8 * (uint64_t)i;
-#pragma unroll
-  for (int g = 0; g < 4; ++g) {
-    out[2 * g] = acc[g][0];
-    out[2 * g + 1] = acc[g][1];
-  }
+  double acc[4][2];
+  def_acc_one(p, i, acc);
+  store_B(p, i, acc);
 }
 
-// Warp-cooperative def reduction: a warp takes 32 consecutive defs.  (1) lanes over the tile's
-// out-edge positions (def-major order, coalesced def_perm): the products S_j[r]*share and
-// SL_j[r]*share of every candidate reason, gathered from the use rows by 32 lanes at once and staged
-// in shared memory with the Fig. 6 group of the EXEC reason; (2) lane = def: the sums over its
-// positions in order, reasons MEM, EXEC, SYNC -- the sequential order of def_reduce_one, so B is
-// bit-identical.  Tiles with more than kDefTileEdges positions take def_reduce_one per lane.
-constexpr uint32_t kDefTileEdges = 128;
+// Warp-cooperative def reduction: a warp per tile of 32 consecutive defs (def_tile_acc,
+// gpa_internal.cuh)
 constexpr uint32_t kDefWarps = 4;
 struct DefSmem {
-  double2 sprod[kDefWarps][3][kDefTileEdges];   // (all, lat) * share per dependency reason
-  uint8_t sm[kDefWarps][kDefTileEdges];         // candidate mask | exec group is WAR << 3
+  DefWarpSmem w[kDefWarps];
 };
 __device__ __forceinline__ void body_def_tiles(DevProgram p, uint32_t bx, uint32_t gx) {
   pdl_wait();
   DefSmem &S = dyn_smem<DefSmem>();
-  auto &sprod = S.sprod;
-  auto &sm = S.sm;
   const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint32_t n_tiles = (p.n + 31) / 32, warps = gx * kDefWarps;
-  double2(*prod)[kDefTileEdges] = sprod[wib];
-  uint8_t *m_ = sm[wib];
   for (uint32_t tile = bx * kDefWarps + wib; tile < n_tiles; tile += warps) {
-    const uint32_t i0 = tile * 32, i = i0 + lane;
-    const uint32_t K0 = p.def_ptr[i0], K1 = p.def_ptr[min(i0 + 32, p.n)];
-    if (K1 - K0 > kDefTileEdges) {   // rare: a long tile
-      if (i < p.n) def_reduce_one(p, i);
-      continue;
-    }
-    // (1) lanes over positions
-    for (uint32_t k = K0 + lane; k < K1; k += 32) {
-      const uint32_t e = p.def_perm[k];
-      const uint32_t m = p.cand[e];
-      uint32_t mm = m;
-      if (m) {
-        const uint64_t *row = p.C + (uint64_t)p.edge_use[e] * 2 * p.R;
-        if (p.edge_kind[e] & K_WAR) mm |= 8u;
-#pragma unroll
-        for (uint32_t r = R_MEM; r <= R_SYNC; ++r) {
-          if (!(m & (1u << (r - 1)))) continue;
-          const double sh = p.share[3 * (uint64_t)e + (r - 1)];
-          const uint64_t lat = row[p.R + r], all = row[r] + lat;
-          prod[r - 1][k - K0] = make_double2(__dmul_rn((double)all, sh), __dmul_rn((double)lat, sh));
-        }
-      }
-      m_[k - K0] = (uint8_t)mm;
-    }
-    __syncwarp();
-    // (2) lane = def: sums in position order
-    if (i < p.n) {
-      double acc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-      const uint32_t k0 = p.def_ptr[i] - K0, k1 = p.def_ptr[i + 1] - K0;
-      for (uint32_t k = k0; k < k1; ++k) {
-        const uint32_t mm = m_[k];
-        if (!(mm & 7u)) continue;
-#pragma unroll
-        for (uint32_t r = R_MEM; r <= R_SYNC; ++r) {
-          if (!(mm & (1u << (r - 1)))) continue;
-          const uint32_t g = r == R_MEM ? BG_MEM : r == R_SYNC ? BG_SYNC : ((mm & 8u) ? BG_WAR : BG_EXEC);
-          const double2 v = prod[r - 1][k];
-          acc[g][0] = __dadd_rn(acc[g][0], v.x);
-          acc[g][1] = __dadd_rn(acc[g][1], v.y);
-        }
-      }
-      double2 *out = reinterpret_cast<double2 *>(p.B + 8 * (uint64_t)i);
-#pragma unroll
-      for (int g = 0; g < 4; ++g) out[g] = make_double2(acc[g][0], acc[g][1]);
-    }
-    __syncwarp();
+    double acc[4][2];
+    def_tile_acc(p, tile, lane, S.w[wib], acc);
   }
 }
 

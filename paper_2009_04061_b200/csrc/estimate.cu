@@ -144,6 +144,13 @@ __global__ void k_est_edges(DevProgram p, EstimatePlan ep) {
   body_est_edges(p, ep, blockIdx.x, gridDim.x);
 }
 
+// the two independent item passes in one launch: CTAs [0, g_rows) are k_est_rows', the rest
+// k_est_edges' (both read only the blame outputs and C) -- one dependent level fewer in the graph
+__global__ void k_est_items(DevProgram p, EstimatePlan ep, uint32_t g_rows) {
+  if (blockIdx.x < g_rows) body_est_rows(p, ep, blockIdx.x, g_rows);
+  else body_est_edges(p, ep, blockIdx.x - g_rows, gridDim.x - g_rows);
+}
+
 
 struct SegFamily {
   const double *values;     // value row v starts at values + v * row_stride
@@ -335,21 +342,41 @@ inline void make_seg_launches(const DevProgram &p, const EstimatePlan &ep, SegLa
 }  // namespace
 
 #ifndef GPA_FUSED_TU
+static cudaError_t launch_segsums(const DevProgram &p, const EstimatePlan &ep, int n_sms, cudaStream_t s,
+                                  uint64_t *launches);
+
 // matched samples per item, loop / function / kernel sums: reads only the blame rows' outputs
 // (cand, share, selfm) and C, so it can run beside the def reduction and the rollup
 cudaError_t launch_estimate_sums(const DevProgram &p, const EstimatePlan &ep, int n_sms, cudaStream_t s,
                                  uint64_t *launches) {
   const uint32_t n_groups = (ep.n_pat + kEstGroup - 1) / kEstGroup;   // <= 8: a warp per group
   const uint32_t g = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(((uint64_t)p.n + 31) / 32, (uint64_t)n_sms * 64));
-  k_est_rows<<<g, 32 * n_groups, 0, s>>>(p, ep);
   bool any_slot = false;
   for (uint32_t q = 0; q < ep.n_pat; ++q) any_slot |= ep.loop_slot[q] >= 0;
+#ifndef GPA_EST_MERGE
+#define GPA_EST_MERGE 1
+#endif
+  if (GPA_EST_MERGE && any_slot && p.E && p.n < kPdlMaxInstr) {   // config 4: separate kernels measured faster
+    const uint32_t bt = 32 * n_groups;
+    const uint32_t ge = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(((uint64_t)p.E + bt - 1) / bt, (uint64_t)n_sms * 32));
+    k_est_items<<<g + ge, bt, 0, s>>>(p, ep, g);
+    *launches += 1;
+    return launch_segsums(p, ep, n_sms, s, launches);
+  }
+  k_est_rows<<<g, 32 * n_groups, 0, s>>>(p, ep);
   if (any_slot && p.E) {
     const uint32_t ge = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(((uint64_t)p.E + 255) / 256, (uint64_t)n_sms * 16));
     const cudaError_t e = launch_pdl(p.n, k_est_edges, ge, 256, 0, s, p, ep);
     if (e != cudaSuccess) return e;
     *launches += 1;
   }
+  *launches += 1;
+  return launch_segsums(p, ep, n_sms, s, launches);
+}
+
+// the two segment-sum stages over the item values
+static cudaError_t launch_segsums(const DevProgram &p, const EstimatePlan &ep, int n_sms, cudaStream_t s,
+                                  uint64_t *launches) {
   SegLaunch a, b;
   make_seg_launches(p, ep, a, b);
   const uint64_t w1 = std::max<uint64_t>((uint64_t)p.n_loops, p.n_funcs) * ep.n_pat;
@@ -359,7 +386,7 @@ cudaError_t launch_estimate_sums(const DevProgram &p, const EstimatePlan &ep, in
   const uint64_t w2 = std::max<uint64_t>((uint64_t)p.n_loops, p.n_kernels) * ep.n_pat;
   dim3 g2((uint32_t)std::max<uint64_t>(1, std::min<uint64_t>((w2 + 3) / 4, (uint64_t)n_sms * 32)), 2);
   e = launch_pdl(p.n, k_segsum, g2, 128, 0, s, b);
-  *launches += 3;
+  *launches += 2;
   return e;
 }
 

@@ -197,8 +197,10 @@ cudaError_t launch_estimate_sums(const DevProgram &p, const EstimatePlan &ep, in
                                  uint64_t *launches);
 cudaError_t launch_estimate_final(const DevProgram &p, const EstimatePlan &ep, int n_sms, cudaStream_t s,
                                   uint64_t *launches);
+// with_def: the def reduction runs inside the rollup tiles (k_def_rollup_tiles), replacing
+// launch_def_reduce before it
 cudaError_t launch_rollup(const DevProgram &p, const RollupPlan &rp, int n_sms, cudaStream_t s,
-                          uint64_t *launches);
+                          uint64_t *launches, bool with_def = false);
 cudaError_t launch_estimate(const DevProgram &p, const EstimatePlan &ep, int n_sms,
                             cudaStream_t s, uint64_t *launches);
 cudaError_t launch_vrows(const DevProgram &p, double *vbuf, int n_sms, cudaStream_t s);
@@ -243,6 +245,99 @@ __device__ __forceinline__ double vvalue(const DevProgram &p, uint32_t i, uint32
   return (double)(c ? lat : row[r] + lat);
 }
 
+
+// ---- def-side reduction (rows a5-a6), shared by the def tiles (blame.cu) and the
+// fused def + rollup tiles (rollup.cu): one def's S_j[r]*share and SL_j[r]*share over its
+// out-edges in def-major order, summed into its four Fig. 6 groups
+__device__ __forceinline__ void def_acc_one(const DevProgram &p, uint32_t i, double (&acc)[4][2]) {
+#pragma unroll
+  for (int g = 0; g < 4; ++g) acc[g][0] = acc[g][1] = 0.0;
+  for (uint32_t k = p.def_ptr[i]; k < p.def_ptr[i + 1]; ++k) {
+    const uint32_t e = p.def_perm[k];
+    const uint32_t m = p.cand[e];
+    if (!m) continue;
+    const uint64_t *row = p.C + (uint64_t)p.edge_use[e] * 2 * p.R;
+#pragma unroll
+    for (uint32_t r = R_MEM; r <= R_SYNC; ++r) {
+      if (!(m & (1u << (r - 1)))) continue;
+      const double sh = p.share[3 * (uint64_t)e + (r - 1)];
+      const uint64_t lat = row[p.R + r], all = row[r] + lat;
+      const uint32_t g = r == R_MEM ? BG_MEM : r == R_SYNC ? BG_SYNC : ((p.edge_kind[e] & K_WAR) ? BG_WAR : BG_EXEC);
+      acc[g][0] = __dadd_rn(acc[g][0], __dmul_rn((double)all, sh));
+      acc[g][1] = __dadd_rn(acc[g][1], __dmul_rn((double)lat, sh));
+    }
+  }
+}
+__device__ __forceinline__ void store_B(const DevProgram &p, uint32_t i, const double (&acc)[4][2]) {
+  double2 *out = reinterpret_cast<double2 *>(p.B + 8 * (uint64_t)i);
+#pragma unroll
+  for (int g = 0; g < 4; ++g) out[g] = make_double2(acc[g][0], acc[g][1]);
+}
+
+// Warp-cooperative def reduction of a tile of 32 consecutive defs.  (1) lanes over the tile's
+// out-edge positions (def-major order, coalesced def_perm): the products S_j[r]*share and
+// SL_j[r]*share of every candidate reason, gathered from the use rows by 32 lanes at once and staged
+// in shared memory with the Fig. 6 group of the EXEC reason; (2) lane = def: the sums over its
+// positions in order, reasons MEM, EXEC, SYNC -- the sequential order of def_acc_one, so B is
+// bit-identical.  Tiles with more than kDefTileEdges positions take def_acc_one per lane.  Stores
+// B and leaves the lane's def sums in acc (i < n); ends with the warp converged.
+constexpr uint32_t kDefTileEdges = 128;
+struct DefWarpSmem {
+  double2 prod[3][kDefTileEdges];   // (all, lat) * share per dependency reason
+  uint8_t m[kDefTileEdges];         // candidate mask | exec group is WAR << 3
+};
+__device__ __forceinline__ void def_tile_acc(const DevProgram &p, uint32_t tile, uint32_t lane, DefWarpSmem &S,
+                                             double (&acc)[4][2]) {
+  const uint32_t i0 = tile * 32, i = i0 + lane;
+  const uint32_t K0 = p.def_ptr[i0], K1 = p.def_ptr[min(i0 + 32, p.n)];
+  if (K1 - K0 > kDefTileEdges) {   // rare: a long tile
+    if (i < p.n) {
+      def_acc_one(p, i, acc);
+      store_B(p, i, acc);
+    }
+    __syncwarp();
+    return;
+  }
+  // (1) lanes over positions
+  for (uint32_t k = K0 + lane; k < K1; k += 32) {
+    const uint32_t e = p.def_perm[k];
+    const uint32_t m = p.cand[e];
+    uint32_t mm = m;
+    if (m) {
+      const uint64_t *row = p.C + (uint64_t)p.edge_use[e] * 2 * p.R;
+      if (p.edge_kind[e] & K_WAR) mm |= 8u;
+#pragma unroll
+      for (uint32_t r = R_MEM; r <= R_SYNC; ++r) {
+        if (!(m & (1u << (r - 1)))) continue;
+        const double sh = p.share[3 * (uint64_t)e + (r - 1)];
+        const uint64_t lat = row[p.R + r], all = row[r] + lat;
+        S.prod[r - 1][k - K0] = make_double2(__dmul_rn((double)all, sh), __dmul_rn((double)lat, sh));
+      }
+    }
+    S.m[k - K0] = (uint8_t)mm;
+  }
+  __syncwarp();
+  // (2) lane = def: sums in position order
+  if (i < p.n) {
+#pragma unroll
+    for (int g = 0; g < 4; ++g) acc[g][0] = acc[g][1] = 0.0;
+    const uint32_t k0 = p.def_ptr[i] - K0, k1 = p.def_ptr[i + 1] - K0;
+    for (uint32_t k = k0; k < k1; ++k) {
+      const uint32_t mm = S.m[k];
+      if (!(mm & 7u)) continue;
+#pragma unroll
+      for (uint32_t r = R_MEM; r <= R_SYNC; ++r) {
+        if (!(mm & (1u << (r - 1)))) continue;
+        const uint32_t g = r == R_MEM ? BG_MEM : r == R_SYNC ? BG_SYNC : ((mm & 8u) ? BG_WAR : BG_EXEC);
+        const double2 v = S.prod[r - 1][k];
+        acc[g][0] = __dadd_rn(acc[g][0], v.x);
+        acc[g][1] = __dadd_rn(acc[g][1], v.y);
+      }
+    }
+    store_B(p, i, acc);
+  }
+  __syncwarp();
+}
 
 // ---- pattern matching shared by the estimate and advice kernels (Table 2)
 __device__ __forceinline__ uint32_t classify(uint32_t r, uint32_t cls, uint32_t kind) {
