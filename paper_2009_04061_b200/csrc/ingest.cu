@@ -39,6 +39,10 @@ constexpr int kIngestThreads = 1024;
 #define GPA_INGEST_UNROLL 4
 #endif
 constexpr int kUnroll = GPA_INGEST_UNROLL;   // 16-byte loads in flight per thread (variants S and L)
+#ifndef GPA_SMEM_U16
+#define GPA_SMEM_U16 1
+#endif
+constexpr bool kSmemU16 = GPA_SMEM_U16;      // variant S: u16 counters in shared memory
 
 __device__ __forceinline__ uint4 ld_stream(const uint4 *p) {
   uint4 v;
@@ -95,8 +99,10 @@ k_ingest(const uint2 *__restrict__ rec, uint64_t n_rec, uint32_t head, uint32_t 
          uint32_t bins, uint64_t *__restrict__ C, uint32_t *__restrict__ partials,
          uint64_t *__restrict__ stats) {
   extern __shared__ uint32_t tab[];
+  // kSmemU16: u16 counters, two bins per word (bins = n * 2R is even); else one u32 counter per bin
+  const uint32_t words = kSmemU16 ? bins / 2 : bins;
   if (kSmem) {
-    for (uint32_t b = threadIdx.x; b < bins; b += blockDim.x) tab[b] = 0;
+    for (uint32_t b = threadIdx.x; b < words; b += blockDim.x) tab[b] = 0;
     __syncthreads();
   }
   IngestStats st{0, 0, 0};
@@ -104,7 +110,19 @@ k_ingest(const uint2 *__restrict__ rec, uint64_t n_rec, uint32_t head, uint32_t 
     uint32_t bin, cnt;
     if (decode(pc, w, n_instr, R, bin, cnt)) {
       st.valid += cnt;
-      if (kSmem) {
+      if (kSmem && kSmemU16) {
+        // u16 counters (half the table: half the zeroing, flush and reduction traffic).  The
+        // atomic's returned word decides, exactly and race-free, what a field overflow did, and the
+        // difference goes to C through L2 atomics (rare): a low field wrapping past 0xffff carries
+        // +1 into the high field (C[hi] -= 1; if that wraps the high field too, C[hi] += 65536),
+        // a high field wrapping drops 65536 out of the word.
+        const uint32_t sh = (bin & 1u) * 16u;
+        const uint32_t old = atomicAdd(&tab[bin >> 1], cnt << sh);
+        if (((old >> sh) & 0xffffu) + cnt > 0xffffu) {
+          atomicAdd((unsigned long long *)&C[bin], 65536ull);
+          if (!sh) atomicAdd((unsigned long long *)&C[bin + 1], (old >> 16) == 0xffffu ? 65535ull : ~0ull);
+        }
+      } else if (kSmem) {
         const uint32_t old = atomicAdd(&tab[bin], cnt);
         if (old > 0xffffffffu - cnt) atomicAdd((unsigned long long *)&C[bin], 1ull << 32);  // u32 wrap
       } else {
@@ -148,8 +166,8 @@ k_ingest(const uint2 *__restrict__ rec, uint64_t n_rec, uint32_t head, uint32_t 
   flush_stats(st, stats);
   if (kSmem) {
     // __syncthreads() inside flush_stats ordered every table update before this read-out
-    uint32_t *dst = partials + (uint64_t)blockIdx.x * bins;
-    for (uint32_t b = threadIdx.x; b < bins; b += blockDim.x) dst[b] = tab[b];
+    uint32_t *dst = partials + (uint64_t)blockIdx.x * words;
+    for (uint32_t b = threadIdx.x; b < words; b += blockDim.x) dst[b] = tab[b];
   }
 }
 
@@ -161,14 +179,26 @@ __global__ void k_ingest_reduce(const uint32_t *__restrict__ partials, uint32_t 
                                 uint32_t bins, uint64_t *__restrict__ C) {
   pdl_wait();   // launched as a programmatic dependent of k_ingest: scheduled during its tail
   const uint32_t c0 = blockIdx.y * kReduceGroup;
-  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < bins; b += gridDim.x * blockDim.x) {
+  const uint32_t words = kSmemU16 ? bins / 2 : bins;   // a word = two u16 bins, or one u32 bin
+  for (uint32_t b = blockIdx.x * blockDim.x + threadIdx.x; b < words; b += gridDim.x * blockDim.x) {
     uint32_t v[kReduceGroup];
 #pragma unroll
-    for (uint32_t c = 0; c < kReduceGroup; ++c) v[c] = c0 + c < n_ctas ? partials[(uint64_t)(c0 + c) * bins + b] : 0u;
-    uint64_t s = 0;
+    for (uint32_t c = 0; c < kReduceGroup; ++c) v[c] = c0 + c < n_ctas ? partials[(uint64_t)(c0 + c) * words + b] : 0u;
+    if (kSmemU16) {
+      uint64_t lo = 0, hi = 0;
 #pragma unroll
-    for (uint32_t c = 0; c < kReduceGroup; ++c) s += v[c];
-    if (s) atomicAdd((unsigned long long *)&C[b], (unsigned long long)s);
+      for (uint32_t c = 0; c < kReduceGroup; ++c) {
+        lo += v[c] & 0xffffu;
+        hi += v[c] >> 16;
+      }
+      if (lo) atomicAdd((unsigned long long *)&C[2 * b], (unsigned long long)lo);
+      if (hi) atomicAdd((unsigned long long *)&C[2 * b + 1], (unsigned long long)hi);
+    } else {
+      uint64_t s = 0;
+#pragma unroll
+      for (uint32_t c = 0; c < kReduceGroup; ++c) s += v[c];
+      if (s) atomicAdd((unsigned long long *)&C[b], (unsigned long long)s);
+    }
   }
 }
 
@@ -837,8 +867,8 @@ cudaError_t launch_ingest(const DevProgram &p, int variant, const void *records,
   const uint64_t per_cta = 1ull << 15;
   uint32_t grid = (uint32_t)std::min<uint64_t>((uint64_t)n_sms, std::max<uint64_t>(1, (n + per_cta - 1) / per_cta));
   if (variant == VAR_SMEM) {
-    const size_t smem = ingest_smem_bytes(p);
-    if (smem > smem_optin || smem > kSmemTableMax) return cudaErrorInvalidValue;
+    if (ingest_smem_bytes(p) > smem_optin || ingest_smem_bytes(p) > kSmemTableMax) return cudaErrorInvalidValue;
+    const size_t smem = kSmemU16 ? ingest_smem_bytes(p) / 2 : ingest_smem_bytes(p);
     grid = std::min<uint32_t>(grid, kMaxIngestCtas);
     cudaError_t e = cudaFuncSetAttribute(k_ingest<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -846,7 +876,8 @@ cudaError_t launch_ingest(const DevProgram &p, int variant, const void *records,
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const uint32_t groups = (grid + kReduceGroup - 1) / kReduceGroup;
-    const uint32_t rgrid = std::max<uint32_t>(1, std::min<uint32_t>((bins + 255) / 256, 4 * n_sms));
+    const uint32_t words = kSmemU16 ? bins / 2 : bins;
+    const uint32_t rgrid = std::max<uint32_t>(1, std::min<uint32_t>((words + 255) / 256, 4 * n_sms));
     return launch_pdl(p.n, k_ingest_reduce, dim3(rgrid, groups), dim3(256), 0, s, (const uint32_t *)p.partials, grid,
                       bins, p.C);
   }

@@ -271,3 +271,27 @@ def test_smem_table_u32_wrap_carried():
     o = run_oracle(prog, recs)
     assert int(o["C"].max()) > 2 ** 32 * 100
     compare(g, o, rel=REL)
+
+
+def test_smem_table_u16_field_overflows():
+    """Variant S counts in u16 fields, two bins per 32-bit word: a low field that wraps carries into
+    its high neighbour (and may wrap it too), a high field that wraps drops out of the word.  Two hot
+    bins of one word, (pc 5, ACT, NONE) and (pc 5, ACT, MEM), take 90 % of 10^7 records with random
+    counts up to 65535, so every case occurs many times in every CTA; counts stay exact."""
+    prog = gp.random_program(300, 2, 6, 3, seed=71)
+    rng = np.random.default_rng(72)
+    n = 10_000_000
+    recs = StreamSpec(prog, seed=73, count_max=4).host(0, n)
+    hot = rng.random(n)
+    reason = np.where(hot < 0.5, 0, 1).astype(np.uint64)        # bins 2*5*R + 0 (even) and + 1 (odd)
+    cnt = rng.integers(1, 65536, n, dtype=np.uint64)
+    cnt[rng.random(n) < 0.3] = 65535
+    h = np.uint64(5) | (cnt << np.uint64(32)) | (reason << np.uint64(48))   # ACT (flags 0)
+    sel = hot < 0.9
+    recs[sel] = h[sel]
+    g = run_gpu(prog, recs)
+    assert g["program"].variant == "smem"
+    o = run_oracle(prog, recs)
+    R = prog.n_reasons
+    assert int(o["C"].reshape(-1)[10 * R]) > 2 ** 36 and int(o["C"].reshape(-1)[10 * R + 1]) > 2 ** 36
+    compare(g, o, rel=REL)
