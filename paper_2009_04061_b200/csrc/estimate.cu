@@ -356,7 +356,10 @@ cudaError_t launch_estimate_sums(const DevProgram &p, const EstimatePlan &ep, in
 #ifndef GPA_EST_MERGE
 #define GPA_EST_MERGE 1
 #endif
-  if (GPA_EST_MERGE && any_slot && p.E && p.n < kPdlMaxInstr) {   // config 4: separate kernels measured faster
+#ifndef GPA_EST_MERGE_MAX_N
+#define GPA_EST_MERGE_MAX_N kPdlMaxInstr
+#endif
+  if (GPA_EST_MERGE && any_slot && p.E && p.n < (uint32_t)(GPA_EST_MERGE_MAX_N)) {   // config 4: separate kernels measured faster
     const uint32_t bt = 32 * n_groups;
     const uint32_t ge = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(((uint64_t)p.E + bt - 1) / bt, (uint64_t)n_sms * 32));
     k_est_items<<<g + ge, bt, 0, s>>>(p, ep, g);

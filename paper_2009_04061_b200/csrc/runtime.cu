@@ -836,7 +836,10 @@ static gpa_status analyze_graph(gpa_program *p, uint32_t npat, void *stream) {
     // the def reduction fused into the rollup tiles (one dependent level fewer: config 3's analysis
     // 63 -> 61 us, config 2's 34 -> 33 us), or its own kernel (from 2^20 instructions on: config 4
     // measured 0.5 % slower fused)
-    const bool dr = GPA_DEF_ROLL && p->d.n < kPdlMaxInstr && p->rp.n_tiles == (p->d.n + 31) / 32;
+#ifndef GPA_DEF_ROLL_MAX_N
+#define GPA_DEF_ROLL_MAX_N kPdlMaxInstr
+#endif
+    const bool dr = GPA_DEF_ROLL && p->d.n < (uint32_t)(GPA_DEF_ROLL_MAX_N) && p->rp.n_tiles == (p->d.n + 31) / 32;
     if (e == cudaSuccess && !dr) e = launch_def_reduce(p->d, p->n_sms, cs, &n);
     if (e == cudaSuccess)
       e = launch_rollup(p->d, p->rp, p->n_sms, cs, &n, dr);
