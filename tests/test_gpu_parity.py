@@ -295,3 +295,4 @@ def test_smem_table_u16_field_overflows():
     R = prog.n_reasons
     assert int(o["C"].reshape(-1)[10 * R]) > 2 ** 36 and int(o["C"].reshape(-1)[10 * R + 1]) > 2 ** 36
     compare(g, o, rel=REL)
+
