@@ -310,12 +310,55 @@ constexpr uint32_t kMinLocalBits = 13, kMaxLocalBits = 15;
 constexpr uint32_t kMaxKeyCount = 7;
 template <uint32_t LB> constexpr uint32_t key_max_count() { return (1u << (16 - LB)) - 1 < kMaxKeyCount ? (1u << (16 - LB)) - 1 : kMaxKeyCount; }
 constexpr uint32_t kDummyCount = 1u << 30;        // dummy-bucket counter start (never < kPartCap)
-// a chunk adds at most G * cap * 7 samples to any one table entry: a launch of at most kFlushEvery
-// chunks (the host splits longer streams) keeps every entry below 2^32 until the final flush
+// a chunk adds at most G * cap * 7 samples to any one table entry: a launch of at most
+// flush_every(shape) chunks (the host splits longer streams) keeps every entry below 2^32 until the
+// final flush
 constexpr uint32_t kBarProc = 2;   // named barrier of the processor warps (0 is __syncthreads)
-constexpr uint32_t kFlushEvery = (uint32_t)(0xffffffffull / ((uint64_t)kPartMaxCtas * kPartCap * kMaxKeyCount));
-static_assert(kPartChunk % (2 * kDecodeThreads) == 0, "whole record pairs per decode thread");
-static_assert((kPartCap * 2) % 16 == 0, "slots must be whole 16-byte units for bulk copies");
+// Exchange shapes (records per CTA per chunk, slot capacity, staging / inbox ring depths, exchange
+// buffers).  Base: the shape above (tuning macros GPA_PART_*).  Wide: bigger chunks with fuller
+// slots (mean 60.5 keys of 80 instead of 43 of 56 at G = 148) and a 2-deep inbox, used when the
+// CTA then stays within kWideSmemMax -- the shared-memory size above which the SM's L1 carve-out
+// shrinks (config 3: 142 KB; 2.21 -> 2.15 ms); tables too large for it keep Base.
+template <int CHUNK, int CAP, int STAGE, int INBOX, int BUFS>
+struct PartCfg {
+  static constexpr int kChunk = CHUNK, kCap = CAP, kStage = STAGE, kInbox = INBOX, kBufs = BUFS;
+  static_assert(CHUNK % (2 * kDecodeThreads) == 0, "whole record pairs per decode thread");
+  static_assert((CAP * 2) % 16 == 0, "slots must be whole 16-byte units for bulk copies");
+  static_assert(BUFS <= kPartBufs && CAP * BUFS <= kPartCap * kPartBufs, "exchange fits the reserved buffers");
+};
+#ifndef GPA_PARTW_CHUNK
+#define GPA_PARTW_CHUNK 8960
+#endif
+#ifndef GPA_PARTW_CAP
+#define GPA_PARTW_CAP 80
+#endif
+#ifndef GPA_PARTW_STAGE
+#define GPA_PARTW_STAGE 3
+#endif
+#ifndef GPA_PARTW_INBOX
+#define GPA_PARTW_INBOX 2
+#endif
+#ifndef GPA_PARTW_BUFS
+#define GPA_PARTW_BUFS 8
+#endif
+#ifndef GPA_PARTW_MAX_SMEM
+#define GPA_PARTW_MAX_SMEM (164 * 1024)
+#endif
+using PartBase = PartCfg<kPartChunk, kPartCap, kStage, kInbox, kPartBufs>;
+using PartWide = PartCfg<GPA_PARTW_CHUNK, GPA_PARTW_CAP, GPA_PARTW_STAGE, GPA_PARTW_INBOX, GPA_PARTW_BUFS>;
+constexpr size_t kWideSmemMax = GPA_PARTW_MAX_SMEM;
+struct PartShape {
+  uint32_t chunk, cap, stage, inbox, bufs;
+};
+template <class Cfg>
+constexpr PartShape shape_of() {
+  return PartShape{(uint32_t)Cfg::kChunk, (uint32_t)Cfg::kCap, (uint32_t)Cfg::kStage, (uint32_t)Cfg::kInbox,
+                   (uint32_t)Cfg::kBufs};
+}
+// chunks per launch that keep every u32 table entry wrap-free until the kernel's final flush
+inline uint32_t flush_every(const PartShape &c) {
+  return (uint32_t)(0xffffffffull / ((uint64_t)kPartMaxCtas * c.cap * kMaxKeyCount));
+}
 static_assert(kConsBase + kConsThreads == kPartThreads, "warp roles cover the CTA");
 
 __device__ __forceinline__ void named_bar(uint32_t id, uint32_t threads) {
@@ -355,8 +398,11 @@ __device__ __forceinline__ void tma_tile_load_2d(void *dst, const CUtensorMap *t
       : "memory");
 }
 
-template <uint32_t LB>
+template <uint32_t LB, class Cfg>
 __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, const __grid_constant__ CUtensorMap xmap) {
+  // the exchange shape of this instantiation (shadows the Base constants of the same names)
+  constexpr int kPartChunk = Cfg::kChunk, kPartCap = Cfg::kCap, kStage = Cfg::kStage, kInbox = Cfg::kInbox,
+                kPartBufs = Cfg::kBufs;
   constexpr uint32_t kLocalBits = LB, kKeyMaxCount = key_max_count<LB>();
   constexpr int CHUNK = kPartChunk;
   constexpr int kDecodeRecs = CHUNK / kDecodeThreads;   // records per decode thread per chunk
@@ -809,7 +855,7 @@ k_ingest_seg(const uint2 *__restrict__ rec, uint64_t n_rec, const uint64_t *__re
 
 // 2-D view of the exchange buffers for the consumers' column loads: element = 2-byte key,
 // cols = G * cap (one row = a producer's G slots), rows = kPartBufs * kPartMaxCtas, box = {cap, G}
-static cudaError_t make_exchange_map(CUtensorMap *tm, void *X, uint32_t G) {
+static cudaError_t make_exchange_map(CUtensorMap *tm, void *X, uint32_t G, const PartShape &c) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     void *fn = nullptr;
@@ -818,9 +864,9 @@ static cudaError_t make_exchange_map(CUtensorMap *tm, void *X, uint32_t G) {
     if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn) return cudaErrorNotSupported;
     encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
   }
-  const cuuint64_t dims[2] = {(cuuint64_t)G * kPartCap, (cuuint64_t)kPartBufs * kPartMaxCtas};
-  const cuuint64_t strides[1] = {(cuuint64_t)G * kPartCap * 2};
-  const cuuint32_t box[2] = {(cuuint32_t)kPartCap, G};
+  const cuuint64_t dims[2] = {(cuuint64_t)G * c.cap, (cuuint64_t)c.bufs * kPartMaxCtas};
+  const cuuint64_t strides[1] = {(cuuint64_t)G * c.cap * 2};
+  const cuuint32_t box[2] = {c.cap, G};
   const cuuint32_t estr[2] = {1, 1};
   CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, X, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                       CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -834,11 +880,12 @@ extern "C" int gpa_debug_read_timing(unsigned long long *out) {
 }
 #endif
 
-size_t part_smem_bytes(uint32_t bpb, uint32_t G) {
-  const size_t ibuf = ((size_t)G * kPartCap * 2 + 127) & ~(size_t)127;
-  return (kInbox + kStage) * ibuf + kTrash * 4 + kStage * (kPartMaxCtas + 8) * 4 +
-         (2 * kStage + kPartBufs + 2 * kInbox) * 8 + (size_t)(bpb + kTrash) * 4;
+static size_t part_smem_bytes(uint32_t bpb, uint32_t G, const PartShape &c) {
+  const size_t ibuf = ((size_t)G * c.cap * 2 + 127) & ~(size_t)127;
+  return (c.inbox + c.stage) * ibuf + kTrash * 4 + c.stage * (kPartMaxCtas + 8) * 4 +
+         (2 * c.stage + c.bufs + 2 * c.inbox) * 8 + (size_t)(bpb + kTrash) * 4;
 }
+size_t part_smem_bytes(uint32_t bpb, uint32_t G) { return part_smem_bytes(bpb, G, shape_of<PartBase>()); }
 
 static uint32_t part_grid(int n_sms) { return (uint32_t)std::min(n_sms, kPartMaxCtas); }
 
@@ -851,9 +898,9 @@ static bool part_shape(const DevProgram &p, int n_sms, uint32_t &G, uint32_t &pp
   return bpb < (1u << kMaxLocalBits) && G <= 256;   // 2-byte keys: <= 15-bit local bins; TMA box <= 256
 }
 
-bool part_feasible(const DevProgram &p, int n_sms, size_t smem_optin) {
+bool part_feasible(const DevProgram &p, int n_sms, size_t smem_optin) {   // Base is the smaller shape
   uint32_t G, ppb, bpb;
-  return part_shape(p, n_sms, G, ppb, bpb) && part_smem_bytes(bpb, G) + 256 <= smem_optin;
+  return part_shape(p, n_sms, G, ppb, bpb) && part_smem_bytes(bpb, G, shape_of<PartBase>()) + 256 <= smem_optin;
 }
 
 size_t ingest_smem_bytes(const DevProgram &p) { return (size_t)p.n * 2 * p.R * 4; }
@@ -908,12 +955,23 @@ cudaError_t launch_ingest(const DevProgram &p, int variant, const void *records,
 #endif
     const uint32_t lbits = GPA_PART_FORCE_LB ? GPA_PART_FORCE_LB
                                              : std::max<uint32_t>(kMinLocalBits, 32u - __builtin_clz(bpb));   // bpb < 2^lbits
-    const void *kern = lbits == 13 ? (const void *)k_ingest_part<13> : lbits == 14 ? (const void *)k_ingest_part<14>
-                                                                                    : (const void *)k_ingest_part<15>;
-    const size_t smem = part_smem_bytes(a.bpb, G);
+#ifndef GPA_PART_WIDE
+#define GPA_PART_WIDE 1
+#endif
+    // the Wide exchange shape when the CTA stays within kWideSmemMax with it, else Base
+    const PartShape wide_c = shape_of<PartWide>(), base_c = shape_of<PartBase>();
+    const size_t smem_w = part_smem_bytes(a.bpb, G, wide_c);
+    const bool use_wide = GPA_PART_WIDE && smem_w <= kWideSmemMax && smem_w + 256 <= smem_optin;
+    const PartShape &c = use_wide ? wide_c : base_c;
+    const void *kern =
+        use_wide ? (lbits == 13 ? (const void *)k_ingest_part<13, PartWide>
+                                : lbits == 14 ? (const void *)k_ingest_part<14, PartWide> : (const void *)k_ingest_part<15, PartWide>)
+                 : (lbits == 13 ? (const void *)k_ingest_part<13, PartBase>
+                                : lbits == 14 ? (const void *)k_ingest_part<14, PartBase> : (const void *)k_ingest_part<15, PartBase>);
+    const size_t smem = part_smem_bytes(a.bpb, G, c);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    e = cudaMemsetAsync(p.part_sync, 0, 2 * kPartBufs * sizeof(unsigned int), s);
+    e = cudaMemsetAsync(p.part_sync, 0, 2 * c.bufs * sizeof(unsigned int), s);
     if (e != cudaSuccess) return e;
     if (head || ((n - head) & 1ull)) {
       k_ingest_edges<<<1, 32, 0, s>>>(rec, n, head, p.n, p.R, p.C, p.stats);
@@ -922,23 +980,23 @@ cudaError_t launch_ingest(const DevProgram &p, int variant, const void *records,
     }
     if (a.n_even == 0) return cudaSuccess;
     CUtensorMap xmap;
-    e = make_exchange_map(&xmap, p.part_x, G);
+    e = make_exchange_map(&xmap, p.part_x, G, c);
     if (e != cudaSuccess) return e;
-    // a launch runs at most kFlushEvery chunks, so no u32 table entry can wrap before the
+    // a launch runs at most flush_every(c) chunks, so no u32 table entry can wrap before the
     // kernel's final flush into the u64 table (> 6.5e10 records: several launches)
     // (GPA_PART_LAUNCH_CHUNKS lowers the limit: a test hook that exercises the split on small streams)
-    uint64_t launch_chunks = kFlushEvery;
+    uint64_t launch_chunks = flush_every(c);
     if (const char *env = getenv("GPA_PART_LAUNCH_CHUNKS")) {
       const unsigned long long v = strtoull(env, nullptr, 10);
       if (v > 0 && v < launch_chunks) launch_chunks = v;
     }
-    const uint64_t body = a.n_even, max_launch = launch_chunks * G * kPartChunk;
+    const uint64_t body = a.n_even, max_launch = launch_chunks * G * c.chunk;
     const uint2 *base = a.rec;
     for (uint64_t off = 0; off < body; off += max_launch) {
       a.rec = base + off;
       a.n_even = std::min<uint64_t>(max_launch, body - off);
       if (off > 0) {
-        e = cudaMemsetAsync(p.part_sync, 0, 2 * kPartBufs * sizeof(unsigned int), s);
+        e = cudaMemsetAsync(p.part_sync, 0, 2 * c.bufs * sizeof(unsigned int), s);
         if (e != cudaSuccess) return e;
       }
       void *args[] = {&a, &xmap};
