@@ -8,10 +8,14 @@ h = rows[hi]
 k, mn, v, idc = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("ID")
 per = OrderedDict()
 for r in rows[hi + 1:]:
-    per.setdefault((r[idc], r[k].split("(")[0][-34:]), {})[r[mn]] = float(r[v].replace(",", ""))
+    full = r[k].split("(")[0]
+    name = full.replace("gpa::<unnamed>::", "")   # template arguments may repeat the namespace
+    name = ("gpa::" + name if "gpa::" in full else name)
+    name = name[:34] if "part" in name else name[-34:]   # keep the kernel name of the long template ids
+    per.setdefault((r[idc], name, flt in full), {})[r[mn]] = float(r[v].replace(",", ""))
 tot = 0.0
-for (i, name), m in per.items():
-    if flt not in name:
+for (i, name, keep), m in per.items():
+    if not keep:
         continue
     t = m.get("gpu__time_duration.sum", 0) / 1e3
     tot += t
