@@ -95,7 +95,9 @@ def test_part_large_tables_smaller_chunk(n_instr, R):
 
 
 @pytest.mark.parametrize("n_instr,R,count_max", [(150_000, 9, 1), (150_000, 9, 5), (100_000, 16, 3),
-                                                 (120_000, 9, 3)])
+                                                 (120_000, 9, 3),
+                                                 (80_000, 9, 4),     # 14-bit local bins on the Wide exchange shape
+                                                 (45_000, 12, 9)])   # 13-bit, Wide, R = 12, counts past the key
 def test_part_wide_local_bins(n_instr, R, count_max):
     """PeleC / Quicksilver-sized kernels: per-CTA tables of 9,126-21,632
     bins need 14- or 15-bit local keys (1-2 count bits), and stay on the exchange path instead of
