@@ -1011,7 +1011,10 @@ cudaError_t launch_ingest(const DevProgram &p, int variant, const void *records,
 cudaError_t launch_ingest_segments(const DevProgram &p, const void *records, uint64_t n, const uint64_t *seg_begin,
                                    const uint32_t *seg_kernel, uint32_t n_seg, uint32_t pc_base, uint32_t max_tab_bins,
                                    int n_sms, cudaStream_t s) {
-  const size_t smem = (size_t)max_tab_bins * 4;
+#ifndef GPA_SEG_SMEM_PAD
+#define GPA_SEG_SMEM_PAD 0   // tuning probe: extra dynamic shared memory per CTA (fewer CTAs per SM)
+#endif
+  const size_t smem = (size_t)max_tab_bins * 4 + GPA_SEG_SMEM_PAD;
   cudaError_t e = cudaFuncSetAttribute(k_ingest_seg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 1;
