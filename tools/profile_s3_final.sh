@@ -1,6 +1,7 @@
 #!/bin/bash
 # Round 2, final session: smoke, the full GPU suite, bench lines for every workload and the
-# reference arm, ncu launch lists (config 3, config 2, config 4), sanitizers on the changed kernels.
+# reference arm, ncu launch lists (config 3, config 2, config 4), ncu --set full of the ingest kernel
+# (compute-sanitizer is closed on the pool).
 set -x
 TAG=r02
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/smi_$TAG.txt
@@ -17,13 +18,6 @@ timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
     --log-file gpurun_out/launches_config2_$TAG.csv python bench.py --workload rodinia --steps 2 --warmup 1 --e2e-steps 0 --no-cpu-baseline > /dev/null 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv \
     --log-file gpurun_out/launches_config4_$TAG.csv python tools/batch_profile.py > /dev/null 2>&1
-out=gpurun_out/sanitizer_$TAG.txt
-echo "# compute-sanitizer on the B200 (round 2, final session: u16 smem ingest, PDL reduce, def+rollup tiles, estimate items)" > $out
-run() { echo "## $1: $2" >> $out; shift; tool=$1; shift
-  timeout 1500 compute-sanitizer --tool $tool --print-limit 10 python -m pytest -q -x "$@" 2>&1 | grep -E "passed|failed|SUMMARY|Error|hazard" | head -30 >> $out; }
-run synccheck synccheck tests/test_gpu_parity.py -k "tiny or ragged or random_programs or wide_local or u16"
-run memcheck memcheck tests/test_gpu_parity.py -k "tiny or ragged or random_programs or wide_local or skewed or u16"
-run memcheck memcheck tests/test_gpu_estimate_cases.py tests/test_gpu_advice.py tests/test_gpu_fused.py
-run racecheck racecheck tests/test_gpu_parity.py -k "tiny or random_programs or u16"
-run racecheck racecheck tests/test_gpu_fused.py -k "tiny or rodinia"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_ingest_part -c 1 \
+    -o gpurun_out/prof_ingest_$TAG python bench.py --profile > gpurun_out/ncu_ingest_$TAG.log 2>&1
 ls -la gpurun_out/
