@@ -82,6 +82,7 @@ constexpr int kPartCap = GPA_PART_CAP;                // keys per (src, dst) slo
                                             // excess -> L2 atomics
 constexpr int kPartMaxCtas = 160;           // < 255: bucket ids fit a byte
 size_t part_smem_bytes(uint32_t bpb, uint32_t G);
+constexpr size_t kPartZeroBytes = 64 * 1024;  // >= one staging buffer of any exchange shape
 
 // stall reasons
 constexpr uint32_t R_NONE = 0, R_MEM = 1, R_EXEC = 2, R_SYNC = 3;
@@ -124,6 +125,7 @@ struct DevProgram {
   uint32_t *partials;               // [kMaxIngestCtas][n*2R] per-CTA tables (smem variant)
   uint32_t *part_x;                 // [kPartBufs][kPartMaxCtas dst][G src][kPartCap] 2-byte exchange keys
   unsigned int *part_sync;          // [2*kPartBufs]: per exchange buffer, CTAs that produced / consumed it
+  const uint16_t *part_zero;        // [kPartZeroBytes] zeros (GPA_PART_TMA_ZERO staging clears)
   uint8_t *cand, *selfm;
   double *share, *B;
   uint32_t al_pre;                  // 1: k_summaries fills AL before the blame (n >= kPdlMaxInstr)

@@ -278,6 +278,7 @@ struct PartArgs {
   uint64_t *C, *stats;
   uint16_t *X;            // [kPartBufs][src < kPartMaxCtas][dst < G][kPartCap] 2-byte keys, zero-padded
   unsigned int *sync;     // [kPartBufs] produced, [kPartBufs] consumed
+  const uint16_t *zero;   // kPartZeroBytes of zeros (staging clears by bulk copy, GPA_PART_TMA_ZERO)
 };
 
 // warp roles of the 1024-thread CTA
@@ -319,12 +320,16 @@ constexpr uint32_t kBarProc = 2;   // named barrier of the processor warps (0 is
 // slots (mean 60.5 keys of 80 instead of 43 of 56 at G = 148) and a 2-deep inbox, used when the
 // CTA then stays within kWideSmemMax -- the shared-memory size above which the SM's L1 carve-out
 // shrinks (config 3: 142 KB; 2.21 -> 2.15 ms); tables too large for it keep Base.
-template <int CHUNK, int CAP, int STAGE, int INBOX, int BUFS>
+template <int CHUNK, int CAP, int STAGE, int INBOX, int BUFS, bool TMA_ZERO>
 struct PartCfg {
   static constexpr int kChunk = CHUNK, kCap = CAP, kStage = STAGE, kInbox = INBOX, kBufs = BUFS;
+  // staging buffers cleared by a bulk copy from a zero block (no LSU wavefronts) instead of
+  // shared-memory stores: measured faster for Base's large-table (PeleC-scale) CTAs, slower for Wide
+  static constexpr bool kTmaZero = TMA_ZERO;
   static_assert(CHUNK % (2 * kDecodeThreads) == 0, "whole record pairs per decode thread");
   static_assert((CAP * 2) % 16 == 0, "slots must be whole 16-byte units for bulk copies");
   static_assert(BUFS <= kPartBufs && CAP * BUFS <= kPartCap * kPartBufs, "exchange fits the reserved buffers");
+  static_assert((size_t)kPartMaxCtas * CAP * 2 <= kPartZeroBytes, "the zero block covers a staging buffer");
 };
 #ifndef GPA_PARTW_CHUNK
 #define GPA_PARTW_CHUNK 8960
@@ -344,8 +349,15 @@ struct PartCfg {
 #ifndef GPA_PARTW_MAX_SMEM
 #define GPA_PARTW_MAX_SMEM (164 * 1024)
 #endif
-using PartBase = PartCfg<kPartChunk, kPartCap, kStage, kInbox, kPartBufs>;
-using PartWide = PartCfg<GPA_PARTW_CHUNK, GPA_PARTW_CAP, GPA_PARTW_STAGE, GPA_PARTW_INBOX, GPA_PARTW_BUFS>;
+#ifndef GPA_PART_TMA_ZERO
+#define GPA_PART_TMA_ZERO 1      // Base shape
+#endif
+#ifndef GPA_PARTW_TMA_ZERO
+#define GPA_PARTW_TMA_ZERO 0     // Wide shape
+#endif
+using PartBase = PartCfg<kPartChunk, kPartCap, kStage, kInbox, kPartBufs, GPA_PART_TMA_ZERO>;
+using PartWide = PartCfg<GPA_PARTW_CHUNK, GPA_PARTW_CAP, GPA_PARTW_STAGE, GPA_PARTW_INBOX, GPA_PARTW_BUFS,
+                         GPA_PARTW_TMA_ZERO>;
 constexpr size_t kWideSmemMax = GPA_PARTW_MAX_SMEM;
 struct PartShape {
   uint32_t chunk, cap, stage, inbox, bufs;
@@ -621,11 +633,25 @@ __global__ void __launch_bounds__(kPartThreads, 1) k_ingest_part(PartArgs a, con
       PT_MARK(15);
       if (k + kStage < n_chunks) {
         const uint32_t ob = k % kStage;
-        uint4 *z = reinterpret_cast<uint4 *>(stag + ob * ibuf_keys);
-        for (uint32_t i = lane; i < slot_keys / 8; i += 32) z[i] = make_uint4(0, 0, 0, 0);
         for (uint32_t i = lane; i <= G; i += 32) cnt[ob * (kPartMaxCtas + 8) + i] = i == G ? kDummyCount : 0u;
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&buf_ready[ob]);
+        if constexpr (Cfg::kTmaZero) {
+          // the staging buffer cleared by a bulk copy from a zero block (async proxy, no LSU
+          // wavefronts); buf_ready completes when its bytes have landed
+          __syncwarp();
+          if (lane == 0) {
+            mbar_expect_tx(&buf_ready[ob], slot_keys * 2);
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_addr(stag + ob * ibuf_keys)),
+                "l"(a.zero), "r"(slot_keys * 2), "r"(smem_addr(&buf_ready[ob]))
+                : "memory");
+          }
+        } else {
+          uint4 *z = reinterpret_cast<uint4 *>(stag + ob * ibuf_keys);
+          for (uint32_t i = lane; i < slot_keys / 8; i += 32) z[i] = make_uint4(0, 0, 0, 0);
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&buf_ready[ob]);
+        }
       }
       PT_MARK(7);
     }
@@ -950,6 +976,7 @@ cudaError_t launch_ingest(const DevProgram &p, int variant, const void *records,
     a.stats = p.stats;
     a.X = reinterpret_cast<uint16_t *>(p.part_x);
     a.sync = p.part_sync;
+    a.zero = p.part_zero;
 #ifndef GPA_PART_FORCE_LB
 #define GPA_PART_FORCE_LB 0   // tuning probe: force the local-bin width
 #endif

@@ -303,7 +303,7 @@ struct Offsets {
       part_v, part_al, rows_v, rows_al;
   size_t pats, mval, mrow, loop_items, loop_item_ptr, pre_perm, pre_begin, pre_end, kloop_ptr, kloops,
       loop_func, lM_excl, lM_incl, fM, kM, est, hot, n_hot, rank, cov, occ;
-  size_t C, stats, AL, cand, selfm, share, B, partials, part_x, part_sync;
+  size_t C, stats, AL, cand, selfm, share, B, partials, part_x, part_sync, part_zero;
   bool part_reserved = false;
   size_t total;
 };
@@ -329,6 +329,7 @@ Offsets layout(const gpa_program_desc *d, const HostPlan &h) {
     const size_t pairs = (size_t)kPartBufs * kPartMaxCtas * kPartMaxCtas;
     o.part_x = a.take(part ? pairs * kPartCap * 2 : 0);   // 2-byte keys
     o.part_sync = a.take(part ? 2 * kPartBufs * 4 : 0);   // producer + consumer counters per buffer
+    o.part_zero = a.take(part ? kPartZeroBytes : 0);       // zeros: source of the staging-buffer clears
     o.part_reserved = part;
   }
   o.dinfo = a.take(n * sizeof(DefInfo));
@@ -483,6 +484,7 @@ gpa_status gpa_program_create(const gpa_program_desc *d, void *d_workspace, size
   UP(o.kloops, h.kloops.data(), h.kloops.size());
   UP(o.loop_func, h.loop_func.data(), h.loop_func.size());
   CUDA_TRY(cudaMemsetAsync(ws + o.C, 0, o.partials - o.C, s));   // outputs zeroed
+  if (o.part_reserved) CUDA_TRY(cudaMemsetAsync(ws + o.part_zero, 0, kPartZeroBytes, s));
   CUDA_TRY(cudaStreamSynchronize(s));
 
   int device = 0, n_sms = 0, optin = 0;   // queried before the handle exists: a failure leaks nothing
@@ -514,6 +516,7 @@ gpa_status gpa_program_create(const gpa_program_desc *d, void *d_workspace, size
   DP(cand, uint8_t *, cand); DP(selfm, uint8_t *, selfm); DP(share, double *, share);
   DP(B, double *, B); DP(partials, uint32_t *, partials);
   DP(part_x, uint32_t *, part_x); DP(part_sync, unsigned int *, part_sync);
+  DP(part_zero, const uint16_t *, part_zero);
 #undef DP
   RollupPlan &rp = p->rp;
   rp.tile_run_ptr = (const uint32_t *)(ws + o.tile_run_ptr);
