@@ -296,7 +296,7 @@ constexpr int kDecodeThreads = kDecodeWarps * 32;
 constexpr int kConsThreads = kConsWarps * 32;
 constexpr int kConsBase = (kPubWarp + 1) * 32;
 #ifndef GPA_PART_INBOX
-#define GPA_PART_INBOX 3
+#define GPA_PART_INBOX 2
 #endif
 constexpr int kInbox = GPA_PART_INBOX;                          // consumer inbox depth (exchange chunks)
 #ifndef GPA_PART_STAGE
