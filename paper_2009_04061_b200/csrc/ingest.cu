@@ -328,6 +328,7 @@ struct PartCfg {
   static constexpr bool kTmaZero = TMA_ZERO;
   static_assert(CHUNK % (2 * kDecodeThreads) == 0, "whole record pairs per decode thread");
   static_assert((CAP * 2) % 16 == 0, "slots must be whole 16-byte units for bulk copies");
+  static_assert(STAGE >= 2 && INBOX >= 2, "the ring hand-offs need two buffers (one deadlocks)");
   static_assert(BUFS <= kPartBufs && CAP * BUFS <= kPartCap * kPartBufs, "exchange fits the reserved buffers");
   static_assert((size_t)kPartMaxCtas * CAP * 2 <= kPartZeroBytes, "the zero block covers a staging buffer");
 };
